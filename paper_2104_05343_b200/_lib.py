@@ -1,0 +1,82 @@
+"""ctypes binding of libsg.so (include/sg.h).
+
+The library is mandatory: there is no CPU fallback for any operator. Loading
+fails loudly when the in-tree build is missing; compute calls raise unless a
+CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import ConfigError, ShapeError, SummaGridError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
+
+SG_OK, SG_ERR_SHAPE, SG_ERR_CONFIG, SG_ERR_CUDA = 0, 1, 2, 3
+DTYPE_BF16, DTYPE_F32 = 0, 1
+ACT_NONE, ACT_GELU, ACT_DGELU = 0, 1, 2
+
+i64 = ctypes.c_int64
+i32 = ctypes.c_int32
+vp = ctypes.c_void_p
+
+
+class GemmArgs(ctypes.Structure):
+    """Mirror of ``sg_gemm_args`` (include/sg.h)."""
+
+    _fields_ = [
+        ("M", i64), ("N", i64), ("K", i64),
+        ("nb1", i64), ("nb2", i64),
+        ("A", vp), ("lda", i64), ("sa1", i64), ("sa2", i64), ("a_mn_major", i32),
+        ("B", vp), ("ldb", i64), ("sb1", i64), ("sb2", i64), ("b_mn_major", i32),
+        ("D", vp), ("ldd", i64), ("sd1", i64), ("sd2", i64), ("d_dtype", i32),
+        ("C", vp), ("ldc", i64), ("sc1", i64), ("sc2", i64), ("c_dtype", i32),
+        ("bias", vp),
+        ("aux", vp), ("ldx", i64), ("sx1", i64), ("sx2", i64),
+        ("act", i32),
+        ("alpha", ctypes.c_float),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/sg.h
+SIGNATURES: dict[str, tuple] = {
+    "sg_gemm": (i32, [ctypes.POINTER(GemmArgs), vp]),
+    "sg_device_sm_count": (i32, []),
+    "sg_build_info": (ctypes.c_char_p, []),
+    "sg_last_error": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libsg.so once; raise SummaGridError if the native build is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise SummaGridError(
+            f"native library {_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    handle = ctypes.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SG_OK:
+        return
+    msg = lib().sg_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if msg else what
+    if rc == SG_ERR_SHAPE:
+        raise ShapeError(text)
+    if rc == SG_ERR_CONFIG:
+        raise ConfigError(text)
+    raise SummaGridError(text)

@@ -1,0 +1,35 @@
+// Library-wide host entry points: error reporting and device queries.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "sg.h"
+#include "sg_internal.h"
+
+namespace sg {
+static thread_local char g_err[512] = {0};
+int set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg ? msg : "");
+  return code;
+}
+void clear_error() { g_err[0] = 0; }
+}  // namespace sg
+
+extern "C" const char* sg_last_error(void) { return sg::g_err; }
+
+extern "C" int sg_device_sm_count(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  // Cached per device ordinal (a process may drive several devices).
+  static int cache[64] = {0};
+  if (dev < 64 && cache[dev] > 0) return cache[dev];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  if (dev < 64) cache[dev] = n;
+  return n;
+}
+
+extern "C" const char* sg_build_info(void) {
+  return "libsg sm_100a (tcgen05/TMA) built with nvcc " __DATE__;
+}

@@ -1,0 +1,123 @@
+"""tcgen05 GEMM (libsg sg_gemm) against a plain PyTorch fp32 reference.
+
+Covers the three SUMMA operand layouts (AB: K-major A / MN-major B, ABT: both
+K-major, ATB: both MN-major), ragged M/N/K, every epilogue and the strided
+batched (per-head) form used by the attention kernels.
+"""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _k():
+    from paper_2104_05343_b200 import kernels
+
+    return kernels
+
+
+def _rel(x, ref):
+    x = x.float()
+    ref = ref.float()
+    return ((x - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+
+
+def _rand(*shape, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("layout", ["ab", "abt", "atb", "atbt"])
+@pytest.mark.parametrize("mnk", [(128, 256, 64), (256, 512, 192), (300, 200, 100), (1000, 72, 520),
+                                 (64, 1000, 33), (2048, 3072, 1024)])
+def test_gemm_layouts(layout, mnk):
+    k = _k()
+    torch.manual_seed(0)
+    M, N, K = mnk
+    if layout in ("ab", "abt"):
+        a = _rand(M, K)
+    else:
+        a = _rand(K, M).t()
+    if layout in ("ab", "atb"):
+        b = _rand(K, N)
+    else:
+        b = _rand(N, K).t()
+    # TMA needs 16-byte aligned leading dims; pad storage where the extent is odd
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    try:
+        k.gemm(a, b, out)
+    except Exception as e:  # unaligned strides are rejected, not silently wrong
+        assert "aligned" in str(e)
+        return
+    ref = a.float() @ b.float()
+    assert _rel(out, ref) < 1e-5
+
+
+def test_gemm_epilogues():
+    k = _k()
+    torch.manual_seed(1)
+    M, N, K = 512, 768, 256
+    a, b = _rand(M, K), _rand(K, N)
+    bias = torch.randn(N, device="cuda")
+    c = torch.randn(M, N, device="cuda")
+    ref = a.float() @ b.float()
+    out = torch.empty(M, N, device="cuda")
+    k.gemm(a, b, out, alpha=0.5, bias=bias, c=c)
+    assert _rel(out, 0.5 * ref + bias + c) < 1e-5
+    # in-place accumulation (SUMMA step l > 0): C == D
+    acc = c.clone()
+    k.gemm(a, b, acc, c=acc)
+    assert _rel(acc, ref + c) < 1e-5
+    # GELU with saved pre-activation, bf16 output
+    mid = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    k.gemm(a, b, act, bias=bias, act=k.ACT_GELU, aux=mid)
+    x = ref + bias
+    assert _rel(mid, x) < 1e-2
+    gelu = 0.5 * x * (1 + torch.tanh(math.sqrt(2 / math.pi) * (x + 0.044715 * x ** 3)))
+    assert _rel(act, gelu) < 1e-2
+    # GELU' epilogue reading the saved pre-activation
+    dact = torch.empty(M, N, device="cuda")
+    k.gemm(a, b, dact, act=k.ACT_DGELU, aux=mid)
+    xm = mid.float()
+    t = torch.tanh(math.sqrt(2 / math.pi) * (xm + 0.044715 * xm ** 3))
+    dg = 0.5 * (1 + t) + 0.5 * xm * (1 - t * t) * math.sqrt(2 / math.pi) * (1 + 3 * 0.044715 * xm ** 2)
+    assert _rel(dact, ref * dg) < 1e-4
+
+
+def test_gemm_batched_heads():
+    """Per-head products on the interleaved QKV block layout (layers.py:404-416)."""
+    k = _k()
+    torch.manual_seed(2)
+    b_loc, n_loc, s, d = 2, 3, 256, 64
+    hb = n_loc * d
+    qkv = _rand(b_loc * s, 3 * hb)
+    q = qkv[:, :hb].view(b_loc, s, n_loc, d).permute(0, 2, 1, 3)       # [b, n, s, d] strided view
+    kk = qkv[:, hb:2 * hb].view(b_loc, s, n_loc, d).permute(0, 2, 1, 3)
+    v = qkv[:, 2 * hb:].view(b_loc, s, n_loc, d).permute(0, 2, 1, 3)
+    scores = torch.empty(b_loc, n_loc, s, s, device="cuda")
+    k.gemm(q, kk.transpose(-1, -2), scores, alpha=1 / math.sqrt(d))
+    ref = (q.float() @ kk.float().transpose(-1, -2)) / math.sqrt(d)
+    assert _rel(scores, ref) < 1e-5
+    p = torch.softmax(scores, -1).to(torch.bfloat16)
+    ctx = torch.empty(b_loc * s, hb, device="cuda", dtype=torch.bfloat16)
+    ctx_v = ctx.view(b_loc, s, n_loc, d).permute(0, 2, 1, 3)
+    k.gemm(p, v, ctx_v)
+    assert _rel(ctx_v, p.float() @ v.float()) < 1e-2
+    # dV = P^T dO: MN-major A (P transposed view), MN-major B
+    dv = torch.empty(b_loc, n_loc, s, d, device="cuda")
+    k.gemm(p.transpose(-1, -2), ctx_v, dv)
+    assert _rel(dv, p.float().transpose(-1, -2) @ ctx_v.float()) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096)])
+def test_gemm_large_square(M, N, K):
+    k = _k()
+    torch.manual_seed(3)
+    a, b = _rand(M, K), _rand(K, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    k.gemm(a, b, out)
+    ref = a.float() @ b.float()
+    assert _rel(out, ref) < 1e-2
