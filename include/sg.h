@@ -70,6 +70,74 @@ typedef struct sg_gemm_args {
 
 int sg_gemm(const sg_gemm_args* args, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * HBM-bound per-device kernels (row kernels: one warp per row, 16-byte
+ * vector accesses). dtype arguments are SG_DTYPE_*; leading dimensions are in
+ * elements and must keep rows 16-byte aligned.
+ * ------------------------------------------------------------------------- */
+
+/* LayerNorm phase 1: stats[r] = (sum_c x, sum_c x^2) — the packed pair the
+ * reference all-reduces along the mesh row (layers.py:274-280). */
+int sg_ln_stats(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, float* stats, void* stream);
+/* LayerNorm phase 2: y = (x-mu)*rstd*gamma + beta over the global hidden size
+ * h_total (layers.py:295-303). stats == NULL computes them locally (only valid
+ * when cols == h_total, i.e. a 1-column mesh). Saves mean / rstd per row. */
+int sg_ln_fwd(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, const float* stats, int64_t h_total,
+              float eps, const float* gamma, const float* beta, void* y, int ydt, int64_t ldy, float* mean,
+              float* rstd, void* stream);
+/* LayerNorm backward phase 1: stats[r] = (sum x^ g, sum g), g = dy*gamma (layers.py:319-326). */
+int sg_ln_bwd_stats(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx, const float* mean,
+                    const float* rstd, const float* gamma, int64_t rows, int64_t cols, float* stats, void* stream);
+/* LayerNorm backward phase 2: dx = rstd*(g - sum_g/h - x^ sum_xg/h) + resid (fp32),
+ * optional bf16 copy dx2, dgamma/dbeta += column sums (layers.py:329-342, 744-753). */
+int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx, const float* mean,
+              const float* rstd, const float* gamma, int64_t rows, int64_t cols, const float* stats, int64_t h_total,
+              const void* resid, int rdt, int64_t ldr, void* dx, int dxdt, int64_t lddx, void* dx2, int64_t lddx2,
+              float* dgamma, float* dbeta, void* stream);
+/* out[c] (+)= sum_r x[r,c]: bias gradients before the column reduce (layers.py:238). */
+int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, float* out, int accumulate,
+              void* stream);
+/* x[r,c] += bias[c] in place (layers.py:228). */
+int sg_bias_add(void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, const float* bias, void* stream);
+/* Row softmax with max subtraction (dense.py:67-75) and its backward
+ * dS = P*(dP - rowsum(dP*P))*scale (layers.py:447-450). */
+int sg_softmax_rows(const void* s, int sdt, int64_t rows, int64_t cols, int64_t lds, void* p, int pdt, int64_t ldp,
+                    void* stream);
+int sg_softmax_bwd(const void* dp, int dpdt, int64_t lddp, const void* p, int pdt, int64_t ldp, int64_t rows,
+                   int64_t cols, float scale, void* ds, int dsdt, int64_t ldds, void* stream);
+/* Vocab-parallel cross entropy (layers.py:539-624). Local pass over the device's
+ * vocabulary block: lmax, gmax (= lmax, to be max-all-reduced along the row),
+ * packed = (sum e^{x-lmax}, x_label). Then sg_xent_rescale re-bases the sums on
+ * the row max before the packed sum all-reduce, sg_xent_loss forms per-row
+ * losses and their sum, sg_xent_bwd writes dlogits = (softmax - onehot)*scale. */
+int sg_xent_local(const void* logits, int ldt, int64_t rows, int64_t ldl, int64_t n_real, const int64_t* labels,
+                  int64_t col_lo, float* lmax, float* gmax, float* packed, void* stream);
+int sg_xent_rescale(int64_t rows, const float* lmax, const float* gmax, float* packed, void* stream);
+int sg_xent_loss(int64_t rows, const float* gmax, const float* packed, float* loss_rows, float* partial,
+                 void* stream);
+int sg_xent_bwd(const void* logits, int ldt, int64_t rows, int64_t ldl, int64_t n_real, int64_t ncols,
+                const int64_t* labels, int64_t col_lo, const float* gmax, const float* packed, float scale, void* dl,
+                int dldt, int64_t lddl, void* stream);
+/* Embedding gather for ids in [lo, lo+vb) and its scatter-add backward (layers.py:178-205). */
+int sg_embed_fwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const void* table, int tdt, int64_t ldt,
+                 int64_t hc, void* out, int odt, int64_t ldo, void* stream);
+int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const void* dout, int ddt, int64_t ldd,
+                 int64_t hc, float* grad, int64_t ldg, void* stream);
+/* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
+int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
+           int64_t cols, void* stream);
+/* out = act(alpha*x + bias + C) on an fp32 partial sum: the sg_gemm epilogue for
+ * products whose mesh reduce had to complete first (dist AB^T forms). */
+int sg_epilogue(const float* x, int64_t rows, int64_t cols, int64_t ldx, float alpha, const float* bias,
+                const void* cin, int cdt, int64_t ldc, int act, void* aux, int64_t ldaux, void* out, int odt,
+                int64_t ldo, void* stream);
+/* Element-wise cast, memset and ordered fold dst = [dst op] src0 op src1 ...
+ * (op: 0 sum, 1 max) — the rank-ordered reduce of mesh.py:458-499. */
+int sg_cast(const void* src, int sdt, void* dst, int ddt, int64_t n, void* stream);
+int sg_zero(void* ptr, int64_t bytes, void* stream);
+int sg_fold(void* dst, int dt, const void* const* srcs, int nsrc, int64_t n, int accumulate, int op_max,
+            void* stream);
+
 /* Number of SMs of the current device and library build id (sanity). */
 int sg_device_sm_count(void);
 const char* sg_build_info(void);

@@ -44,6 +44,26 @@ class GemmArgs(ctypes.Structure):
 # name -> (restype, argtypes); every symbol declared in include/sg.h
 SIGNATURES: dict[str, tuple] = {
     "sg_gemm": (i32, [ctypes.POINTER(GemmArgs), vp]),
+    "sg_ln_stats": (i32, [vp, i32, i64, i64, i64, vp, vp]),
+    "sg_ln_fwd": (i32, [vp, i32, i64, i64, i64, vp, i64, ctypes.c_float, vp, vp, vp, i32, i64, vp, vp, vp]),
+    "sg_ln_bwd_stats": (i32, [vp, i32, i64, vp, i32, i64, vp, vp, vp, i64, i64, vp, vp]),
+    "sg_ln_bwd": (i32, [vp, i32, i64, vp, i32, i64, vp, vp, vp, i64, i64, vp, i64, vp, i32, i64, vp, i32, i64,
+                        vp, i64, vp, vp, vp]),
+    "sg_colsum": (i32, [vp, i32, i64, i64, i64, vp, i32, vp]),
+    "sg_bias_add": (i32, [vp, i32, i64, i64, i64, vp, vp]),
+    "sg_softmax_rows": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),
+    "sg_softmax_bwd": (i32, [vp, i32, i64, vp, i32, i64, i64, i64, ctypes.c_float, vp, i32, i64, vp]),
+    "sg_xent_local": (i32, [vp, i32, i64, i64, i64, vp, i64, vp, vp, vp, vp]),
+    "sg_xent_rescale": (i32, [i64, vp, vp, vp, vp]),
+    "sg_xent_loss": (i32, [i64, vp, vp, vp, vp, vp]),
+    "sg_xent_bwd": (i32, [vp, i32, i64, i64, i64, i64, vp, i64, vp, vp, ctypes.c_float, vp, i32, i64, vp]),
+    "sg_embed_fwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i32, i64, vp]),
+    "sg_embed_bwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i64, vp]),
+    "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
+    "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),
+    "sg_cast": (i32, [vp, i32, vp, i32, i64, vp]),
+    "sg_zero": (i32, [vp, i64, vp]),
+    "sg_fold": (i32, [vp, i32, ctypes.POINTER(vp), i32, i64, i32, i32, vp]),
     "sg_device_sm_count": (i32, []),
     "sg_build_info": (ctypes.c_char_p, []),
     "sg_last_error": (ctypes.c_char_p, []),

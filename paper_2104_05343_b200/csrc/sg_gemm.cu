@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -316,6 +317,62 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
+
+// ------------------------------------------------------------------ SIMT path
+// CUDA-core fallback for operands the TMA unit cannot address (row pitches or
+// batch strides that are not 16-byte multiples, e.g. head_dim 4 in the
+// reference's unit-test configurations). Same semantics and epilogue.
+struct SimtParams {
+  GemmParams p;
+  const __nv_bfloat16* A;
+  long long lda, sa1, sa2;
+  int a_mn;
+  const __nv_bfloat16* B;
+  long long ldb, sb1, sb2;
+  int b_mn;
+  int nb1;
+};
+
+__global__ void gemm_simt_kernel(const __grid_constant__ SimtParams sp) {
+  const GemmParams& p = sp.p;
+  const long long total = (long long)sp.nb1 * p.nb2 * p.M * p.N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(idx % p.N);
+    long long t = idx / p.N;
+    const int m = (int)(t % p.M);
+    t /= p.M;
+    const int z2 = (int)(t % p.nb2);
+    const int z1 = (int)(t / p.nb2);
+    const __nv_bfloat16* a = sp.A + z1 * sp.sa1 + z2 * sp.sa2;
+    const __nv_bfloat16* b = sp.B + z1 * sp.sb1 + z2 * sp.sb2;
+    float acc = 0.f;
+    for (int k = 0; k < p.K; ++k) {
+      const float av = __bfloat162float(sp.a_mn ? a[(long long)k * sp.lda + m] : a[(long long)m * sp.lda + k]);
+      const float bv = __bfloat162float(sp.b_mn ? b[(long long)k * sp.ldb + n] : b[(long long)n * sp.ldb + k]);
+      acc = fmaf(av, bv, acc);
+    }
+    float v = acc * p.alpha;
+    if (p.bias) v += p.bias[n];
+    if (p.C) {
+      const size_t ci = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2 + (size_t)m * p.ldc + n;
+      v += p.c_f32 ? static_cast<const float*>(p.C)[ci] : __bfloat162float(static_cast<const __nv_bfloat16*>(p.C)[ci]);
+    }
+    const size_t xi = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2 + (size_t)m * p.ldx + n;
+    if (p.act == SG_ACT_GELU) {
+      if (p.aux) static_cast<__nv_bfloat16*>(p.aux)[xi] = __float2bfloat16_rn(v);
+      v = gelu_f(v);
+    } else if (p.act == SG_ACT_DGELU) {
+      v *= gelu_grad_f(__bfloat162float(static_cast<const __nv_bfloat16*>(p.aux)[xi]));
+    }
+    const size_t di = (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 + (size_t)m * p.ldd + n;
+    if (p.d_f32)
+      static_cast<float*>(p.D)[di] = v;
+    else
+      static_cast<__nv_bfloat16*>(p.D)[di] = __float2bfloat16_rn(v);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -461,6 +518,26 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.vec_ok = al(a->D, a->ldd, a->sd1, a->sd2, p.d_f32 ? 4 : 2) && al(a->C, a->ldc, a->sc1, a->sc2, p.c_f32 ? 4 : 2) &&
              al(a->aux, a->ldx, a->sx1, a->sx2, 2);
 
+  // TMA needs 16-byte aligned bases, row pitches and batch strides; otherwise
+  // take the CUDA-core path (tiny / odd-shaped operands only).
+  auto tma_ok = [](const void* ptr, long long ld, long long n1, long long s1, long long n2, long long s2) {
+    return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (ld * 2) % 16 == 0 && (n1 <= 1 || (s1 * 2) % 16 == 0) &&
+           (n2 <= 1 || (s2 * 2) % 16 == 0);
+  };
+  if (!tma_ok(a->A, a->lda, a->nb1, a->sa1, a->nb2, a->sa2) || !tma_ok(a->B, a->ldb, a->nb1, a->sb1, a->nb2, a->sb2)) {
+    SimtParams sp;
+    sp.p = p;
+    sp.A = static_cast<const __nv_bfloat16*>(a->A);
+    sp.lda = a->lda; sp.sa1 = a->sa1; sp.sa2 = a->sa2; sp.a_mn = a->a_mn_major;
+    sp.B = static_cast<const __nv_bfloat16*>(a->B);
+    sp.ldb = a->ldb; sp.sb1 = a->sb1; sp.sb2 = a->sb2; sp.b_mn = a->b_mn_major;
+    sp.nb1 = (int)a->nb1;
+    const long long total = a->nb1 * a->nb2 * a->M * a->N;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+    gemm_simt_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(sp);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+  }
   CUtensorMap ta, tb;
   int rc;
   // A: K-major -> (K, M); MN-major -> (M, K)

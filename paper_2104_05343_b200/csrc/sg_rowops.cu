@@ -1,0 +1,911 @@
+// HBM-bound per-device kernels of the 2D transformer: LayerNorm (two-phase,
+// so only the per-row (sum, sumsq) / (sum x^ g, sum g) scalars cross the mesh
+// row), attention softmax and its backward, vocab-parallel cross entropy,
+// embedding gather / scatter-add, bias column sums, SGD and the ordered
+// element-wise folds the single-GPU mesh simulation uses for its reduces.
+//
+// Row kernels map one warp to one row and move 8 elements per lane per step
+// with 16-byte vector accesses (bf16) or 2x16-byte (fp32); grids are sized as
+// multiples of the SM count. Reference math: layers.py:253-351 (LayerNorm),
+// dense.py:67-75 + layers.py:444-452 (softmax fwd/bwd), layers.py:539-624
+// (cross entropy), layers.py:151-211 (embedding), layers.py:218-246 (bias).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdint>
+
+#include "sg.h"
+#include "sg_internal.h"
+
+namespace sg {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---- 8-wide element access (n = number of valid elements, <= 8) ----------
+__device__ __forceinline__ void ld8(const float* p, int n, float (&v)[8]) {
+  if (n == 8) {
+    float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < n ? p[i] : 0.f;
+  }
+}
+__device__ __forceinline__ void ld8(const bf16* p, int n, float (&v)[8]) {
+  if (n == 8) {
+    uint4 a = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < n ? __bfloat162float(p[i]) : 0.f;
+  }
+}
+__device__ __forceinline__ void st8(float* p, int n, const float (&v)[8]) {
+  if (n == 8) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < n) p[i] = v[i];
+  }
+}
+__device__ __forceinline__ void st8(bf16* p, int n, const float (&v)[8]) {
+  if (n == 8) {
+    uint4 a;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = a;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < n) p[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float ld1(const T* p);
+template <>
+__device__ __forceinline__ float ld1<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ld1<bf16>(const bf16* p) { return __bfloat162float(*p); }
+
+static int g_sms = 0;
+static int grid_for(long long work_items, int per_block, int waves = 8) {
+  if (g_sms <= 0) g_sms = sg_device_sm_count();
+  long long need = (work_items + per_block - 1) / per_block;
+  long long cap = (long long)(g_sms > 0 ? g_sms : 148) * waves;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+static int launch_check() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+static bool aligned16(const void* p, long long ld, int esz) {
+  return p == nullptr || ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * esz) % 16 == 0);
+}
+
+#define SG_DISPATCH_T(dt, T, ...)            \
+  do {                                       \
+    if ((dt) == SG_DTYPE_F32) {              \
+      typedef float T;                       \
+      __VA_ARGS__;                           \
+    } else {                                 \
+      typedef bf16 T;                        \
+      __VA_ARGS__;                           \
+    }                                        \
+  } while (0)
+
+// ============================================================ LayerNorm
+// stats[row] = (sum x, sum x^2) over the local columns (layers.py:274-275)
+template <typename TX>
+__global__ void ln_stats_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
+                                float* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const TX* xr = x + r * ldx;
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane * 8; c < cols; c += 256) {
+      float v[8];
+      ld8(xr + c, min(8, cols - c), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s1 += v[i];
+        s2 += v[i] * v[i];
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      stats[2 * r] = s1;
+      stats[2 * r + 1] = s2;
+    }
+  }
+}
+
+// y = (x - mu) * rstd * gamma + beta with mu, var from the (row all-reduced)
+// stats or, when stats == nullptr, from this device's row (1 x c == 1 x 1).
+template <typename TX, typename TY>
+__global__ void ln_fwd_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
+                              const float* __restrict__ stats, float inv_h, float eps,
+                              const float* __restrict__ gamma, const float* __restrict__ beta, TY* __restrict__ y,
+                              long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const TX* xr = x + r * ldx;
+    float s1, s2;
+    if (stats) {
+      s1 = stats[2 * r];
+      s2 = stats[2 * r + 1];
+    } else {
+      s1 = 0.f;
+      s2 = 0.f;
+      for (int c = lane * 8; c < cols; c += 256) {
+        float v[8];
+        ld8(xr + c, min(8, cols - c), v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          s1 += v[i];
+          s2 += v[i] * v[i];
+        }
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+    }
+    const float mu = s1 * inv_h;
+    const float var = s2 * inv_h - mu * mu;  // one-pass variance, layers.py:296-297
+    const float rs = 1.0f / sqrtf(var + eps);
+    for (int c = lane * 8; c < cols; c += 256) {
+      const int n = min(8, cols - c);
+      float v[8], g[8], b[8];
+      ld8(xr + c, n, v);
+      ld8(gamma + c, n, g);
+      ld8(beta + c, n, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * g[i] + b[i];
+      st8(y + r * ldy + c, n, v);
+    }
+    if (lane == 0) {
+      if (mean_out) mean_out[r] = mu;
+      if (rstd_out) rstd_out[r] = rs;
+    }
+  }
+}
+
+// stats[row] = (sum x^ g, sum g), g = dy * gamma (layers.py:319-321)
+template <typename TD, typename TX>
+__global__ void ln_bwd_stats_kernel(const TD* __restrict__ dy, long long lddy, const TX* __restrict__ x,
+                                    long long ldx, const float* __restrict__ mean, const float* __restrict__ rstd,
+                                    const float* __restrict__ gamma, long long rows, int cols,
+                                    float* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const float mu = mean[r], rs = rstd[r];
+    float sxg = 0.f, sg = 0.f;
+    for (int c = lane * 8; c < cols; c += 256) {
+      const int n = min(8, cols - c);
+      float d[8], v[8], g[8];
+      ld8(dy + r * lddy + c, n, d);
+      ld8(x + r * ldx + c, n, v);
+      ld8(gamma + c, n, g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gg = d[i] * g[i];
+        sxg += (v[i] - mu) * rs * gg;
+        sg += gg;
+      }
+    }
+    sxg = warp_sum(sxg);
+    sg = warp_sum(sg);
+    if (lane == 0) {
+      stats[2 * r] = sxg;
+      stats[2 * r + 1] = sg;
+    }
+  }
+}
+
+// dx = rstd * (g - sum_g/h - x^ * sum_xg/h) [+ resid]; dgamma += sum_rows dy x^,
+// dbeta += sum_rows dy (layers.py:329-342). Grid: (row blocks, 1024-col segments).
+constexpr int kSeg = 1024;
+template <typename TD, typename TX, typename TR, typename TO>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(
+    const TD* __restrict__ dy, long long lddy, const TX* __restrict__ x, long long ldx,
+    const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma, long long rows,
+    int cols, const float* __restrict__ stats, float inv_h, const TR* __restrict__ resid, long long ldr,
+    TO* __restrict__ dx, long long lddx, bf16* __restrict__ dx2, long long lddx2, float* __restrict__ dgamma,
+    float* __restrict__ dbeta) {
+  __shared__ float s_dg[kSeg], s_db[kSeg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * kSeg;
+  const int seg = min(kSeg, cols - c0);
+  const bool want_g = dgamma != nullptr;
+  if (want_g) {
+    for (int i = threadIdx.x; i < kSeg; i += blockDim.x) {
+      s_dg[i] = 0.f;
+      s_db[i] = 0.f;
+    }
+    __syncthreads();
+  }
+  float ag[4][8], ab[4][8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = 0.f;
+  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
+    const float mu = mean[r], rs = rstd[r];
+    const float m_xg = stats[2 * r] * inv_h, m_g = stats[2 * r + 1] * inv_h;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = k * 256 + lane * 8;
+      if (c >= seg) break;
+      const int n = min(8, seg - c);
+      const int cc = c0 + c;
+      float d[8], v[8], g[8], o[8];
+      ld8(dy + r * lddy + cc, n, d);
+      ld8(x + r * ldx + cc, n, v);
+      ld8(gamma + cc, n, g);
+      if (resid)
+        ld8(resid + r * ldr + cc, n, o);
+      else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (v[i] - mu) * rs;
+        o[i] += rs * (d[i] * g[i] - m_g - xh * m_xg);
+        ag[k][i] += d[i] * xh;
+        ab[k][i] += d[i];
+      }
+      st8(dx + r * lddx + cc, n, o);
+      if (dx2) st8(dx2 + r * lddx2 + cc, n, o);
+    }
+  }
+  if (want_g) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = k * 256 + lane * 8;
+      if (c >= seg) break;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c + i < seg) {
+          atomicAdd(&s_dg[c + i], ag[k][i]);
+          atomicAdd(&s_db[c + i], ab[k][i]);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < seg; i += blockDim.x) {
+      atomicAdd(&dgamma[c0 + i], s_dg[i]);
+      atomicAdd(&dbeta[c0 + i], s_db[i]);
+    }
+  }
+}
+
+// ============================================================ column sums
+// out[c] (+)= sum_r x[r, c]  (bias gradient before the column reduce, layers.py:238)
+template <typename TX>
+__global__ void __launch_bounds__(256) colsum_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
+                                                     float* __restrict__ out) {
+  __shared__ float s[kSeg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * kSeg;
+  const int seg = min(kSeg, cols - c0);
+  for (int i = threadIdx.x; i < kSeg; i += blockDim.x) s[i] = 0.f;
+  __syncthreads();
+  float a[4][8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[k][i] = 0.f;
+  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = k * 256 + lane * 8;
+      if (c >= seg) break;
+      float v[8];
+      ld8(x + r * ldx + c0 + c, min(8, seg - c), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[k][i] += v[i];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = k * 256 + lane * 8;
+    if (c >= seg) break;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (c + i < seg) atomicAdd(&s[c + i], a[k][i]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < seg; i += blockDim.x) atomicAdd(&out[c0 + i], s[i]);
+}
+
+// x[r, c] += bias[c]  (layers.py:228)
+template <typename TX>
+__global__ void bias_add_kernel(TX* __restrict__ x, long long rows, int cols, long long ldx,
+                                const float* __restrict__ bias) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw)
+    for (int c = lane * 8; c < cols; c += 256) {
+      const int n = min(8, cols - c);
+      float v[8], b[8];
+      ld8(x + r * ldx + c, n, v);
+      ld8(bias + c, n, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += b[i];
+      st8(x + r * ldx + c, n, v);
+    }
+}
+
+// ============================================================ softmax
+// P = softmax(S) row-wise with max subtraction (dense.py:67-75)
+template <typename TS, typename TP>
+__global__ void softmax_kernel(const TS* __restrict__ S, long long rows, int cols, long long lds, TP* __restrict__ P,
+                               long long ldp) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const TS* sr = S + r * lds;
+    float m = -FLT_MAX;
+    for (int c = lane * 8; c < cols; c += 256) {
+      float v[8];
+      const int n = min(8, cols - c);
+      ld8(sr + c, n, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < n) m = fmaxf(m, v[i]);
+    }
+    m = warp_max(m);
+    float z = 0.f;
+    for (int c = lane * 8; c < cols; c += 256) {
+      float v[8];
+      const int n = min(8, cols - c);
+      ld8(sr + c, n, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < n) z += __expf(v[i] - m);
+    }
+    const float inv = 1.0f / warp_sum(z);
+    for (int c = lane * 8; c < cols; c += 256) {
+      float v[8];
+      const int n = min(8, cols - c);
+      ld8(sr + c, n, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __expf(v[i] - m) * inv;
+      st8(P + r * ldp + c, n, v);
+    }
+  }
+}
+
+// dS = P * (dP - sum(dP * P)) * scale  (layers.py:449-450)
+template <typename TD, typename TP, typename TO>
+__global__ void softmax_bwd_kernel(const TD* __restrict__ dP, long long lddp, const TP* __restrict__ P, long long ldp,
+                                   long long rows, int cols, float scale, TO* __restrict__ dS, long long ldds) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    float acc = 0.f;
+    for (int c = lane * 8; c < cols; c += 256) {
+      float a[8], p[8];
+      const int n = min(8, cols - c);
+      ld8(dP + r * lddp + c, n, a);
+      ld8(P + r * ldp + c, n, p);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += a[i] * p[i];
+    }
+    acc = warp_sum(acc);
+    for (int c = lane * 8; c < cols; c += 256) {
+      float a[8], p[8];
+      const int n = min(8, cols - c);
+      ld8(dP + r * lddp + c, n, a);
+      ld8(P + r * ldp + c, n, p);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = p[i] * (a[i] - acc) * scale;
+      st8(dS + r * ldds + c, n, a);
+    }
+  }
+}
+
+// ============================================================ cross entropy
+// Local pass over this device's vocabulary block (layers.py:557-584): online
+// (max, sum e^{x-max}) over the n_real valid columns and the label logit when
+// the label falls in [col_lo, col_lo + ncols). Writes lmax[r], gmax[r]
+// (= lmax, to be max-all-reduced in place) and packed[r] = (sum, x_label).
+template <typename TL>
+__global__ void xent_local_kernel(const TL* __restrict__ logits, long long rows, long long ldl, int n_real,
+                                  const int64_t* __restrict__ labels, long long col_lo, float* __restrict__ lmax,
+                                  float* __restrict__ gmax, float* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const TL* lr = logits + r * ldl;
+    float m = -INFINITY, s = 0.f;
+    for (int c = lane * 8; c < n_real; c += 256) {
+      float v[8];
+      const int n = min(8, n_real - c);
+      ld8(lr + c, n, v);
+      float cm = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < n) cm = fmaxf(cm, v[i]);
+      if (cm > m) {
+        s *= __expf(m - cm);
+        m = cm;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < n) s += __expf(v[i] - m);
+    }
+    // combine (m, s) across lanes
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+      const float nm = fmaxf(m, om);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+      m = nm;
+    }
+    if (lane == 0) {
+      const long long lab = labels[r] - col_lo;
+      const float xl = (lab >= 0 && lab < n_real) ? ld1(lr + lab) : 0.f;
+      lmax[r] = m;
+      gmax[r] = m;
+      packed[2 * r] = s;
+      packed[2 * r + 1] = xl;
+    }
+  }
+}
+
+// packed[r].sum *= e^{lmax - gmax} so the row all-reduce sums share one max.
+__global__ void xent_rescale_kernel(long long rows, const float* __restrict__ lmax, const float* __restrict__ gmax,
+                                    float* __restrict__ packed) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += gridDim.x * (long long)blockDim.x) {
+    const float lm = lmax[r];
+    packed[2 * r] = lm == -INFINITY ? 0.f : packed[2 * r] * __expf(lm - gmax[r]);
+  }
+}
+
+// loss[r] = log(sum) + max - x_label; *partial (+)= sum_r loss[r]  (layers.py:597-599)
+__global__ void xent_loss_kernel(long long rows, const float* __restrict__ gmax, const float* __restrict__ packed,
+                                 float* __restrict__ loss_rows, float* __restrict__ partial) {
+  float acc = 0.f;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += gridDim.x * (long long)blockDim.x) {
+    const float l = logf(packed[2 * r]) + gmax[r] - packed[2 * r + 1];
+    if (loss_rows) loss_rows[r] = l;
+    acc += l;
+  }
+  acc = warp_sum(acc);
+  __shared__ float sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) atomicAdd(partial, v);
+  }
+}
+
+// dlogits = (e^{x - max} / sum - [col == label]) * scale; padded columns -> 0
+// (layers.py:611-624). In place (dl == logits) is allowed.
+template <typename TL, typename TO>
+__global__ void xent_bwd_kernel(const TL* logits, long long rows, long long ldl, int n_real, int ncols,
+                                const int64_t* __restrict__ labels, long long col_lo, const float* __restrict__ gmax,
+                                const float* __restrict__ packed, float scale, TO* dl, long long lddl) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    const float m = gmax[r];
+    const float inv = 1.0f / packed[2 * r];
+    const long long lab = labels[r] - col_lo;
+    for (int c = lane * 8; c < ncols; c += 256) {
+      float v[8];
+      const int n = min(8, ncols - c);
+      ld8(logits + r * ldl + c, n, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int cc = c + i;
+        float g = cc < n_real ? __expf(v[i] - m) * inv : 0.f;
+        if (cc == lab) g -= 1.f;
+        v[i] = g * scale;
+      }
+      st8(dl + r * lddl + c, n, v);
+    }
+  }
+}
+
+// ============================================================ embedding
+// out[t, :] = table[ids[t] - lo, :] for ids in [lo, lo + vb)  (layers.py:178-181)
+template <typename TT, typename TO>
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, long long n, long long lo, long long vb,
+                                 const TT* __restrict__ table, long long ldt, int hc, TO* __restrict__ out,
+                                 long long ldo) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long t = wid; t < n; t += nw) {
+    const long long row = ids[t] - lo;
+    if (row < 0 || row >= vb) continue;
+    for (int c = lane * 8; c < hc; c += 256) {
+      float v[8];
+      const int k = min(8, hc - c);
+      ld8(table + row * ldt + c, k, v);
+      st8(out + t * ldo + c, k, v);
+    }
+  }
+}
+
+// grad[ids[t] - lo, :] += dout[t, :] for ids in the block; repeated ids accumulate (layers.py:202-205)
+template <typename TD>
+__global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, long long lo, long long vb,
+                                 const TD* __restrict__ dout, long long ldd, int hc, float* __restrict__ grad,
+                                 long long ldg) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long t = wid; t < n; t += nw) {
+    const long long row = ids[t] - lo;
+    if (row < 0 || row >= vb) continue;
+    for (int c = lane * 8; c < hc; c += 256) {
+      float v[8];
+      const int k = min(8, hc - c);
+      ld8(dout + t * ldd + c, k, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < k) atomicAdd(grad + row * ldg + c + i, v[i]);
+    }
+  }
+}
+
+// ============================================================ element-wise
+// w -= lr * g (fp32 master), optional bf16 shadow copy for the GEMMs (layers.py:761-772);
+// 2-D with independent row pitches so padding columns are never touched.
+__global__ void sgd_kernel(float* __restrict__ w, long long ldw, bf16* __restrict__ wl, long long ldl,
+                           const float* __restrict__ g, long long ldg, float lr, long long rows, long long cols) {
+  const long long n = rows * cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
+    const long long r = i / cols, c = i - r * cols;
+    const float v = w[r * ldw + c] - lr * g[r * ldg + c];
+    w[r * ldw + c] = v;
+    if (wl) wl[r * ldl + c] = __float2bfloat16_rn(v);
+  }
+}
+
+template <typename TS, typename TD>
+__global__ void cast_kernel(const TS* __restrict__ s, TD* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
+    if constexpr (sizeof(TD) == 4)
+      d[i] = ld1(s + i);
+    else
+      d[i] = __float2bfloat16_rn(ld1(s + i));
+  }
+}
+
+struct SrcList {
+  const void* p[8];
+};
+// dst = [dst (op)] src0 (op) src1 ... in list order: the rank-ordered fold of
+// the reference's reduce / all-reduce (mesh.py:464-466, 490-497).
+template <typename T>
+__global__ void fold_kernel(T* __restrict__ dst, SrcList srcs, int nsrc, long long n, int accumulate, int op_max) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
+    float acc = accumulate ? ld1(dst + i) : ld1(static_cast<const T*>(srcs.p[0]) + i);
+    for (int k = accumulate ? 0 : 1; k < nsrc; ++k) {
+      const float v = ld1(static_cast<const T*>(srcs.p[k]) + i);
+      acc = op_max ? fmaxf(acc, v) : acc + v;
+    }
+    if constexpr (sizeof(T) == 4)
+      dst[i] = acc;
+    else
+      dst[i] = __float2bfloat16_rn(acc);
+  }
+}
+
+// ============================================================ epilogue
+// out = act(alpha * x + bias + C) — the sg_gemm epilogue applied to fp32 partial
+// sums that were reduced over the mesh before it could run (dist AB^T forms).
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(c * (x + a * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float t = tanhf(c * (x + a * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+}
+template <typename TC, typename TO>
+__global__ void epilogue_kernel(const float* __restrict__ x, long long rows, int cols, long long ldx, float alpha,
+                                const float* __restrict__ bias, const TC* __restrict__ cin, long long ldc, int act,
+                                bf16* __restrict__ aux, long long ldaux, TO* __restrict__ out, long long ldo) {
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw)
+    for (int c = lane * 8; c < cols; c += 256) {
+      const int n = min(8, cols - c);
+      float v[8], t[8];
+      ld8(x + r * ldx + c, n, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= alpha;
+      if (bias) {
+        ld8(bias + c, n, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += t[i];
+      }
+      if (cin) {
+        ld8(cin + r * ldc + c, n, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += t[i];
+      }
+      if (act == SG_ACT_GELU) {
+        if (aux) st8(aux + r * ldaux + c, n, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gelu_tanh(v[i]);
+      } else if (act == SG_ACT_DGELU) {
+        ld8(aux + r * ldaux + c, n, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= gelu_tanh_grad(t[i]);
+      }
+      st8(out + r * ldo + c, n, v);
+    }
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" int sg_zero(void* ptr, int64_t bytes, void* stream) {
+  clear_error();
+  if (bytes <= 0) return SG_OK;
+  if (cudaMemsetAsync(ptr, 0, (size_t)bytes, S(stream)) != cudaSuccess) return set_error(SG_ERR_CUDA, "memset");
+  return SG_OK;
+}
+
+extern "C" int sg_ln_stats(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, float* stats,
+                           void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "ln_stats: bad extents");
+  if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "ln_stats: unaligned");
+  if (rows == 0) return SG_OK;
+  const int grid = grid_for(rows, 8);
+  SG_DISPATCH_T(xdt, TX, (ln_stats_kernel<TX><<<grid, 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, stats)));
+  return launch_check();
+}
+
+extern "C" int sg_ln_fwd(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, const float* stats,
+                         int64_t h_total, float eps, const float* gamma, const float* beta, void* y, int ydt,
+                         int64_t ldy, float* mean, float* rstd, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1 || h_total < cols) return set_error(SG_ERR_SHAPE, "ln_fwd: bad extents");
+  if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(y, ldy, ydt == SG_DTYPE_F32 ? 4 : 2) ||
+      !aligned16(gamma, 0, 4) || !aligned16(beta, 0, 4))
+    return set_error(SG_ERR_SHAPE, "ln_fwd: unaligned");
+  if (!stats && h_total != cols) return set_error(SG_ERR_CONFIG, "ln_fwd: sharded row needs all-reduced stats");
+  if (rows == 0) return SG_OK;
+  const int grid = grid_for(rows, 8);
+  const float inv_h = 1.0f / (float)h_total;
+  SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(ydt, TY, (ln_fwd_kernel<TX, TY><<<grid, 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, stats, inv_h, eps, gamma, beta, static_cast<TY*>(y), ldy, mean, rstd))));
+  return launch_check();
+}
+
+extern "C" int sg_ln_bwd_stats(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx,
+                               const float* mean, const float* rstd, const float* gamma, int64_t rows, int64_t cols,
+                               float* stats, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "ln_bwd_stats: bad extents");
+  if (!aligned16(dy, lddy, dydt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "ln_bwd_stats: unaligned");
+  if (rows == 0) return SG_OK;
+  const int grid = grid_for(rows, 8);
+  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, (ln_bwd_stats_kernel<TD, TX><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats))));
+  return launch_check();
+}
+
+extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx,
+                         const float* mean, const float* rstd, const float* gamma, int64_t rows, int64_t cols,
+                         const float* stats, int64_t h_total, const void* resid, int rdt, int64_t ldr, void* dx,
+                         int dxdt, int64_t lddx, void* dx2, int64_t lddx2, float* dgamma, float* dbeta,
+                         void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1 || h_total < cols || !stats) return set_error(SG_ERR_SHAPE, "ln_bwd: bad arguments");
+  if ((dgamma == nullptr) != (dbeta == nullptr)) return set_error(SG_ERR_CONFIG, "ln_bwd: dgamma/dbeta pair");
+  if (!aligned16(dy, lddy, dydt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2) ||
+      !aligned16(resid, ldr, rdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(dx, lddx, dxdt == SG_DTYPE_F32 ? 4 : 2) ||
+      !aligned16(dx2, lddx2, 2))
+    return set_error(SG_ERR_SHAPE, "ln_bwd: unaligned");
+  if (rows == 0) return SG_OK;
+  const int segs = (int)((cols + kSeg - 1) / kSeg);
+  const int gx = std::max(1, grid_for(rows, 64, 4) / segs);
+  dim3 grid(gx, segs);
+  const float inv_h = 1.0f / (float)h_total;
+  if (rdt != SG_DTYPE_BF16) rdt = SG_DTYPE_F32;
+  // dx is fp32 (residual-stream gradient); the optional dx2 is its bf16 GEMM operand copy
+  if (dxdt != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "ln_bwd: dx must be fp32");
+  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, float><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta)))));
+  return launch_check();
+}
+
+extern "C" int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, float* out,
+                         int accumulate, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "colsum: bad extents");
+  if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "colsum: unaligned");
+  if (!accumulate && cudaMemsetAsync(out, 0, cols * sizeof(float), S(stream)) != cudaSuccess)
+    return set_error(SG_ERR_CUDA, "memset");
+  if (rows == 0) return SG_OK;
+  const int segs = (int)((cols + kSeg - 1) / kSeg);
+  const int gx = std::max(1, grid_for(rows, 64, 4) / segs);
+  SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX><<<dim3(gx, segs), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
+  return launch_check();
+}
+
+extern "C" int sg_bias_add(void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, const float* bias,
+                           void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "bias_add: bad extents");
+  if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(bias, 0, 4))
+    return set_error(SG_ERR_SHAPE, "bias_add: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(xdt, TX, (bias_add_kernel<TX><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<TX*>(x), rows, (int)cols, ldx, bias)));
+  return launch_check();
+}
+
+extern "C" int sg_softmax_rows(const void* s, int sdt, int64_t rows, int64_t cols, int64_t lds, void* p, int pdt,
+                               int64_t ldp, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "softmax: bad extents");
+  if (!aligned16(s, lds, sdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(p, ldp, pdt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "softmax: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(pdt, TP, (softmax_kernel<TS, TP><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TS*>(s), rows, (int)cols, lds, static_cast<TP*>(p), ldp))));
+  return launch_check();
+}
+
+extern "C" int sg_softmax_bwd(const void* dp, int dpdt, int64_t lddp, const void* p, int pdt, int64_t ldp,
+                              int64_t rows, int64_t cols, float scale, void* ds, int dsdt, int64_t ldds,
+                              void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "softmax_bwd: bad extents");
+  if (!aligned16(dp, lddp, dpdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(p, ldp, pdt == SG_DTYPE_F32 ? 4 : 2) ||
+      !aligned16(ds, ldds, dsdt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "softmax_bwd: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(dpdt, TD, SG_DISPATCH_T(pdt, TP, SG_DISPATCH_T(dsdt, TO, (softmax_bwd_kernel<TD, TP, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TD*>(dp), lddp, static_cast<const TP*>(p), ldp, rows, (int)cols, scale, static_cast<TO*>(ds), ldds)))));
+  return launch_check();
+}
+
+extern "C" int sg_xent_local(const void* logits, int ldt, int64_t rows, int64_t ldl, int64_t n_real,
+                             const int64_t* labels, int64_t col_lo, float* lmax, float* gmax, float* packed,
+                             void* stream) {
+  clear_error();
+  if (rows < 0 || n_real < 0) return set_error(SG_ERR_SHAPE, "xent_local: bad extents");
+  if (!aligned16(logits, ldl, ldt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "xent_local: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(ldt, TL, (xent_local_kernel<TL><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TL*>(logits), rows, ldl, (int)n_real, labels, col_lo, lmax, gmax, packed)));
+  return launch_check();
+}
+
+extern "C" int sg_xent_rescale(int64_t rows, const float* lmax, const float* gmax, float* packed, void* stream) {
+  clear_error();
+  if (rows <= 0) return SG_OK;
+  xent_rescale_kernel<<<grid_for(rows, 256), 256, 0, S(stream)>>>(rows, lmax, gmax, packed);
+  return launch_check();
+}
+
+extern "C" int sg_xent_loss(int64_t rows, const float* gmax, const float* packed, float* loss_rows, float* partial,
+                            void* stream) {
+  clear_error();
+  if (cudaMemsetAsync(partial, 0, sizeof(float), S(stream)) != cudaSuccess) return set_error(SG_ERR_CUDA, "memset");
+  if (rows <= 0) return SG_OK;
+  xent_loss_kernel<<<grid_for(rows, 256, 2), 256, 0, S(stream)>>>(rows, gmax, packed, loss_rows, partial);
+  return launch_check();
+}
+
+extern "C" int sg_xent_bwd(const void* logits, int ldt, int64_t rows, int64_t ldl, int64_t n_real, int64_t ncols,
+                           const int64_t* labels, int64_t col_lo, const float* gmax, const float* packed, float scale,
+                           void* dl, int dldt, int64_t lddl, void* stream) {
+  clear_error();
+  if (rows < 0 || n_real < 0 || ncols < n_real) return set_error(SG_ERR_SHAPE, "xent_bwd: bad extents");
+  if (!aligned16(logits, ldl, ldt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(dl, lddl, dldt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "xent_bwd: unaligned");
+  if (rows == 0 || ncols == 0) return SG_OK;
+  SG_DISPATCH_T(ldt, TL, SG_DISPATCH_T(dldt, TO, (xent_bwd_kernel<TL, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TL*>(logits), rows, ldl, (int)n_real, (int)ncols, labels, col_lo, gmax, packed, scale, static_cast<TO*>(dl), lddl))));
+  return launch_check();
+}
+
+extern "C" int sg_embed_fwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const void* table, int tdt,
+                            int64_t ldt, int64_t hc, void* out, int odt, int64_t ldo, void* stream) {
+  clear_error();
+  if (n < 0 || hc < 1 || vb < 0) return set_error(SG_ERR_SHAPE, "embed_fwd: bad extents");
+  if (!aligned16(table, ldt, tdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "embed_fwd: unaligned");
+  if (n == 0) return SG_OK;
+  SG_DISPATCH_T(tdt, TT, SG_DISPATCH_T(odt, TO, (embed_fwd_kernel<TT, TO><<<grid_for(n, 8), 256, 0, S(stream)>>>(ids, n, lo, vb, static_cast<const TT*>(table), ldt, (int)hc, static_cast<TO*>(out), ldo))));
+  return launch_check();
+}
+
+extern "C" int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const void* dout, int ddt,
+                            int64_t ldd, int64_t hc, float* grad, int64_t ldg, void* stream) {
+  clear_error();
+  if (n < 0 || hc < 1 || vb < 0) return set_error(SG_ERR_SHAPE, "embed_bwd: bad extents");
+  if (!aligned16(dout, ldd, ddt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "embed_bwd: unaligned");
+  if (n == 0) return SG_OK;
+  SG_DISPATCH_T(ddt, TD, (embed_bwd_kernel<TD><<<grid_for(n, 8), 256, 0, S(stream)>>>(ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
+  return launch_check();
+}
+
+extern "C" int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr,
+                      int64_t rows, int64_t cols, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 0) return set_error(SG_ERR_SHAPE, "sgd: bad extents");
+  if (rows == 0 || cols == 0) return SG_OK;
+  sgd_kernel<<<grid_for(rows * cols, 256, 4), 256, 0, S(stream)>>>(w, ldw, static_cast<bf16*>(w_bf16), ldl, g, ldg, lr,
+                                                                   rows, cols);
+  return launch_check();
+}
+
+extern "C" int sg_cast(const void* src, int sdt, void* dst, int ddt, int64_t n, void* stream) {
+  clear_error();
+  if (n <= 0) return SG_OK;
+  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(ddt, TD, (cast_kernel<TS, TD><<<grid_for(n, 256, 4), 256, 0, S(stream)>>>(static_cast<const TS*>(src), static_cast<TD*>(dst), n))));
+  return launch_check();
+}
+
+extern "C" int sg_fold(void* dst, int dt, const void* const* srcs, int nsrc, int64_t n, int accumulate, int op_max,
+                       void* stream) {
+  clear_error();
+  if (nsrc < 0 || nsrc > 8 || (nsrc == 0 && !accumulate)) return set_error(SG_ERR_CONFIG, "fold: 1..8 sources");
+  if (n <= 0 || nsrc == 0) return SG_OK;
+  SrcList l{};
+  for (int i = 0; i < nsrc; ++i) l.p[i] = srcs[i];
+  SG_DISPATCH_T(dt, T, (fold_kernel<T><<<grid_for(n, 256, 4), 256, 0, S(stream)>>>(static_cast<T*>(dst), l, nsrc, n, accumulate, op_max)));
+  return launch_check();
+}
+
+extern "C" int sg_epilogue(const float* x, int64_t rows, int64_t cols, int64_t ldx, float alpha, const float* bias,
+                           const void* cin, int cdt, int64_t ldc, int act, void* aux, int64_t ldaux, void* out,
+                           int odt, int64_t ldo, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "epilogue: bad extents");
+  if (act == SG_ACT_DGELU && !aux) return set_error(SG_ERR_CONFIG, "epilogue: DGELU needs aux");
+  if (!aligned16(x, ldx, 4) || !aligned16(cin, ldc, cdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(aux, ldaux, 2) ||
+      !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(bias, 0, 4))
+    return set_error(SG_ERR_SHAPE, "epilogue: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(cdt, TC, SG_DISPATCH_T(odt, TO, (epilogue_kernel<TC, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(x, rows, (int)cols, ldx, alpha, bias, static_cast<const TC*>(cin), ldc, act, static_cast<bf16*>(aux), ldaux, static_cast<TO*>(out), ldo))));
+  return launch_check();
+}

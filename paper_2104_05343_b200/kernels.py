@@ -109,3 +109,183 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     with torch.cuda.device(out.device):
         check(_lib.lib().sg_gemm(ctypes.byref(args), _stream(out)), "sg_gemm")
     return out
+
+
+# ---------------------------------------------------------------- row kernels
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ConfigError("libsg operators take CUDA tensors (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _dt(t):
+    return DTYPE_F32 if t is None else _dtype_code(t)
+
+
+def _rows2d(t: torch.Tensor) -> tuple[int, int, int]:
+    """(rows, cols, ld) of a row-major 2-D view (leading dims flattened when contiguous)."""
+    if t.dim() != 2:
+        if not t.is_contiguous():
+            raise ShapeError("row kernels need 2-D views or contiguous tensors")
+        t = t.reshape(-1, t.shape[-1])
+    if t.stride(-1) != 1 and t.shape[-1] > 1:
+        raise ShapeError("row kernels need unit column stride")
+    if t.shape[0] <= 1:  # the stride of a single row is irrelevant; report an aligned one
+        return t.shape[0], t.shape[1], -(-t.shape[1] // 8) * 8
+    return t.shape[0], t.shape[1], t.stride(0)
+
+
+def _call(name: str, *args):
+    check(getattr(_lib.lib(), name)(*args), name)
+
+
+def ln_stats(x, stats):
+    rows, cols, ldx = _rows2d(x)
+    _call("sg_ln_stats", _p(x), _dt(x), rows, cols, ldx, _p(stats), _stream(x))
+
+
+def ln_fwd(x, stats, h_total, eps, gamma, beta, y, mean, rstd):
+    rows, cols, ldx = _rows2d(x)
+    _, _, ldy = _rows2d(y)
+    _call("sg_ln_fwd", _p(x), _dt(x), rows, cols, ldx, _p(stats), h_total, eps, _p(gamma), _p(beta), _p(y), _dt(y),
+          ldy, _p(mean), _p(rstd), _stream(x))
+
+
+def ln_bwd_stats(dy, x, mean, rstd, gamma, stats):
+    rows, cols, lddy = _rows2d(dy)
+    _, _, ldx = _rows2d(x)
+    _call("sg_ln_bwd_stats", _p(dy), _dt(dy), lddy, _p(x), _dt(x), ldx, _p(mean), _p(rstd), _p(gamma), rows, cols,
+          _p(stats), _stream(x))
+
+
+def ln_bwd(dy, x, mean, rstd, gamma, stats, h_total, resid, dx, dx2=None, dgamma=None, dbeta=None):
+    rows, cols, lddy = _rows2d(dy)
+    _, _, ldx = _rows2d(x)
+    ldr = _rows2d(resid)[2] if resid is not None else 0
+    lddx = _rows2d(dx)[2]
+    lddx2 = _rows2d(dx2)[2] if dx2 is not None else 0
+    _call("sg_ln_bwd", _p(dy), _dt(dy), lddy, _p(x), _dt(x), ldx, _p(mean), _p(rstd), _p(gamma), rows, cols,
+          _p(stats), h_total, _p(resid), _dt(resid), ldr, _p(dx), _dt(dx), lddx, _p(dx2), lddx2, _p(dgamma),
+          _p(dbeta), _stream(x))
+
+
+def colsum(x, out, accumulate=False):
+    rows, cols, ldx = _rows2d(x)
+    _call("sg_colsum", _p(x), _dt(x), rows, cols, ldx, _p(out), int(accumulate), _stream(x))
+
+
+def bias_add(x, bias):
+    rows, cols, ldx = _rows2d(x)
+    _call("sg_bias_add", _p(x), _dt(x), rows, cols, ldx, _p(bias), _stream(x))
+
+
+def softmax_rows(s, p):
+    rows, cols, lds = _rows2d(s)
+    _, _, ldp = _rows2d(p)
+    _call("sg_softmax_rows", _p(s), _dt(s), rows, cols, lds, _p(p), _dt(p), ldp, _stream(s))
+
+
+def softmax_bwd(dp, p, scale, ds):
+    rows, cols, lddp = _rows2d(dp)
+    _, _, ldp = _rows2d(p)
+    _, _, ldds = _rows2d(ds)
+    _call("sg_softmax_bwd", _p(dp), _dt(dp), lddp, _p(p), _dt(p), ldp, rows, cols, scale, _p(ds), _dt(ds), ldds,
+          _stream(dp))
+
+
+def xent_local(logits, n_real, labels, col_lo, lmax, gmax, packed):
+    rows, _, ldl = _rows2d(logits)
+    _call("sg_xent_local", _p(logits), _dt(logits), rows, ldl, n_real, _p(labels), col_lo, _p(lmax), _p(gmax),
+          _p(packed), _stream(logits))
+
+
+def xent_rescale(lmax, gmax, packed):
+    _call("sg_xent_rescale", lmax.numel(), _p(lmax), _p(gmax), _p(packed), _stream(lmax))
+
+
+def xent_loss(gmax, packed, loss_rows, partial):
+    _call("sg_xent_loss", gmax.numel(), _p(gmax), _p(packed), _p(loss_rows), _p(partial), _stream(gmax))
+
+
+def xent_bwd(logits, n_real, labels, col_lo, gmax, packed, scale, dl):
+    rows, ncols, ldl = _rows2d(logits)
+    _, _, lddl = _rows2d(dl)
+    _call("sg_xent_bwd", _p(logits), _dt(logits), rows, ldl, n_real, ncols, _p(labels), col_lo, _p(gmax),
+          _p(packed), scale, _p(dl), _dt(dl), lddl, _stream(logits))
+
+
+def embed_fwd(ids, lo, vb, table, out):
+    _, hc, ldt = _rows2d(table)
+    _, _, ldo = _rows2d(out)
+    _call("sg_embed_fwd", _p(ids), ids.numel(), lo, vb, _p(table), _dt(table), ldt, hc, _p(out), _dt(out), ldo,
+          _stream(out))
+
+
+def embed_bwd(ids, lo, vb, dout, grad):
+    _, hc, ldd = _rows2d(dout)
+    _, _, ldg = _rows2d(grad)
+    _call("sg_embed_bwd", _p(ids), ids.numel(), lo, vb, _p(dout), _dt(dout), ldd, hc, _p(grad), ldg, _stream(dout))
+
+
+def sgd(w, w_bf16, g, lr):
+    """w -= lr * g on fp32 master ``w`` (1-D or padded 2-D), refreshing the bf16 copy."""
+    if w.dim() == 1:
+        w2, g2, l2 = w.view(1, -1), g.view(1, -1), None if w_bf16 is None else w_bf16.view(1, -1)
+    else:
+        w2, g2, l2 = w, g, w_bf16
+    rows, cols, ldw = _rows2d(w2)
+    ldg = _rows2d(g2)[2]
+    ldl = _rows2d(l2)[2] if l2 is not None else 0
+    if tuple(g2.shape) != tuple(w2.shape) or (l2 is not None and tuple(l2.shape) != tuple(w2.shape)):
+        raise ShapeError("sgd: parameter / gradient shapes differ")
+    _call("sg_sgd", _p(w2), ldw, _p(l2), ldl, _p(g2), ldg, lr, rows, cols, _stream(w))
+
+
+def cast(src, dst):
+    if src.numel() != dst.numel() or not (src.is_contiguous() and dst.is_contiguous()):
+        raise ShapeError("cast needs equal-size contiguous tensors")
+    _call("sg_cast", _p(src), _dt(src), _p(dst), _dt(dst), src.numel(), _stream(dst))
+
+
+def zero(t):
+    if not t.is_contiguous():
+        raise ShapeError("zero needs a contiguous tensor")
+    _call("sg_zero", _p(t), t.numel() * t.element_size(), _stream(t))
+
+
+def _flat_storage(t):
+    """Contiguous 1-D view of a tensor, or of the padded rows behind a 2-D block view."""
+    if t.is_contiguous():
+        return t.reshape(-1)
+    if t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]:
+        return torch.as_strided(t, (t.shape[0] * t.stride(0),), (1,))
+    raise ShapeError("expected a contiguous tensor or a padded 2-D block")
+
+
+def fold(dst, srcs, accumulate=False, op_max=False):
+    """dst = [dst op] srcs[0] op srcs[1] ... in list order (op: + or max).
+
+    Padded 2-D blocks with equal row pitch are folded over their full storage.
+    """
+    d = _flat_storage(dst)
+    ss = []
+    for s in srcs:
+        f = _flat_storage(s)
+        if f.numel() != d.numel() or s.dtype != dst.dtype or tuple(s.shape) != tuple(dst.shape):
+            raise ShapeError("fold sources must match the destination")
+        ss.append(f)
+    arr = (ctypes.c_void_p * max(1, len(ss)))(*[s.data_ptr() for s in ss])
+    _call("sg_fold", _p(d), _dt(d), arr, len(ss), d.numel(), int(accumulate), int(op_max), _stream(d))
+
+
+def epilogue(x, out, *, bias=None, c=None, act=ACT_NONE, aux=None, alpha=1.0):
+    """out = act(alpha*x + bias + c) for an fp32 x (the GEMM epilogue as a pass)."""
+    rows, cols, ldx = _rows2d(x)
+    ldc = _rows2d(c)[2] if c is not None else 0
+    ldaux = _rows2d(aux)[2] if aux is not None else 0
+    _, _, ldo = _rows2d(out)
+    _call("sg_epilogue", _p(x), rows, cols, ldx, alpha, _p(bias), _p(c), _dt(c), ldc, act, _p(aux), ldaux, _p(out),
+          _dt(out), ldo, _stream(x))

@@ -1,0 +1,288 @@
+"""End-to-end 2D model: embedding -> N pre-norm layers -> tied lm-head -> mean CE.
+
+Drop-in for summagrid model.py:97-424 (MeshModel, init_global_params,
+run_loss_and_grads). Parameters live on the mesh as fp32 masters with bf16
+twins for the tensor-core GEMMs; the table is padded with zero rows to
+v_padded and stored in the SUMMA weight layout; the QKV weight is
+column-interleaved per mesh column and de-interleaved on gather, so loss and
+gathered gradients are independent of the mesh shape.
+
+``train_step`` is the sync-free training step (forward, backward, SGD) the
+bench times and captures into a CUDA graph; ``forward`` / ``backward`` keep
+the reference's signatures.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import ConfigError, ShapeError
+from .layers import (
+    LayerGrads,
+    LayerParams,
+    ModelConfig,
+    RowHostedVector,
+    TransformerLayer,
+    _device_ids,
+    cross_entropy_backward,
+    cross_entropy_forward,
+    deinterleave_qkv,
+    embedding_backward,
+    embedding_forward,
+    interleave_qkv,
+    sgd_matrix,
+    sgd_vector,
+)
+from .membuf import CheckpointStore, Workspace, checkpointed_backward, checkpointed_forward, clone_to_conjunction, \
+    padded_empty
+from .mesh import Mesh
+from .summa import BF16, F32, ShardedMatrix, as_bf16, gather, scatter, summa_ab, summa_abt, summa_atb
+
+_LAYER_KEYS = ("ln1_gamma", "ln1_beta", "w_qkv", "b_qkv", "w_dense", "b_dense", "ln2_gamma", "ln2_beta", "w1", "b1",
+               "w2", "b2")
+_MATS = ("w_qkv", "w_dense", "w1", "w2")
+
+
+def param_declaration_order(cfg: ModelConfig) -> list[str]:
+    """Parameter names in the reference's declaration order (model.py:71-79)."""
+    names = ["table"]
+    for i in range(cfg.num_layers):
+        names += [f"layers.{i}.{k}" for k in _LAYER_KEYS]
+    return names
+
+
+def param_shape(cfg: ModelConfig, name: str) -> tuple[int, ...]:
+    h = cfg.h
+    base = name.rsplit(".", 1)[-1]
+    return {"table": (cfg.v, h), "w_qkv": (h, 3 * h), "b_qkv": (3 * h,), "w_dense": (h, h), "w1": (h, 4 * h),
+            "b1": (4 * h,), "w2": (4 * h, h)}.get(base, (h,))
+
+
+def init_global_params(cfg: ModelConfig, seed: int, classifier: bool = False) -> dict[str, np.ndarray]:
+    """Host float64 parameters, identical for every mesh (model.py:97-119).
+
+    PCG64(seed) draws U[-1/sqrt(h), 1/sqrt(h)) in the order table, then per
+    layer w_qkv, w_dense, w1, w2; vectors start at identity (gamma=1, rest 0).
+    """
+    if classifier:
+        raise ConfigError("the sequence-classifier branch is outside this build's hot path")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    lim = 1.0 / math.sqrt(cfg.h)
+    out = {"table": rng.uniform(-lim, lim, size=(cfg.v, cfg.h))}
+    for i in range(cfg.num_layers):
+        pre = f"layers.{i}."
+        for name in _LAYER_KEYS:
+            shape = param_shape(cfg, name)
+            if name in _MATS:
+                out[pre + name] = rng.uniform(-lim, lim, size=shape)
+            else:
+                out[pre + name] = (np.ones if name.endswith("gamma") else np.zeros)(shape)
+    return out
+
+
+@dataclass
+class ModelGrads:
+    table: ShardedMatrix
+    layers: list
+    cls_w: Optional[list] = None
+
+
+@dataclass
+class ModelSaved:
+    tokens: object
+    labels: object
+    x_final: ShardedMatrix
+    ce_ctx: object
+    layer_saves: Optional[list] = None
+    store: Optional[CheckpointStore] = None
+    ids: Optional[list] = None
+
+
+def _with_twin(m: ShardedMatrix) -> ShardedMatrix:
+    m.bf16_twin = as_bf16(m) if m.dtype != BF16 else m
+    if m.bf16_twin is m:
+        raise ConfigError("masters must be fp32")
+    return m
+
+
+class MeshModel:
+    """Distributed transformer bound to one mesh (model.py:152-411)."""
+
+    def __init__(self, mesh: Mesh, cfg: ModelConfig, global_params: dict | None = None, classifier: bool = False,
+                 skip_dead_recompute: bool = False, *, seed: int = 0, logits_dtype: torch.dtype = BF16) -> None:
+        if classifier:
+            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
+        cfg.validate_mesh(mesh)
+        self.mesh = mesh
+        self.cfg = cfg
+        self.classifier = False
+        self.logits_dtype = logits_dtype
+        c = mesh.c
+        v_pad = cfg.v_padded(mesh)
+        if global_params is None:
+            self.table = _device_random(mesh, v_pad, cfg.h, cfg, seed, rows_real=cfg.v)
+        else:
+            tab = np.asarray(global_params["table"], dtype=np.float64)
+            if v_pad != cfg.v:
+                tab = np.vstack([tab, np.zeros((v_pad - cfg.v, cfg.h))])
+            self.table = _with_twin(scatter(tab, mesh, layout="weight"))
+        self.layers: list[TransformerLayer] = []
+        for i in range(cfg.num_layers):
+            pre = f"layers.{i}."
+            if global_params is None:
+                kw = {name: _device_random(mesh, *param_shape(cfg, name), cfg, seed * 1000 + 10 * i + k)
+                      for k, name in enumerate(_MATS)}
+                kw["w_qkv"] = kw["w_qkv"]  # random init is layout-agnostic
+                vec = {name: RowHostedVector.split(
+                    (np.ones if name.endswith("gamma") else np.zeros)(param_shape(cfg, name)), c, mesh=mesh)
+                    for name in _LAYER_KEYS if name not in _MATS}
+            else:
+                g = global_params
+                kw = {"w_qkv": _with_twin(scatter(interleave_qkv(np.asarray(g[pre + "w_qkv"]), c), mesh,
+                                                  layout="weight")),
+                      "w_dense": _with_twin(scatter(g[pre + "w_dense"], mesh, layout="weight")),
+                      "w1": _with_twin(scatter(g[pre + "w1"], mesh, layout="weight")),
+                      "w2": _with_twin(scatter(g[pre + "w2"], mesh, layout="weight"))}
+                vec = {name: RowHostedVector.split(
+                    interleave_qkv(np.asarray(g[pre + name]), c) if name == "b_qkv" else g[pre + name], c, mesh=mesh)
+                    for name in _LAYER_KEYS if name not in _MATS}
+            params = LayerParams(**kw, **vec)
+            self.layers.append(TransformerLayer(mesh, cfg, params, skip_dead_recompute=skip_dead_recompute))
+
+    # ------------------------------------------------------------------ workspace
+    def make_workspace(self, checkpointing: bool = True, eager_update: bool = False, merge_fwd_bwd: bool = False,
+                       planned: bool = False) -> Workspace:
+        """Per-position arenas. Accounting only: the fused kernels allocate
+        differently from the reference's plan, so capacities are not enforced."""
+        return Workspace(self.mesh.p, capacities=None, merge_fwd_bwd=merge_fwd_bwd, device=self.mesh.device())
+
+    # ------------------------------------------------------------------ forward / backward
+    def forward(self, tokens, labels, ws: Workspace, store: CheckpointStore | None = None, cls_labels=None, *,
+                return_tensor: bool = False):
+        """Loss (python float, or a device tensor with return_tensor) and saved state (model.py:296-324)."""
+        cfg = self.cfg
+        if tuple(tokens.shape) != (cfg.b, cfg.s):
+            raise ShapeError(f"tokens must be [{cfg.b}, {cfg.s}], got {tuple(tokens.shape)}")
+        if cls_labels is not None:
+            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
+        ws.reset_all("forward")
+        ws.reset_all("free")
+        ids = _device_ids(self.mesh, tokens)
+        x = embedding_forward(tokens, self.table, cfg, ws, out_category="forward", ids=ids)
+        layer_saves = None
+        if store is not None:
+            x = checkpointed_forward(self.layers, x, store, ws)
+        else:
+            layer_saves = []
+            for layer in self.layers:
+                x, saved = layer.forward(x, ws)
+                layer_saves.append(saved)
+        logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
+        loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor)
+        return loss, ModelSaved(tokens=tokens, labels=labels, x_final=x, ce_ctx=ce_ctx, layer_saves=layer_saves,
+                                store=store, ids=ids)
+
+    def backward(self, saved: ModelSaved, ws: Workspace, upstream: float = 1.0, eager_update: bool = False,
+                 lr: float = 0.0) -> ModelGrads:
+        """Gradients of every parameter (model.py:326-354); the tied table gets
+        lm-head dW plus the embedding scatter-add, accumulated in place."""
+        cfg, mesh = self.cfg, self.mesh
+        dl = cross_entropy_backward(saved.ce_ctx, mesh, ws, upstream, in_place=True)
+        dlogits = ShardedMatrix(mesh, cfg.b * cfg.s, cfg.v_padded(mesh), dl)
+        dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32)
+        table_grad = summa_atb(dlogits, saved.x_final, ws, out_category="param_grad_tied", tag="lmhead")
+        if saved.store is not None:
+            dx0, layer_grads = checkpointed_backward(self.layers, dx, saved.store, ws, eager_update=eager_update,
+                                                     lr=lr)
+        else:
+            layer_grads = [None] * len(self.layers)
+            dy = dx
+            for li in reversed(range(len(self.layers))):
+                ws.reset_all("backward")
+                dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws)
+                if eager_update:
+                    self.layers[li].apply_sgd(g, lr)
+                else:
+                    layer_grads[li] = g
+            dx0 = dy
+        embedding_backward(dx0, saved.tokens, self.table, cfg, ws, ids=saved.ids, accumulate_into=table_grad)
+        return ModelGrads(table=table_grad, layers=layer_grads)
+
+    def apply_sgd(self, grads: ModelGrads, lr: float) -> None:
+        sgd_matrix(self.table, grads.table, lr)
+        for layer, g in zip(self.layers, grads.layers):
+            if g is not None:
+                layer.apply_sgd(g, lr)
+
+    def train_step(self, tokens, labels, ws: Workspace, lr: float, checkpointing: bool = False) -> torch.Tensor:
+        """One fwd + bwd + SGD step with no host synchronisation; returns the loss tensor."""
+        store = CheckpointStore(self.mesh.p) if checkpointing else None
+        loss, saved = self.forward(tokens, labels, ws, store=store, return_tensor=True)
+        grads = self.backward(saved, ws, eager_update=True, lr=lr)
+        sgd_matrix(self.table, grads.table, lr)
+        return loss
+
+    # ------------------------------------------------------------------ gather for parity
+    def gather_params(self) -> dict[str, np.ndarray]:
+        c, cfg = self.mesh.c, self.cfg
+        out = {"table": gather(self.table)[:cfg.v]}
+        for i, layer in enumerate(self.layers):
+            out.update(_gather_layer(f"layers.{i}.", layer.params, c))
+        return out
+
+    def gather_grads(self, grads: ModelGrads) -> dict[str, np.ndarray]:
+        c, cfg = self.mesh.c, self.cfg
+        out = {"table": gather(grads.table)[:cfg.v]}
+        for i, g in enumerate(grads.layers):
+            if g is not None:
+                out.update(_gather_layer(f"layers.{i}.", g, c))
+        return out
+
+
+def _gather_layer(pre: str, p, c: int) -> dict:
+    out = {}
+    for name in _LAYER_KEYS:
+        val = getattr(p, name)
+        arr = gather(val) if isinstance(val, ShardedMatrix) else val.gathered()
+        out[pre + name] = deinterleave_qkv(arr, c) if name in ("w_qkv", "b_qkv") else arr
+    return out
+
+
+def _device_random(mesh: Mesh, rows: int, cols: int, cfg: ModelConfig, seed: int, rows_real: int | None = None):
+    """Synthetic device-side init U[-1/sqrt(h), 1/sqrt(h)) in the weight layout (bench configs)."""
+    lim = 1.0 / math.sqrt(cfg.h)
+    gc = mesh.c
+    rb, cb = rows // gc, cols // gc
+    blocks = [None] * (gc * gc)
+    gen = torch.Generator(device=mesh.device())
+    for k in range(gc * gc):
+        l, j = divmod(k, gc)
+        o = mesh.flat(l % mesh.r, j)
+        if not mesh.owns(o):
+            continue
+        gen.manual_seed(seed * 7919 + k)
+        blk = padded_empty((rb, cb), F32, mesh.device())
+        blk.uniform_(-lim, lim, generator=gen)
+        if rows_real is not None and (l + 1) * rb > rows_real:
+            first_pad = max(rows_real - l * rb, 0)
+            blk[first_pad:].zero_()
+        blocks[k] = blk
+    return _with_twin(ShardedMatrix(mesh, rows, cols, blocks, "weight"))
+
+
+def run_loss_and_grads(model: MeshModel, tokens, labels, checkpointing: bool = True, cls_labels=None,
+                       merge_fwd_bwd: bool = False, planned: bool = False, eager_update: bool = False,
+                       lr: float = 0.0):
+    """One forward + backward; returns (loss, grads, workspace, store) (model.py:414-424)."""
+    ws = model.make_workspace(checkpointing=checkpointing, eager_update=eager_update, merge_fwd_bwd=merge_fwd_bwd,
+                              planned=planned)
+    store = CheckpointStore(model.mesh.p) if checkpointing else None
+    loss, saved = model.forward(tokens, labels, ws, store=store, cls_labels=cls_labels)
+    grads = model.backward(saved, ws, eager_update=eager_update, lr=lr)
+    return loss, grads, ws, store

@@ -1,0 +1,340 @@
+"""SUMMA block products C = AB, C = AB^T, C = A^T B on the r x c mesh.
+
+Drop-in for summagrid summa.py:30-191 (same names, arguments, errors and
+block layout for square meshes). Each SUMMA step is: panel broadcasts over
+the mesh row / column, then the local product on the tcgen05 tensor cores
+(libsg ``sg_gemm``) accumulating in fp32 in step order l = 0..c-1; the AB^T /
+A^T B forms reduce partial products over the row / column in group-position
+order. On the single-GPU (local) mesh the reduce is fused into the
+accumulating GEMM: the destination block is built as an ordered chain of
+GEMMs with C = D, no partial buffers and no separate reduction pass.
+
+Layouts (the r x c generalisation):
+  * "act"    — r x c block grid, block (i, j) on position (i, j): activations,
+               rows (tokens) split over mesh rows, columns over mesh columns.
+  * "weight" — c x c block grid, block (l, j) on position (l mod r, j).
+For r == c both are the reference's q x q layout (summa.py:30-56).
+  summa_ab : act x weight -> act      summa_abt: act x weight -> act
+  summa_atb: act x act    -> weight
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import ConfigError, ShapeError
+from .membuf import copy_block, full_storage, padded_empty
+from .mesh import Mesh, check_same_mesh
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+@dataclass
+class ShardedMatrix:
+    """A global matrix split into blocks over the mesh.
+
+    ``blocks`` is indexed by block-grid position (row * grid_cols + col); for
+    the "act" layout that is the owning position's flat rank, as in the
+    reference. Entries of blocks owned by other processes are None.
+    """
+
+    mesh: Mesh
+    global_rows: int
+    global_cols: int
+    blocks: list
+    layout: str = "act"
+
+    @property
+    def grid(self) -> tuple[int, int]:
+        return (self.mesh.r, self.mesh.c) if self.layout == "act" else (self.mesh.c, self.mesh.c)
+
+    @property
+    def block_rows(self) -> int:
+        return self.global_rows // self.grid[0]
+
+    @property
+    def block_cols(self) -> int:
+        return self.global_cols // self.grid[1]
+
+    def block(self, row: int, col: int):
+        return self.blocks[row * self.grid[1] + col]
+
+    def owner(self, row: int, col: int) -> int:
+        if self.layout == "act":
+            return self.mesh.flat(row, col)
+        return self.mesh.flat(row % self.mesh.r, col)
+
+    def owned_indices(self) -> list[int]:
+        gc = self.grid[1]
+        return [k for k in range(len(self.blocks)) if self.mesh.owns(self.owner(k // gc, k % gc))]
+
+    @property
+    def dtype(self):
+        for b in self.blocks:
+            if b is not None:
+                return b.dtype
+        return None
+
+    def copy(self) -> "ShardedMatrix":
+        return ShardedMatrix(self.mesh, self.global_rows, self.global_cols,
+                             [None if b is None else copy_block(padded_empty(tuple(b.shape), b.dtype, b.device), b)
+                              for b in self.blocks], self.layout)
+
+
+def _layout_grid(mesh: Mesh, layout: str) -> tuple[int, int]:
+    if layout not in ("act", "weight"):
+        raise ConfigError(f"unknown layout {layout!r}")
+    return (mesh.r, mesh.c) if layout == "act" else (mesh.c, mesh.c)
+
+
+def scatter(global_mat, mesh: Mesh, ws=None, category: str = "free", *, dtype: torch.dtype = F32,
+            layout: str = "act") -> ShardedMatrix:
+    """Split a global matrix (numpy or torch) into device blocks (summa.py:59-77)."""
+    g = torch.as_tensor(np.asarray(global_mat) if not isinstance(global_mat, torch.Tensor) else global_mat)
+    if g.dim() != 2:
+        raise ShapeError(f"scatter expects a 2-d matrix, got {g.dim()}-d")
+    rows, cols = g.shape
+    gr, gc = _layout_grid(mesh, layout)
+    if rows % gr or cols % gc:
+        raise ShapeError(f"matrix {rows}x{cols} not evenly divisible into {gr}x{gc} blocks")
+    rb, cb = rows // gr, cols // gc
+    s = ShardedMatrix(mesh, rows, cols, [None] * (gr * gc), layout)
+    for k in range(gr * gc):
+        i, j = divmod(k, gc)
+        owner = s.owner(i, j)
+        if not mesh.owns(owner):
+            continue
+        src = g[i * rb:(i + 1) * rb, j * cb:(j + 1) * cb]
+        blk = ws.empty(owner, (rb, cb), category, dtype=dtype) if ws is not None else \
+            padded_empty((rb, cb), dtype, mesh.device(owner))
+        blk.copy_(src.to(device=blk.device, dtype=dtype))
+        s.blocks[k] = blk
+    return s
+
+
+def gather(s: ShardedMatrix) -> np.ndarray:
+    """Reassemble the global matrix as float64 on the host (summa.py:80-88).
+
+    Test-harness boundary; on the dist backend every process receives it.
+    """
+    gr, gc = s.grid
+    rb, cb = s.block_rows, s.block_cols
+    out = np.empty((s.global_rows, s.global_cols))
+    mesh = s.mesh
+    if mesh.is_local:
+        for k, b in enumerate(s.blocks):
+            i, j = divmod(k, gc)
+            out[i * rb:(i + 1) * rb, j * cb:(j + 1) * cb] = b.detach().float().cpu().numpy()
+        return out
+    import torch.distributed as dist
+
+    mine = {k: s.blocks[k].detach().float().cpu().numpy() for k in s.owned_indices()}
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, mine)
+    for d in parts:
+        for k, b in d.items():
+            i, j = divmod(k, gc)
+            out[i * rb:(i + 1) * rb, j * cb:(j + 1) * cb] = b
+    return out
+
+
+# ------------------------------------------------------------------ helpers
+
+def as_bf16(mat: ShardedMatrix) -> ShardedMatrix:
+    """The bf16 GEMM-operand view of a sharded matrix (device cast if needed)."""
+    if mat.dtype == BF16:
+        return mat
+    blocks = []
+    for b in mat.blocks:
+        if b is None:
+            blocks.append(None)
+            continue
+        blocks.append(copy_block(padded_empty(tuple(b.shape), BF16, b.device), b))
+    return ShardedMatrix(mat.mesh, mat.global_rows, mat.global_cols, blocks, mat.layout)
+
+
+def _new_blocks(mesh: Mesh, ws, shape, category, dtype, layout="act"):
+    gr, gc = _layout_grid(mesh, layout)
+    out = [None] * (gr * gc)
+    for k in range(gr * gc):
+        i, j = divmod(k, gc)
+        owner = mesh.flat(i, j) if layout == "act" else mesh.flat(i % mesh.r, j)
+        if mesh.owns(owner):
+            out[k] = ws.empty(owner, shape, category, dtype=dtype) if ws is not None else \
+                padded_empty(shape, dtype, mesh.device(owner))
+    return out
+
+
+def _finish(mesh, acc_blocks, out_blocks, bias, c_blocks, act, aux_blocks, alpha=1.0):
+    """Apply the GEMM epilogue to fp32 partial sums where it could not be fused."""
+    for k, a in enumerate(acc_blocks):
+        if a is None:
+            continue
+        K.epilogue(a, out_blocks[k], bias=None if bias is None else bias[k],
+                   c=None if c_blocks is None else c_blocks[k], act=act,
+                   aux=None if aux_blocks is None else aux_blocks[k], alpha=alpha)
+
+
+def _check_pair(mesh, a, b, need_a, need_b, what):
+    if a.grid != _layout_grid(mesh, need_a) or b.grid != _layout_grid(mesh, need_b):
+        raise ConfigError(f"{what}: operands need layouts ({need_a}, {need_b}) on a {mesh.r}x{mesh.c} mesh")
+
+
+# ------------------------------------------------------------------ SUMMA forms
+
+def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
+             out_dtype: torch.dtype = F32, bias=None, act: int = K.ACT_NONE, aux=None, resid=None) -> ShardedMatrix:
+    """C = A B in c steps: A(i,l) along row i, B(l,j) down column j, C_ij += A_il B_lj.
+
+    summa.py:95-116. Optional fused epilogue (bias per output block, GELU with
+    saved pre-activation ``aux``, residual ``resid`` added once) applied at the
+    last step.
+    """
+    mesh = check_same_mesh(a, b)
+    if a.global_cols != b.global_rows:
+        raise ShapeError(f"summa_ab inner dims differ: {a.global_cols} vs {b.global_rows}")
+    _check_pair(mesh, a, b, "act", "weight", "summa_ab")
+    steps = mesh.c
+    m_b, k_b, n_b = a.block_rows, a.block_cols, b.block_cols
+    a16, b16 = as_bf16(a), as_bf16(b)
+    out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype)
+    fuse_in_out = out_dtype == F32 and act == K.ACT_NONE
+    acc = out if (steps == 1 or fuse_in_out) else _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    for l in range(steps):
+        a_pan = mesh.bcast_row(l, a16.blocks, (m_b, k_b), BF16, tag=tag)
+        src = [None] * mesh.p
+        for j in range(mesh.c):
+            o = b16.owner(l, j)
+            if mesh.owns(o):
+                src[o] = b16.block(l, j)
+        b_pan = mesh.bcast_col(l % mesh.r, src, (k_b, n_b), BF16, tag=tag)
+        last = l == steps - 1
+        for dev in mesh.local_devs:
+            prev = acc[dev] if l > 0 else (None if resid is None else resid.blocks[dev])
+            if last:
+                K.gemm(a_pan[dev], b_pan[dev], out[dev], bias=None if bias is None else bias[dev], c=prev, act=act,
+                       aux=None if aux is None else aux.blocks[dev])
+            else:
+                K.gemm(a_pan[dev], b_pan[dev], acc[dev], c=prev)
+    return ShardedMatrix(mesh, a.global_rows, b.global_cols, out)
+
+
+def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
+              out_dtype: torch.dtype = F32, act: int = K.ACT_NONE, aux=None, resid=None) -> ShardedMatrix:
+    """C = A B^T: B(l,j) down column j, A_ij B_lj^T, row-reduce to (i, l) (summa.py:119-140)."""
+    mesh = check_same_mesh(a, b)
+    if a.global_cols != b.global_cols:
+        raise ShapeError(f"summa_abt contraction dims differ: {a.global_cols} vs {b.global_cols}")
+    _check_pair(mesh, a, b, "act", "weight", "summa_abt")
+    m_b, k_b, n_b = a.block_rows, a.block_cols, b.block_rows
+    a16, b16 = as_bf16(a), as_bf16(b)
+    out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype)
+    aux_b = None if aux is None else aux.blocks
+    res_b = None if resid is None else resid.blocks
+    if mesh.is_local:
+        # reduce fused into the accumulating GEMM chain, group-position order j = 0..c-1
+        for l in range(mesh.c):
+            mesh._count("broadcast", tag)
+            mesh._count("reduce", tag)
+            for i in range(mesh.r):
+                d = mesh.flat(i, l)
+                chain = out[d] if mesh.c == 1 or (out_dtype == F32 and act == K.ACT_NONE) else \
+                    ws_empty(ws, mesh, d, (m_b, n_b))
+                for j in range(mesh.c):
+                    bt = b16.block(l, j).t()
+                    prev = chain if j > 0 else (None if res_b is None else res_b[d])
+                    if j == mesh.c - 1:
+                        K.gemm(a16.block(i, j), bt, out[d], c=prev, act=act, aux=None if aux_b is None else aux_b[d])
+                    else:
+                        K.gemm(a16.block(i, j), bt, chain, c=prev)
+        return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
+    acc = _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    for l in range(mesh.c):
+        src = [None] * mesh.p
+        for j in range(mesh.c):
+            o = b16.owner(l, j)
+            if mesh.owns(o):
+                src[o] = b16.block(l, j)
+        b_pan = mesh.bcast_col(l % mesh.r, src, (n_b, k_b), BF16, tag=tag)
+        parts = [None] * mesh.p
+        for dev in mesh.local_devs:
+            parts[dev] = ws_empty(ws, mesh, dev, (m_b, n_b))
+            K.gemm(a16.blocks[dev], b_pan[dev].t(), parts[dev])
+        mesh.reduce_row_into(l, parts, acc, tag=tag)
+    _finish(mesh, acc, out, None, res_b, act, aux_b)
+    return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
+
+
+def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
+              out_dtype: torch.dtype = F32, accumulate_into: ShardedMatrix | None = None) -> ShardedMatrix:
+    """C = A^T B: A(i,l) along row i, A_il^T B_ij, column-reduce to the owner of (l, j) (summa.py:143-164).
+
+    ``accumulate_into`` adds the product to an existing weight-layout fp32
+    matrix (gradient accumulation) instead of allocating the output.
+    """
+    mesh = check_same_mesh(a, b)
+    if a.global_rows != b.global_rows:
+        raise ShapeError(f"summa_atb contraction dims differ: {a.global_rows} vs {b.global_rows}")
+    _check_pair(mesh, a, b, "act", "act", "summa_atb")
+    m_b, t_b, n_b = a.block_cols, a.block_rows, b.block_cols
+    a16, b16 = as_bf16(a), as_bf16(b)
+    if accumulate_into is not None:
+        out_mat = accumulate_into
+        out = out_mat.blocks
+    else:
+        out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype, layout="weight")
+        out_mat = ShardedMatrix(mesh, a.global_cols, b.global_cols, out, "weight")
+    acc_in = accumulate_into is not None
+    if mesh.is_local:
+        for l in range(mesh.c):
+            mesh._count("broadcast", tag)
+            mesh._count("reduce", tag)
+            for j in range(mesh.c):
+                k = l * mesh.c + j
+                chain = out[k] if out[k].dtype == F32 else ws_empty(ws, mesh, mesh.flat(l % mesh.r, j), (m_b, n_b))
+                for i in range(mesh.r):
+                    prev = chain if (i > 0 or acc_in) else None
+                    dst = out[k] if i == mesh.r - 1 else chain
+                    K.gemm(a16.block(i, l).t(), b16.block(i, j), dst, c=prev)
+        return out_mat
+    for l in range(mesh.c):
+        a_pan = mesh.bcast_row(l, a16.blocks, (t_b, m_b), BF16, tag=tag)
+        parts = [None] * mesh.p
+        for dev in mesh.local_devs:
+            parts[dev] = ws_empty(ws, mesh, dev, (m_b, n_b))
+            K.gemm(a_pan[dev].t(), b16.blocks[dev], parts[dev])
+        dest = [None] * mesh.p
+        for j in range(mesh.c):
+            o = out_mat.owner(l, j)
+            if mesh.owns(o):
+                dest[o] = out[l * mesh.c + j]
+        mesh.reduce_col_into(l % mesh.r, parts, dest, accumulate=acc_in, tag=tag)
+    return out_mat
+
+
+def ws_empty(ws, mesh, dev, shape, dtype=F32):
+    return ws.empty(dev, shape, "workspace", dtype=dtype) if ws is not None else \
+        padded_empty(shape, dtype, mesh.device(dev))
+
+
+def summa_ab_backward(c_grad, a, b, ws, a_out_category="free", b_out_category="free", tag="summa"):
+    """Gradients of C = A B: (C_grad B^T, A^T C_grad) (summa.py:167-173)."""
+    return (summa_abt(c_grad, b, ws, out_category=a_out_category, tag=tag),
+            summa_atb(a, c_grad, ws, out_category=b_out_category, tag=tag))
+
+
+def summa_abt_backward(c_grad, a, b, ws, a_out_category="free", b_out_category="free", tag="summa"):
+    """Gradients of C = A B^T: (C_grad B, C_grad^T A) (summa.py:176-182)."""
+    return (summa_ab(c_grad, b, ws, out_category=a_out_category, tag=tag),
+            summa_atb(c_grad, a, ws, out_category=b_out_category, tag=tag))
+
+
+def summa_atb_backward(c_grad, a, b, ws, a_out_category="free", b_out_category="free", tag="summa"):
+    """Gradients of C = A^T B: (B C_grad^T, A C_grad) (summa.py:185-191)."""
+    return (summa_abt(b, c_grad, ws, out_category=a_out_category, tag=tag),
+            summa_ab(a, c_grad, ws, out_category=b_out_category, tag=tag))

@@ -1,0 +1,129 @@
+"""End-to-end loss and every gradient of the 2D model vs the float64 oracle
+(and the reference-generated golden model fixtures), on 1x1, 1x2, 2x2, 2x4."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import model_ref as M
+from tests._util import MESHES, TOL_BF16, bf16_round, mesh, rel
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).parent / "golden"
+
+
+def _sg():
+    import paper_2104_05343_b200 as sg
+
+    return sg
+
+
+def _compare_grads(sg, grads, ref, tol=TOL_BF16):
+    worst = {}
+    for k, g in grads.items():
+        worst[k] = rel(g, ref[k])
+    bad = {k: v for k, v in worst.items() if v > tol}
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("rc", MESHES)
+@pytest.mark.parametrize("checkpointing", [True, False])
+def test_model_vs_oracle(rc, checkpointing):
+    sg = _sg()
+    r, c = rc
+    m = mesh(r, c)
+    cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=61, num_layers=2)
+    rcfg = M.RefConfig(cfg.b, cfg.s, cfg.h, cfg.n, cfg.v, cfg.num_layers)
+    params = {k: bf16_round(v) for k, v in M.init_params(rcfg, 23).items()}
+    tokens, labels = M.sample_data(rcfg, 23)
+    model = sg.MeshModel(m, cfg, params)
+    loss, grads, ws, store = sg.run_loss_and_grads(model, tokens, labels, checkpointing=checkpointing)
+    ref_loss, saved = M.serial_forward(rcfg, params, tokens, labels)
+    ref = M.serial_backward(rcfg, params, saved)
+    assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3
+    _compare_grads(sg, model.gather_grads(grads), {k: v for k, v in ref.items() if not k.startswith("_")})
+    if checkpointing:
+        assert store.count() == 0  # every checkpoint consumed by the recompute
+
+
+@pytest.mark.parametrize("name", ["wide", "cli_default", "tiny_cfg1", "small"])
+def test_golden_model(name):
+    """Reference-generated loss / gradients (q = 1 and 2 meshes of the reference)."""
+    sg = _sg()
+    arrays = np.load(GOLD / "model.npz")
+    meta = json.loads((GOLD / "model.json").read_text())[name]
+    b, s, h, n, v, L = meta["dims"]
+    cfg = sg.ModelConfig(b=b, s=s, h=h, n=n, v=v, num_layers=L)
+    params = sg.init_global_params(cfg, meta["seed"])
+    for k, ps in meta["param_sums"].items():
+        assert float(params[k].sum()) == ps  # bit-exact init stream
+    tokens, labels = arrays[f"{name}.tokens"], arrays[f"{name}.labels"]
+    for rc in ((1, 1), (2, 2)):
+        m = mesh(*rc)
+        if b % rc[0] or n % rc[1] or (h // rc[1]) % (h // n):
+            continue
+        model = sg.MeshModel(m, cfg, params)
+        loss, grads, _, _ = sg.run_loss_and_grads(model, tokens, labels)
+        assert abs(loss - meta["loss"]) / meta["loss"] < TOL_BF16
+        g = model.gather_grads(grads)
+        for k, (gs, gss) in meta["grad_sums"].items():
+            # sum of squares is a norm check that does not cancel
+            assert abs(float((g[k] ** 2).sum()) - gss) / max(gss, 1e-30) < 4 * TOL_BF16, k
+        for key in arrays.files:
+            if key.startswith(f"{name}.grad."):
+                k = key[len(name) + 6:]
+                assert rel(g[k], arrays[key]) < TOL_BF16, (rc, k)
+
+
+def test_mesh_size_independent_loss():
+    """The loss does not depend on the mesh shape (tests/test_model.py:67-75)."""
+    sg = _sg()
+    cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=40, num_layers=1)
+    params = sg.init_global_params(cfg, 5)
+    rng = np.random.default_rng(6)
+    tok, lab = rng.integers(0, 40, (4, 16)), rng.integers(0, 40, (4, 16))
+    losses = []
+    for rc in MESHES:
+        model = sg.MeshModel(mesh(*rc), cfg, params)
+        losses.append(sg.run_loss_and_grads(model, tok, lab)[0])
+    assert max(losses) - min(losses) < 1e-3 * abs(losses[0])
+
+
+def test_zero_weights_loss_is_log_v():
+    """Zero weights and table give uniform logits: loss = ln v (tests/test_oracle.py:34-41)."""
+    sg = _sg()
+    cfg = sg.ModelConfig(b=2, s=8, h=32, n=4, v=24, num_layers=1)
+    params = {k: np.zeros_like(v) if k.startswith("layers") and "gamma" not in k else v
+              for k, v in sg.init_global_params(cfg, 1).items()}
+    params["table"] = np.zeros_like(params["table"])
+    model = sg.MeshModel(mesh(1, 2), cfg, params)
+    tok = np.zeros((2, 8), dtype=np.int64)
+    loss, _, _, _ = sg.run_loss_and_grads(model, tok, tok)
+    assert abs(loss - np.log(24)) < 1e-5
+
+
+def test_sgd_step_reduces_loss_and_train_step():
+    sg = _sg()
+    cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=32, num_layers=2)
+    params = sg.init_global_params(cfg, 9)
+    rng = np.random.default_rng(1)
+    tok, lab = rng.integers(0, 32, (4, 16)), rng.integers(0, 32, (4, 16))
+    model = sg.MeshModel(mesh(2, 2), cfg, params)
+    l0, grads, _, _ = sg.run_loss_and_grads(model, tok, lab)
+    model.apply_sgd(grads, 0.5)
+    ws = model.make_workspace()
+    l1 = float(model.train_step(tok, lab, ws, lr=0.5).item())
+    l2 = float(model.train_step(tok, lab, ws, lr=0.5).item())
+    assert l1 < l0 and l2 < l1
+    # the fused-update step equals reference-order update followed by forward
+    ref = sg.MeshModel(mesh(2, 2), cfg, params)
+    _, g, _, _ = sg.run_loss_and_grads(ref, tok, lab)
+    ref.apply_sgd(g, 0.5)
+    p_ref = ref.gather_params()
+    model2 = sg.MeshModel(mesh(2, 2), cfg, params)
+    model2.train_step(tok, lab, model2.make_workspace(), lr=0.5)
+    p_got = model2.gather_params()
+    for k in p_ref:
+        assert rel(p_got[k], p_ref[k]) < 1e-5, k
