@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Bench: 2D (SUMMA) transformer training throughput on B200 — BASELINE.json's metric
+"2D transformer train samples/sec & SUMMA TFLOP/s at 1/2/4/8 B200 vs CPU ref".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+
+Workload (configs[2]): BERT-large-shaped 2D stack — 24 pre-norm layers, h=1024,
+16 heads, s=512, global batch 32, BERT vocabulary 30522 with the tied lm-head
+and cross entropy — trained with SGD on an r x c mesh (1 -> 1x1, 2 -> 1x2,
+4 -> 2x2, 8 -> 2x4), global batch fixed ("strong"). Synthetic random-init
+weights and uniform random token / label ids (no datasets offline).
+
+value : samples/s with inputs resident in HBM, K steps between barrier +
+        synchronize, CUDA events, max over ranks.
+e2e   : same metric through the public API (MeshModel.train_step) with the
+        tokens / labels copied from pinned host memory and the loss read back
+        every step.
+summa : SUMMA AB / AB^T / A^T B TFLOP/s at N=8192 bf16 on the same mesh (configs[1]).
+roofline : tcgen05 GEMM kernel, algorithmic FLOPs / CUDA-event time of every
+        launch of one instrumented step, vs measured cuBLAS sustained peak.
+cpu_baseline : the float64 oracle restatement of the reference on the host
+        cores, bounded sample (oracle/cpu_bench.py), rank 0 at N = 1.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "2D transformer train samples/sec & SUMMA TFLOP/s at 1/2/4/8 B200 vs CPU ref"
+WORKLOADS = {
+    "bert": dict(b=32, s=512, h=1024, n=16, v=30522, layers=24, name="bert-large-2d-stack-train"),
+    "gpt": dict(b=8, s=2048, h=4096, n=32, v=50257, layers=24, name="gpt-h4096-2d-stack-train"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="bert")
+    ap.add_argument("--batch", type=int, default=0, help="override the global batch")
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count")
+    ap.add_argument("--no-graph", action="store_true", help="do not capture the step into a CUDA graph")
+    ap.add_argument("--checkpointing", action="store_true", help="activation checkpointing (recompute)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--summa-n", type=int, default=8192)
+    return ap.parse_args()
+
+
+def workload(args) -> dict:
+    w = dict(WORKLOADS[args.workload])
+    if args.batch:
+        w["b"] = args.batch
+    if args.layers:
+        w["layers"] = args.layers
+    return w
+
+
+def model_flops(w: dict) -> float:
+    """Algorithmic FLOPs of one fwd+bwd step (costmodel.py:63-65 x3, + lm-head 2bsvh x3)."""
+    b, s, h, v, L = w["b"], w["s"], w["h"], w["v"], w["layers"]
+    per_layer_fwd = 2.0 * (12 * b * s * h * h + 2 * b * s * s * h)
+    return 3.0 * (L * per_layer_fwd + 2.0 * b * s * v * h)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"bf16_burst": d.get("bf16_tflops", 1590.0), "bf16_sustained": d.get("bf16_tflops_sustained", 1409.0),
+                "hbm": d.get("hbm_gbs", 6650.0), "src": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "200"], stdout=self.out,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        self.out.flush()
+        rows = []
+        for line in Path(self.out.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9 and parts[1].isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(float(r[1]) for r in rows), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()) if rows else None}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+
+    w = workload(args)
+    cores = cpu_bench.host_cores()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
+        if i >= args.warmup:
+            vals.append(r["samples_per_s"])
+    v = statistics.mean(vals)
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w["b"] / v * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(w, args.gpus, args, extra={"note": "reference CPU algorithm (numpy f64 oracle port)"}),
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "port", "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(w, n_gpus, args, extra=None) -> dict:
+    from paper_2104_05343_b200.mesh import mesh_for_world
+
+    mc = mesh_for_world(n_gpus)
+    cfg = {"workload": w["name"], "model": f"2D transformer L={w['layers']} h={w['h']} n={w['n']} v={w['v']}",
+           "global_batch": w["b"], "seq_len": w["s"], "hidden": w["h"], "heads": w["n"], "layers": w["layers"],
+           "vocab": w["v"], "mesh": f"{mc.rows}x{mc.cols}", "parallelism": f"2d-summa r{mc.rows}xc{mc.cols}",
+           "checkpointing": bool(args.checkpointing), "cuda_graph": (not args.no_graph) and n_gpus == 1,
+           "optimizer": "sgd", "l2": "working set (weights fp32+bf16, >10 GB activations) larger than the 126 MB L2"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_05343_b200 as sg
+    from paper_2104_05343_b200 import kernels as K
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args)
+    mesh = sg.create_mesh(sg.mesh_for_world(world), backend="dist" if world > 1 else "local")
+    cfg = sg.ModelConfig(b=w["b"], s=w["s"], h=w["h"], n=w["n"], v=w["v"], num_layers=w["layers"])
+    model = sg.MeshModel(mesh, cfg, None, seed=1234)
+    ws = model.make_workspace(checkpointing=args.checkpointing)
+    rng = np.random.default_rng(0)
+    tok_h = torch.from_numpy(rng.integers(0, cfg.v, (cfg.b, cfg.s))).pin_memory()
+    lab_h = torch.from_numpy(rng.integers(0, cfg.v, (cfg.b, cfg.s))).pin_memory()
+    tok_d, lab_d = tok_h.cuda(), lab_h.cuda()
+    lr = 1e-4
+
+    def step():
+        return model.train_step(tok_d, lab_d, ws, lr, checkpointing=args.checkpointing)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        loss = step()
+    torch.cuda.synchronize()
+    use_graph = (not args.no_graph) and world == 1
+    graph = None
+    if use_graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            loss = step()
+        graph.replay()
+        torch.cuda.synchronize()
+        run = graph.replay
+    else:
+        def run():
+            nonlocal loss
+            loss = step()
+
+    # ------------------------------------------------------------- timed region (device-resident inputs)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = K.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            run()
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = K.launch_count() - launches0
+    if use_graph:  # replays do not pass through the host wrappers: count one captured step
+        l0 = K.launch_count()
+        step()
+        torch.cuda.synchronize()
+        launches = (K.launch_count() - l0) * args.steps
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = cfg.b * args.steps / (ms * 1e-3)
+    final_loss = float(loss.item())
+
+    # ------------------------------------------------------------- end to end (host buffers)
+    h2d = (tok_h.numel() * tok_h.element_size() + lab_h.numel() * lab_h.element_size()) * world
+    d2h = 4 * world
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        tok_d.copy_(tok_h, non_blocking=True)
+        lab_d.copy_(lab_h, non_blocking=True)
+        run()
+        _ = float(loss.item())  # D2H of the step's loss
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = cfg.b * args.steps / (e2e_ms * 1e-3)
+
+    # ------------------------------------------------------------- roofline of the dominant kernel
+    torch.cuda.synchronize()
+    s_ev0, s_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with K.profile_gemms() as prof:
+        s_ev0.record()
+        step()
+        s_ev1.record()
+    torch.cuda.synchronize()
+    gsum = prof.summary()
+    inst_step_ms = s_ev0.elapsed_time(s_ev1)
+    pk = peaks()
+    roof = {"kernel": "sg_gemm (tcgen05 persistent GEMM)", "bound": "tensor", "achieved": gsum["tflops"],
+            "peak": pk["bf16_sustained"], "unit": "TFLOP/s", "frac": gsum["tflops"] / pk["bf16_sustained"],
+            "traffic": None, "peak_source": pk["src"] + " sustained bf16",
+            "launches_per_step": gsum["launches"], "gemm_ms_per_step": gsum["ms"],
+            "gemm_share_of_step": gsum["ms"] / inst_step_ms if inst_step_ms > 0 else None,
+            "algorithmic_flops_per_step": gsum["flops"]}
+
+    # ------------------------------------------------------------- SUMMA sweep point (configs[1])
+    summa = summa_point(sg, K, mesh, args.summa_n, pk, barrier, world)
+
+    # ------------------------------------------------------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_bench
+
+        r = cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
+        cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": cpu_bench.host_cores(), "kind": "port",
+               "sample": r["sample"]}
+
+    if rank == 0:
+        flops = model_flops(w)
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids)",
+                "config": _config(w, world, args),
+                "model_tflops": flops / (ms_step * 1e-3) / 1e12,
+                "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches), "roofline": roof, "summa": summa, "cpu_baseline": cpu,
+                "clocks": clocks.summary(), "final_loss": final_loss}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def summa_point(sg, K, mesh, n, pk, barrier, world) -> dict:
+    """TFLOP/s of the three SUMMA forms at N x N x N bf16 on the bench mesh."""
+    import torch
+
+    out = {"N": n, "mesh": f"{mesh.r}x{mesh.c}", "peak": pk["bf16_burst"], "peak_source": pk["src"] + " burst bf16"}
+    ws = sg.Workspace(mesh.p)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(0)
+
+    def rand_mat(layout):
+        m = sg.ShardedMatrix(mesh, n, n, [None] * (mesh.r * mesh.c if layout == "act" else mesh.c * mesh.c), layout)
+        gr, gc = m.grid
+        for k in range(gr * gc):
+            if mesh.owns(m.owner(k // gc, k % gc)):
+                m.blocks[k] = torch.randn(n // gr, n // gc, device="cuda", generator=gen).bfloat16()
+        return m
+
+    A, W, A2 = rand_mat("act"), rand_mat("weight"), rand_mat("act")
+    forms = {"ab": lambda: sg.summa_ab(A, W, ws, out_dtype=torch.bfloat16),
+             "abt": lambda: sg.summa_abt(A, W, ws, out_dtype=torch.bfloat16),
+             "atb": lambda: sg.summa_atb(A, A2, ws)}
+    flops_dev = 2.0 * n ** 3 / mesh.p
+    for name, fn in forms.items():
+        for _ in range(2):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters = 10
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        tf = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+        out[name] = {"ms": ms, "tflops": tf, "tflops_per_gpu": flops_dev / (ms * 1e-3) / 1e12,
+                     "frac": flops_dev / (ms * 1e-3) / 1e12 / pk["bf16_burst"]}
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,8 @@ int sg_fold(void* dst, int dt, const void* const* srcs, int nsrc, int64_t n, int
 /* Number of SMs of the current device and library build id (sanity). */
 int sg_device_sm_count(void);
 const char* sg_build_info(void);
+/* Number of kernels this library has launched in the process (instrumentation). */
+int64_t sg_launch_count(void);
 /* Message of the last failing call on this thread ("" if none). */
 const char* sg_last_error(void);
 

@@ -65,6 +65,7 @@ SIGNATURES: dict[str, tuple] = {
     "sg_zero": (i32, [vp, i64, vp]),
     "sg_fold": (i32, [vp, i32, ctypes.POINTER(vp), i32, i64, i32, i32, vp]),
     "sg_device_sm_count": (i32, []),
+    "sg_launch_count": (i64, []),
     "sg_build_info": (ctypes.c_char_p, []),
     "sg_last_error": (ctypes.c_char_p, []),
 }

@@ -3,6 +3,8 @@
 
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <cstdint>
 
 #include "sg.h"
 #include "sg_internal.h"
@@ -17,6 +19,13 @@ void clear_error() { g_err[0] = 0; }
 }  // namespace sg
 
 extern "C" const char* sg_last_error(void) { return sg::g_err; }
+
+namespace sg {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace sg
+
+extern "C" int64_t sg_launch_count(void) { return sg::g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int sg_device_sm_count(void) {
   int dev = 0;

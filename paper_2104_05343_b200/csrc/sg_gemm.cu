@@ -439,6 +439,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
     attr_set = true;
   }
   kern<<<grid, 256, Cfg::SMEM, stream>>>(ta, tb, p);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   return SG_OK;
@@ -535,6 +536,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     const long long total = a->nb1 * a->nb2 * a->M * a->N;
     const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
     gemm_simt_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(sp);
+    count_launch();
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   }

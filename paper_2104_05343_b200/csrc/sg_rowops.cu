@@ -99,6 +99,7 @@ static int grid_for(long long work_items, int per_block, int waves = 8) {
 }
 
 static int launch_check() {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
 }

@@ -106,9 +106,50 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
         raise ConfigError("gemm: DGELU epilogue needs the saved pre-activation (aux)")
     args.act = act
     args.alpha = alpha
+    prof = _GEMM_PROFILE
+    if prof is not None:
+        s = torch.cuda.current_stream(out.device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
     with torch.cuda.device(out.device):
         check(_lib.lib().sg_gemm(ctypes.byref(args), _stream(out)), "sg_gemm")
+    if prof is not None:
+        e1.record(s)
+        prof.append((2.0 * M * N * K * args.nb1 * args.nb2, e0, e1, (M, N, K, args.nb1 * args.nb2)))
     return out
+
+
+_GEMM_PROFILE = None
+
+
+class profile_gemms:
+    """Record CUDA events around every sg_gemm launch on its stream.
+
+    ``records`` holds (algorithmic flops, start event, end event, shape) per
+    launch; ``summary()`` (after a synchronize) gives total flops, time and
+    TFLOP/s of the GEMM kernel.
+    """
+
+    def __enter__(self):
+        global _GEMM_PROFILE
+        self.records = []
+        _GEMM_PROFILE = self.records
+        return self
+
+    def __exit__(self, *exc):
+        global _GEMM_PROFILE
+        _GEMM_PROFILE = None
+
+    def summary(self) -> dict:
+        flops = sum(r[0] for r in self.records)
+        ms = sum(r[1].elapsed_time(r[2]) for r in self.records)
+        return {"launches": len(self.records), "flops": flops, "ms": ms,
+                "tflops": flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0}
+
+
+def launch_count() -> int:
+    """Kernels launched by libsg so far in this process."""
+    return int(_lib.lib().sg_launch_count())
 
 
 # ---------------------------------------------------------------- row kernels
