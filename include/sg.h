@@ -36,6 +36,10 @@ extern "C" {
 #define SG_ACT_GELU 1  /* D = gelu(x); aux (if set) <- x (bf16 pre-activation) */
 #define SG_ACT_DGELU 2 /* D = x * gelu'(aux) with aux the saved pre-activation */
 
+#define SG_EPI_NORMAL 0      /* x = alpha*acc + bias + C; D = act(x) (+ D2, colsum) */
+#define SG_EPI_SOFTMAX 1     /* D = softmax_row(alpha*acc), whole row in one tile (N <= 512) */
+#define SG_EPI_SOFTMAX_BWD 2 /* D = aux*(acc - rowsum(acc*aux))*alpha, aux = P (N <= 512) */
+
 /*
  * Batched local GEMM on the 5th-gen tensor cores (tcgen05, TMEM accumulators,
  * TMA-fed SWIZZLE_128B operand tiles), bf16 operands, fp32 accumulate:
@@ -53,7 +57,10 @@ extern "C" {
  *   summa_atb c_tmp = A_il^T B_ij   (a: MN-major, b: MN-major) summa.py:159-160
  * and of the per-head attention products (layers.py:409-411, 447-452).
  * The optional C operand implements SUMMA step accumulation (C == D allowed)
- * and the fused residual adds (layers.py:706-707, 722-723).
+ * and the fused residual adds (layers.py:706-707, 722-723); colsum fuses the
+ * bias gradients (layers.py:238); the softmax modes fuse the attention
+ * softmax (dense.py:67-75) and its backward (layers.py:447-450) into the
+ * QK^T / dO V^T products.
  */
 typedef struct sg_gemm_args {
   int64_t M, N, K;
@@ -66,6 +73,11 @@ typedef struct sg_gemm_args {
   void* aux; int64_t ldx, sx1, sx2;
   int32_t act;
   float alpha;
+  /* optional bf16 copy of D (e.g. the GEMM operand twin of an fp32 gradient) */
+  void* D2; int64_t ld2, s21, s22;
+  /* optional fused column sums: colsum[z1*scs1 + z2*scs2 + n] += sum_m D[z](m, n) */
+  float* colsum; int64_t scs1, scs2;
+  int32_t mode; /* SG_EPI_* */
 } sg_gemm_args;
 
 int sg_gemm(const sg_gemm_args* args, void* stream);
@@ -89,11 +101,12 @@ int sg_ln_fwd(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, c
 int sg_ln_bwd_stats(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx, const float* mean,
                     const float* rstd, const float* gamma, int64_t rows, int64_t cols, float* stats, void* stream);
 /* LayerNorm backward phase 2: dx = rstd*(g - sum_g/h - x^ sum_xg/h) + resid (fp32),
- * optional bf16 copy dx2, dgamma/dbeta += column sums (layers.py:329-342, 744-753). */
+ * optional bf16 copy dx2, dgamma/dbeta += column sums (layers.py:329-342, 744-753)
+ * and dsum += column sums of dx itself (the next bias gradient, layers.py:238). */
 int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, int xdt, int64_t ldx, const float* mean,
               const float* rstd, const float* gamma, int64_t rows, int64_t cols, const float* stats, int64_t h_total,
               const void* resid, int rdt, int64_t ldr, void* dx, int dxdt, int64_t lddx, void* dx2, int64_t lddx2,
-              float* dgamma, float* dbeta, void* stream);
+              float* dgamma, float* dbeta, float* dsum, void* stream);
 /* out[c] (+)= sum_r x[r,c]: bias gradients before the column reduce (layers.py:238). */
 int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int64_t ldx, float* out, int accumulate,
               void* stream);

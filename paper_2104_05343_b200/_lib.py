@@ -18,6 +18,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
 SG_OK, SG_ERR_SHAPE, SG_ERR_CONFIG, SG_ERR_CUDA = 0, 1, 2, 3
 DTYPE_BF16, DTYPE_F32 = 0, 1
 ACT_NONE, ACT_GELU, ACT_DGELU = 0, 1, 2
+EPI_NORMAL, EPI_SOFTMAX, EPI_SOFTMAX_BWD = 0, 1, 2
 
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32
@@ -38,6 +39,9 @@ class GemmArgs(ctypes.Structure):
         ("aux", vp), ("ldx", i64), ("sx1", i64), ("sx2", i64),
         ("act", i32),
         ("alpha", ctypes.c_float),
+        ("D2", vp), ("ld2", i64), ("s21", i64), ("s22", i64),
+        ("colsum", vp), ("scs1", i64), ("scs2", i64),
+        ("mode", i32),
     ]
 
 
@@ -48,7 +52,7 @@ SIGNATURES: dict[str, tuple] = {
     "sg_ln_fwd": (i32, [vp, i32, i64, i64, i64, vp, i64, ctypes.c_float, vp, vp, vp, i32, i64, vp, vp, vp]),
     "sg_ln_bwd_stats": (i32, [vp, i32, i64, vp, i32, i64, vp, vp, vp, i64, i64, vp, vp]),
     "sg_ln_bwd": (i32, [vp, i32, i64, vp, i32, i64, vp, vp, vp, i64, i64, vp, i64, vp, i32, i64, vp, i32, i64,
-                        vp, i64, vp, vp, vp]),
+                        vp, i64, vp, vp, vp, vp]),
     "sg_colsum": (i32, [vp, i32, i64, i64, i64, vp, i32, vp]),
     "sg_bias_add": (i32, [vp, i32, i64, i64, i64, vp, vp]),
     "sg_softmax_rows": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),

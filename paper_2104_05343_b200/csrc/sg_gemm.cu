@@ -4,14 +4,27 @@
 // `a @ b` via mesh.py:349-361) and of the per-head attention products of
 // layers.py:404-459.
 //
-// CTA layout (256 threads, 1 CTA per SM, grid = min(#tiles, #SMs)):
+// CTA layout (384 threads, 1 CTA per SM, grid = min(#tiles, #SMs)):
 //   warp 0      TMA producer (one lane): A/B tiles -> SWIZZLE_128B smem ring
-//   warp 1      MMA issuer (one lane): tcgen05.mma 128 x BN x 16 into TMEM
+//   warp 1      MMA issuer (one lane): tcgen05.mma 128 x min(BN,256) x 16 into TMEM
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld -> alpha, bias, C/residual, GELU/GELU' ->
-//               bf16/fp32 stores; warp w reads TMEM lane quadrant (w % 4)
-// Two TMEM accumulator buffers let the epilogue of tile i overlap the MMAs of
-// tile i+1; the smem ring has STAGES slots guarded by full/empty mbarriers.
+//   warps 4..11 epilogue; warp w owns TMEM lane quadrant (w % 4) = 32 tile rows and
+//               every other 32-column chunk, so two warps share a quadrant
+// Two TMEM accumulator buffers (one when BN = 512) let the epilogue of tile i
+// overlap the MMAs of tile i+1; the smem ring has STAGES slots guarded by
+// full/empty mbarriers.
+//
+// Epilogue modes:
+//   NORMAL       tcgen05.ld (thread = row, 32 columns) -> alpha, bias, +C, GELU
+//                (saves the pre-activation) or GELU', bf16/fp32 D, optional
+//                bf16 copy D2 — 16-byte vector row accesses, every load of a
+//                chunk issued before its stores (C may alias D); optional
+//                column sums (bias gradients) via a swizzled smem transpose and
+//                one atomic per column per warp.
+//   SOFTMAX      D = softmax_row(alpha * acc) over the whole row (N <= 512 fits
+//                TMEM): attention probabilities without an fp32 score matrix.
+//   SOFTMAX_BWD  D = aux * (acc - rowsum(acc * aux)) * alpha with aux = P:
+//                dS straight from the dP = dO V^T product (layers.py:447-450).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,6 +45,7 @@ struct GemmParams {
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int a_b2_first, b_b2_first;
+  int mode;
   void* D;
   long long ldd, sd1, sd2;
   int d_f32;
@@ -41,6 +55,10 @@ struct GemmParams {
   const float* bias;
   void* aux;
   long long ldx, sx1, sx2;
+  __nv_bfloat16* D2;
+  long long ld2, s21, s22;
+  float* colsum;
+  long long scs1, scs2;
   int act;
   float alpha;
   int vec_ok;
@@ -48,14 +66,20 @@ struct GemmParams {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
+constexpr int kStg = 32 * 32;     // per-warp XOR-swizzled transpose staging for column sums (floats)
+constexpr int kEpiWarps = 8;      // two epilogue warps per TMEM lane quadrant
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int MMA_N = BN > 256 ? 256 : BN;
+  static constexpr int NSPLIT = BN / MMA_N;
+  static constexpr int ACC_BUFS = 2 * BN <= 512 ? 2 : 1;
+  static constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = BN * kBK * 2;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  static constexpr int STAGES = BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + kEpiWarps * kStg * 4 + 1024 + 256;
 };
 
 __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer,
@@ -76,6 +100,17 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb,
   z2 = z - z1 * p.nb2;
 }
 
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  return 0.5f * x * (1.f + tanh_fast(c * (x + a * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float t = tanh_fast(c * (x + a * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+}
+
+// 32 consecutive elements of one row: 16-byte vector accesses when aligned.
 __device__ __forceinline__ void load_row32(const void* base, bool f32, bool vec, int n, float (&v)[32]) {
   if (f32) {
     const float* s = static_cast<const float*>(base);
@@ -139,18 +174,32 @@ __device__ __forceinline__ void store_row32(void* base, bool f32, bool vec, int 
   }
 }
 
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Named barrier for the two epilogue warps sharing a TMEM lane quadrant.
+__device__ __forceinline__ void quad_sync(int q) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+}
+
 template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int ACC = Cfg::ACC_BUFS;
   constexpr uint32_t A_BYTES = Cfg::A_BYTES, B_BYTES = Cfg::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  float* stg_all = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
+  float* red_all = stg_all + kEpiWarps * kStg;  // [2 halves][4 quadrants][32 rows] row partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red_all + 256);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
@@ -169,7 +218,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -200,7 +249,10 @@ __global__ void __launch_bounds__(256, 1)
                        p.a_b2_first);
           }
           if (!B_MN) {
-            load_box(&tmB, b_dst, &full[stage], kb * kBK, nb * BN, z2, z1, p.b_b2_first);
+#pragma unroll
+            for (int h = 0; h < Cfg::NSPLIT; ++h)
+              load_box(&tmB, b_dst + h * Cfg::MMA_N * kBK * 2, &full[stage], kb * kBK, nb * BN + h * Cfg::MMA_N, z2,
+                       z1, p.b_b2_first);
           } else {
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
@@ -217,10 +269,12 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t IDESC = umma_idesc_bf16(kBM, BN, A_MN, B_MN);
+      constexpr uint32_t IDESC = umma_idesc_bf16(kBM, Cfg::MMA_N, A_MN, B_MN);
+      // byte offset of the second MMA_N-wide half of B inside a stage
+      constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;
       uint32_t stage = 0, phase = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const uint32_t as = it & 1, aph = (it >> 1) & 1;
+        const uint32_t as = it % ACC, aph = (it / ACC) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
@@ -237,9 +291,13 @@ __global__ void __launch_bounds__(256, 1)
             //   stride (kBK rows x 128 B), SBO = 1024 B between 8-row K groups.
             const uint64_t ad = A_MN ? umma_desc_sw128(a_base + k * 2048, kBK * 128, 1024)
                                      : umma_desc_sw128(a_base + k * 32, 0, 1024);
-            const uint64_t bd = B_MN ? umma_desc_sw128(b_base + k * 2048, kBK * 128, 1024)
-                                     : umma_desc_sw128(b_base + k * 32, 0, 1024);
-            umma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < Cfg::NSPLIT; ++h) {
+              const uint32_t bb = b_base + h * B_HALF;
+              const uint64_t bd = B_MN ? umma_desc_sw128(bb + k * 2048, kBK * 128, 1024)
+                                       : umma_desc_sw128(bb + k * 32, 0, 1024);
+              umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            }
           }
           umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -252,62 +310,181 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
+    // warp w: TMEM lane quadrant q = w % 4 (rows 32q..32q+31), column chunks c % 2 == half
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    float* stg = stg_all + (warp - 4) * kStg;
     uint32_t it = 0;
     const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0, vec = p.vec_ok != 0;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    constexpr int NCH = BN / 32;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       int mb, nb, z1, z2;
       decode_tile(p, t, mb, nb, z1, z2);
-      const uint32_t as = it & 1, aph = (it >> 1) & 1;
+      const uint32_t as = it % ACC, aph = (it / ACC) & 1;
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
+      const uint32_t tacc = tmem_base + lane_base + as * BN;
       const int row = mb * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const size_t d_row = (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 + (size_t)row * p.ldd;
       const size_t c_row = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2 + (size_t)row * p.ldc;
       const size_t x_row = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2 + (size_t)row * p.ldx;
+      const size_t o2_row = (size_t)z1 * p.s21 + (size_t)z2 * p.s22 + (size_t)row * p.ld2;
+      if (p.mode == SG_EPI_NORMAL) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c * 32, r);
-        tmem_wait_ld();
-        if (c == BN / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[as]);
+        for (int c = half; c < NCH; c += 2) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_wait_ld();
+          if (c + 2 >= NCH) {  // this warp's last chunk of the tile
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[as]);
+          }
+          const int col0 = nb * BN + c * 32;
+          if (col0 >= p.N) continue;  // warp-uniform
+          const int ncols = min(32, p.N - col0);
+          const bool vfull = vec && ncols == 32;
+          float v[32];
+          // issue every global load of the chunk before any store (C may alias D)
+          float cv[32], xv[32];
+          if (p.C && row_ok) {
+            const void* cb = c_f32 ? static_cast<const void*>(static_cast<const float*>(p.C) + c_row + col0)
+                                   : static_cast<const void*>(static_cast<const __nv_bfloat16*>(p.C) + c_row + col0);
+            load_row32(cb, c_f32, vfull, ncols, cv);
+          }
+          if (p.act == SG_ACT_DGELU && row_ok)
+            load_row32(static_cast<const __nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, xv);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (j < ncols) ? __ldg(p.bias + col0 + j) : 0.f;
+          }
+          if (p.C) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += cv[j];
+          }
+          if (p.act == SG_ACT_GELU) {
+            if (p.aux && row_ok) store_row32(static_cast<__nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+          } else if (p.act == SG_ACT_DGELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(xv[j]);
+          }
+          if (row_ok) {
+            void* db = d_f32 ? static_cast<void*>(static_cast<float*>(p.D) + d_row + col0)
+                             : static_cast<void*>(static_cast<__nv_bfloat16*>(p.D) + d_row + col0);
+            store_row32(db, d_f32, vfull, ncols, v);
+            if (p.D2) store_row32(p.D2 + o2_row + col0, false, vfull, ncols, v);
+          }
+          if (p.colsum) {
+            // column sums over this warp's 32 rows: transpose through smem, lane = column
+#pragma unroll
+            for (int j = 0; j < 32; ++j) stg[j * 32 + (lane ^ j)] = row_ok ? v[j] : 0.f;
+            __syncwarp();
+            float cs = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) cs += stg[lane * 32 + (i ^ lane)];
+            if (lane < ncols) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col0 + lane, cs);
+            __syncwarp();
+          }
         }
-        const int col0 = nb * BN + c * 32;
-        if (!row_ok || col0 >= p.N) continue;
-        const int ncols = min(32, p.N - col0);
-        const bool vfull = vec && ncols == 32;
-        float v[32];
+      } else {
+        // row-softmax modes: thread = row; the row's chunks are split between the
+        // two warps of the quadrant, row partials combined through smem
+        float* red = red_all + q * 32;  // [half][4 quadrants x 32]
+        if (p.mode == SG_EPI_SOFTMAX) {
+          const float sl2 = p.alpha * 1.4426950408889634f;  // alpha * log2(e)
+          float m = -INFINITY;
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-        if (p.bias) {
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < p.N) m = fmaxf(m, __uint_as_float(r[j]));
+          }
+          red[half * 128 + lane] = m;
+          quad_sync(q);
+          m = fmaxf(red[lane], red[128 + lane]);
+          const float ms = m * sl2;
+          float z = 0.f;
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += (j < ncols) ? __ldg(p.bias + col0 + j) : 0.f;
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < p.N) z += ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms));
+          }
+          quad_sync(q);  // both warps have read the max slots
+          red[half * 128 + lane] = z;
+          quad_sync(q);
+          const float inv = 1.f / (red[lane] + red[128 + lane]);
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_wait_ld();
+            if (c + 2 >= NCH) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[as]);
+            }
+            const int col0 = c * 32;
+            if (!row_ok || col0 >= p.N) continue;
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms)) * inv;
+            store_row32(static_cast<__nv_bfloat16*>(p.D) + d_row + col0, false, vec && p.N - col0 >= 32,
+                        min(32, p.N - col0), v);
+          }
+          quad_sync(q);  // smem partials free for the next tile
+        } else {  // SG_EPI_SOFTMAX_BWD: D = P * (dP - sum(dP * P)) * alpha
+          const __nv_bfloat16* pr = static_cast<const __nv_bfloat16*>(p.aux) + x_row;
+          float acc = 0.f;
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_wait_ld();
+            const int col0 = c * 32;
+            if (!row_ok || col0 >= p.N) continue;
+            float pv[32];
+            load_row32(pr + col0, false, vec && p.N - col0 >= 32, min(32, p.N - col0), pv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc = fmaf(__uint_as_float(r[j]), pv[j], acc);
+          }
+          red[half * 128 + lane] = acc;
+          quad_sync(q);
+          acc = red[lane] + red[128 + lane];
+#pragma unroll 1
+          for (int c = half; c < NCH; c += 2) {
+            uint32_t r[32];
+            tmem_ld32(tacc + c * 32, r);
+            tmem_wait_ld();
+            if (c + 2 >= NCH) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[as]);
+            }
+            const int col0 = c * 32;
+            if (!row_ok || col0 >= p.N) continue;
+            const bool v32 = vec && p.N - col0 >= 32;
+            const int n = min(32, p.N - col0);
+            float pv[32], v[32];
+            load_row32(pr + col0, false, v32, n, pv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = pv[j] * (__uint_as_float(r[j]) - acc) * p.alpha;
+            store_row32(static_cast<__nv_bfloat16*>(p.D) + d_row + col0, false, v32, n, v);
+          }
+          quad_sync(q);
         }
-        if (p.C) {
-          float cv[32];
-          const void* cb = c_f32 ? static_cast<const void*>(static_cast<const float*>(p.C) + c_row + col0)
-                                 : static_cast<const void*>(static_cast<const __nv_bfloat16*>(p.C) + c_row + col0);
-          load_row32(cb, c_f32, vfull, ncols, cv);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += cv[j];
-        }
-        if (p.act == SG_ACT_GELU) {
-          if (p.aux) store_row32(static_cast<__nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-        } else if (p.act == SG_ACT_DGELU) {
-          float xv[32];
-          load_row32(static_cast<const __nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, xv);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(xv[j]);
-        }
-        void* db = d_f32 ? static_cast<void*>(static_cast<float*>(p.D) + d_row + col0)
-                         : static_cast<void*>(static_cast<__nv_bfloat16*>(p.D) + d_row + col0);
-        store_row32(db, d_f32, vfull, ncols, v);
       }
     }
   }
@@ -317,11 +494,10 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
-
 // ------------------------------------------------------------------ SIMT path
 // CUDA-core fallback for operands the TMA unit cannot address (row pitches or
 // batch strides that are not 16-byte multiples, e.g. head_dim 4 in the
-// reference's unit-test configurations). Same semantics and epilogue.
+// reference's unit-test configurations). NORMAL-mode semantics.
 struct SimtParams {
   GemmParams p;
   const __nv_bfloat16* A;
@@ -370,6 +546,8 @@ __global__ void gemm_simt_kernel(const __grid_constant__ SimtParams sp) {
       static_cast<float*>(p.D)[di] = v;
     else
       static_cast<__nv_bfloat16*>(p.D)[di] = __float2bfloat16_rn(v);
+    if (p.D2) p.D2[(size_t)z1 * p.s21 + (size_t)z2 * p.s22 + (size_t)m * p.ld2 + n] = __float2bfloat16_rn(v);
+    if (p.colsum) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + n, v);
   }
 }
 
@@ -438,7 +616,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
       return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
     attr_set = true;
   }
-  kern<<<grid, 256, Cfg::SMEM, stream>>>(ta, tb, p);
+  kern<<<grid, kThreads, Cfg::SMEM, stream>>>(ta, tb, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -454,7 +632,12 @@ static int dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUten
   return launch_gemm<BN, true, true>(ta, tb, p, s, grid);
 }
 
-static int pick_bn(long long M, long long N, long long batch, int sms) {
+static int pick_bn(long long M, long long N, long long batch, int sms, int mode) {
+  if (mode != SG_EPI_NORMAL) {  // the whole row in one tile
+    for (int bn : {64, 128, 256, 512})
+      if (N <= bn) return bn;
+    return -1;
+  }
   if (N <= 64) return 64;
   if (N <= 128) return 128;
   // Largest tile unless it leaves the last wave badly underfilled.
@@ -488,6 +671,14 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (!a->A || !a->B || !a->D) return set_error(SG_ERR_CONFIG, "gemm: null operand");
   if ((a->act == SG_ACT_DGELU) && !a->aux) return set_error(SG_ERR_CONFIG, "gemm: DGELU needs aux");
   if (a->d_dtype != SG_DTYPE_BF16 && a->d_dtype != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "gemm: d_dtype");
+  if (a->mode != SG_EPI_NORMAL) {
+    if (a->mode != SG_EPI_SOFTMAX && a->mode != SG_EPI_SOFTMAX_BWD) return set_error(SG_ERR_CONFIG, "gemm: mode");
+    if (a->N > 512) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need N <= 512");
+    if (a->d_dtype != SG_DTYPE_BF16 || a->C || a->bias || a->act || a->D2 || a->colsum)
+      return set_error(SG_ERR_CONFIG, "gemm: softmax epilogues write bf16 D only");
+    if (a->mode == SG_EPI_SOFTMAX_BWD && !a->aux) return set_error(SG_ERR_CONFIG, "gemm: softmax bwd needs P");
+    if (a->mode == SG_EPI_SOFTMAX && a->alpha <= 0.f) return set_error(SG_ERR_CONFIG, "gemm: softmax alpha > 0");
+  }
   const int sms = sg_device_sm_count();
   if (sms <= 0) return set_error(SG_ERR_CUDA, "no CUDA device");
 
@@ -496,8 +687,9 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.N = (int)a->N;
   p.K = (int)a->K;
   p.nb2 = (int)a->nb2;
+  p.mode = a->mode;
   const long long batch = a->nb1 * a->nb2;
-  const int bn = pick_bn(a->M, a->N, batch, sms);
+  const int bn = pick_bn(a->M, a->N, batch, sms, a->mode);
   p.m_tiles = (int)((a->M + kBM - 1) / kBM);
   p.n_tiles = (int)((a->N + bn - 1) / bn);
   p.k_blocks = (int)((a->K + kBK - 1) / kBK);
@@ -508,16 +700,17 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.C = a->C; p.ldc = a->ldc; p.sc1 = a->sc1; p.sc2 = a->sc2; p.c_f32 = a->c_dtype == SG_DTYPE_F32;
   p.bias = a->bias;
   p.aux = a->aux; p.ldx = a->ldx; p.sx1 = a->sx1; p.sx2 = a->sx2;
+  p.D2 = static_cast<__nv_bfloat16*>(a->D2); p.ld2 = a->ld2; p.s21 = a->s21; p.s22 = a->s22;
+  p.colsum = a->colsum; p.scs1 = a->scs1; p.scs2 = a->scs2;
   p.act = a->act;
   p.alpha = a->alpha;
-  // 16-byte vector epilogue when every row start of D / C / aux is 16-byte aligned.
+  // 16-byte vector row access (softmax modes) when every row start of D / aux is 16-byte aligned.
   auto al = [](const void* ptr, long long ld, long long s1, long long s2, int esz) {
     if (!ptr) return true;
     return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0 && (ld * esz) % 16 == 0 && (s1 * esz) % 16 == 0 &&
            (s2 * esz) % 16 == 0;
   };
-  p.vec_ok = al(a->D, a->ldd, a->sd1, a->sd2, p.d_f32 ? 4 : 2) && al(a->C, a->ldc, a->sc1, a->sc2, p.c_f32 ? 4 : 2) &&
-             al(a->aux, a->ldx, a->sx1, a->sx2, 2);
+  p.vec_ok = al(a->D, a->ldd, a->sd1, a->sd2, p.d_f32 ? 4 : 2) && al(a->aux, a->ldx, a->sx1, a->sx2, 2);
 
   // TMA needs 16-byte aligned bases, row pitches and batch strides; otherwise
   // take the CUDA-core path (tiny / odd-shaped operands only).
@@ -526,6 +719,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
            (n2 <= 1 || (s2 * 2) % 16 == 0);
   };
   if (!tma_ok(a->A, a->lda, a->nb1, a->sa1, a->nb2, a->sa2) || !tma_ok(a->B, a->ldb, a->nb1, a->sb1, a->nb2, a->sb2)) {
+    if (a->mode != SG_EPI_NORMAL) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need TMA-aligned operands");
     SimtParams sp;
     sp.p = p;
     sp.A = static_cast<const __nv_bfloat16*>(a->A);
@@ -548,8 +742,9 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   else
     rc = make_operand_map(&ta, a->A, a->M, a->K, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBK, &p.a_b2_first);
   if (rc) return rc;
+  const int b_box = std::min(bn, 256);
   if (!a->b_mn_major)
-    rc = make_operand_map(&tb, a->B, a->K, a->N, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, bn, &p.b_b2_first);
+    rc = make_operand_map(&tb, a->B, a->K, a->N, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, b_box, &p.b_b2_first);
   else
     rc = make_operand_map(&tb, a->B, a->N, a->K, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, kBK, &p.b_b2_first);
   if (rc) return rc;
@@ -560,6 +755,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   switch (bn) {
     case 64: return dispatch_major<64>(amn, bmn, ta, tb, p, s, grid);
     case 128: return dispatch_major<128>(amn, bmn, ta, tb, p, s, grid);
-    default: return dispatch_major<256>(amn, bmn, ta, tb, p, s, grid);
+    case 256: return dispatch_major<256>(amn, bmn, ta, tb, p, s, grid);
+    default: return dispatch_major<512>(amn, bmn, ta, tb, p, s, grid);
   }
 }

@@ -242,24 +242,25 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma, long long rows,
     int cols, const float* __restrict__ stats, float inv_h, const TR* __restrict__ resid, long long ldr,
     TO* __restrict__ dx, long long lddx, bf16* __restrict__ dx2, long long lddx2, float* __restrict__ dgamma,
-    float* __restrict__ dbeta) {
-  __shared__ float s_dg[kSeg], s_db[kSeg];
+    float* __restrict__ dbeta, float* __restrict__ dsum) {
+  __shared__ float s_dg[kSeg], s_db[kSeg], s_ds[kSeg];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * kSeg;
   const int seg = min(kSeg, cols - c0);
-  const bool want_g = dgamma != nullptr;
-  if (want_g) {
+  const bool want_g = dgamma != nullptr, want_s = dsum != nullptr;
+  if (want_g || want_s) {
     for (int i = threadIdx.x; i < kSeg; i += blockDim.x) {
       s_dg[i] = 0.f;
       s_db[i] = 0.f;
+      s_ds[i] = 0.f;
     }
     __syncthreads();
   }
-  float ag[4][8], ab[4][8];
+  float ag[4][8], ab[4][8], as[4][8];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = 0.f;
+    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = as[k][i] = 0.f;
   for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
     const float mu = mean[r], rs = rstd[r];
     const float m_xg = stats[2 * r] * inv_h, m_g = stats[2 * r + 1] * inv_h;
@@ -285,12 +286,13 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
         o[i] += rs * (d[i] * g[i] - m_g - xh * m_xg);
         ag[k][i] += d[i] * xh;
         ab[k][i] += d[i];
+        as[k][i] += o[i];
       }
       st8(dx + r * lddx + cc, n, o);
       if (dx2) st8(dx2 + r * lddx2 + cc, n, o);
     }
   }
-  if (want_g) {
+  if (want_g || want_s) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = k * 256 + lane * 8;
@@ -298,14 +300,20 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (c + i < seg) {
-          atomicAdd(&s_dg[c + i], ag[k][i]);
-          atomicAdd(&s_db[c + i], ab[k][i]);
+          if (want_g) {
+            atomicAdd(&s_dg[c + i], ag[k][i]);
+            atomicAdd(&s_db[c + i], ab[k][i]);
+          }
+          if (want_s) atomicAdd(&s_ds[c + i], as[k][i]);
         }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < seg; i += blockDim.x) {
-      atomicAdd(&dgamma[c0 + i], s_dg[i]);
-      atomicAdd(&dbeta[c0 + i], s_db[i]);
+      if (want_g) {
+        atomicAdd(&dgamma[c0 + i], s_dg[i]);
+        atomicAdd(&dbeta[c0 + i], s_db[i]);
+      }
+      if (want_s) atomicAdd(&dsum[c0 + i], s_ds[i]);
     }
   }
 }
@@ -740,7 +748,7 @@ extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, 
                          const float* mean, const float* rstd, const float* gamma, int64_t rows, int64_t cols,
                          const float* stats, int64_t h_total, const void* resid, int rdt, int64_t ldr, void* dx,
                          int dxdt, int64_t lddx, void* dx2, int64_t lddx2, float* dgamma, float* dbeta,
-                         void* stream) {
+                         float* dsum, void* stream) {
   clear_error();
   if (rows < 0 || cols < 1 || h_total < cols || !stats) return set_error(SG_ERR_SHAPE, "ln_bwd: bad arguments");
   if ((dgamma == nullptr) != (dbeta == nullptr)) return set_error(SG_ERR_CONFIG, "ln_bwd: dgamma/dbeta pair");
@@ -756,7 +764,7 @@ extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, 
   if (rdt != SG_DTYPE_BF16) rdt = SG_DTYPE_F32;
   // dx is fp32 (residual-stream gradient); the optional dx2 is its bf16 GEMM operand copy
   if (dxdt != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "ln_bwd: dx must be fp32");
-  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, float><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta)))));
+  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, float><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta, dsum)))));
   return launch_check();
 }
 

@@ -11,10 +11,11 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import ACT_DGELU, ACT_GELU, ACT_NONE, DTYPE_BF16, DTYPE_F32, GemmArgs, check
+from ._lib import (ACT_DGELU, ACT_GELU, ACT_NONE, DTYPE_BF16, DTYPE_F32, EPI_NORMAL, EPI_SOFTMAX,
+                   EPI_SOFTMAX_BWD, GemmArgs, check)
 from .errors import ConfigError, ShapeError
 
-__all__ = ["gemm", "ACT_NONE", "ACT_GELU", "ACT_DGELU"]
+__all__ = ["gemm", "ACT_NONE", "ACT_GELU", "ACT_DGELU", "EPI_NORMAL", "EPI_SOFTMAX", "EPI_SOFTMAX_BWD"]
 
 
 def _stream(t: torch.Tensor) -> int:
@@ -46,13 +47,19 @@ def _batch(t: torch.Tensor, nbatch: int) -> tuple[int, int, int, int]:
 
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
          bias: torch.Tensor | None = None, c: torch.Tensor | None = None, act: int = ACT_NONE,
-         aux: torch.Tensor | None = None) -> torch.Tensor:
+         aux: torch.Tensor | None = None, out2: torch.Tensor | None = None, colsum: torch.Tensor | None = None,
+         mode: int = EPI_NORMAL) -> torch.Tensor:
     """out = act(alpha * a @ b + bias + c) on the tcgen05 tensor cores.
 
     ``a`` [..., M, K] and ``b`` [..., K, N] are bf16 logical views; either may
     be a transposed view (unit stride on M / N instead of K), which selects the
-    MN-major operand path instead of copying. ``out``/``c``/``aux`` are
-    [..., M, N] with unit column stride. Up to two leading batch dims.
+    MN-major operand path instead of copying. ``out``/``c``/``aux``/``out2``
+    are [..., M, N] with unit column stride. Up to two leading batch dims.
+    ``out2`` receives a bf16 copy of the result, ``colsum`` (fp32, [..., N]
+    per batch, broadcast over size-1 batch strides) accumulates its column
+    sums. ``mode`` selects the row-softmax epilogues (EPI_SOFTMAX: out =
+    softmax(alpha * a @ b); EPI_SOFTMAX_BWD: out = aux * (acc - rowsum(acc *
+    aux)) * alpha).
     """
     _require_cuda(a, b, out, bias, c, aux)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
@@ -104,6 +111,26 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
         args.aux, args.ldx, args.sx1, args.sx2 = aux.data_ptr(), aux.stride(-2), sx1, sx2
     elif act == ACT_DGELU:
         raise ConfigError("gemm: DGELU epilogue needs the saved pre-activation (aux)")
+    if out2 is not None:
+        if tuple(out2.shape) != tuple(out.shape) or out2.dtype != torch.bfloat16 or out2.stride(-1) != 1:
+            raise ShapeError("gemm: out2 must be bf16 with the output shape")
+        _, _, s21, s22 = _batch(out2, nbd)
+        args.D2, args.ld2, args.s21, args.s22 = out2.data_ptr(), out2.stride(-2), s21, s22
+    if colsum is not None:
+        # colsum: [N] (summed over every batch) or [*batch, N] with size-1 dims broadcast
+        if colsum.dtype != torch.float32 or colsum.stride(-1) != 1 or colsum.shape[-1] != N:
+            raise ShapeError("gemm: colsum must be fp32 [..., N] with unit stride")
+        lead = tuple(colsum.shape[:-1])
+        if len(lead) not in (0, nbd):
+            raise ShapeError("gemm: colsum batch dims must match the output's")
+        cs = []
+        for i, n_c in enumerate(lead):
+            if n_c not in (1, out.shape[i]):
+                raise ShapeError("gemm: colsum batch dim must be 1 or the output's")
+            cs.append(colsum.stride(i) if n_c > 1 else 0)
+        cs = [0] * (2 - len(cs)) + cs
+        args.colsum, args.scs1, args.scs2 = colsum.data_ptr(), cs[0], cs[1]
+    args.mode = mode
     args.act = act
     args.alpha = alpha
     prof = _GEMM_PROFILE
@@ -202,7 +229,7 @@ def ln_bwd_stats(dy, x, mean, rstd, gamma, stats):
           _p(stats), _stream(x))
 
 
-def ln_bwd(dy, x, mean, rstd, gamma, stats, h_total, resid, dx, dx2=None, dgamma=None, dbeta=None):
+def ln_bwd(dy, x, mean, rstd, gamma, stats, h_total, resid, dx, dx2=None, dgamma=None, dbeta=None, dsum=None):
     rows, cols, lddy = _rows2d(dy)
     _, _, ldx = _rows2d(x)
     ldr = _rows2d(resid)[2] if resid is not None else 0
@@ -210,7 +237,7 @@ def ln_bwd(dy, x, mean, rstd, gamma, stats, h_total, resid, dx, dx2=None, dgamma
     lddx2 = _rows2d(dx2)[2] if dx2 is not None else 0
     _call("sg_ln_bwd", _p(dy), _dt(dy), lddy, _p(x), _dt(x), ldx, _p(mean), _p(rstd), _p(gamma), rows, cols,
           _p(stats), h_total, _p(resid), _dt(resid), ldr, _p(dx), _dt(dx), lddx, _p(dx2), lddx2, _p(dgamma),
-          _p(dbeta), _stream(x))
+          _p(dbeta), _p(dsum), _stream(x))
 
 
 def colsum(x, out, accumulate=False):

@@ -307,9 +307,28 @@ def _colsum_parts(mesh: Mesh, x: ShardedMatrix, ws: Workspace) -> list:
 
 
 def bias_add_backward(out_grad: ShardedMatrix, ws: Workspace, tag: str = "bias"):
-    """(out_grad, column sums over the mesh column) (layers.py:232-246)."""
+    """(out_grad, column sums over the mesh column) (layers.py:232-246).
+
+    When the producer of ``out_grad`` already accumulated its per-position
+    column sums in its epilogue (``colsum_parts``), only the column
+    all-reduce remains.
+    """
     mesh = out_grad.mesh
-    return out_grad, _vec_grad(mesh, _colsum_parts(mesh, out_grad, ws), tag)
+    parts = getattr(out_grad, "colsum_parts", None)
+    if parts is None:
+        parts = _colsum_parts(mesh, out_grad, ws)
+    else:
+        out_grad.colsum_parts = None  # consumed (all-reduced in place)
+    return out_grad, _vec_grad(mesh, parts, tag)
+
+
+def new_colsum_parts(mesh: Mesh, ws: Workspace, width: int) -> list:
+    """Zeroed per-position fp32 column-sum accumulators for a fused epilogue."""
+    parts = [None] * mesh.p
+    for dev in mesh.local_devs:
+        parts[dev] = ws.empty(dev, (width,), "param_grad", dtype=F32)
+        K.zero(parts[dev])
+    return parts
 
 
 # ------------------------------------------------------------------ layer norm
@@ -364,12 +383,13 @@ def layernorm_forward(x: ShardedMatrix, gamma: RowHostedVector, beta_param: RowH
 
 def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: ModelConfig, ws: Workspace,
                        out_category: str = "free", tag: str = "layernorm", *, resid: ShardedMatrix | None = None,
-                       want_bf16: bool = False):
+                       want_bf16: bool = False, want_colsum: bool = False):
     """dx = rstd (g - mean_h g - x^ mean_h(x^ g)), g = dy gamma; the two row sums in
     one packed all-reduce; (dgamma, dbeta) column-all-reduced (layers.py:310-351).
 
     ``resid`` adds a residual-stream gradient in the same pass; with
-    ``want_bf16`` the result also carries a bf16 twin for the next GEMMs.
+    ``want_bf16`` the result also carries a bf16 twin for the next GEMMs and
+    with ``want_colsum`` its column sums (the upstream bias gradient).
     """
     mesh = out_grad.mesh
     rows, cols = out_grad.block_rows, out_grad.block_cols
@@ -381,6 +401,7 @@ def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: Mode
     if mesh.c > 1:
         mesh.allreduce_row(stats, tag=tag)
     dx, dx16, gb = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
+    dsum = new_colsum_parts(mesh, ws, cols) if want_colsum else [None] * mesh.p
     for dev in mesh.local_devs:
         dx[dev] = ws.empty(dev, (rows, cols), out_category, dtype=F32)
         if want_bf16:
@@ -389,7 +410,8 @@ def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: Mode
         K.zero(gb[dev])
         K.ln_bwd(out_grad.blocks[dev], ctx.x.blocks[dev], ctx.mean[dev], ctx.rstd[dev],
                  ctx.gamma.for_position(mesh, dev), stats[dev], cfg.h,
-                 None if resid is None else resid.blocks[dev], dx[dev], dx16[dev], gb[dev][0], gb[dev][1])
+                 None if resid is None else resid.blocks[dev], dx[dev], dx16[dev], gb[dev][0], gb[dev][1],
+                 dsum[dev])
     flat = [None if g is None else g.reshape(-1) for g in gb]
     mesh.allreduce_col(flat, tag=tag)
     g_sh, b_sh = [None] * mesh.c, [None] * mesh.c
@@ -400,6 +422,8 @@ def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: Mode
     out = ShardedMatrix(mesh, out_grad.global_rows, out_grad.global_cols, dx)
     if want_bf16:
         out.bf16_twin = ShardedMatrix(mesh, out_grad.global_rows, out_grad.global_cols, dx16)
+    if want_colsum:
+        out.colsum_parts = dsum
     return out, RowHostedVector(g_sh), RowHostedVector(b_sh)
 
 
@@ -444,17 +468,26 @@ def _heads_view(blk: torch.Tensor, b_loc: int, s: int, n_loc: int, d: int) -> to
     return torch.as_strided(blk, (b_loc, n_loc, s, d), (s * ld, d, ld, 1))
 
 
+def fused_softmax_ok(cfg: ModelConfig) -> bool:
+    """The row-softmax GEMM epilogues hold a whole score row in TMEM (s <= 512)
+    and need TMA-aligned head slices."""
+    return cfg.s <= 512 and cfg.s % 8 == 0 and cfg.head_dim % 8 == 0
+
+
 def _local_attention(cfg: ModelConfig, mesh: Mesh, qkv_blk, ctx_blk, ws, dev):
     b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
     hb = cfg.h // mesh.c
     q = _heads_view(qkv_blk[:, :hb], b_loc, s, n_loc, d)
     k = _heads_view(qkv_blk[:, hb:2 * hb], b_loc, s, n_loc, d)
     v = _heads_view(qkv_blk[:, 2 * hb:], b_loc, s, n_loc, d)
-    scores = ws.empty(dev, (b_loc * n_loc * s, s), "free", dtype=F32).view(b_loc, n_loc, s, s) \
-        if s % 8 == 0 else padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
-    K.gemm(q, k.transpose(-1, -2), scores, alpha=1.0 / math.sqrt(d))
     probs = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
-    K.softmax_rows(_rows_view(scores), _rows_view(probs))
+    if fused_softmax_ok(cfg):
+        # P = softmax(Q K^T / sqrt(d)) straight out of TMEM: no fp32 score matrix in HBM
+        K.gemm(q, k.transpose(-1, -2), probs, alpha=1.0 / math.sqrt(d), mode=K.EPI_SOFTMAX)
+    else:
+        scores = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
+        K.gemm(q, k.transpose(-1, -2), scores, alpha=1.0 / math.sqrt(d))
+        K.softmax_rows(_rows_view(scores), _rows_view(probs))
     K.gemm(probs, v, _heads_view(ctx_blk, b_loc, s, n_loc, d))
     return probs
 
@@ -509,6 +542,8 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     _, b_dense_grad = bias_add_backward(out_grad, ws)
     dctx = summa_abt(dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
     w_dense_grad = summa_atb(ctx.ctx_mat, dy16, ws, out_category="param_grad")
+    fused = fused_softmax_ok(cfg)
+    bq_parts = new_colsum_parts(mesh, ws, 3 * hb)  # b_qkv gradient fused into dQ / dK / dV epilogues
     dqkv_blocks = [None] * mesh.p
     for dev in mesh.local_devs:
         blk = ctx.qkv.blocks[dev]
@@ -519,14 +554,22 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
         dqkv_blocks[dev] = dq_blk
         dheads = _heads_view(dctx.blocks[dev], b_loc, s, n_loc, d)
         p_mat = ctx.probs[dev]
-        dp = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
-        K.gemm(dheads, v.transpose(-1, -2), dp)                                  # dP = dO V^T
-        K.gemm(p_mat.transpose(-1, -2), dheads, _heads_view(dq_blk[:, 2 * hb:], b_loc, s, n_loc, d))  # dV
+        cs = [bq_parts[dev][i * hb:(i + 1) * hb].view(1, n_loc, d) for i in range(3)]
         ds = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
-        K.softmax_bwd(_rows_view(dp), _rows_view(p_mat), scale, _rows_view(ds))
-        K.gemm(ds, k, _heads_view(dq_blk[:, :hb], b_loc, s, n_loc, d))           # dQ = dS K
-        K.gemm(ds.transpose(-1, -2), q, _heads_view(dq_blk[:, hb:2 * hb], b_loc, s, n_loc, d))  # dK = dS^T Q
+        if fused:
+            # dS = P (dP - rowsum(dP P)) / sqrt(d) straight out of the dP = dO V^T accumulator
+            K.gemm(dheads, v.transpose(-1, -2), ds, alpha=scale, mode=K.EPI_SOFTMAX_BWD, aux=p_mat)
+        else:
+            dp = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
+            K.gemm(dheads, v.transpose(-1, -2), dp)                              # dP = dO V^T
+            K.softmax_bwd(_rows_view(dp), _rows_view(p_mat), scale, _rows_view(ds))
+        K.gemm(p_mat.transpose(-1, -2), dheads, _heads_view(dq_blk[:, 2 * hb:], b_loc, s, n_loc, d),
+               colsum=cs[2])                                                     # dV = P^T dO
+        K.gemm(ds, k, _heads_view(dq_blk[:, :hb], b_loc, s, n_loc, d), colsum=cs[0])          # dQ = dS K
+        K.gemm(ds.transpose(-1, -2), q, _heads_view(dq_blk[:, hb:2 * hb], b_loc, s, n_loc, d),
+               colsum=cs[1])                                                     # dK = dS^T Q
     dqkv = ShardedMatrix(mesh, cfg.b * cfg.s, 3 * cfg.h, dqkv_blocks)
+    dqkv.colsum_parts = bq_parts
     _, b_qkv_grad = bias_add_backward(dqkv, ws)
     x_grad = summa_abt(dqkv, w_qkv, ws, out_category="backward", out_dtype=F32)
     w_qkv_grad = summa_atb(ctx.x_in, dqkv, ws, out_category="param_grad")
@@ -564,9 +607,13 @@ def mlp_forward(x: ShardedMatrix, w1: ShardedMatrix, b1: RowHostedVector, w2: Sh
 def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2: ShardedMatrix,
                  cfg: ModelConfig, ws: Workspace):
     """(dx, dW1, db1, dW2, db2) with GELU' fused into the dAct product (layers.py:494-508)."""
+    mesh = out_grad.mesh
     dy16 = _bf16_of(out_grad, ws)
     _, b2_grad = bias_add_backward(out_grad, ws)
-    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid)
+    b1_parts = new_colsum_parts(mesh, ws, ctx.mid.block_cols)
+    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
+                     colsum=b1_parts)
+    dmid.colsum_parts = b1_parts
     w2_grad = summa_atb(ctx.act, dy16, ws, out_category="param_grad")
     _, b1_grad = bias_add_backward(dmid, ws)
     x_grad = summa_abt(dmid, w1, ws, out_category="backward", out_dtype=F32)
@@ -784,9 +831,11 @@ class TransformerLayer:
         for dev in mesh.local_devs:
             ws.release_forward(dev, (4 if self._last_was_skip else 5) * bsh_p)
         da2, w1_g, b1_g, w2_g, b2_g = mlp_backward(out_grad, saved.mlp, p.w1, p.w2, cfg, ws)
-        dy1, ln2_g, ln2_b = layernorm_backward(da2, saved.ln2, cfg, ws, resid=out_grad, want_bf16=True)
+        dy1, ln2_g, ln2_b = layernorm_backward(da2, saved.ln2, cfg, ws, resid=out_grad, want_bf16=True,
+                                               want_colsum=True)
         da1, wqkv_g, bqkv_g, wd_g, bd_g = attention_backward(dy1, saved.attn, p.w_qkv, p.w_dense, cfg, ws)
-        dx, ln1_g, ln1_b = layernorm_backward(da1, saved.ln1, cfg, ws, resid=dy1, want_bf16=True)
+        dx, ln1_g, ln1_b = layernorm_backward(da1, saved.ln1, cfg, ws, resid=dy1, want_bf16=True,
+                                              want_colsum=True)
         return dx, LayerGrads(w_qkv=wqkv_g, b_qkv=bqkv_g, w_dense=wd_g, b_dense=bd_g, w1=w1_g, b1=b1_g, w2=w2_g,
                               b2=b2_g, ln1_gamma=ln1_g, ln1_beta=ln1_b, ln2_gamma=ln2_g, ln2_beta=ln2_b)
 

@@ -227,7 +227,12 @@ def clone_to_conjunction(x, ws: Workspace):
             blocks.append(None)
             continue
         blocks.append(copy_block(ws.empty(dev, tuple(b.shape), "conjunction", dtype=b.dtype), b))
-    return ShardedMatrix(x.mesh, x.global_rows, x.global_cols, blocks, x.layout)
+    out = ShardedMatrix(x.mesh, x.global_rows, x.global_cols, blocks, x.layout)
+    # fused by-products of the producer stay valid: the bf16 operand copy and the column sums
+    for attr in ("bf16_twin", "colsum_parts"):
+        if getattr(x, attr, None) is not None:
+            setattr(out, attr, getattr(x, attr))
+    return out
 
 
 def checkpointed_forward(layers: Sequence, x0, store: CheckpointStore, ws: Workspace):

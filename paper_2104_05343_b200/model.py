@@ -195,7 +195,12 @@ class MeshModel:
         cfg, mesh = self.cfg, self.mesh
         dl = cross_entropy_backward(saved.ce_ctx, mesh, ws, upstream, in_place=True)
         dlogits = ShardedMatrix(mesh, cfg.b * cfg.s, cfg.v_padded(mesh), dl)
-        dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32)
+        from .layers import new_colsum_parts
+
+        parts = new_colsum_parts(mesh, ws, cfg.h // mesh.c)  # last layer's b2 gradient, fused
+        dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32,
+                      want_bf16=True, colsum=parts)
+        dx.colsum_parts = parts
         table_grad = summa_atb(dlogits, saved.x_final, ws, out_category="param_grad_tied", tag="lmhead")
         if saved.store is not None:
             dx0, layer_grads = checkpointed_backward(self.layers, dx, saved.store, ws, eager_update=eager_update,

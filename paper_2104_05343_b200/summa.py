@@ -146,9 +146,13 @@ def gather(s: ShardedMatrix) -> np.ndarray:
 # ------------------------------------------------------------------ helpers
 
 def as_bf16(mat: ShardedMatrix) -> ShardedMatrix:
-    """The bf16 GEMM-operand view of a sharded matrix (device cast if needed)."""
+    """The bf16 GEMM-operand view of a sharded matrix: itself, its attached
+    ``bf16_twin`` (weights, fused-epilogue gradients) or a device cast."""
     if mat.dtype == BF16:
         return mat
+    twin = getattr(mat, "bf16_twin", None)
+    if twin is not None:
+        return twin
     blocks = []
     for b in mat.blocks:
         if b is None:
@@ -188,7 +192,8 @@ def _check_pair(mesh, a, b, need_a, need_b, what):
 # ------------------------------------------------------------------ SUMMA forms
 
 def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
-             out_dtype: torch.dtype = F32, bias=None, act: int = K.ACT_NONE, aux=None, resid=None) -> ShardedMatrix:
+             out_dtype: torch.dtype = F32, bias=None, act: int = K.ACT_NONE, aux=None, resid=None,
+             want_bf16: bool = False, colsum=None) -> ShardedMatrix:
     """C = A B in c steps: A(i,l) along row i, B(l,j) down column j, C_ij += A_il B_lj.
 
     summa.py:95-116. Optional fused epilogue (bias per output block, GELU with
@@ -205,6 +210,7 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
     out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype)
     fuse_in_out = out_dtype == F32 and act == K.ACT_NONE
     acc = out if (steps == 1 or fuse_in_out) else _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    out2 = _new_blocks(mesh, ws, (m_b, n_b), "free", BF16) if want_bf16 else None
     for l in range(steps):
         a_pan = mesh.bcast_row(l, a16.blocks, (m_b, k_b), BF16, tag=tag)
         src = [None] * mesh.p
@@ -218,14 +224,19 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
             prev = acc[dev] if l > 0 else (None if resid is None else resid.blocks[dev])
             if last:
                 K.gemm(a_pan[dev], b_pan[dev], out[dev], bias=None if bias is None else bias[dev], c=prev, act=act,
-                       aux=None if aux is None else aux.blocks[dev])
+                       aux=None if aux is None else aux.blocks[dev], out2=None if out2 is None else out2[dev],
+                       colsum=None if colsum is None else colsum[dev])
             else:
                 K.gemm(a_pan[dev], b_pan[dev], acc[dev], c=prev)
-    return ShardedMatrix(mesh, a.global_rows, b.global_cols, out)
+    res = ShardedMatrix(mesh, a.global_rows, b.global_cols, out)
+    if out2 is not None:
+        res.bf16_twin = ShardedMatrix(mesh, a.global_rows, b.global_cols, out2)
+    return res
 
 
 def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
-              out_dtype: torch.dtype = F32, act: int = K.ACT_NONE, aux=None, resid=None) -> ShardedMatrix:
+              out_dtype: torch.dtype = F32, act: int = K.ACT_NONE, aux=None, resid=None,
+              colsum=None) -> ShardedMatrix:
     """C = A B^T: B(l,j) down column j, A_ij B_lj^T, row-reduce to (i, l) (summa.py:119-140)."""
     mesh = check_same_mesh(a, b)
     if a.global_cols != b.global_cols:
@@ -249,7 +260,8 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                     bt = b16.block(l, j).t()
                     prev = chain if j > 0 else (None if res_b is None else res_b[d])
                     if j == mesh.c - 1:
-                        K.gemm(a16.block(i, j), bt, out[d], c=prev, act=act, aux=None if aux_b is None else aux_b[d])
+                        K.gemm(a16.block(i, j), bt, out[d], c=prev, act=act, aux=None if aux_b is None else aux_b[d],
+                               colsum=None if colsum is None else colsum[d])
                     else:
                         K.gemm(a16.block(i, j), bt, chain, c=prev)
         return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
@@ -267,6 +279,9 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
             K.gemm(a16.blocks[dev], b_pan[dev].t(), parts[dev])
         mesh.reduce_row_into(l, parts, acc, tag=tag)
     _finish(mesh, acc, out, None, res_b, act, aux_b)
+    if colsum is not None:
+        for dev in mesh.local_devs:
+            K.colsum(out[dev], colsum[dev], accumulate=True)
     return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
 
 

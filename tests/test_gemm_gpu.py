@@ -121,3 +121,46 @@ def test_gemm_large_square(M, N, K):
     k.gemm(a, b, out)
     ref = a.float() @ b.float()
     assert _rel(out, ref) < 1e-2
+
+
+def test_gemm_colsum_and_bf16_copy():
+    k = _k()
+    torch.manual_seed(4)
+    M, N, K = 700, 520, 256
+    a, b = _rand(M, K), _rand(K, N)
+    out = torch.empty(M, N, device="cuda")
+    out2 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.zeros(N, device="cuda")
+    k.gemm(a, b, out, out2=out2, colsum=cs)
+    ref = a.float() @ b.float()
+    assert _rel(out, ref) < 1e-5
+    assert torch.equal(out2, out.to(torch.bfloat16))
+    assert _rel(cs, ref.sum(0)) < 1e-5
+    # batched heads, column sums shared over the batch dim (the b_qkv gradient)
+    bl, nl, s, d = 2, 3, 128, 64
+    x = _rand(bl, nl, s, s)
+    y = _rand(bl, nl, s, d)
+    o = torch.empty(bl, nl, s, d, device="cuda")
+    cs = torch.zeros(1, nl, d, device="cuda")
+    k.gemm(x, y, o, colsum=cs)
+    assert _rel(cs[0], (x.float() @ y.float()).sum(dim=(0, 2))) < 1e-5
+
+
+@pytest.mark.parametrize("s", [64, 200, 512])
+def test_gemm_softmax_epilogues(s):
+    """P = softmax(alpha Q K^T) and dS = P (dP - rowsum(dP P)) alpha, fused in the epilogue."""
+    k = _k()
+    torch.manual_seed(5)
+    bl, nl, d = 2, 4, 64
+    alpha = 1 / math.sqrt(d)
+    q, kk, do, v = (_rand(bl, nl, s, d) for _ in range(4))
+    p = torch.empty(bl, nl, s, s, device="cuda", dtype=torch.bfloat16)
+    k.gemm(q, kk.transpose(-1, -2), p, alpha=alpha, mode=k.EPI_SOFTMAX)
+    ref = torch.softmax(alpha * (q.float() @ kk.float().transpose(-1, -2)), -1)
+    assert (p.float() - ref).abs().max().item() < 4e-3
+    ds = torch.empty_like(p)
+    k.gemm(do, v.transpose(-1, -2), ds, alpha=alpha, mode=k.EPI_SOFTMAX_BWD, aux=p)
+    dp = do.float() @ v.float().transpose(-1, -2)
+    pf = p.float()
+    ref_ds = pf * (dp - (dp * pf).sum(-1, keepdim=True)) * alpha
+    assert _rel(ds, ref_ds) < 1e-2
