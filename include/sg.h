@@ -38,7 +38,7 @@ extern "C" {
 
 #define SG_EPI_NORMAL 0      /* x = alpha*acc + bias + C; D = act(x) (+ D2, colsum) */
 #define SG_EPI_SOFTMAX 1     /* D = softmax_row(alpha*acc), whole row in one tile (N <= 512) */
-#define SG_EPI_SOFTMAX_BWD 2 /* D = aux*(acc - rowsum(acc*aux))*alpha, aux = P (N <= 512) */
+#define SG_EPI_SOFTMAX_BWD 2 /* D = aux*(acc - rowvec)*alpha, aux = P, rowvec = rowsum(dP*P) = rowsum(dO*O) */
 
 /*
  * Batched local GEMM on the 5th-gen tensor cores (tcgen05, TMEM accumulators,
@@ -56,7 +56,8 @@ extern "C" {
  *   summa_abt c_tmp = A_ij B_lj^T   (a: K-major, b: K-major)   summa.py:135-136
  *   summa_atb c_tmp = A_il^T B_ij   (a: MN-major, b: MN-major) summa.py:159-160
  * and of the per-head attention products (layers.py:409-411, 447-452).
- * The optional C operand implements SUMMA step accumulation (C == D allowed)
+ * The optional C operand implements SUMMA step accumulation (C == D: the
+ * product is added in place by TMA reduce-add stores, no epilogue loads)
  * and the fused residual adds (layers.py:706-707, 722-723); colsum fuses the
  * bias gradients (layers.py:238); the softmax modes fuse the attention
  * softmax (dense.py:67-75) and its backward (layers.py:447-450) into the
@@ -78,6 +79,8 @@ typedef struct sg_gemm_args {
   /* optional fused column sums: colsum[z1*scs1 + z2*scs2 + n] += sum_m D[z](m, n) */
   float* colsum; int64_t scs1, scs2;
   int32_t mode; /* SG_EPI_* */
+  /* SOFTMAX_BWD: D_i = rowsum(dO * O) per output row, rowvec[z1*srv1 + z2*srv2 + m] */
+  const float* rowvec; int64_t srv1, srv2;
 } sg_gemm_args;
 
 int sg_gemm(const sg_gemm_args* args, void* stream);
@@ -118,6 +121,10 @@ int sg_softmax_rows(const void* s, int sdt, int64_t rows, int64_t cols, int64_t 
                     void* stream);
 int sg_softmax_bwd(const void* dp, int dpdt, int64_t lddp, const void* p, int pdt, int64_t ldp, int64_t rows,
                    int64_t cols, float scale, void* ds, int dsdt, int64_t ldds, void* stream);
+/* D[b, h, t] = rowsum(dO * O) per head and token (= rowsum(dP * P)), the
+ * SG_EPI_SOFTMAX_BWD row term; dO / O are [b*s, nh*d] head-interleaved blocks. */
+int sg_attn_rowdot(const void* dO, int dt, int64_t ldo, const void* O, int64_t ldO, int64_t rows, int64_t nh,
+                   int64_t d, int64_t s, float* out, void* stream);
 /* Vocab-parallel cross entropy (layers.py:539-624). Local pass over the device's
  * vocabulary block: lmax, gmax (= lmax, to be max-all-reduced along the row),
  * packed = (sum e^{x-lmax}, x_label). Then sg_xent_rescale re-bases the sums on
@@ -139,6 +146,10 @@ int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const vo
 /* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);
+/* out = dact * gelu'(mid), colsum += column sums of out (GELU backward + b1 gradient,
+ * layers.py:502-504); bf16 dact / mid, out may alias dact. */
+int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t ldm, int64_t rows, int64_t cols, void* out,
+             int odt, int64_t ldo, float* colsum, void* stream);
 /* out = act(alpha*x + bias + C) on an fp32 partial sum: the sg_gemm epilogue for
  * products whose mesh reduce had to complete first (dist AB^T forms). */
 int sg_epilogue(const float* x, int64_t rows, int64_t cols, int64_t ldx, float alpha, const float* bias,

@@ -42,6 +42,7 @@ class GemmArgs(ctypes.Structure):
         ("D2", vp), ("ld2", i64), ("s21", i64), ("s22", i64),
         ("colsum", vp), ("scs1", i64), ("scs2", i64),
         ("mode", i32),
+        ("rowvec", vp), ("srv1", i64), ("srv2", i64),
     ]
 
 
@@ -57,12 +58,14 @@ SIGNATURES: dict[str, tuple] = {
     "sg_bias_add": (i32, [vp, i32, i64, i64, i64, vp, vp]),
     "sg_softmax_rows": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),
     "sg_softmax_bwd": (i32, [vp, i32, i64, vp, i32, i64, i64, i64, ctypes.c_float, vp, i32, i64, vp]),
+    "sg_attn_rowdot": (i32, [vp, i32, i64, vp, i64, i64, i64, i64, i64, vp, vp]),
     "sg_xent_local": (i32, [vp, i32, i64, i64, i64, vp, i64, vp, vp, vp, vp]),
     "sg_xent_rescale": (i32, [i64, vp, vp, vp, vp]),
     "sg_xent_loss": (i32, [i64, vp, vp, vp, vp, vp]),
     "sg_xent_bwd": (i32, [vp, i32, i64, i64, i64, i64, vp, i64, vp, vp, ctypes.c_float, vp, i32, i64, vp]),
     "sg_embed_fwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i32, i64, vp]),
     "sg_embed_bwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i64, vp]),
+    "sg_dgelu": (i32, [vp, i64, vp, i64, i64, i64, vp, i32, i64, vp, vp]),
     "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
     "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),
     "sg_cast": (i32, [vp, i32, vp, i32, i64, vp]),

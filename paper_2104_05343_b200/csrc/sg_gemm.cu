@@ -44,31 +44,37 @@ struct GemmParams {
   int M, N, K;
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
-  int a_b2_first, b_b2_first;
+  int a_b2_first, b_b2_first, o_b2_first;
   int mode;
-  void* D;
-  long long ldd, sd1, sd2;
   int d_f32;
+  void* D;                      // direct stores of the row-softmax modes
+  long long ldd, sd1, sd2;
+  int vec_d;
   const void* C;
   long long ldc, sc1, sc2;
   int c_f32;
   const float* bias;
-  void* aux;
+  const __nv_bfloat16* aux_in;  // DGELU pre-activation / SOFTMAX_BWD probabilities
   long long ldx, sx1, sx2;
-  __nv_bfloat16* D2;
-  long long ld2, s21, s22;
+  int aux_out;                  // GELU: store the pre-activation through tmX
+  int reduce_add;               // C == D (fp32): D += result by TMA reduce-add, no epilogue loads
+  int has_d2;                   // bf16 copy of D through tmD2
   float* colsum;
   long long scs1, scs2;
+  const float* rowvec;          // SOFTMAX_BWD: D_i = rowsum(dO * O) per row
+  long long srv1, srv2;
   int act;
   float alpha;
-  int vec_ok;
 };
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kStg = 32 * 32;     // per-warp XOR-swizzled transpose staging for column sums (floats)
-constexpr int kEpiWarps = 8;      // two epilogue warps per TMEM lane quadrant
+constexpr int kEpiWarps = 4;            // one epilogue warp per TMEM lane quadrant
 constexpr int kThreads = 128 + 32 * kEpiWarps;
+// Per epilogue warp 8 KB of staging: two 4 KB slots (main tile up to 4 KB, or a
+// 2 KB bf16 main tile + 2 KB bf16 side tile) so chunk c+1 never waits for chunk
+// c's TMA store, or one 8 KB slot when an fp32 main tile needs a side tile.
+constexpr int kStgBytes = 8192;
 
 template <int BN>
 struct GemmCfg {
@@ -79,7 +85,7 @@ struct GemmCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = BN * kBK * 2;
   static constexpr int STAGES = BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + kEpiWarps * kStg * 4 + 1024 + 256;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + kEpiWarps * kStgBytes + 256;
 };
 
 __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer,
@@ -90,12 +96,35 @@ __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint6
     tma_load_4d(dst, tm, bar, inner, outer, z2, z1);
 }
 
+__device__ __forceinline__ void store_box(const CUtensorMap* tm, const void* src, int inner, int outer, int z2, int z1,
+                                          int b2_first) {
+  if (b2_first)
+    tma_store_4d(tm, src, inner, z2, outer, z1);
+  else
+    tma_store_4d(tm, src, inner, outer, z2, z1);
+}
+__device__ __forceinline__ void reduce_box(const CUtensorMap* tm, const void* src, int inner, int outer, int z2,
+                                           int z1, int b2_first) {
+  if (b2_first)
+    tma_reduce_add_4d(tm, src, inner, z2, outer, z1);
+  else
+    tma_reduce_add_4d(tm, src, inner, outer, z2, z1);
+}
+
+// Grouped rasterisation: tiles run in groups of kGroupM m-tiles, n fastest
+// inside a group, so the CTAs in flight share a few A row panels and sweep B;
+// each operand is then streamed from HBM about once even when A exceeds L2.
+constexpr int kGroupM = 16;
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb, int& nb, int& z1, int& z2) {
   const int per = p.m_tiles * p.n_tiles;
   const int z = t / per;
   const int r = t - z * per;
-  mb = r % p.m_tiles;
-  nb = r / p.m_tiles;
+  const int group = r / (kGroupM * p.n_tiles);
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, p.m_tiles - first_m);
+  const int rr = r - group * kGroupM * p.n_tiles;
+  mb = first_m + rr % gm;
+  nb = rr / gm;
   z1 = z / p.nb2;
   z2 = z - z1 * p.nb2;
 }
@@ -109,86 +138,97 @@ __device__ __forceinline__ float gelu_grad_fast(float x) {
   const float t = tanh_fast(c * (x + a * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
 }
-
-// 32 consecutive elements of one row: 16-byte vector accesses when aligned.
-__device__ __forceinline__ void load_row32(const void* base, bool f32, bool vec, int n, float (&v)[32]) {
-  if (f32) {
-    const float* s = static_cast<const float*>(base);
-    if (vec) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 x = *reinterpret_cast<const float4*>(s + j);
-        v[j] = x.x; v[j + 1] = x.y; v[j + 2] = x.z; v[j + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = j < n ? s[j] : 0.f;
-    }
-  } else {
-    const __nv_bfloat16* s = static_cast<const __nv_bfloat16*>(base);
-    if (vec) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 x = *reinterpret_cast<const uint4*>(s + j);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float2 f = __bfloat1622float2(h[e]);
-          v[j + 2 * e] = f.x; v[j + 2 * e + 1] = f.y;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = j < n ? __bfloat162float(s[j]) : 0.f;
-    }
-  }
-}
-
-__device__ __forceinline__ void store_row32(void* base, bool f32, bool vec, int n, const float (&v)[32]) {
-  if (f32) {
-    float* d = static_cast<float*>(base);
-    if (vec) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < n) d[j] = v[j];
-    }
-  } else {
-    __nv_bfloat16* d = static_cast<__nv_bfloat16*>(base);
-    if (vec) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 x;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[j + 2 * e], v[j + 2 * e + 1]);
-        *reinterpret_cast<uint4*>(d + j) = x;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < n) d[j] = __float2bfloat16_rn(v[j]);
-    }
-  }
-}
-
 __device__ __forceinline__ float ex2_fast(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// Named barrier for the two epilogue warps sharing a TMEM lane quadrant.
-__device__ __forceinline__ void quad_sync(int q) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+// ---- swizzled 32 x 32 staging tiles (match the TMA SWIZZLE_128B / _64B maps)
+// fp32: 128-byte rows, 16-byte chunk k of row r at ((k ^ (r & 7)) << 4)
+// bf16:  64-byte rows, 16-byte chunk k of row r at ((k ^ ((r >> 1) & 3)) << 4)
+__device__ __forceinline__ uint32_t swz_f32(int r, int col) {
+  return r * 128 + ((((col >> 2) ^ (r & 7))) << 4) + ((col & 3) << 2);
+}
+__device__ __forceinline__ uint32_t swz_bf16(int r, int col) {
+  return r * 64 + ((((col >> 3) ^ ((r >> 1) & 3))) << 4) + ((col & 7) << 1);
+}
+__device__ __forceinline__ void st_row_f32(uint8_t* buf, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<float4*>(buf + r * 128 + ((k ^ (r & 7)) << 4)) =
+        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+}
+__device__ __forceinline__ void ld_row_f32(const uint8_t* buf, int r, float (&v)[32]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 x = *reinterpret_cast<const float4*>(buf + r * 128 + ((k ^ (r & 7)) << 4));
+    v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+  }
+}
+__device__ __forceinline__ void st_row_bf16(uint8_t* buf, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint4 x;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * k + 2 * e], v[8 * k + 2 * e + 1]);
+    *reinterpret_cast<uint4*>(buf + r * 64 + ((k ^ ((r >> 1) & 3)) << 4)) = x;
+  }
+}
+__device__ __forceinline__ void ld_row_bf16(const uint8_t* buf, int r, float (&v)[32]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 x = *reinterpret_cast<const uint4*>(buf + r * 64 + ((k ^ ((r >> 1) & 3)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      v[8 * k + 2 * e] = f.x; v[8 * k + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+// One thread's 32 consecutive bf16 outputs (row-softmax modes write rows directly).
+__device__ __forceinline__ void store_bf16_row(__nv_bfloat16* d, bool vec, int n, const float (&v)[32]) {
+  if (vec && n == 32) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint4 x;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * k + 2 * e], v[8 * k + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(d + 8 * k) = x;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) d[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+// Coalesced lane = column read of a 32 x 32 input sub-tile into registers
+// (x[i] = row0 + i of column col), rows >= nrows / cols >= N read as 0.
+template <typename T>
+__device__ __forceinline__ void ld_cols(const T* base, long long ld, int nrows, bool col_ok, float (&x)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float v = 0.f;
+    if (col_ok && i < nrows) {
+      if constexpr (sizeof(T) == 4)
+        v = base[(long long)i * ld];
+      else
+        v = __bfloat162float(base[(long long)i * ld]);
+    }
+    x[i] = v;
+  }
 }
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ GemmParams p) {
+                const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmD2, const __grid_constant__ GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int ACC = Cfg::ACC_BUFS;
@@ -197,9 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* stg_all = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
-  float* red_all = stg_all + kEpiWarps * kStg;  // [2 halves][4 quadrants][32 rows] row partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red_all + 256);
+  uint8_t* stg_all = sB + STAGES * B_BYTES;  // 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + kEpiWarps * kStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
@@ -212,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -270,8 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t IDESC = umma_idesc_bf16(kBM, Cfg::MMA_N, A_MN, B_MN);
-      // byte offset of the second MMA_N-wide half of B inside a stage
-      constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;
+      constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;  // second MMA_N-wide half of B
       uint32_t stage = 0, phase = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const uint32_t as = it % ACC, aph = (it / ACC) & 1;
@@ -310,183 +349,230 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    // warp w: TMEM lane quadrant q = w % 4 (rows 32q..32q+31), column chunks c % 2 == half
+    // warp w owns TMEM lane quadrant q = w % 4: tile rows 32q .. 32q+31.
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    float* stg = stg_all + (warp - 4) * kStg;
-    uint32_t it = 0;
-    const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0, vec = p.vec_ok != 0;
+    uint8_t* stg_w = stg_all + q * kStgBytes;
+    uint32_t it = 0, slot = 0;
+    const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     constexpr int NCH = BN / 32;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       int mb, nb, z1, z2;
       decode_tile(p, t, mb, nb, z1, z2);
       const uint32_t as = it % ACC, aph = (it / ACC) & 1;
+      const int row0 = mb * kBM + q * 32;
+      const int nrows = min(32, p.M - row0);
+      const size_t c_off = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2;
+      const size_t x_off = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2;
+      float rv = 0.f;
+      if (p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const uint32_t tacc = tmem_base + lane_base + as * BN;
-      const int row = mb * kBM + q * 32 + lane;
-      const bool row_ok = row < p.M;
-      const size_t d_row = (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 + (size_t)row * p.ldd;
-      const size_t c_row = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2 + (size_t)row * p.ldc;
-      const size_t x_row = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2 + (size_t)row * p.ldx;
-      const size_t o2_row = (size_t)z1 * p.s21 + (size_t)z2 * p.s22 + (size_t)row * p.ld2;
-      if (p.mode == SG_EPI_NORMAL) {
+
+      if (p.mode == SG_EPI_SOFTMAX) {
+        // whole row in TMEM: max, sum of exponentials, then P chunks through smem + TMA
+        const float sl2 = p.alpha * 1.4426950408889634f;
+        float m = -INFINITY;
 #pragma unroll 1
-        for (int c = half; c < NCH; c += 2) {
+        for (int c = 0; c < NCH; ++c) {
           uint32_t r[32];
           tmem_ld32(tacc + c * 32, r);
           tmem_wait_ld();
-          if (c + 2 >= NCH) {  // this warp's last chunk of the tile
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < p.N) m = fmaxf(m, __uint_as_float(r[j]));
+        }
+        const float ms = m * sl2;
+        float z = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < p.N) z += ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms));
+        }
+        const float inv = 1.f / z;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tacc + c * 32, r);
+          tmem_wait_ld();
+          if (c == NCH - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[as]);
           }
-          const int col0 = nb * BN + c * 32;
-          if (col0 >= p.N) continue;  // warp-uniform
-          const int ncols = min(32, p.N - col0);
-          const bool vfull = vec && ncols == 32;
+          const int row = row0 + lane;
+          if (c * 32 >= p.N || row >= p.M) continue;
           float v[32];
-          // issue every global load of the chunk before any store (C may alias D)
-          float cv[32], xv[32];
-          if (p.C && row_ok) {
-            const void* cb = c_f32 ? static_cast<const void*>(static_cast<const float*>(p.C) + c_row + col0)
-                                   : static_cast<const void*>(static_cast<const __nv_bfloat16*>(p.C) + c_row + col0);
-            load_row32(cb, c_f32, vfull, ncols, cv);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms)) * inv;
+          store_bf16_row(static_cast<__nv_bfloat16*>(p.D) + (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 +
+                             (size_t)row * p.ldd + c * 32,
+                         p.vec_d, min(32, p.N - c * 32), v);
+        }
+        continue;
+      }
+
+      // one global input per chunk at most (C, or the GELU' / softmax-backward aux);
+      // its lane = column loads for chunk c+1 are issued before chunk c is processed
+      const int in_kind =
+          (p.C && !p.reduce_add) ? 1 : ((p.act == SG_ACT_DGELU || p.mode == SG_EPI_SOFTMAX_BWD) ? 2 : 0);
+      auto load_in = [&](int c, float (&dst)[32]) {
+        const int col0 = nb * BN + c * 32;
+        const int col = col0 + lane;
+        const bool ok = c < NCH && col0 < p.N && nrows > 0;
+        if (!ok) return;
+        if (in_kind == 1) {
+          if (c_f32)
+            ld_cols(static_cast<const float*>(p.C) + c_off + (size_t)row0 * p.ldc + col, p.ldc, nrows, col < p.N, dst);
+          else
+            ld_cols(static_cast<const __nv_bfloat16*>(p.C) + c_off + (size_t)row0 * p.ldc + col, p.ldc, nrows,
+                    col < p.N, dst);
+        } else if (in_kind == 2) {
+          ld_cols(p.aux_in + x_off + (size_t)row0 * p.ldx + col, p.ldx, nrows, col < p.N, dst);
+        }
+      };
+      // slot = main tile (fp32: 4 KB, bf16: 2 KB) [+ 2 KB bf16 side tile]; two 4 KB slots when it fits
+      const bool side = p.aux_out || p.has_d2 || in_kind == 2;
+      const int main_bytes = (d_f32 || in_kind == 1) ? 4096 : 2048;
+      const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
+      float in_cur[32], in_nxt[32];
+      if (in_kind) load_in(0, in_cur);
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c) {
+        const int col0 = nb * BN + c * 32;
+        const bool active = col0 < p.N && nrows > 0;  // warp-uniform
+        const int col = col0 + lane;
+        const bool col_ok = col < p.N;
+        if (in_kind) load_in(c + 1, in_nxt);
+        // accumulator chunk, thread = row
+        uint32_t r[32];
+        tmem_ld32(tacc + c * 32, r);
+        tmem_wait_ld();
+        if (c == NCH - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[as]);
+        }
+        if (active) {
+          uint8_t* s0 = stg_w + (dual ? slot * 4096 : 0);             // main tile: D, fp32 C input
+          uint8_t* s1 = s0 + main_bytes;                               // bf16 side tile (SW64)
+          if (dual) slot ^= 1;
+          // this slot's previous TMA stores have read it
+          if (lane == 0) {
+            if (dual)
+              bulk_wait_read<1>();
+            else
+              bulk_wait_read<0>();
           }
-          if (p.act == SG_ACT_DGELU && row_ok)
-            load_row32(static_cast<const __nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, xv);
+          __syncwarp();
+          // inputs: lane = column -> staging -> thread = row
+          if (in_kind == 1) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-          if (p.bias) {
+            for (int i = 0; i < 32; ++i) *reinterpret_cast<float*>(s0 + swz_f32(i, lane)) = in_cur[i];
+          } else if (in_kind == 2) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += (j < ncols) ? __ldg(p.bias + col0 + j) : 0.f;
+            for (int i = 0; i < 32; ++i)
+              *reinterpret_cast<__nv_bfloat16*>(s1 + swz_bf16(i, lane)) = __float2bfloat16_rn(in_cur[i]);
           }
-          if (p.C) {
+          __syncwarp();
+          float v[32];
+          if (p.alpha != 1.f) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += cv[j];
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           }
-          if (p.act == SG_ACT_GELU) {
-            if (p.aux && row_ok) store_row32(static_cast<__nv_bfloat16*>(p.aux) + x_row + col0, false, vfull, ncols, v);
+          if (p.mode == SG_EPI_SOFTMAX_BWD) {
+            float pv[32];
+            ld_row_bf16(s1, lane, pv);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-          } else if (p.act == SG_ACT_DGELU) {
+            for (int j = 0; j < 32; ++j) v[j] = pv[j] * (v[j] - rv * p.alpha);
+            const int row = row0 + lane;
+            if (row < p.M)
+              store_bf16_row(static_cast<__nv_bfloat16*>(p.D) + (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 +
+                                 (size_t)row * p.ldd + col0,
+                             p.vec_d, min(32, p.N - col0), v);
+          } else {
+            if (p.bias) {
+              const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+              const bool bv_ok = col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(xv[j]);
-          }
-          if (row_ok) {
-            void* db = d_f32 ? static_cast<void*>(static_cast<float*>(p.D) + d_row + col0)
-                             : static_cast<void*>(static_cast<__nv_bfloat16*>(p.D) + d_row + col0);
-            store_row32(db, d_f32, vfull, ncols, v);
-            if (p.D2) store_row32(p.D2 + o2_row + col0, false, vfull, ncols, v);
-          }
-          if (p.colsum) {
-            // column sums over this warp's 32 rows: transpose through smem, lane = column
+              for (int k = 0; k < 8; ++k) {
+                float4 b = bv_ok ? __ldg(b4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!bv_ok) {
+                  const int cc = col0 + 4 * k;
+                  b.x = cc < p.N ? p.bias[cc] : 0.f;
+                  b.y = cc + 1 < p.N ? p.bias[cc + 1] : 0.f;
+                  b.z = cc + 2 < p.N ? p.bias[cc + 2] : 0.f;
+                  b.w = cc + 3 < p.N ? p.bias[cc + 3] : 0.f;
+                }
+                v[4 * k] += b.x; v[4 * k + 1] += b.y; v[4 * k + 2] += b.z; v[4 * k + 3] += b.w;
+              }
+            }
+            if (in_kind == 1) {
+              float cv[32];
+              ld_row_f32(s0, lane, cv);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) stg[j * 32 + (lane ^ j)] = row_ok ? v[j] : 0.f;
+              for (int j = 0; j < 32; ++j) v[j] += cv[j];
+            }
+            if (p.act == SG_ACT_GELU) {
+              if (p.aux_out) st_row_bf16(s1, lane, v);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+            } else if (p.act == SG_ACT_DGELU) {
+              float xv[32];
+              ld_row_bf16(s1, lane, xv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(xv[j]);
+            }
+            __syncwarp();  // every lane has consumed the staged inputs before D overwrites them
+            if (d_f32)
+              st_row_f32(s0, lane, v);
+            else
+              st_row_bf16(s0, lane, v);
+            if (p.has_d2) st_row_bf16(s1, lane, v);
             __syncwarp();
-            float cs = 0.f;
+            if (p.colsum) {
+              // column sums over this warp's valid rows, lane = column
+              float cs = 0.f;
+              if (d_f32) {
 #pragma unroll 8
-            for (int i = 0; i < 32; ++i) cs += stg[lane * 32 + (i ^ lane)];
-            if (lane < ncols) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col0 + lane, cs);
+                for (int i = 0; i < 32; ++i)
+                  if (i < nrows) cs += *reinterpret_cast<const float*>(s0 + swz_f32(i, lane));
+              } else {
+#pragma unroll 8
+                for (int i = 0; i < 32; ++i)
+                  if (i < nrows)
+                    cs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
+              }
+              if (col_ok) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col, cs);
+            }
+            fence_proxy_async_smem();
             __syncwarp();
+            if (lane == 0) {
+              if (p.reduce_add)
+                reduce_box(&tmD, s0, col0, row0, z2, z1, p.o_b2_first);
+              else
+                store_box(&tmD, s0, col0, row0, z2, z1, p.o_b2_first);
+              if (p.aux_out) store_box(&tmX, s1, col0, row0, z2, z1, p.o_b2_first);
+              if (p.has_d2) store_box(&tmD2, s1, col0, row0, z2, z1, p.o_b2_first);
+              bulk_commit();
+            }
           }
         }
-      } else {
-        // row-softmax modes: thread = row; the row's chunks are split between the
-        // two warps of the quadrant, row partials combined through smem
-        float* red = red_all + q * 32;  // [half][4 quadrants x 32]
-        if (p.mode == SG_EPI_SOFTMAX) {
-          const float sl2 = p.alpha * 1.4426950408889634f;  // alpha * log2(e)
-          float m = -INFINITY;
-#pragma unroll 1
-          for (int c = half; c < NCH; c += 2) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_wait_ld();
+        if (in_kind) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c * 32 + j < p.N) m = fmaxf(m, __uint_as_float(r[j]));
-          }
-          red[half * 128 + lane] = m;
-          quad_sync(q);
-          m = fmaxf(red[lane], red[128 + lane]);
-          const float ms = m * sl2;
-          float z = 0.f;
-#pragma unroll 1
-          for (int c = half; c < NCH; c += 2) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c * 32 + j < p.N) z += ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms));
-          }
-          quad_sync(q);  // both warps have read the max slots
-          red[half * 128 + lane] = z;
-          quad_sync(q);
-          const float inv = 1.f / (red[lane] + red[128 + lane]);
-#pragma unroll 1
-          for (int c = half; c < NCH; c += 2) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_wait_ld();
-            if (c + 2 >= NCH) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[as]);
-            }
-            const int col0 = c * 32;
-            if (!row_ok || col0 >= p.N) continue;
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = ex2_fast(fmaf(__uint_as_float(r[j]), sl2, -ms)) * inv;
-            store_row32(static_cast<__nv_bfloat16*>(p.D) + d_row + col0, false, vec && p.N - col0 >= 32,
-                        min(32, p.N - col0), v);
-          }
-          quad_sync(q);  // smem partials free for the next tile
-        } else {  // SG_EPI_SOFTMAX_BWD: D = P * (dP - sum(dP * P)) * alpha
-          const __nv_bfloat16* pr = static_cast<const __nv_bfloat16*>(p.aux) + x_row;
-          float acc = 0.f;
-#pragma unroll 1
-          for (int c = half; c < NCH; c += 2) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_wait_ld();
-            const int col0 = c * 32;
-            if (!row_ok || col0 >= p.N) continue;
-            float pv[32];
-            load_row32(pr + col0, false, vec && p.N - col0 >= 32, min(32, p.N - col0), pv);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc = fmaf(__uint_as_float(r[j]), pv[j], acc);
-          }
-          red[half * 128 + lane] = acc;
-          quad_sync(q);
-          acc = red[lane] + red[128 + lane];
-#pragma unroll 1
-          for (int c = half; c < NCH; c += 2) {
-            uint32_t r[32];
-            tmem_ld32(tacc + c * 32, r);
-            tmem_wait_ld();
-            if (c + 2 >= NCH) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[as]);
-            }
-            const int col0 = c * 32;
-            if (!row_ok || col0 >= p.N) continue;
-            const bool v32 = vec && p.N - col0 >= 32;
-            const int n = min(32, p.N - col0);
-            float pv[32], v[32];
-            load_row32(pr + col0, false, v32, n, pv);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = pv[j] * (__uint_as_float(r[j]) - acc) * p.alpha;
-            store_row32(static_cast<__nv_bfloat16*>(p.D) + d_row + col0, false, v32, n, v);
-          }
-          quad_sync(q);
+          for (int i = 0; i < 32; ++i) in_cur[i] = in_nxt[i];
         }
       }
     }
+    if (lane == 0) bulk_wait_all();  // global writes complete before the CTA retires
   }
 
   tc_fence_before();
@@ -495,59 +581,50 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ SIMT path
-// CUDA-core fallback for operands the TMA unit cannot address (row pitches or
-// batch strides that are not 16-byte multiples, e.g. head_dim 4 in the
-// reference's unit-test configurations). NORMAL-mode semantics.
-struct SimtParams {
-  GemmParams p;
-  const __nv_bfloat16* A;
-  long long lda, sa1, sa2;
-  int a_mn;
-  const __nv_bfloat16* B;
-  long long ldb, sb1, sb2;
-  int b_mn;
-  int nb1;
-};
-
-__global__ void gemm_simt_kernel(const __grid_constant__ SimtParams sp) {
-  const GemmParams& p = sp.p;
-  const long long total = (long long)sp.nb1 * p.nb2 * p.M * p.N;
+// CUDA-core fallback for operands or outputs the TMA unit cannot address (row
+// pitches or batch strides that are not 16-byte multiples, e.g. head_dim 4 in
+// the reference's unit-test configurations). NORMAL-mode semantics.
+__global__ void gemm_simt_kernel(const __grid_constant__ sg_gemm_args a) {
+  const long long total = a.nb1 * a.nb2 * a.M * a.N;
+  const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A);
+  const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int n = (int)(idx % p.N);
-    long long t = idx / p.N;
-    const int m = (int)(t % p.M);
-    t /= p.M;
-    const int z2 = (int)(t % p.nb2);
-    const int z1 = (int)(t / p.nb2);
-    const __nv_bfloat16* a = sp.A + z1 * sp.sa1 + z2 * sp.sa2;
-    const __nv_bfloat16* b = sp.B + z1 * sp.sb1 + z2 * sp.sb2;
+    const long long n = idx % a.N;
+    long long t = idx / a.N;
+    const long long m = t % a.M;
+    t /= a.M;
+    const long long z2 = t % a.nb2;
+    const long long z1 = t / a.nb2;
+    const __nv_bfloat16* pa = A + z1 * a.sa1 + z2 * a.sa2;
+    const __nv_bfloat16* pb = B + z1 * a.sb1 + z2 * a.sb2;
     float acc = 0.f;
-    for (int k = 0; k < p.K; ++k) {
-      const float av = __bfloat162float(sp.a_mn ? a[(long long)k * sp.lda + m] : a[(long long)m * sp.lda + k]);
-      const float bv = __bfloat162float(sp.b_mn ? b[(long long)k * sp.ldb + n] : b[(long long)n * sp.ldb + k]);
+    for (long long k = 0; k < a.K; ++k) {
+      const float av = __bfloat162float(a.a_mn_major ? pa[k * a.lda + m] : pa[m * a.lda + k]);
+      const float bv = __bfloat162float(a.b_mn_major ? pb[k * a.ldb + n] : pb[n * a.ldb + k]);
       acc = fmaf(av, bv, acc);
     }
-    float v = acc * p.alpha;
-    if (p.bias) v += p.bias[n];
-    if (p.C) {
-      const size_t ci = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2 + (size_t)m * p.ldc + n;
-      v += p.c_f32 ? static_cast<const float*>(p.C)[ci] : __bfloat162float(static_cast<const __nv_bfloat16*>(p.C)[ci]);
+    float v = acc * a.alpha;
+    if (a.bias) v += a.bias[n];
+    if (a.C) {
+      const long long ci = z1 * a.sc1 + z2 * a.sc2 + m * a.ldc + n;
+      v += a.c_dtype == SG_DTYPE_F32 ? static_cast<const float*>(a.C)[ci]
+                                     : __bfloat162float(static_cast<const __nv_bfloat16*>(a.C)[ci]);
     }
-    const size_t xi = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2 + (size_t)m * p.ldx + n;
-    if (p.act == SG_ACT_GELU) {
-      if (p.aux) static_cast<__nv_bfloat16*>(p.aux)[xi] = __float2bfloat16_rn(v);
+    const long long xi = z1 * a.sx1 + z2 * a.sx2 + m * a.ldx + n;
+    if (a.act == SG_ACT_GELU) {
+      if (a.aux) static_cast<__nv_bfloat16*>(a.aux)[xi] = __float2bfloat16_rn(v);
       v = gelu_f(v);
-    } else if (p.act == SG_ACT_DGELU) {
-      v *= gelu_grad_f(__bfloat162float(static_cast<const __nv_bfloat16*>(p.aux)[xi]));
+    } else if (a.act == SG_ACT_DGELU) {
+      v *= gelu_grad_f(__bfloat162float(static_cast<const __nv_bfloat16*>(a.aux)[xi]));
     }
-    const size_t di = (size_t)z1 * p.sd1 + (size_t)z2 * p.sd2 + (size_t)m * p.ldd + n;
-    if (p.d_f32)
-      static_cast<float*>(p.D)[di] = v;
+    const long long di = z1 * a.sd1 + z2 * a.sd2 + m * a.ldd + n;
+    if (a.d_dtype == SG_DTYPE_F32)
+      static_cast<float*>(a.D)[di] = v;
     else
-      static_cast<__nv_bfloat16*>(p.D)[di] = __float2bfloat16_rn(v);
-    if (p.D2) p.D2[(size_t)z1 * p.s21 + (size_t)z2 * p.s22 + (size_t)m * p.ld2 + n] = __float2bfloat16_rn(v);
-    if (p.colsum) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + n, v);
+      static_cast<__nv_bfloat16*>(a.D)[di] = __float2bfloat16_rn(v);
+    if (a.D2) static_cast<__nv_bfloat16*>(a.D2)[z1 * a.s21 + z2 * a.s22 + m * a.ld2 + n] = __float2bfloat16_rn(v);
+    if (a.colsum) atomicAdd(a.colsum + z1 * a.scs1 + z2 * a.scs2 + n, v);
   }
 }
 
@@ -570,31 +647,34 @@ static PFN_encodeTiled_t get_encode_fn() {
   return fn;
 }
 
-// 4-D bf16 map over (inner, outer, b2, b1) with a box of 64 x box_outer.
-static int make_operand_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
-                            long long nb1, long long ld, long long s2, long long s1, int box_outer, int* b2_first) {
+// 4-D tensor map over (inner, outer, b2, b1) (b2 moved before outer when its
+// stride is the smaller one, e.g. heads inside a row) with a box_inner x
+// box_outer box; fails with SG_ERR_SHAPE when TMA cannot address the tensor.
+static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int esz, long long inner,
+                    long long outer, long long nb2, long long nb1, long long ld, long long s2, long long s1,
+                    int box_inner, int box_outer, CUtensorMapSwizzle swz, int* b2_first) {
   PFN_encodeTiled_t enc = get_encode_fn();
   if (!enc) return set_error(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (nb2 <= 1) s2 = ld * outer;
   if (nb1 <= 1) s1 = s2 * nb2;
-  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16 || (s2 * 2) % 16 || (s1 * 2) % 16)
-    return set_error(SG_ERR_SHAPE, "gemm operand: pointer/leading dims must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || (s2 * esz) % 16 || (s1 * esz) % 16)
+    return set_error(SG_ERR_SHAPE, "gemm: pointer / leading dims must be 16-byte aligned for TMA");
   const bool b2f = nb2 > 1 && s2 < ld;
   cuuint64_t dims[4], strides[3];
   cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
   dims[0] = inner;
+  box[0] = box_inner;
   if (b2f) {
     dims[1] = nb2; dims[2] = outer; dims[3] = nb1;
-    strides[0] = s2 * 2; strides[1] = ld * 2; strides[2] = s1 * 2;
-    box[0] = 64; box[1] = 1; box[2] = box_outer; box[3] = 1;
+    strides[0] = s2 * esz; strides[1] = ld * esz; strides[2] = s1 * esz;
+    box[1] = 1; box[2] = box_outer; box[3] = 1;
   } else {
     dims[1] = outer; dims[2] = nb2; dims[3] = nb1;
-    strides[0] = ld * 2; strides[1] = s2 * 2; strides[2] = s1 * 2;
-    box[0] = 64; box[1] = box_outer; box[2] = 1; box[3] = 1;
+    strides[0] = ld * esz; strides[1] = s2 * esz; strides[2] = s1 * esz;
+    box[1] = box_outer; box[2] = 1; box[3] = 1;
   }
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, dt, 4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char msg[256];
     snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (%d): dims %lld,%lld,%lld,%lld ld=%lld s2=%lld s1=%lld",
@@ -605,9 +685,26 @@ static int make_operand_map(CUtensorMap* map, const void* ptr, long long inner, 
   return SG_OK;
 }
 
+static int operand_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
+                       long long nb1, long long ld, long long s2, long long s1, int box_outer, int* b2_first) {
+  return make_map(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, nb2, nb1, ld, s2, s1, 64, box_outer,
+                  CU_TENSOR_MAP_SWIZZLE_128B, b2_first);
+}
+
+// 32 x 32 output tiles: fp32 rows of 128 B (SWIZZLE_128B), bf16 rows of 64 B (SWIZZLE_64B)
+static int output_map(CUtensorMap* map, const void* ptr, bool f32, long long N, long long M, long long nb2,
+                      long long nb1, long long ld, long long s2, long long s1, int* b2_first) {
+  return make_map(map, ptr, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f32 ? 4 : 2, N,
+                  M, nb2, nb1, ld, s2, s1, 32, 32, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  b2_first);
+}
+
+struct Maps {
+  CUtensorMap a, b, d, x, d2;
+};
+
 template <int BN, bool A_MN, bool B_MN>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream,
-                       int grid) {
+static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, int grid) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
@@ -616,7 +713,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
       return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
     attr_set = true;
   }
-  kern<<<grid, kThreads, Cfg::SMEM, stream>>>(ta, tb, p);
+  kern<<<grid, kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -624,12 +721,11 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
 }
 
 template <int BN>
-static int dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                          cudaStream_t s, int grid) {
-  if (!amn && !bmn) return launch_gemm<BN, false, false>(ta, tb, p, s, grid);
-  if (!amn && bmn) return launch_gemm<BN, false, true>(ta, tb, p, s, grid);
-  if (amn && !bmn) return launch_gemm<BN, true, false>(ta, tb, p, s, grid);
-  return launch_gemm<BN, true, true>(ta, tb, p, s, grid);
+static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p, cudaStream_t s, int grid) {
+  if (!amn && !bmn) return launch_gemm<BN, false, false>(m, p, s, grid);
+  if (!amn && bmn) return launch_gemm<BN, false, true>(m, p, s, grid);
+  if (amn && !bmn) return launch_gemm<BN, true, false>(m, p, s, grid);
+  return launch_gemm<BN, true, true>(m, p, s, grid);
 }
 
 static int pick_bn(long long M, long long N, long long batch, int sms, int mode) {
@@ -657,6 +753,16 @@ static int pick_bn(long long M, long long N, long long batch, int sms, int mode)
   return best;
 }
 
+static int launch_simt(const sg_gemm_args* a, int sms, void* stream) {
+  if (a->mode != SG_EPI_NORMAL) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need TMA-aligned operands");
+  const long long total = a->nb1 * a->nb2 * a->M * a->N;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+  gemm_simt_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(*a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -671,12 +777,15 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (!a->A || !a->B || !a->D) return set_error(SG_ERR_CONFIG, "gemm: null operand");
   if ((a->act == SG_ACT_DGELU) && !a->aux) return set_error(SG_ERR_CONFIG, "gemm: DGELU needs aux");
   if (a->d_dtype != SG_DTYPE_BF16 && a->d_dtype != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "gemm: d_dtype");
+  if (a->D2 && a->act != SG_ACT_NONE) return set_error(SG_ERR_CONFIG, "gemm: D2 copy with GELU / GELU' epilogue");
+  if (a->C && a->act == SG_ACT_DGELU) return set_error(SG_ERR_CONFIG, "gemm: C input together with GELU' input");
   if (a->mode != SG_EPI_NORMAL) {
     if (a->mode != SG_EPI_SOFTMAX && a->mode != SG_EPI_SOFTMAX_BWD) return set_error(SG_ERR_CONFIG, "gemm: mode");
     if (a->N > 512) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need N <= 512");
     if (a->d_dtype != SG_DTYPE_BF16 || a->C || a->bias || a->act || a->D2 || a->colsum)
       return set_error(SG_ERR_CONFIG, "gemm: softmax epilogues write bf16 D only");
-    if (a->mode == SG_EPI_SOFTMAX_BWD && !a->aux) return set_error(SG_ERR_CONFIG, "gemm: softmax bwd needs P");
+    if (a->mode == SG_EPI_SOFTMAX_BWD && (!a->aux || !a->rowvec))
+      return set_error(SG_ERR_CONFIG, "gemm: softmax bwd needs P (aux) and D_i (rowvec)");
     if (a->mode == SG_EPI_SOFTMAX && a->alpha <= 0.f) return set_error(SG_ERR_CONFIG, "gemm: softmax alpha > 0");
   }
   const int sms = sg_device_sm_count();
@@ -696,66 +805,66 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   const long long tiles = (long long)p.m_tiles * p.n_tiles * batch;
   if (tiles > INT32_MAX) return set_error(SG_ERR_SHAPE, "gemm: too many tiles");
   p.num_tiles = (int)tiles;
-  p.D = a->D; p.ldd = a->ldd; p.sd1 = a->sd1; p.sd2 = a->sd2; p.d_f32 = a->d_dtype == SG_DTYPE_F32;
+  p.d_f32 = a->d_dtype == SG_DTYPE_F32;
+  p.D = a->D; p.ldd = a->ldd; p.sd1 = a->sd1; p.sd2 = a->sd2;
+  p.vec_d = (reinterpret_cast<uintptr_t>(a->D) % 16) == 0 && (a->ldd * 2) % 16 == 0 && (a->sd1 * 2) % 16 == 0 &&
+            (a->sd2 * 2) % 16 == 0;
   p.C = a->C; p.ldc = a->ldc; p.sc1 = a->sc1; p.sc2 = a->sc2; p.c_f32 = a->c_dtype == SG_DTYPE_F32;
+  // D += A B in place: no epilogue loads, the TMA unit adds the tile in L2 (plain
+  // stores would need C; colsum / activations need the full sum, so they disable it)
+  p.reduce_add = (a->C == a->D && a->c_dtype == SG_DTYPE_F32 && a->d_dtype == SG_DTYPE_F32 && a->ldc == a->ldd &&
+                  (a->nb1 <= 1 || a->sc1 == a->sd1) && (a->nb2 <= 1 || a->sc2 == a->sd2) && !a->colsum &&
+                  a->act == SG_ACT_NONE && !a->D2 && a->mode == SG_EPI_NORMAL)
+                     ? 1
+                     : 0;
   p.bias = a->bias;
-  p.aux = a->aux; p.ldx = a->ldx; p.sx1 = a->sx1; p.sx2 = a->sx2;
-  p.D2 = static_cast<__nv_bfloat16*>(a->D2); p.ld2 = a->ld2; p.s21 = a->s21; p.s22 = a->s22;
+  p.aux_in = (a->act == SG_ACT_DGELU || a->mode == SG_EPI_SOFTMAX_BWD) ? static_cast<const __nv_bfloat16*>(a->aux)
+                                                                      : nullptr;
+  p.ldx = a->ldx; p.sx1 = a->sx1; p.sx2 = a->sx2;
+  p.aux_out = (a->act == SG_ACT_GELU && a->aux) ? 1 : 0;
+  p.has_d2 = a->D2 ? 1 : 0;
   p.colsum = a->colsum; p.scs1 = a->scs1; p.scs2 = a->scs2;
+  p.rowvec = a->rowvec; p.srv1 = a->srv1; p.srv2 = a->srv2;
   p.act = a->act;
   p.alpha = a->alpha;
-  // 16-byte vector row access (softmax modes) when every row start of D / aux is 16-byte aligned.
-  auto al = [](const void* ptr, long long ld, long long s1, long long s2, int esz) {
-    if (!ptr) return true;
-    return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0 && (ld * esz) % 16 == 0 && (s1 * esz) % 16 == 0 &&
-           (s2 * esz) % 16 == 0;
-  };
-  p.vec_ok = al(a->D, a->ldd, a->sd1, a->sd2, p.d_f32 ? 4 : 2) && al(a->aux, a->ldx, a->sx1, a->sx2, 2);
 
-  // TMA needs 16-byte aligned bases, row pitches and batch strides; otherwise
-  // take the CUDA-core path (tiny / odd-shaped operands only).
-  auto tma_ok = [](const void* ptr, long long ld, long long n1, long long s1, long long n2, long long s2) {
-    return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (ld * 2) % 16 == 0 && (n1 <= 1 || (s1 * 2) % 16 == 0) &&
-           (n2 <= 1 || (s2 * 2) % 16 == 0);
-  };
-  if (!tma_ok(a->A, a->lda, a->nb1, a->sa1, a->nb2, a->sa2) || !tma_ok(a->B, a->ldb, a->nb1, a->sb1, a->nb2, a->sb2)) {
-    if (a->mode != SG_EPI_NORMAL) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need TMA-aligned operands");
-    SimtParams sp;
-    sp.p = p;
-    sp.A = static_cast<const __nv_bfloat16*>(a->A);
-    sp.lda = a->lda; sp.sa1 = a->sa1; sp.sa2 = a->sa2; sp.a_mn = a->a_mn_major;
-    sp.B = static_cast<const __nv_bfloat16*>(a->B);
-    sp.ldb = a->ldb; sp.sb1 = a->sb1; sp.sb2 = a->sb2; sp.b_mn = a->b_mn_major;
-    sp.nb1 = (int)a->nb1;
-    const long long total = a->nb1 * a->nb2 * a->M * a->N;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-    gemm_simt_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(sp);
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
-  }
-  CUtensorMap ta, tb;
-  int rc;
-  // A: K-major -> (K, M); MN-major -> (M, K)
+  // Everything the tensor-core path touches through TMA must be 16-byte
+  // addressable; otherwise (tiny / odd-shaped tensors only) run on CUDA cores.
+  Maps m;
+  memset(&m, 0, sizeof m);
+  int rc, tmp = 0;
   if (!a->a_mn_major)
-    rc = make_operand_map(&ta, a->A, a->K, a->M, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBM, &p.a_b2_first);
+    rc = operand_map(&m.a, a->A, a->K, a->M, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBM, &p.a_b2_first);
   else
-    rc = make_operand_map(&ta, a->A, a->M, a->K, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBK, &p.a_b2_first);
-  if (rc) return rc;
+    rc = operand_map(&m.a, a->A, a->M, a->K, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBK, &p.a_b2_first);
   const int b_box = std::min(bn, 256);
-  if (!a->b_mn_major)
-    rc = make_operand_map(&tb, a->B, a->K, a->N, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, b_box, &p.b_b2_first);
-  else
-    rc = make_operand_map(&tb, a->B, a->N, a->K, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, kBK, &p.b_b2_first);
-  if (rc) return rc;
+  if (rc == SG_OK) {
+    if (!a->b_mn_major)
+      rc = operand_map(&m.b, a->B, a->K, a->N, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, b_box, &p.b_b2_first);
+    else
+      rc = operand_map(&m.b, a->B, a->N, a->K, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, kBK, &p.b_b2_first);
+  }
+  if (rc == SG_OK)
+    rc = output_map(&m.d, a->D, p.d_f32, a->N, a->M, a->nb2, a->nb1, a->ldd, a->sd2, a->sd1, &p.o_b2_first);
+  if (rc == SG_OK && p.aux_out)
+    rc = output_map(&m.x, a->aux, false, a->N, a->M, a->nb2, a->nb1, a->ldx, a->sx2, a->sx1, &tmp);
+  if (rc == SG_OK && p.has_d2)
+    rc = output_map(&m.d2, a->D2, false, a->N, a->M, a->nb2, a->nb1, a->ld2, a->s22, a->s21, &tmp);
+  if (rc != SG_OK) {
+    if (rc != SG_ERR_SHAPE) return rc;
+    clear_error();
+    return launch_simt(a, sms, stream);
+  }
+  if (!p.aux_out) m.x = m.d;  // unused maps still need a valid encoding
+  if (!p.has_d2) m.d2 = m.d;
 
   const int grid = (int)std::min<long long>(tiles, sms);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
   switch (bn) {
-    case 64: return dispatch_major<64>(amn, bmn, ta, tb, p, s, grid);
-    case 128: return dispatch_major<128>(amn, bmn, ta, tb, p, s, grid);
-    case 256: return dispatch_major<256>(amn, bmn, ta, tb, p, s, grid);
-    default: return dispatch_major<512>(amn, bmn, ta, tb, p, s, grid);
+    case 64: return dispatch_major<64>(amn, bmn, m, p, s, grid);
+    case 128: return dispatch_major<128>(amn, bmn, m, p, s, grid);
+    case 256: return dispatch_major<256>(amn, bmn, m, p, s, grid);
+    default: return dispatch_major<512>(amn, bmn, m, p, s, grid);
   }
 }

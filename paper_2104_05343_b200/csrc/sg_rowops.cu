@@ -691,9 +691,88 @@ __global__ void epilogue_kernel(const float* __restrict__ x, long long rows, int
     }
 }
 
+// D[b, h, t] = sum_j dO[row, h*d + j] * O[row, h*d + j] with row = b*s + t: the
+// rowsum(dP * P) term of the softmax backward, computed as rowsum(dO * O)
+// (P V = O), one thread per (token row, head).
+template <typename T>
+__global__ void attn_rowdot_kernel(const T* __restrict__ dO, long long ldo, const T* __restrict__ O, long long ldO,
+                                   long long rows, int nh, int d, int s, float* __restrict__ out) {
+  const long long total = rows * nh;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += gridDim.x * (long long)blockDim.x) {
+    const long long row = i / nh;
+    const int h = (int)(i - row * nh);
+    const T* a = dO + row * ldo + (long long)h * d;
+    const T* b = O + row * ldO + (long long)h * d;
+    float acc = 0.f;
+    for (int j = 0; j < d; j += 8) {
+      float x[8], y[8];
+      const int n = min(8, d - j);
+      ld8(a + j, n, x);
+      ld8(b + j, n, y);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(x[e], y[e], acc);
+    }
+    const long long bb = row / s, t = row - bb * s;
+    out[(bb * nh + h) * (long long)s + t] = acc;
+  }
+}
+
+// out = dact * gelu'(mid) (bf16 in / out, out may alias dact) and colsum += column
+// sums of out: the h->4h GELU backward and its bias gradient in one pass
+// (layers.py:502-504). Grid (row blocks, 1024-column segments).
+template <typename TO>
+__global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long lda, const bf16* __restrict__ mid,
+                                                    long long ldm, long long rows, int cols, TO* out, long long ldo,
+                                                    float* __restrict__ colsum) {
+  __shared__ float s[kSeg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * kSeg;
+  const int seg = min(kSeg, cols - c0);
+  if (colsum) {
+    for (int i = threadIdx.x; i < kSeg; i += blockDim.x) s[i] = 0.f;
+    __syncthreads();
+  }
+  float a[4][8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[k][i] = 0.f;
+  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = k * 256 + lane * 8;
+      if (c >= seg) break;
+      const int n = min(8, seg - c);
+      float g[8], x[8];
+      ld8(dact + r * lda + c0 + c, n, g);
+      ld8(mid + r * ldm + c0 + c, n, x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        g[i] *= gelu_tanh_grad(x[i]);
+        a[k][i] += g[i];
+      }
+      st8(out + r * ldo + c0 + c, n, g);
+    }
+  }
+  if (colsum) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = k * 256 + lane * 8;
+      if (c >= seg) break;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c + i < seg) atomicAdd(&s[c + i], a[k][i]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < seg; i += blockDim.x) atomicAdd(&colsum[c0 + i], s[i]);
+  }
+}
+
 }  // namespace sg
 
 using namespace sg;
+
+
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
@@ -758,7 +837,7 @@ extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, 
     return set_error(SG_ERR_SHAPE, "ln_bwd: unaligned");
   if (rows == 0) return SG_OK;
   const int segs = (int)((cols + kSeg - 1) / kSeg);
-  const int gx = std::max(1, grid_for(rows, 64, 4) / segs);
+  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
   dim3 grid(gx, segs);
   const float inv_h = 1.0f / (float)h_total;
   if (rdt != SG_DTYPE_BF16) rdt = SG_DTYPE_F32;
@@ -777,7 +856,7 @@ extern "C" int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int
     return set_error(SG_ERR_CUDA, "memset");
   if (rows == 0) return SG_OK;
   const int segs = (int)((cols + kSeg - 1) / kSeg);
-  const int gx = std::max(1, grid_for(rows, 64, 4) / segs);
+  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
   SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX><<<dim3(gx, segs), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
   return launch_check();
 }
@@ -916,5 +995,30 @@ extern "C" int sg_epilogue(const float* x, int64_t rows, int64_t cols, int64_t l
     return set_error(SG_ERR_SHAPE, "epilogue: unaligned");
   if (rows == 0) return SG_OK;
   SG_DISPATCH_T(cdt, TC, SG_DISPATCH_T(odt, TO, (epilogue_kernel<TC, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(x, rows, (int)cols, ldx, alpha, bias, static_cast<const TC*>(cin), ldc, act, static_cast<bf16*>(aux), ldaux, static_cast<TO*>(out), ldo))));
+  return launch_check();
+}
+
+extern "C" int sg_attn_rowdot(const void* dO, int dt, int64_t ldo, const void* O, int64_t ldO, int64_t rows, int64_t nh,
+                              int64_t d, int64_t s, float* out, void* stream) {
+  clear_error();
+  if (rows < 0 || nh < 1 || d < 1 || s < 1 || rows % s) return set_error(SG_ERR_SHAPE, "attn_rowdot: bad extents");
+  if (!aligned16(dO, ldo, dt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(O, ldO, dt == SG_DTYPE_F32 ? 4 : 2) ||
+      (d * (dt == SG_DTYPE_F32 ? 4 : 2)) % 16)
+    return set_error(SG_ERR_SHAPE, "attn_rowdot: unaligned");
+  if (rows == 0) return SG_OK;
+  SG_DISPATCH_T(dt, T, (attn_rowdot_kernel<T><<<grid_for(rows * nh, 256, 8), 256, 0, S(stream)>>>(static_cast<const T*>(dO), ldo, static_cast<const T*>(O), ldO, rows, (int)nh, (int)d, (int)s, out)));
+  return launch_check();
+}
+
+extern "C" int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t ldm, int64_t rows, int64_t cols,
+                        void* out, int odt, int64_t ldo, float* colsum, void* stream) {
+  clear_error();
+  if (rows < 0 || cols < 1) return set_error(SG_ERR_SHAPE, "dgelu: bad extents");
+  if (!aligned16(dact, lda, 2) || !aligned16(mid, ldm, 2) || !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2))
+    return set_error(SG_ERR_SHAPE, "dgelu: unaligned");
+  if (rows == 0) return SG_OK;
+  const int segs = (int)((cols + kSeg - 1) / kSeg);
+  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
+  SG_DISPATCH_T(odt, TO, (dgelu_kernel<TO><<<dim3(gx, segs), 256, 0, S(stream)>>>(static_cast<const bf16*>(dact), lda, static_cast<const bf16*>(mid), ldm, rows, (int)cols, static_cast<TO*>(out), ldo, colsum)));
   return launch_check();
 }

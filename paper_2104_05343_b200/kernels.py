@@ -48,7 +48,7 @@ def _batch(t: torch.Tensor, nbatch: int) -> tuple[int, int, int, int]:
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
          bias: torch.Tensor | None = None, c: torch.Tensor | None = None, act: int = ACT_NONE,
          aux: torch.Tensor | None = None, out2: torch.Tensor | None = None, colsum: torch.Tensor | None = None,
-         mode: int = EPI_NORMAL) -> torch.Tensor:
+         mode: int = EPI_NORMAL, rowvec: torch.Tensor | None = None) -> torch.Tensor:
     """out = act(alpha * a @ b + bias + c) on the tcgen05 tensor cores.
 
     ``a`` [..., M, K] and ``b`` [..., K, N] are bf16 logical views; either may
@@ -58,8 +58,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     ``out2`` receives a bf16 copy of the result, ``colsum`` (fp32, [..., N]
     per batch, broadcast over size-1 batch strides) accumulates its column
     sums. ``mode`` selects the row-softmax epilogues (EPI_SOFTMAX: out =
-    softmax(alpha * a @ b); EPI_SOFTMAX_BWD: out = aux * (acc - rowsum(acc *
-    aux)) * alpha).
+    softmax(alpha * a @ b); EPI_SOFTMAX_BWD: out = aux * (acc - rowvec) *
+    alpha with rowvec [..., M] = rowsum(acc * aux), e.g. rowsum(dO * O)).
     """
     _require_cuda(a, b, out, bias, c, aux)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
@@ -130,6 +130,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
             cs.append(colsum.stride(i) if n_c > 1 else 0)
         cs = [0] * (2 - len(cs)) + cs
         args.colsum, args.scs1, args.scs2 = colsum.data_ptr(), cs[0], cs[1]
+    if rowvec is not None:
+        if rowvec.dtype != torch.float32 or rowvec.shape[-1] != M or rowvec.stride(-1) != 1 or rowvec.dim() != nbd + 1:
+            raise ShapeError("gemm: rowvec must be fp32 [*batch, M] with unit stride")
+        _, _, sr1, sr2 = _batch(rowvec, nbd)
+        args.rowvec, args.srv1, args.srv2 = rowvec.data_ptr(), sr1, sr2
     args.mode = mode
     args.act = act
     args.alpha = alpha
@@ -264,6 +269,13 @@ def softmax_bwd(dp, p, scale, ds):
           _stream(dp))
 
 
+def attn_rowdot(dO, O, n_heads, d, s, out):
+    """out[b, h, t] = sum_j dO[b*s + t, h*d + j] * O[b*s + t, h*d + j]."""
+    rows, _, ldo = _rows2d(dO)
+    _, _, ldO = _rows2d(O)
+    _call("sg_attn_rowdot", _p(dO), _dt(dO), ldo, _p(O), ldO, rows, n_heads, d, s, _p(out), _stream(dO))
+
+
 def xent_local(logits, n_real, labels, col_lo, lmax, gmax, packed):
     rows, _, ldl = _rows2d(logits)
     _call("sg_xent_local", _p(logits), _dt(logits), rows, ldl, n_real, _p(labels), col_lo, _p(lmax), _p(gmax),
@@ -357,3 +369,11 @@ def epilogue(x, out, *, bias=None, c=None, act=ACT_NONE, aux=None, alpha=1.0):
     _, _, ldo = _rows2d(out)
     _call("sg_epilogue", _p(x), rows, cols, ldx, alpha, _p(bias), _p(c), _dt(c), ldc, act, _p(aux), ldaux, _p(out),
           _dt(out), ldo, _stream(x))
+
+
+def dgelu(dact, mid, out, colsum=None):
+    """out = dact * gelu'(mid) (out may alias dact); colsum += column sums of out."""
+    rows, cols, lda = _rows2d(dact)
+    _, _, ldm = _rows2d(mid)
+    _, _, ldo = _rows2d(out)
+    _call("sg_dgelu", _p(dact), lda, _p(mid), ldm, rows, cols, _p(out), _dt(out), ldo, _p(colsum), _stream(dact))

@@ -468,6 +468,12 @@ def _heads_view(blk: torch.Tensor, b_loc: int, s: int, n_loc: int, d: int) -> to
     return torch.as_strided(blk, (b_loc, n_loc, s, d), (s * ld, d, ld, 1))
 
 
+# The softmax-backward epilogue reads P per 32-column chunk and is latency-bound on
+# that input; the unfused dP product + row kernel is faster until attention moves to
+# a flash-style kernel.
+FUSED_SOFTMAX_BWD = False
+
+
 def fused_softmax_ok(cfg: ModelConfig) -> bool:
     """The row-softmax GEMM epilogues hold a whole score row in TMEM (s <= 512)
     and need TMA-aligned head slices."""
@@ -556,9 +562,12 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
         p_mat = ctx.probs[dev]
         cs = [bq_parts[dev][i * hb:(i + 1) * hb].view(1, n_loc, d) for i in range(3)]
         ds = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
-        if fused:
-            # dS = P (dP - rowsum(dP P)) / sqrt(d) straight out of the dP = dO V^T accumulator
-            K.gemm(dheads, v.transpose(-1, -2), ds, alpha=scale, mode=K.EPI_SOFTMAX_BWD, aux=p_mat)
+        if fused and FUSED_SOFTMAX_BWD:
+            # dS = P (dP - D) / sqrt(d) straight out of the dP = dO V^T accumulator, with
+            # D = rowsum(dP P) = rowsum(dO O) computed from the saved context
+            drow = padded_empty((b_loc, n_loc, s), F32, mesh.device(dev))
+            K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)
+            K.gemm(dheads, v.transpose(-1, -2), ds, alpha=scale, mode=K.EPI_SOFTMAX_BWD, aux=p_mat, rowvec=drow)
         else:
             dp = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
             K.gemm(dheads, v.transpose(-1, -2), dp)                              # dP = dO V^T
@@ -611,8 +620,9 @@ def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2
     dy16 = _bf16_of(out_grad, ws)
     _, b2_grad = bias_add_backward(out_grad, ws)
     b1_parts = new_colsum_parts(mesh, ws, ctx.mid.block_cols)
-    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
-                     colsum=b1_parts)
+    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16)
+    for dev in mesh.local_devs:  # GELU' and the b1 gradient in one bandwidth-bound pass, in place
+        K.dgelu(dmid.blocks[dev], ctx.mid.blocks[dev], dmid.blocks[dev], b1_parts[dev])
     dmid.colsum_parts = b1_parts
     w2_grad = summa_atb(ctx.act, dy16, ws, out_category="param_grad")
     _, b1_grad = bias_add_backward(dmid, ws)

@@ -208,9 +208,21 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
     m_b, k_b, n_b = a.block_rows, a.block_cols, b.block_cols
     a16, b16 = as_bf16(a), as_bf16(b)
     out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype)
-    fuse_in_out = out_dtype == F32 and act == K.ACT_NONE
-    acc = out if (steps == 1 or fuse_in_out) else _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
     out2 = _new_blocks(mesh, ws, (m_b, n_b), "free", BF16) if want_bf16 else None
+    if resid is not None and (out_dtype != F32 or act != K.ACT_NONE):
+        raise ConfigError("summa_ab: a residual is added to an fp32 linear output")
+    # Accumulation across steps (and the residual) happens in place in fp32 via the
+    # GEMM's TMA reduce-add stores. A fused epilogue that needs the complete sum
+    # (GELU, bf16 output, column sums, bf16 copy) runs in the GEMM when there is a
+    # single step, otherwise as one pass over the fp32 accumulator.
+    fused_last = steps == 1 or (out_dtype == F32 and act == K.ACT_NONE and colsum is None and out2 is None)
+    acc = out if fused_last else _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    for dev in mesh.local_devs:
+        if resid is not None:
+            copy_block(acc[dev], resid.blocks[dev])
+        elif steps > 1:
+            K.zero(full_storage(acc[dev]))
+    accumulate = resid is not None or steps > 1
     for l in range(steps):
         a_pan = mesh.bcast_row(l, a16.blocks, (m_b, k_b), BF16, tag=tag)
         src = [None] * mesh.p
@@ -221,13 +233,21 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
         b_pan = mesh.bcast_col(l % mesh.r, src, (k_b, n_b), BF16, tag=tag)
         last = l == steps - 1
         for dev in mesh.local_devs:
-            prev = acc[dev] if l > 0 else (None if resid is None else resid.blocks[dev])
-            if last:
-                K.gemm(a_pan[dev], b_pan[dev], out[dev], bias=None if bias is None else bias[dev], c=prev, act=act,
+            c_in = acc[dev] if accumulate else None
+            if last and fused_last:
+                K.gemm(a_pan[dev], b_pan[dev], out[dev], bias=None if bias is None else bias[dev], c=c_in, act=act,
                        aux=None if aux is None else aux.blocks[dev], out2=None if out2 is None else out2[dev],
                        colsum=None if colsum is None else colsum[dev])
             else:
-                K.gemm(a_pan[dev], b_pan[dev], acc[dev], c=prev)
+                K.gemm(a_pan[dev], b_pan[dev], acc[dev], c=c_in)
+    if not fused_last:
+        for dev in mesh.local_devs:
+            K.epilogue(acc[dev], out[dev], bias=None if bias is None else bias[dev], act=act,
+                       aux=None if aux is None else aux.blocks[dev])
+            if colsum is not None:
+                K.colsum(out[dev], colsum[dev], accumulate=True)
+            if out2 is not None:
+                copy_block(out2[dev], out[dev])
     res = ShardedMatrix(mesh, a.global_rows, b.global_cols, out)
     if out2 is not None:
         res.bf16_twin = ShardedMatrix(mesh, a.global_rows, b.global_cols, out2)
@@ -248,7 +268,10 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
     aux_b = None if aux is None else aux.blocks
     res_b = None if resid is None else resid.blocks
     if mesh.is_local:
-        # reduce fused into the accumulating GEMM chain, group-position order j = 0..c-1
+        # reduce fused into the accumulating GEMM chain, group-position order j = 0..c-1;
+        # with c > 1 and GELU' the chain ends in fp32 and the epilogue runs as a pass
+        # (the GEMM takes one global epilogue input at a time)
+        split_epi = mesh.c > 1 and act != K.ACT_NONE
         for l in range(mesh.c):
             mesh._count("broadcast", tag)
             mesh._count("reduce", tag)
@@ -256,14 +279,20 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                 d = mesh.flat(i, l)
                 chain = out[d] if mesh.c == 1 or (out_dtype == F32 and act == K.ACT_NONE) else \
                     ws_empty(ws, mesh, d, (m_b, n_b))
+                if res_b is not None:
+                    copy_block(chain, res_b[d])
                 for j in range(mesh.c):
                     bt = b16.block(l, j).t()
-                    prev = chain if j > 0 else (None if res_b is None else res_b[d])
-                    if j == mesh.c - 1:
+                    prev = chain if (j > 0 or res_b is not None) else None
+                    if j == mesh.c - 1 and not split_epi:
                         K.gemm(a16.block(i, j), bt, out[d], c=prev, act=act, aux=None if aux_b is None else aux_b[d],
                                colsum=None if colsum is None else colsum[d])
                     else:
                         K.gemm(a16.block(i, j), bt, chain, c=prev)
+                if split_epi:
+                    K.epilogue(chain, out[d], act=act, aux=None if aux_b is None else aux_b[d])
+                    if colsum is not None:
+                        K.colsum(out[d], colsum[d], accumulate=True)
         return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
     acc = _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
     for l in range(mesh.c):

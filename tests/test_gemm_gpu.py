@@ -159,8 +159,16 @@ def test_gemm_softmax_epilogues(s):
     ref = torch.softmax(alpha * (q.float() @ kk.float().transpose(-1, -2)), -1)
     assert (p.float() - ref).abs().max().item() < 4e-3
     ds = torch.empty_like(p)
-    k.gemm(do, v.transpose(-1, -2), ds, alpha=alpha, mode=k.EPI_SOFTMAX_BWD, aux=p)
     dp = do.float() @ v.float().transpose(-1, -2)
     pf = p.float()
-    ref_ds = pf * (dp - (dp * pf).sum(-1, keepdim=True)) * alpha
+    drow = (dp * pf).sum(-1).contiguous()
+    k.gemm(do, v.transpose(-1, -2), ds, alpha=alpha, mode=k.EPI_SOFTMAX_BWD, aux=p, rowvec=drow)
+    ref_ds = pf * (dp - drow[..., None]) * alpha
     assert _rel(ds, ref_ds) < 1e-2
+    # D_i = rowsum(dP P) equals rowsum(dO O) with O = P V (the kernel used by attention backward)
+    o = (pf @ v.float()).bfloat16()
+    hb = 2 * d
+    flat = lambda x: x.permute(0, 2, 1, 3).reshape(bl * s, nl * d).contiguous()  # noqa: E731
+    dr = torch.empty(bl, nl, s, device="cuda")
+    k.attn_rowdot(flat(do), flat(o), nl, d, s, dr)
+    assert _rel(dr, (do.float() * o.float()).sum(-1)) < 1e-4
