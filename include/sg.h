@@ -121,6 +121,19 @@ int sg_softmax_rows(const void* s, int sdt, int64_t rows, int64_t cols, int64_t 
                     void* stream);
 int sg_softmax_bwd(const void* dp, int dpdt, int64_t lddp, const void* p, int pdt, int64_t ldp, int64_t rows,
                    int64_t cols, float scale, void* ds, int dsdt, int64_t ldds, void* stream);
+/* Flash-style attention forward for one mesh position (layers.py:404-416):
+ * qkv is the [b*s, 3*nh*d] QKV block (columns [Q heads | K heads | V heads]),
+ * out the [b*s, nh*d] context block, lse [b, nh, s] the natural log-sum-exp
+ * of the scaled scores; d in {64, 128}. The probabilities are never stored. */
+int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_t s, int64_t nh, int64_t d, void* out,
+                      int64_t ldo, float* lse, void* stream);
+/* Flash-style attention backward (d = 64): recomputes P from lse, writes dK, dV
+ * (bf16) into the K / V column ranges of the [b*s, 3*nh*d] gradient block dqkv and
+ * ADDS dQ into the fp32 accumulator dq_acc [b*s, >= nh*d] (zero it first);
+ * drow = rowsum(dO * O) from sg_attn_rowdot. */
+int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
+                      const float* drow, int64_t b, int64_t s, int64_t nh, int64_t d, float* dq_acc, int64_t lddq,
+                      void* dqkv, int64_t ldg, void* stream);
 /* D[b, h, t] = rowsum(dO * O) per head and token (= rowsum(dP * P)), the
  * SG_EPI_SOFTMAX_BWD row term; dO / O are [b*s, nh*d] head-interleaved blocks. */
 int sg_attn_rowdot(const void* dO, int dt, int64_t ldo, const void* O, int64_t ldO, int64_t rows, int64_t nh,

@@ -1,0 +1,598 @@
+// Flash-style multi-head attention forward on the 5th-gen tensor cores
+// (layers.py:404-416 of the reference: softmax(Q K^T / sqrt(d)) V per head, no
+// mask), without materialising the [b, n, s, s] probability matrix.
+//
+// One CTA = (128 query rows, head, batch); 256 threads:
+//   warp 0   TMA producer: Q once, then K_j / V_j key blocks (double-buffered)
+//   warp 1   MMA issuer: S_j = Q K_j^T (128 x 128 x d) into TMEM, then
+//            PV_j = P_j V_j (128 x d x 128) with P_j from shared memory
+//   warp 2   TMEM allocator (256 columns: S | PV)
+//   warps 4-7 softmax, thread = query row: online max / sum in the log2
+//            domain, P_j -> swizzled smem (the UMMA A operand), O kept in
+//            registers and rescaled per block (O = O * alpha + PV_j)
+// Outputs: O (bf16) straight into the interleaved context block and the row
+// log-sum-exp (fp32) for the backward. Q/K/V are read in place from the QKV
+// block through 4-D TMA maps (no head split copies).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "sg.h"
+#include "sg_internal.h"
+#include "sg_ptx.cuh"
+#include "sg_tmap.h"
+
+namespace sg {
+
+struct FlashFwdParams {
+  int s;            // sequence length (keys = queries)
+  int nh;           // heads in the block
+  int q_b2_first, k_b2_first, v_b2_first;
+  float scale_log2; // log2(e) / sqrt(d)
+  __nv_bfloat16* O;
+  long long ldo;    // row pitch of the context block
+  float* lse;       // [b, nh, s] natural-log log-sum-exp of the scaled scores
+};
+
+constexpr int kQB = 128;   // query rows per CTA
+constexpr int kKB = 128;   // keys per block
+
+template <int HD>
+struct FlashCfg {
+  static constexpr int ATOMS = HD / 64;                    // 64-wide swizzle atoms along d
+  static constexpr uint32_t Q_BYTES = kQB * HD * 2;
+  static constexpr uint32_t KV_BYTES = kKB * HD * 2;
+  static constexpr uint32_t P_BYTES = kQB * kKB * 2;       // 2 atoms of 64 keys
+  // no alignment slack: the dynamic window starts 1024-aligned (no static smem), which
+  // keeps d = 64 at 112 KB + barriers -> two CTAs per SM
+  static constexpr size_t SMEM = Q_BYTES + 4 * KV_BYTES + P_BYTES + 128;
+  static constexpr uint32_t TMEM_COLS = 128 + (HD < 128 ? 128 : HD);  // S | PV (power of two)
+};
+
+__device__ __forceinline__ void tma4(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer, int z2,
+                                     int z1, int b2f) {
+  if (b2f)
+    tma_load_4d(dst, tm, bar, inner, z2, outer, z1);
+  else
+    tma_load_4d(dst, tm, bar, inner, outer, z2, z1);
+}
+
+__device__ __forceinline__ float ex2f_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
+    flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p) {
+  using Cfg = FlashCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::Q_BYTES;            // 2 slots
+  uint8_t* sV = sK + 2 * Cfg::KV_BYTES;       // 2 slots
+  uint8_t* sP = sV + 2 * Cfg::KV_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* v_full = bars + 3;   // [2]
+  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* s_full = bars + 7;
+  uint64_t* p_full = bars + 8;
+  uint64_t* pv_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int nkb = (p.s + kKB - 1) / kKB;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(pv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_pv = tmem + 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < Cfg::ATOMS; ++a)
+        tma4(&tmQ, sQ + a * kQB * 128, q_full, a * 64, qb * kQB, h, b, p.q_b2_first);
+      for (int j = 0; j < nkb; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[slot], Cfg::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a)
+          tma4(&tmK, sK + slot * Cfg::KV_BYTES + a * kKB * 128, &k_full[slot], a * 64, j * kKB, h, b, p.k_b2_first);
+        mbar_arrive_expect_tx(&v_full[slot], Cfg::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < Cfg::ATOMS; ++a)
+          tma4(&tmV, sV + slot * Cfg::KV_BYTES + a * kKB * 128, &v_full[slot], a * 64, j * kKB, h, b, p.v_b2_first);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
+      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, HD, false, true);   // P K-major, V MN-major
+      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int slot = j & 1;
+        mbar_wait(&k_full[slot], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK + slot * Cfg::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kQB * 128) + (kk & 3) * 32;  // atom, 16-element step inside it
+          umma_bf16(t_s, umma_desc_sw128(q_base + off, 0, 1024), umma_desc_sw128(k_base + off, 0, 1024), IDESC_S,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        const int slot = j & 1;
+        mbar_wait(p_full, j & 1);  // P_j in smem (and S_j fully read)
+        mbar_wait(&v_full[slot], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sV + slot * Cfg::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < kKB / 16; ++kk) {
+          // A = P [128 q x 128 keys] K-major: atom kk/4, 32 B per 16 keys inside it.
+          // B = V [128 keys x HD] MN-major: 16 key rows = 2048 B, 64-wide d chunks kKB*128 B apart.
+          const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * (kQB * 128) + (kk & 3) * 32, 0, 1024);
+          const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024);
+          umma_bf16(t_pv, ad, bd, IDESC_PV, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(pv_full);
+        umma_commit(&kv_empty[slot]);
+        if (j + 1 < nkb) issue_s(j + 1);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax / output
+    const int q = warp & 3;
+    const int r = q * 32 + lane;               // row inside the 128-row tile
+    const int qrow = qb * kQB + r;             // query position
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    float o[HD];
+#pragma unroll
+    for (int i = 0; i < HD; ++i) o[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      const int kvalid = min(kKB, p.s - j * kKB);
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      float bm = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < kKB / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_s + lane_base + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kvalid) bm = fmaxf(bm, __uint_as_float(v[i]));
+      }
+      const float m_new = fmaxf(m, bm * p.scale_log2);
+      const float alpha = ex2f_fast(m - m_new);  // 0 on the first block (m = -inf)
+      float psum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < kKB / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_s + lane_base + c * 32, v);
+        tmem_wait_ld();
+        float pv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          pv[i] = (c * 32 + i < kvalid) ? ex2f_fast(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
+          psum += pv[i];
+        }
+        // P row r, keys [32c, 32c+32): atom c/2, 16-byte chunks ((c%2)*4 .. +3) swizzled by r % 8
+        uint8_t* prow = sP + (c >> 1) * (kQB * 128) + r * 128;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 x;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hh[e] = __floats2bfloat162_rn(pv[8 * k + 2 * e], pv[8 * k + 2 * e + 1]);
+          const int chunk = (c & 1) * 4 + k;
+          *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = x;
+        }
+      }
+      l = l * alpha + psum;
+      m = m_new;
+      // P visible to the tensor core (async proxy); S slot fully read
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // O = O * alpha + P_j V_j
+      mbar_wait(pv_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_pv + lane_base + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[c * 32 + i] = fmaf(o[c * 32 + i], alpha, __uint_as_float(v[i]));
+      }
+      tc_fence_before();
+    }
+    if (qrow < p.s) {
+      const float inv = 1.f / l;
+      __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * HD;
+#pragma unroll
+      for (int k = 0; k < HD / 8; ++k) {
+        uint4 x;
+        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hh[e] = __floats2bfloat162_rn(o[8 * k + 2 * e] * inv, o[8 * k + 2 * e + 1] * inv);
+        *reinterpret_cast<uint4*>(dst + 8 * k) = x;
+      }
+      if (p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m + __log2f(l)) * 0.6931471805599453f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+}
+
+template <int HD>
+static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p,
+                      int b, cudaStream_t stream) {
+  using Cfg = FlashCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(flash_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) !=
+        cudaSuccess)
+      return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
+    attr = true;
+  }
+  dim3 grid((p.s + kQB - 1) / kQB, p.nh, b);
+  flash_fwd_kernel<HD><<<grid, 256, Cfg::SMEM, stream>>>(q, k, v, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_t s, int64_t nh, int64_t d,
+                                 void* out, int64_t ldo, float* lse, void* stream) {
+  clear_error();
+  if (b < 1 || s < 1 || nh < 1 || (d != 64 && d != 128)) return set_error(SG_ERR_SHAPE, "flash fwd: d must be 64 or 128");
+  if (ldq < 3 * nh * d || ldo < nh * d) return set_error(SG_ERR_SHAPE, "flash fwd: leading dimensions");
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo * 2) % 16) return set_error(SG_ERR_SHAPE, "flash fwd: unaligned");
+  const __nv_bfloat16* base = static_cast<const __nv_bfloat16*>(qkv);
+  const long long hb = nh * d;
+  CUtensorMap tq, tk, tv;
+  FlashFwdParams p{};
+  p.s = (int)s;
+  p.nh = (int)nh;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)d);
+  p.O = static_cast<__nv_bfloat16*>(out);
+  p.ldo = ldo;
+  p.lse = lse;
+  // [b, s, nh, d] views of the Q / K / V column ranges of the QKV block, box 64 x 128 rows
+  int rc = tmap_bf16_4d(&tq, base, d, s, nh, b, ldq, d, s * ldq, 64, kQB, &p.q_b2_first);
+  if (!rc) rc = tmap_bf16_4d(&tk, base + hb, d, s, nh, b, ldq, d, s * ldq, 64, kKB, &p.k_b2_first);
+  if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, kKB, &p.v_b2_first);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return d == 64 ? launch_fwd<64>(tq, tk, tv, p, (int)b, st) : launch_fwd<128>(tq, tk, tv, p, (int)b, st);
+}
+
+// ============================================================================
+// Backward (d = 64): one CTA = (128-key block, head, batch), loop over query
+// blocks (FlashAttention-2 order). Per query block:
+//   S  = Q K^T,  dP = dO V^T                       (TMEM, M = queries)
+//   P  = exp(S / sqrt(d) - lse),  dS = P (dP - D) / sqrt(d)   (warps 4-7 -> smem)
+//   dV += P^T dO,  dK += dS^T Q                     (TMEM accumulators, M = keys)
+//   dQ  = dS K  -> fp32 accumulator via TMA reduce-add (one CTA per key block adds)
+// with D = rowsum(dO * O) precomputed (sg_attn_rowdot). P / dS are stored once,
+// [queries x keys] in the SWIZZLE_128B layout that is both the K-major A
+// operand of dS K and the MN-major A operand of P^T dO / dS^T Q.
+// ============================================================================
+namespace sg {
+
+struct FlashBwdParams {
+  int s, nh;
+  int q_b2_first, k_b2_first, v_b2_first, do_b2_first, dq_b2_first;
+  float scale, scale_log2;
+  const float* lse;   // [b, nh, s]
+  const float* drow;  // [b, nh, s]
+  __nv_bfloat16* dK;  // [b*s, ldg] head columns h*64
+  __nv_bfloat16* dV;
+  long long ldg;
+};
+
+constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
+
+__global__ void __launch_bounds__(256, 1)
+    flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                     const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* sK = smem;                 // 16 KB
+  uint8_t* sV = sK + kT64;            // 16 KB
+  uint8_t* sQ = sV + kT64;            // 2 slots
+  uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
+  uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
+  uint8_t* sDS = sP + 2 * kT64;       // 32 KB
+  uint8_t* sStg = sDS + 2 * kT64;     // 4 warps x 8 KB dQ staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* dq_full = bars + 7;
+  uint64_t* acc_full = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int nqb = (p.s + 127) / 128;
+  const int kvalid = min(128, p.s - kb * 128);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 4);
+    mbar_init(dq_full, 1);
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * kT64);
+      tma4(&tmK, sK, kv_full, 0, kb * 128, h, b, p.k_b2_first);
+      tma4(&tmV, sV, kv_full, 0, kb * 128, h, b, p.v_b2_first);
+      for (int i = 0; i < nqb; ++i) {
+        const int slot = i & 1;
+        mbar_wait(&qd_empty[slot], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
+        tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
+        tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
+      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
+      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, false, true);    // dQ: A = dS, B = K
+      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+      mbar_wait(kv_full, 0);
+      for (int i = 0; i < nqb; ++i) {
+        const int slot = i & 1;
+        mbar_wait(&qd_full[slot], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
+          umma_bf16(t_s, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
+                    ID_SQ, kk > 0 ? 1u : 0u);
+          umma_bf16(t_dp, umma_desc_sw128(do_base + kk * 32, 0, 1024), umma_desc_sw128(v_base + kk * 32, 0, 1024),
+                    ID_SQ, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+        mbar_wait(ds_full, i & 1);  // P, dS in smem; S / dP read
+        tc_fence_after();
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
+          const uint32_t acc = (i | kq) != 0 ? 1u : 0u;
+          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, 2 * 8192, 1024),
+                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
+          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, 2 * 8192, 1024),
+                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
+        }
+        umma_commit(&qd_empty[slot]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
+          umma_bf16(t_dq, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
+                    umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(dq_full);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sStg + q * 8192;
+    const size_t head_off = ((size_t)b * p.nh + h) * p.s;
+    for (int i = 0; i < nqb; ++i) {
+      const int qrow = i * 128 + r;
+      const bool qok = qrow < p.s;
+      const float lse2 = qok ? p.lse[head_off + qrow] * 1.4426950408889634f : 0.f;
+      const float dd = qok ? p.drow[head_off + qrow] : 0.f;
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld32(t_s + lane_base + c * 32, sv);
+        tmem_ld32(t_dp + lane_base + c * 32, dv);
+        tmem_wait_ld();
+        float pr[32], ds[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = qok && (c * 32 + j) < kvalid;
+          pr[j] = ok ? ex2f_fast(fmaf(__uint_as_float(sv[j]), p.scale_log2, -lse2)) : 0.f;
+          ds[j] = pr[j] * (__uint_as_float(dv[j]) - dd) * p.scale;
+        }
+        uint8_t* prow = sP + (c >> 1) * kT64 + r * 128;
+        uint8_t* drow_ = sDS + (c >> 1) * kT64 + r * 128;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 x, y;
+          __nv_bfloat162* hx = reinterpret_cast<__nv_bfloat162*>(&x);
+          __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hx[e] = __floats2bfloat162_rn(pr[8 * k + 2 * e], pr[8 * k + 2 * e + 1]);
+            hy[e] = __floats2bfloat162_rn(ds[8 * k + 2 * e], ds[8 * k + 2 * e + 1]);
+          }
+          const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
+          *reinterpret_cast<uint4*>(prow + (chunk << 4)) = x;
+          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) = y;
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      // dQ tile of this query block: TMEM -> fp32 staging -> TMA reduce-add
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_dq + lane_base + c * 32, v);
+        tmem_wait_ld();
+        uint8_t* box = stg + c * 4096;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
+                          __uint_as_float(v[4 * k + 3]));
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (p.dq_b2_first)
+            tma_reduce_add_4d(&tmDQ, stg + c * 4096, c * 32, h, i * 128 + q * 32, b);
+          else
+            tma_reduce_add_4d(&tmDQ, stg + c * 4096, c * 32, i * 128 + q * 32, h, b);
+        }
+        bulk_commit();
+      }
+    }
+    // dK, dV of this key block: TMEM (row = key) -> bf16 rows of the dQKV block
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int key = kb * 128 + r;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tsrc = (which == 0 ? t_dk : t_dv) + lane_base;
+      __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tsrc + c * 32, v);
+        tmem_wait_ld();
+        if (key < p.s) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 x;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hh[e] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e]), __uint_as_float(v[8 * k + 2 * e + 1]));
+            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
+          }
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace sg
+
+extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
+                                 const float* drow, int64_t b, int64_t s, int64_t nh, int64_t d, float* dq_acc,
+                                 int64_t lddq, void* dqkv, int64_t ldg, void* stream) {
+  using namespace sg;
+  clear_error();
+  if (b < 1 || s < 1 || nh < 1 || d != 64) return set_error(SG_ERR_SHAPE, "flash bwd: d must be 64");
+  if (ldq < 3 * nh * d || lddo < nh * d || lddq < nh * d || ldg < 3 * nh * d)
+    return set_error(SG_ERR_SHAPE, "flash bwd: leading dimensions");
+  if ((reinterpret_cast<uintptr_t>(dqkv) & 15) || (ldg * 2) % 16) return set_error(SG_ERR_SHAPE, "flash bwd: unaligned");
+  const __nv_bfloat16* base = static_cast<const __nv_bfloat16*>(qkv);
+  const long long hb = nh * d;
+  CUtensorMap tq, tk, tv, tdo, tdq;
+  FlashBwdParams p{};
+  p.s = (int)s;
+  p.nh = (int)nh;
+  p.scale = 1.f / sqrtf((float)d);
+  p.scale_log2 = 1.4426950408889634f * p.scale;
+  p.lse = lse;
+  p.drow = drow;
+  p.dK = static_cast<__nv_bfloat16*>(dqkv) + hb;
+  p.dV = static_cast<__nv_bfloat16*>(dqkv) + 2 * hb;
+  p.ldg = ldg;
+  int rc = tmap_bf16_4d(&tq, base, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.q_b2_first);
+  if (!rc) rc = tmap_bf16_4d(&tk, base + hb, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.k_b2_first);
+  if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.v_b2_first);
+  if (!rc) rc = tmap_bf16_4d(&tdo, dout, d, s, nh, b, lddo, d, s * lddo, 64, 128, &p.do_b2_first);
+  if (!rc) rc = tmap_f32_tile_4d(&tdq, dq_acc, d, s, nh, b, lddq, d, s * lddq, &p.dq_b2_first);
+  if (rc) return rc;
+  constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+      return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
+    attr = true;
+  }
+  dim3 grid((unsigned)((s + 127) / 128), (unsigned)nh, (unsigned)b);
+  flash_bwd_kernel<<<grid, 256, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}

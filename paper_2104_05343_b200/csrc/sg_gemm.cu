@@ -37,6 +37,7 @@
 #include "sg.h"
 #include "sg_internal.h"
 #include "sg_ptx.cuh"
+#include "sg_tmap.h"
 
 namespace sg {
 
@@ -683,6 +684,18 @@ static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, i
   }
   *b2_first = b2f ? 1 : 0;
   return SG_OK;
+}
+
+int tmap_bf16_4d(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2, long long nb1,
+                 long long ld, long long s2, long long s1, int box_inner, int box_outer, int* b2_first) {
+  return make_map(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, nb2, nb1, ld, s2, s1, box_inner,
+                  box_outer, CU_TENSOR_MAP_SWIZZLE_128B, b2_first);
+}
+
+int tmap_f32_tile_4d(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
+                     long long nb1, long long ld, long long s2, long long s1, int* b2_first) {
+  return make_map(map, ptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, inner, outer, nb2, nb1, ld, s2, s1, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_128B, b2_first);
 }
 
 static int operand_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,

@@ -377,3 +377,20 @@ def dgelu(dact, mid, out, colsum=None):
     _, _, ldm = _rows2d(mid)
     _, _, ldo = _rows2d(out)
     _call("sg_dgelu", _p(dact), lda, _p(mid), ldm, rows, cols, _p(out), _dt(out), ldo, _p(colsum), _stream(dact))
+
+
+def flash_attn_fwd(qkv, b, s, n_heads, d, out, lse=None):
+    """Flash-style attention forward: qkv [b*s, 3*nh*d] block -> out [b*s, nh*d], lse [b, nh, s]."""
+    _, _, ldq = _rows2d(qkv)
+    _, _, ldo = _rows2d(out)
+    _call("sg_flash_attn_fwd", _p(qkv), ldq, b, s, n_heads, d, _p(out), ldo, _p(lse), _stream(out))
+
+
+def flash_attn_bwd(qkv, dout, lse, drow, b, s, n_heads, d, dq_acc, dqkv):
+    """dK, dV -> dqkv[:, nh*d:], dQ added into dq_acc (fp32, zeroed by the caller)."""
+    _, _, ldq = _rows2d(qkv)
+    _, _, lddo = _rows2d(dout)
+    _, _, lddq = _rows2d(dq_acc)
+    _, _, ldg = _rows2d(dqkv)
+    _call("sg_flash_attn_bwd", _p(qkv), ldq, _p(dout), lddo, _p(lse), _p(drow), b, s, n_heads, d, _p(dq_acc), lddq,
+          _p(dqkv), ldg, _stream(dqkv))

@@ -1,0 +1,63 @@
+"""Flash-style attention kernels vs a plain PyTorch fp32 reference."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(qkv, b, s, nh, d):
+    hb = nh * d
+    q, k, v = (qkv[:, i * hb:(i + 1) * hb].float().view(b, s, nh, d).permute(0, 2, 1, 3) for i in range(3))
+    sc = (q @ k.transpose(-1, -2)) / math.sqrt(d)
+    p = torch.softmax(sc, -1)
+    o = (p @ v).permute(0, 2, 1, 3).reshape(b * s, hb)
+    lse = torch.logsumexp(sc, -1)
+    return o, lse, p
+
+
+@pytest.mark.parametrize("b,s,nh,d", [(2, 512, 4, 64), (3, 200, 2, 64), (1, 384, 2, 128), (2, 1024, 2, 64),
+                                      (1, 2048, 2, 128), (2, 64, 3, 64)])
+def test_flash_forward(b, s, nh, d):
+    from paper_2104_05343_b200 import kernels as K
+
+    torch.manual_seed(0)
+    hb = nh * d
+    qkv = torch.randn(b * s, 3 * hb, device="cuda").bfloat16()
+    out = torch.empty(b * s, hb, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, nh, s, device="cuda")
+    K.flash_attn_fwd(qkv, b, s, nh, d, out, lse)
+    o, l, _ = _ref(qkv, b, s, nh, d)
+    assert (out.float() - o).abs().max().item() / o.abs().max().item() < 1e-2
+    assert (lse - l).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("b,s,nh,d", [(2, 512, 4, 64), (3, 200, 2, 64), (2, 1024, 2, 64), (2, 64, 3, 64),
+                                      (1, 130, 1, 64)])
+def test_flash_backward(b, s, nh, d):
+    from paper_2104_05343_b200 import kernels as K
+
+    torch.manual_seed(1)
+    hb = nh * d
+    qkv = torch.randn(b * s, 3 * hb, device="cuda").bfloat16()
+    dout = torch.randn(b * s, hb, device="cuda").bfloat16()
+    out = torch.empty(b * s, hb, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, nh, s, device="cuda")
+    K.flash_attn_fwd(qkv, b, s, nh, d, out, lse)
+    drow = torch.empty(b, nh, s, device="cuda")
+    K.attn_rowdot(dout, out, nh, d, s, drow)
+    dq = torch.zeros(b * s, hb, device="cuda")
+    dqkv = torch.full((b * s, 3 * hb), float("nan"), device="cuda", dtype=torch.bfloat16)
+    K.flash_attn_bwd(qkv, dout, lse, drow, b, s, nh, d, dq, dqkv)
+    torch.cuda.synchronize()
+
+    x = qkv.float().requires_grad_(True)
+    o, _, _ = _ref(x, b, s, nh, d)
+    o.backward(dout.float())
+    g = x.grad
+    for i, got in enumerate((dq, dqkv[:, hb:2 * hb].float(), dqkv[:, 2 * hb:].float())):
+        want = g[:, i * hb:(i + 1) * hb]
+        err = (got - want).abs().max().item() / want.abs().max().item()
+        assert err < 2e-2, (i, err)
