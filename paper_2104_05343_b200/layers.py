@@ -431,13 +431,26 @@ def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: Mode
 
 @dataclass
 class AttentionContext:
-    """Saved attention state (layers.py:358-365): input, QKV block, P, context."""
+    """Saved attention state (layers.py:358-365): input, QKV block, context.
+
+    On the flash path the per-row log-sum-exp replaces P; ``probs`` is then
+    rebuilt on demand (the backward never needs it).
+    """
 
     x_in: ShardedMatrix
     qkv: ShardedMatrix
-    probs: list
+    saved_probs: list
     ctx_mat: ShardedMatrix
     cfg: ModelConfig
+    lse: list | None = None
+
+    @property
+    def probs(self) -> list:
+        mesh = self.qkv.mesh
+        for dev in mesh.local_devs:
+            if self.saved_probs[dev] is None:
+                self.saved_probs[dev] = _probs(self.cfg, mesh, self.qkv.blocks[dev], dev)
+        return self.saved_probs
 
     def _heads(self, part: int) -> list:
         mesh = self.qkv.mesh
@@ -480,22 +493,43 @@ def fused_softmax_ok(cfg: ModelConfig) -> bool:
     return cfg.s <= 512 and cfg.s % 8 == 0 and cfg.head_dim % 8 == 0
 
 
-def _local_attention(cfg: ModelConfig, mesh: Mesh, qkv_blk, ctx_blk, ws, dev):
+def flash_ok(cfg: ModelConfig) -> bool:
+    """The tcgen05 flash kernels (sg_attn.cu) cover head_dim 64 at any sequence length."""
+    return FLASH_ATTENTION and cfg.head_dim == 64
+
+
+FLASH_ATTENTION = True
+
+
+def _probs(cfg: ModelConfig, mesh: Mesh, qkv_blk, dev):
+    """P = softmax(Q K^T / sqrt(d)) as bf16 [b, n, s, s] (the reference's saved ``probs``)."""
     b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
     hb = cfg.h // mesh.c
     q = _heads_view(qkv_blk[:, :hb], b_loc, s, n_loc, d)
     k = _heads_view(qkv_blk[:, hb:2 * hb], b_loc, s, n_loc, d)
-    v = _heads_view(qkv_blk[:, 2 * hb:], b_loc, s, n_loc, d)
     probs = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
     if fused_softmax_ok(cfg):
-        # P = softmax(Q K^T / sqrt(d)) straight out of TMEM: no fp32 score matrix in HBM
+        # P straight out of TMEM: no fp32 score matrix in HBM
         K.gemm(q, k.transpose(-1, -2), probs, alpha=1.0 / math.sqrt(d), mode=K.EPI_SOFTMAX)
     else:
         scores = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
         K.gemm(q, k.transpose(-1, -2), scores, alpha=1.0 / math.sqrt(d))
         K.softmax_rows(_rows_view(scores), _rows_view(probs))
-    K.gemm(probs, v, _heads_view(ctx_blk, b_loc, s, n_loc, d))
     return probs
+
+
+def _local_attention(cfg: ModelConfig, mesh: Mesh, qkv_blk, ctx_blk, ws, dev):
+    """Per-position multi-head attention on one block; returns (probs | None, lse | None)."""
+    b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
+    hb = cfg.h // mesh.c
+    if flash_ok(cfg):
+        lse = ws.empty(dev, (b_loc, n_loc, s), "forward", dtype=F32, pad=False)
+        K.flash_attn_fwd(qkv_blk, b_loc, s, n_loc, d, ctx_blk, lse)
+        return None, lse
+    probs = _probs(cfg, mesh, qkv_blk, dev)
+    v = _heads_view(qkv_blk[:, 2 * hb:], b_loc, s, n_loc, d)
+    K.gemm(probs, v, _heads_view(ctx_blk, b_loc, s, n_loc, d))
+    return probs, None
 
 
 def _rows_view(t: torch.Tensor) -> torch.Tensor:
@@ -517,14 +551,15 @@ def attention_forward(x: ShardedMatrix, w_qkv: ShardedMatrix, b_qkv: RowHostedVe
     bs_loc = (cfg.b // mesh.r) * cfg.s
     qkv = summa_ab(x, w_qkv, ws, out_category="forward", tag="summa", out_dtype=BF16,
                    bias=[None if d is None else b_qkv.for_position(mesh, d) for d in _all(mesh)])
-    ctx_blocks, probs = [None] * mesh.p, [None] * mesh.p
+    ctx_blocks, probs, lse = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
     for dev in mesh.local_devs:
         ctx_blocks[dev] = ws.empty(dev, (bs_loc, hb), "free", dtype=BF16)
-        probs[dev] = _local_attention(cfg, mesh, qkv.blocks[dev], ctx_blocks[dev], ws, dev)
+        probs[dev], lse[dev] = _local_attention(cfg, mesh, qkv.blocks[dev], ctx_blocks[dev], ws, dev)
     ctx_mat = ShardedMatrix(mesh, cfg.b * cfg.s, cfg.h, ctx_blocks)
     out = summa_ab(ctx_mat, w_dense, ws, out_category="forward", tag="summa", out_dtype=F32,
                    bias=[None if d is None else b_dense.for_position(mesh, d) for d in _all(mesh)], resid=resid)
-    return out, AttentionContext(x_in=x, qkv=qkv, probs=probs, ctx_mat=ctx_mat, cfg=cfg)
+    return out, AttentionContext(x_in=x, qkv=qkv, saved_probs=probs, ctx_mat=ctx_mat, cfg=cfg,
+                                 lse=lse if flash_ok(cfg) else None)
 
 
 def _all(mesh: Mesh) -> list:
@@ -558,6 +593,15 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
         v = _heads_view(blk[:, 2 * hb:], b_loc, s, n_loc, d)
         dq_blk = ws.empty(dev, (bs_loc, 3 * hb), "free", dtype=BF16)
         dqkv_blocks[dev] = dq_blk
+        if ctx.lse is not None:
+            # flash backward: P rebuilt per tile from lse, never in HBM; D = rowsum(dO O)
+            drow = ws.empty(dev, (b_loc, n_loc, s), "free", dtype=F32, pad=False)
+            K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)
+            dq_acc = ws.alloc(dev, (bs_loc, hb), "free", dtype=F32)
+            K.flash_attn_bwd(blk, dctx.blocks[dev], ctx.lse[dev], drow, b_loc, s, n_loc, d, dq_acc, dq_blk)
+            K.epilogue(dq_acc, dq_blk[:, :hb])
+            K.colsum(dq_blk, bq_parts[dev])
+            continue
         dheads = _heads_view(dctx.blocks[dev], b_loc, s, n_loc, d)
         p_mat = ctx.probs[dev]
         cs = [bq_parts[dev][i * hb:(i + 1) * hb].view(1, n_loc, d) for i in range(3)]
