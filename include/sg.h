@@ -159,6 +159,13 @@ int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const vo
 /* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);
+/* Multi-tensor form: every (w, bf16 twin, g) of a layer / model in one launch per
+ * 96 tensors (the reference's per-parameter loop, layers.py:761-772). */
+typedef struct sg_sgd_item {
+  float* w; void* w_bf16; const float* g;
+  int64_t ldw, ldl, ldg, rows, cols;
+} sg_sgd_item;
+int sg_sgd_multi(const sg_sgd_item* items, int n, float lr, void* stream);
 /* out = dact * gelu'(mid), colsum += column sums of out (GELU backward + b1 gradient,
  * layers.py:502-504); bf16 dact / mid, out may alias dact. */
 int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t ldm, int64_t rows, int64_t cols, void* out,

@@ -46,6 +46,13 @@ class GemmArgs(ctypes.Structure):
     ]
 
 
+class SgdItem(ctypes.Structure):
+    """Mirror of ``sg_sgd_item`` (include/sg.h)."""
+
+    _fields_ = [("w", vp), ("w_bf16", vp), ("g", vp), ("ldw", i64), ("ldl", i64), ("ldg", i64), ("rows", i64),
+                ("cols", i64)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/sg.h
 SIGNATURES: dict[str, tuple] = {
     "sg_gemm": (i32, [ctypes.POINTER(GemmArgs), vp]),
@@ -70,6 +77,7 @@ SIGNATURES: dict[str, tuple] = {
     "sg_dgelu": (i32, [vp, i64, vp, i64, i64, i64, vp, i32, i64, vp, vp]),
     "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
     "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),
+    "sg_sgd_multi": (i32, [ctypes.POINTER(SgdItem), i32, ctypes.c_float, vp]),
     "sg_cast": (i32, [vp, i32, vp, i32, i64, vp]),
     "sg_zero": (i32, [vp, i64, vp]),
     "sg_fold": (i32, [vp, i32, ctypes.POINTER(vp), i32, i64, i32, i32, vp]),

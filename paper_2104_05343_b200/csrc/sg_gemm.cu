@@ -210,18 +210,20 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* d, bool vec, int n
 
 // Coalesced lane = column read of a 32 x 32 input sub-tile into registers
 // (x[i] = row0 + i of column col), rows >= nrows / cols >= N read as 0.
+// The 32 loads are all issued before any is consumed (bf16 values are widened
+// afterwards, outside the predicated loads).
 template <typename T>
 __device__ __forceinline__ void ld_cols(const T* base, long long ld, int nrows, bool col_ok, float (&x)[32]) {
+  if constexpr (sizeof(T) == 4) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float v = 0.f;
-    if (col_ok && i < nrows) {
-      if constexpr (sizeof(T) == 4)
-        v = base[(long long)i * ld];
-      else
-        v = __bfloat162float(base[(long long)i * ld]);
-    }
-    x[i] = v;
+    for (int i = 0; i < 32; ++i) x[i] = (col_ok && i < nrows) ? base[(long long)i * ld] : 0.f;
+  } else {
+    unsigned short raw[32];
+    const unsigned short* b = reinterpret_cast<const unsigned short*>(base);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) raw[i] = (col_ok && i < nrows) ? b[(long long)i * ld] : (unsigned short)0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(static_cast<uint32_t>(raw[i]) << 16);
   }
 }
 

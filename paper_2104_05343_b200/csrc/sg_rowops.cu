@@ -82,6 +82,38 @@ __device__ __forceinline__ void st8(bf16* p, int n, const float (&v)[8]) {
   }
 }
 
+// Raw 8-element vectors: the load is one (bf16) or two (fp32) 16-byte accesses
+// into registers and the conversion to float happens later, so a kernel can
+// issue every load of a row group before the first one is consumed (a
+// conversion right after each load, as in ld8's mixed vector / scalar path,
+// serialises the loads on the scoreboard).
+template <typename T>
+struct Vec8;
+template <>
+struct Vec8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = *reinterpret_cast<const float4*>(p);
+    b = *reinterpret_cast<const float4*>(p + 4);
+  }
+  __device__ __forceinline__ void to(float (&v)[8]) const {
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+};
+template <>
+struct Vec8<bf16> {
+  uint4 a;
+  __device__ __forceinline__ void load(const bf16* p) { a = *reinterpret_cast<const uint4*>(p); }
+  __device__ __forceinline__ void to(float (&v)[8]) const {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+  }
+};
+
 template <typename T>
 __device__ __forceinline__ float ld1(const T* p);
 template <>
@@ -233,128 +265,192 @@ __global__ void ln_bwd_stats_kernel(const TD* __restrict__ dy, long long lddy, c
   }
 }
 
-// dx = rstd * (g - sum_g/h - x^ * sum_xg/h) [+ resid]; dgamma += sum_rows dy x^,
-// dbeta += sum_rows dy (layers.py:329-342). Grid: (row blocks, 1024-col segments).
-constexpr int kSeg = 1024;
-template <typename TD, typename TX, typename TR, typename TO>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
-    const TD* __restrict__ dy, long long lddy, const TX* __restrict__ x, long long ldx,
-    const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma, long long rows,
-    int cols, const float* __restrict__ stats, float inv_h, const TR* __restrict__ resid, long long ldr,
-    TO* __restrict__ dx, long long lddx, bf16* __restrict__ dx2, long long lddx2, float* __restrict__ dgamma,
-    float* __restrict__ dbeta, float* __restrict__ dsum) {
-  __shared__ float s_dg[kSeg], s_db[kSeg], s_ds[kSeg];
+// ---- column-segment row kernels -------------------------------------------
+// Kernels that also produce column sums (LayerNorm backward, GELU', bias
+// gradients) use one layout: a block is 8 warps, blockIdx.y selects a
+// 256-column segment, each lane owns 8 consecutive columns of it, and the warps
+// sweep the rows RU at a time with every load of the RU rows issued before
+// any use (memory-level parallelism without a huge per-thread footprint).
+// Per-column partials stay in registers (8 per quantity) and are folded once
+// per block through shared memory, then one atomic per column per block.
+constexpr int kSegCols = 256;
+constexpr int kSegWarps = 8;
+
+template <int NQ>
+__device__ __forceinline__ void seg_flush(float (&acc)[NQ][8], float* const (&dst)[NQ], int c0, int cols,
+                                          float* sm /* [NQ][8 warps][256] */) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c0 = blockIdx.y * kSeg;
-  const int seg = min(kSeg, cols - c0);
-  const bool want_g = dgamma != nullptr, want_s = dsum != nullptr;
-  if (want_g || want_s) {
-    for (int i = threadIdx.x; i < kSeg; i += blockDim.x) {
-      s_dg[i] = 0.f;
-      s_db[i] = 0.f;
-      s_ds[i] = 0.f;
-    }
-    __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    float4* p = reinterpret_cast<float4*>(sm + (q * kSegWarps + warp) * kSegCols + lane * 8);
+    p[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+    p[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
   }
-  float ag[4][8], ab[4][8], as[4][8];
+  __syncthreads();
+  const int t = threadIdx.x;  // one column per thread
+  if (c0 + t < cols) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+    for (int q = 0; q < NQ; ++q) {
+      if (!dst[q]) continue;
+      float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = as[k][i] = 0.f;
-  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
-    const float mu = mean[r], rs = rstd[r];
-    const float m_xg = stats[2 * r] * inv_h, m_g = stats[2 * r + 1] * inv_h;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = k * 256 + lane * 8;
-      if (c >= seg) break;
-      const int n = min(8, seg - c);
-      const int cc = c0 + c;
-      float d[8], v[8], g[8], o[8];
-      ld8(dy + r * lddy + cc, n, d);
-      ld8(x + r * ldx + cc, n, v);
-      ld8(gamma + cc, n, g);
-      if (resid)
-        ld8(resid + r * ldr + cc, n, o);
-      else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float xh = (v[i] - mu) * rs;
-        o[i] += rs * (d[i] * g[i] - m_g - xh * m_xg);
-        ag[k][i] += d[i] * xh;
-        ab[k][i] += d[i];
-        as[k][i] += o[i];
-      }
-      st8(dx + r * lddx + cc, n, o);
-      if (dx2) st8(dx2 + r * lddx2 + cc, n, o);
-    }
-  }
-  if (want_g || want_s) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = k * 256 + lane * 8;
-      if (c >= seg) break;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (c + i < seg) {
-          if (want_g) {
-            atomicAdd(&s_dg[c + i], ag[k][i]);
-            atomicAdd(&s_db[c + i], ab[k][i]);
-          }
-          if (want_s) atomicAdd(&s_ds[c + i], as[k][i]);
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < seg; i += blockDim.x) {
-      if (want_g) {
-        atomicAdd(&dgamma[c0 + i], s_dg[i]);
-        atomicAdd(&dbeta[c0 + i], s_db[i]);
-      }
-      if (want_s) atomicAdd(&dsum[c0 + i], s_ds[i]);
+      for (int w = 0; w < kSegWarps; ++w) s += sm[(q * kSegWarps + w) * kSegCols + t];
+      atomicAdd(dst[q] + c0 + t, s);
     }
   }
 }
 
-// ============================================================ column sums
-// out[c] (+)= sum_r x[r, c]  (bias gradient before the column reduce, layers.py:238)
-template <typename TX>
-__global__ void __launch_bounds__(256) colsum_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
-                                                     float* __restrict__ out) {
-  __shared__ float s[kSeg];
+static dim3 seg_grid(long long rows, long long cols, int ru, int blocks_per_sm) {
+  if (g_sms <= 0) g_sms = sg_device_sm_count();
+  const int segs = (int)((cols + kSegCols - 1) / kSegCols);
+  const long long row_groups = (rows + (long long)kSegWarps * ru - 1) / ((long long)kSegWarps * ru);
+  long long gx = std::max(1LL, (long long)(g_sms > 0 ? g_sms : 148) * blocks_per_sm / segs);
+  gx = std::min(gx, std::max(1LL, row_groups));
+  return dim3((unsigned)gx, (unsigned)segs);
+}
+
+// dx = rstd * (g - sum_g/h - x^ * sum_xg/h) [+ resid], g = dy * gamma; dgamma +=
+// column sums of dy x^, dbeta += column sums of dy (layers.py:329-342) and dsum +=
+// column sums of dx (the upstream bias gradient, layers.py:238).
+template <typename TD, typename TX, typename TR, int RU, bool FULL>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(
+    const TD* __restrict__ dy, long long lddy, const TX* __restrict__ x, long long ldx,
+    const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma, long long rows,
+    int cols, const float* __restrict__ stats, float inv_h, const TR* __restrict__ resid, long long ldr,
+    float* __restrict__ dx, long long lddx, bf16* __restrict__ dx2, long long lddx2, float* __restrict__ dgamma,
+    float* __restrict__ dbeta, float* __restrict__ dsum) {
+  __shared__ __align__(16) float sm[3 * kSegWarps * kSegCols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c0 = blockIdx.y * kSeg;
-  const int seg = min(kSeg, cols - c0);
-  for (int i = threadIdx.x; i < kSeg; i += blockDim.x) s[i] = 0.f;
-  __syncthreads();
-  float a[4][8];
+  const int c0 = blockIdx.y * kSegCols;
+  const int c = c0 + lane * 8;
+  const int n = max(0, min(8, cols - c));
+  // FULL (cols % 8 == 0): every lane loads unconditionally (idle lanes / rows past
+  // the end read a clamped in-bounds address and discard it)
+  const int cl = FULL ? min(c, cols - 8) : c;
+  float g[8];
+  if (FULL) {
+    Vec8<float> gv;
+    gv.load(gamma + cl);
+    gv.to(g);
+  } else if (n > 0) {
+    ld8(gamma + c, n, g);
+  }
+  float acc[3][8];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int q = 0; q < 3; ++q)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[k][i] = 0.f;
-  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
+    for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+  const long long step = (long long)gridDim.x * kSegWarps * RU;
+  for (long long r0 = ((long long)blockIdx.x * kSegWarps + warp) * RU; r0 < rows; r0 += step) {
+    float d[RU][8], v[RU][8], o[RU][8];
+    if (FULL) {
+      Vec8<TD> rd[RU];
+      Vec8<TX> rx[RU];
+      Vec8<TR> ro[RU];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = k * 256 + lane * 8;
-      if (c >= seg) break;
-      float v[8];
-      ld8(x + r * ldx + c0 + c, min(8, seg - c), v);
+      for (int u = 0; u < RU; ++u) {
+        const long long r = min(r0 + u, rows - 1);
+        rd[u].load(dy + r * lddy + cl);
+        rx[u].load(x + r * ldx + cl);
+        if (resid) ro[u].load(resid + r * ldr + cl);
+      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[k][i] += v[i];
+      for (int u = 0; u < RU; ++u) {
+        rd[u].to(d[u]);
+        rx[u].to(v[u]);
+        if (resid) {
+          ro[u].to(o[u]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[u][i] = 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const long long r = r0 + u;
+        if (r < rows && n > 0) {
+          ld8(dy + r * lddy + c, n, d[u]);
+          ld8(x + r * ldx + c, n, v[u]);
+          if (resid) {
+            ld8(resid + r * ldr + c, n, o[u]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[u][i] = 0.f;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const long long r = r0 + u;
+      if (r >= rows || n <= 0) continue;
+      const float mu = mean[r], rs = rstd[r];
+      const float m_xg = stats[2 * r] * inv_h, m_g = stats[2 * r + 1] * inv_h;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (v[u][i] - mu) * rs;
+        o[u][i] += rs * (d[u][i] * g[i] - m_g - xh * m_xg);
+        acc[0][i] += d[u][i] * xh;
+        acc[1][i] += d[u][i];
+        acc[2][i] += o[u][i];
+      }
+      st8(dx + r * lddx + c, n, o[u]);
+      if (dx2) st8(dx2 + r * lddx2 + c, n, o[u]);
     }
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int c = k * 256 + lane * 8;
-    if (c >= seg) break;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (c + i < seg) atomicAdd(&s[c + i], a[k][i]);
+  if (dgamma || dsum) {
+    float* const dst[3] = {dgamma, dbeta, dsum};
+    seg_flush<3>(acc, dst, c0, cols, sm);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < seg; i += blockDim.x) atomicAdd(&out[c0 + i], s[i]);
+}
+
+// out[c] += sum_r x[r, c]  (bias gradient before the column reduce, layers.py:238)
+template <typename TX, int RU, bool FULL>
+__global__ void __launch_bounds__(256) colsum_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
+                                                     float* __restrict__ out) {
+  __shared__ __align__(16) float sm[kSegWarps * kSegCols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * kSegCols;
+  const int c = c0 + lane * 8;
+  const int n = max(0, min(8, cols - c));
+  const int cl = FULL ? min(c, cols - 8) : c;
+  float acc[1][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[0][i] = 0.f;
+  const long long step = (long long)gridDim.x * kSegWarps * RU;
+  for (long long r0 = ((long long)blockIdx.x * kSegWarps + warp) * RU; r0 < rows; r0 += step) {
+    float v[RU][8];
+    if (FULL) {
+      Vec8<TX> rv[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) rv[u].load(x + min(r0 + u, rows - 1) * ldx + cl);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        rv[u].to(v[u]);
+        if (r0 + u >= rows || n <= 0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (r0 + u < rows && n > 0) {
+          ld8(x + (r0 + u) * ldx + c, n, v[u]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
+  }
+  float* const dst[1] = {out};
+  seg_flush<1>(acc, dst, c0, cols, sm);
 }
 
 // x[r, c] += bias[c]  (layers.py:228)
@@ -462,7 +558,30 @@ __global__ void xent_local_kernel(const TL* __restrict__ logits, long long rows,
   for (long long r = wid; r < rows; r += nw) {
     const TL* lr = logits + r * ldl;
     float m = -INFINITY, s = 0.f;
-    for (int c = lane * 8; c < n_real; c += 256) {
+    int c = lane * 8;
+    // interior: four 8-wide chunks per lane in flight, then one online update
+    for (; c + 3 * 256 + 8 <= n_real; c += 1024) {
+      Vec8<TL> raw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) raw[k].load(lr + c + k * 256);
+      float v[4][8];
+      float cm = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        raw[k].to(v[k]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cm = fmaxf(cm, v[k][i]);
+      }
+      if (cm > m) {
+        s *= __expf(m - cm);
+        m = cm;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += __expf(v[k][i] - m);
+    }
+    for (; c < n_real; c += 256) {
       float v[8];
       const int n = min(8, n_real - c);
       ld8(lr + c, n, v);
@@ -539,7 +658,26 @@ __global__ void xent_bwd_kernel(const TL* logits, long long rows, long long ldl,
     const float m = gmax[r];
     const float inv = 1.0f / packed[2 * r];
     const long long lab = labels[r] - col_lo;
-    for (int c = lane * 8; c < ncols; c += 256) {
+    int c = lane * 8;
+    for (; c + 256 + 8 <= ncols; c += 512) {  // interior, two chunks in flight
+      Vec8<TL> raw[2];
+      raw[0].load(logits + r * ldl + c);
+      raw[1].load(logits + r * ldl + c + 256);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        float v[8];
+        raw[k].to(v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int cc = c + k * 256 + i;
+          float g = cc < n_real ? __expf(v[i] - m) * inv : 0.f;
+          if (cc == lab) g -= 1.f;
+          v[i] = g * scale;
+        }
+        st8(dl + r * lddl + c + k * 256, 8, v);
+      }
+    }
+    for (; c < ncols; c += 256) {
       float v[8];
       const int n = min(8, ncols - c);
       ld8(logits + r * ldl + c, n, v);
@@ -599,19 +737,6 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, l
 }
 
 // ============================================================ element-wise
-// w -= lr * g (fp32 master), optional bf16 shadow copy for the GEMMs (layers.py:761-772);
-// 2-D with independent row pitches so padding columns are never touched.
-__global__ void sgd_kernel(float* __restrict__ w, long long ldw, bf16* __restrict__ wl, long long ldl,
-                           const float* __restrict__ g, long long ldg, float lr, long long rows, long long cols) {
-  const long long n = rows * cols;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
-    const long long r = i / cols, c = i - r * cols;
-    const float v = w[r * ldw + c] - lr * g[r * ldg + c];
-    w[r * ldw + c] = v;
-    if (wl) wl[r * ldl + c] = __float2bfloat16_rn(v);
-  }
-}
-
 template <typename TS, typename TD>
 __global__ void cast_kernel(const TS* __restrict__ s, TD* __restrict__ d, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
@@ -719,52 +844,117 @@ __global__ void attn_rowdot_kernel(const T* __restrict__ dO, long long ldo, cons
 
 // out = dact * gelu'(mid) (bf16 in / out, out may alias dact) and colsum += column
 // sums of out: the h->4h GELU backward and its bias gradient in one pass
-// (layers.py:502-504). Grid (row blocks, 1024-column segments).
-template <typename TO>
+// (layers.py:502-504). Column-segment layout (see ln_bwd_kernel).
+__device__ __forceinline__ float gelu_grad_approx(float x) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(c * (x + a * x * x * x)));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+}
+template <typename TO, int RU, bool FULL>
 __global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long lda, const bf16* __restrict__ mid,
                                                     long long ldm, long long rows, int cols, TO* out, long long ldo,
                                                     float* __restrict__ colsum) {
-  __shared__ float s[kSeg];
+  __shared__ __align__(16) float sm[kSegWarps * kSegCols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c0 = blockIdx.y * kSeg;
-  const int seg = min(kSeg, cols - c0);
-  if (colsum) {
-    for (int i = threadIdx.x; i < kSeg; i += blockDim.x) s[i] = 0.f;
-    __syncthreads();
-  }
-  float a[4][8];
+  const int c0 = blockIdx.y * kSegCols;
+  const int c = c0 + lane * 8;
+  const int n = max(0, min(8, cols - c));
+  const int cl = FULL ? min(c, cols - 8) : c;
+  float acc[1][8];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int i = 0; i < 8; ++i) acc[0][i] = 0.f;
+  const long long step = (long long)gridDim.x * kSegWarps * RU;
+  for (long long r0 = ((long long)blockIdx.x * kSegWarps + warp) * RU; r0 < rows; r0 += step) {
+    float g[RU][8], xm[RU][8];
+    if (FULL) {
+      Vec8<bf16> rg[RU], rm[RU];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[k][i] = 0.f;
-  for (long long r = blockIdx.x * 8LL + warp; r < rows; r += gridDim.x * 8LL) {
+      for (int u = 0; u < RU; ++u) {
+        const long long r = min(r0 + u, rows - 1);
+        rg[u].load(dact + r * lda + cl);
+        rm[u].load(mid + r * ldm + cl);
+      }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = k * 256 + lane * 8;
-      if (c >= seg) break;
-      const int n = min(8, seg - c);
-      float g[8], x[8];
-      ld8(dact + r * lda + c0 + c, n, g);
-      ld8(mid + r * ldm + c0 + c, n, x);
+      for (int u = 0; u < RU; ++u) {
+        rg[u].to(g[u]);
+        rm[u].to(xm[u]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (r0 + u < rows && n > 0) {
+          ld8(dact + (r0 + u) * lda + c, n, g[u]);
+          ld8(mid + (r0 + u) * ldm + c, n, xm[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if (r0 + u >= rows || n <= 0) continue;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        g[i] *= gelu_tanh_grad(x[i]);
-        a[k][i] += g[i];
+        g[u][i] *= gelu_grad_approx(xm[u][i]);
+        acc[0][i] += g[u][i];
       }
-      st8(out + r * ldo + c0 + c, n, g);
+      st8(out + (r0 + u) * ldo + c, n, g[u]);
     }
   }
   if (colsum) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = k * 256 + lane * 8;
-      if (c >= seg) break;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (c + i < seg) atomicAdd(&s[c + i], a[k][i]);
+    float* const dst[1] = {colsum};
+    seg_flush<1>(acc, dst, c0, cols, sm);
+  }
+}
+
+// Multi-tensor SGD: w -= lr * g on fp32 masters (2-D, own row pitches) with the
+// bf16 GEMM twin refreshed in the same pass (layers.py:761-772, model.py:356-364).
+// Blocks are dealt out over fixed 4096-element chunks of all tensors.
+constexpr int kSgdChunk = 4096;
+constexpr int kSgdMax = 96;
+struct SgdBatch {
+  float* w[kSgdMax];
+  bf16* wl[kSgdMax];
+  const float* g[kSgdMax];
+  long long ldw[kSgdMax], ldl[kSgdMax], ldg[kSgdMax], cols[kSgdMax];
+  long long first_chunk[kSgdMax + 1];
+  long long total[kSgdMax];
+  int n;
+  int vec4[kSgdMax];
+  float lr;
+};
+__global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ SgdBatch b) {
+  for (long long ch = blockIdx.x; ch < b.first_chunk[b.n]; ch += gridDim.x) {
+    int t = 0;
+    while (t + 1 < b.n && b.first_chunk[t + 1] <= ch) ++t;
+    const long long e0 = (ch - b.first_chunk[t]) * kSgdChunk;
+    const long long e1 = min(e0 + kSgdChunk, b.total[t]);
+    const long long cols = b.cols[t];
+    float* w = b.w[t];
+    bf16* wl = b.wl[t];
+    const float* g = b.g[t];
+    if (b.vec4[t]) {
+      for (long long e = e0 + threadIdx.x * 4; e < e1; e += 1024) {
+        const long long r = e / cols, cc = e - r * cols;
+        float4 wv = *reinterpret_cast<float4*>(w + r * b.ldw[t] + cc);
+        const float4 gv = *reinterpret_cast<const float4*>(g + r * b.ldg[t] + cc);
+        wv.x -= b.lr * gv.x; wv.y -= b.lr * gv.y; wv.z -= b.lr * gv.z; wv.w -= b.lr * gv.w;
+        *reinterpret_cast<float4*>(w + r * b.ldw[t] + cc) = wv;
+        if (wl) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(wv.x, wv.y), hi = __floats2bfloat162_rn(wv.z, wv.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(wl + r * b.ldl[t] + cc) = pk;
+        }
+      }
+    } else {
+      for (long long e = e0 + threadIdx.x; e < e1; e += 256) {
+        const long long r = e / cols, cc = e - r * cols;
+        const float v = w[r * b.ldw[t] + cc] - b.lr * g[r * b.ldg[t] + cc];
+        w[r * b.ldw[t] + cc] = v;
+        if (wl) wl[r * b.ldl[t] + cc] = __float2bfloat16_rn(v);
+      }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < seg; i += blockDim.x) atomicAdd(&colsum[c0 + i], s[i]);
   }
 }
 
@@ -836,14 +1026,17 @@ extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, 
       !aligned16(dx2, lddx2, 2))
     return set_error(SG_ERR_SHAPE, "ln_bwd: unaligned");
   if (rows == 0) return SG_OK;
-  const int segs = (int)((cols + kSeg - 1) / kSeg);
-  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
-  dim3 grid(gx, segs);
+  const dim3 grid = seg_grid(rows, cols, 2, 2);
   const float inv_h = 1.0f / (float)h_total;
   if (rdt != SG_DTYPE_BF16) rdt = SG_DTYPE_F32;
   // dx is fp32 (residual-stream gradient); the optional dx2 is its bf16 GEMM operand copy
   if (dxdt != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "ln_bwd: dx must be fp32");
-  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, float><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta, dsum)))));
+#define SG_LN_BWD(FULL) SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, 2, FULL><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta, dsum)))))
+  if (cols % 8 == 0)
+    SG_LN_BWD(true);
+  else
+    SG_LN_BWD(false);
+#undef SG_LN_BWD
   return launch_check();
 }
 
@@ -855,9 +1048,10 @@ extern "C" int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int
   if (!accumulate && cudaMemsetAsync(out, 0, cols * sizeof(float), S(stream)) != cudaSuccess)
     return set_error(SG_ERR_CUDA, "memset");
   if (rows == 0) return SG_OK;
-  const int segs = (int)((cols + kSeg - 1) / kSeg);
-  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
-  SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX><<<dim3(gx, segs), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
+  if (cols % 8 == 0)
+    SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX, 4, true><<<seg_grid(rows, cols, 4, 4), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
+  else
+    SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX, 4, false><<<seg_grid(rows, cols, 4, 2), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
   return launch_check();
 }
 
@@ -956,14 +1150,44 @@ extern "C" int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t v
   return launch_check();
 }
 
+extern "C" int sg_sgd_multi(const sg_sgd_item* items, int n, float lr, void* stream) {
+  clear_error();
+  if (n < 0 || (n > 0 && !items)) return set_error(SG_ERR_CONFIG, "sgd: bad item list");
+  for (int base = 0; base < n; base += kSgdMax) {
+    SgdBatch bt{};
+    bt.lr = lr;
+    long long chunks = 0;
+    for (int i = base; i < n && bt.n < kSgdMax; ++i) {
+      const sg_sgd_item& it = items[i];
+      if (it.rows < 0 || it.cols < 0 || !it.w || !it.g) return set_error(SG_ERR_SHAPE, "sgd: bad item");
+      if (it.rows == 0 || it.cols == 0) continue;
+      const int k = bt.n++;
+      bt.w[k] = it.w;
+      bt.wl[k] = static_cast<bf16*>(it.w_bf16);
+      bt.g[k] = it.g;
+      bt.ldw[k] = it.ldw; bt.ldl[k] = it.ldl; bt.ldg[k] = it.ldg; bt.cols[k] = it.cols;
+      bt.total[k] = it.rows * it.cols;
+      bt.vec4[k] = it.cols % 4 == 0 && it.ldw % 4 == 0 && it.ldg % 4 == 0 && (!it.w_bf16 || it.ldl % 4 == 0) &&
+                   (reinterpret_cast<uintptr_t>(it.w) & 15) == 0 && (reinterpret_cast<uintptr_t>(it.g) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(it.w_bf16) & 7) == 0;
+      bt.first_chunk[k] = chunks;
+      chunks += (bt.total[k] + kSgdChunk - 1) / kSgdChunk;
+    }
+    bt.first_chunk[bt.n] = chunks;
+    if (chunks == 0) continue;
+    if (g_sms <= 0) g_sms = sg_device_sm_count();
+    const long long grid = std::min<long long>(chunks, (long long)(g_sms > 0 ? g_sms : 148) * 8);
+    sgd_multi_kernel<<<(int)grid, 256, 0, S(stream)>>>(bt);
+    const int rc = launch_check();
+    if (rc != SG_OK) return rc;
+  }
+  return SG_OK;
+}
+
 extern "C" int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr,
                       int64_t rows, int64_t cols, void* stream) {
-  clear_error();
-  if (rows < 0 || cols < 0) return set_error(SG_ERR_SHAPE, "sgd: bad extents");
-  if (rows == 0 || cols == 0) return SG_OK;
-  sgd_kernel<<<grid_for(rows * cols, 256, 4), 256, 0, S(stream)>>>(w, ldw, static_cast<bf16*>(w_bf16), ldl, g, ldg, lr,
-                                                                   rows, cols);
-  return launch_check();
+  sg_sgd_item it{w, w_bf16, g, ldw, ldl, ldg, rows, cols};
+  return sg_sgd_multi(&it, 1, lr, stream);
 }
 
 extern "C" int sg_cast(const void* src, int sdt, void* dst, int ddt, int64_t n, void* stream) {
@@ -1017,8 +1241,11 @@ extern "C" int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t 
   if (!aligned16(dact, lda, 2) || !aligned16(mid, ldm, 2) || !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "dgelu: unaligned");
   if (rows == 0) return SG_OK;
-  const int segs = (int)((cols + kSeg - 1) / kSeg);
-  const int gx = std::max(1, grid_for(rows, 16, 16) / segs);
-  SG_DISPATCH_T(odt, TO, (dgelu_kernel<TO><<<dim3(gx, segs), 256, 0, S(stream)>>>(static_cast<const bf16*>(dact), lda, static_cast<const bf16*>(mid), ldm, rows, (int)cols, static_cast<TO*>(out), ldo, colsum)));
+#define SG_DGELU(FULL) SG_DISPATCH_T(odt, TO, (dgelu_kernel<TO, 4, FULL><<<seg_grid(rows, cols, 4, 2), 256, 0, S(stream)>>>(static_cast<const bf16*>(dact), lda, static_cast<const bf16*>(mid), ldm, rows, (int)cols, static_cast<TO*>(out), ldo, colsum)))
+  if (cols % 8 == 0)
+    SG_DGELU(true);
+  else
+    SG_DGELU(false);
+#undef SG_DGELU
   return launch_check();
 }

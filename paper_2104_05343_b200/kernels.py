@@ -324,6 +324,30 @@ def sgd(w, w_bf16, g, lr):
     _call("sg_sgd", _p(w2), ldw, _p(l2), ldl, _p(g2), ldg, lr, rows, cols, _stream(w))
 
 
+def sgd_multi(triples, lr):
+    """w -= lr * g for every (w, w_bf16 | None, g) in one launch (multi-tensor SGD)."""
+    items = []
+    stream = None
+    for w, wl, g in triples:
+        if w.dim() == 1:
+            w2, g2, l2 = w.view(1, -1), g.view(1, -1), None if wl is None else wl.view(1, -1)
+        else:
+            w2, g2, l2 = w, g, wl
+        if tuple(g2.shape) != tuple(w2.shape) or (l2 is not None and tuple(l2.shape) != tuple(w2.shape)):
+            raise ShapeError("sgd: parameter / gradient shapes differ")
+        rows, cols, ldw = _rows2d(w2)
+        it = _lib.SgdItem()
+        it.w, it.w_bf16, it.g = _p(w2), _p(l2), _p(g2)
+        it.ldw, it.ldl, it.ldg = ldw, (_rows2d(l2)[2] if l2 is not None else 0), _rows2d(g2)[2]
+        it.rows, it.cols = rows, cols
+        items.append(it)
+        stream = _stream(w) if stream is None else stream
+    if not items:
+        return
+    arr = (_lib.SgdItem * len(items))(*items)
+    _call("sg_sgd_multi", arr, len(items), lr, stream)
+
+
 def cast(src, dst):
     if src.numel() != dst.numel() or not (src.is_contiguous() and dst.is_contiguous()):
         raise ShapeError("cast needs equal-size contiguous tensors")

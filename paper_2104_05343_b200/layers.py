@@ -894,21 +894,29 @@ class TransformerLayer:
                               b2=b2_g, ln1_gamma=ln1_g, ln1_beta=ln1_b, ln2_gamma=ln2_g, ln2_beta=ln2_b)
 
     def apply_sgd(self, grads: LayerGrads, lr: float) -> None:
-        """w -= lr g on the fp32 masters, refreshing the bf16 GEMM copies (layers.py:761-772)."""
+        """w -= lr g on the fp32 masters, refreshing the bf16 GEMM copies (layers.py:761-772);
+        all twelve parameters in one multi-tensor launch."""
+        triples = []
         for name in _MATS:
-            sgd_matrix(getattr(self.params, name), getattr(grads, name), lr)
+            triples += _sgd_triples_matrix(getattr(self.params, name), getattr(grads, name))
         for name in _VECS:
-            sgd_vector(getattr(self.params, name), getattr(grads, name), lr)
+            triples += _sgd_triples_vector(getattr(self.params, name), getattr(grads, name))
+        K.sgd_multi(triples, lr)
+
+
+def _sgd_triples_matrix(w: ShardedMatrix, g: ShardedMatrix) -> list:
+    twin = getattr(w, "bf16_twin", None)
+    return [(blk, None if twin is None else twin.blocks[k], g.blocks[k]) for k, blk in enumerate(w.blocks)
+            if blk is not None]
+
+
+def _sgd_triples_vector(v: RowHostedVector, g: RowHostedVector) -> list:
+    return [(s, None, g.shards[j]) for j, s in enumerate(v.shards) if s is not None]
 
 
 def sgd_matrix(w: ShardedMatrix, g: ShardedMatrix, lr: float) -> None:
-    twin = getattr(w, "bf16_twin", None)
-    for k, blk in enumerate(w.blocks):
-        if blk is not None:
-            K.sgd(blk, None if twin is None else twin.blocks[k], g.blocks[k], lr)
+    K.sgd_multi(_sgd_triples_matrix(w, g), lr)
 
 
 def sgd_vector(v: RowHostedVector, g: RowHostedVector, lr: float) -> None:
-    for j, s in enumerate(v.shards):
-        if s is not None:
-            K.sgd(s, None, g.shards[j], lr)
+    K.sgd_multi(_sgd_triples_vector(v, g), lr)

@@ -217,12 +217,15 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
     # single step, otherwise as one pass over the fp32 accumulator.
     fused_last = steps == 1 or (out_dtype == F32 and act == K.ACT_NONE and colsum is None and out2 is None)
     acc = out if fused_last else _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    # one step: the residual is the epilogue's C input (no copy); several steps: it
+    # seeds the fp32 accumulator that the steps reduce-add into
+    direct_resid = resid is not None and steps == 1
     for dev in mesh.local_devs:
-        if resid is not None:
+        if resid is not None and not direct_resid:
             copy_block(acc[dev], resid.blocks[dev])
         elif steps > 1:
             K.zero(full_storage(acc[dev]))
-    accumulate = resid is not None or steps > 1
+    accumulate = (resid is not None and not direct_resid) or steps > 1
     for l in range(steps):
         a_pan = mesh.bcast_row(l, a16.blocks, (m_b, k_b), BF16, tag=tag)
         src = [None] * mesh.p
@@ -233,7 +236,7 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
         b_pan = mesh.bcast_col(l % mesh.r, src, (k_b, n_b), BF16, tag=tag)
         last = l == steps - 1
         for dev in mesh.local_devs:
-            c_in = acc[dev] if accumulate else None
+            c_in = acc[dev] if accumulate else (resid.blocks[dev] if direct_resid else None)
             if last and fused_last:
                 K.gemm(a_pan[dev], b_pan[dev], out[dev], bias=None if bias is None else bias[dev], c=c_in, act=act,
                        aux=None if aux is None else aux.blocks[dev], out2=None if out2 is None else out2[dev],
