@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -45,6 +46,7 @@ struct GemmParams {
   int M, N, K;
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
+  int k_splits, kb_per_split;   // split-K: work unit = (split, tile), partial sums reduce-added into D
   int a_b2_first, b_b2_first, o_b2_first;
   int mode;
   int d_f32;
@@ -117,6 +119,7 @@ __device__ __forceinline__ void reduce_box(const CUtensorMap* tm, const void* sr
 // each operand is then streamed from HBM about once even when A exceeds L2.
 constexpr int kGroupM = 16;
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb, int& nb, int& z1, int& z2) {
+  t %= p.num_tiles / p.k_splits;  // split-K units share the output tile
   const int per = p.m_tiles * p.n_tiles;
   const int z = t / per;
   const int r = t - z * per;
@@ -128,6 +131,13 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb,
   nb = rr / gm;
   z1 = z / p.nb2;
   z2 = z - z1 * p.nb2;
+}
+
+// k-block range of work unit t (the whole K unless split-K)
+__device__ __forceinline__ void unit_k_range(const GemmParams& p, int t, int& kb0, int& kb1) {
+  const int split = t / (p.num_tiles / p.k_splits);
+  kb0 = split * p.kb_per_split;
+  kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
 }
 
 __device__ __forceinline__ float gelu_fast(float x) {
@@ -278,7 +288,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         int mb, nb, z1, z2;
         decode_tile(p, t, mb, nb, z1, z2);
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        int kb0, kb1;
+        unit_k_range(p, t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
           uint8_t* a_dst = sA + stage * A_BYTES;
@@ -320,7 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        int kb0, kb1;
+        unit_k_range(p, t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t bb = b_base + h * B_HALF;
               const uint64_t bd = B_MN ? umma_desc_sw128(bb + k * 2048, kBK * 128, 1024)
                                        : umma_desc_sw128(bb + k * 32, 0, 1024);
-              umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+              umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
             }
           }
           umma_commit(&empty[stage]);
@@ -445,6 +459,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
       float in_cur[32], in_nxt[32];
       if (in_kind) load_in(0, in_cur);
+      // bias: lane j holds column j of the chunk (one coalesced load, prefetched a
+      // chunk ahead) and the row-threads pick it up by shuffle
+      auto load_bias = [&](int c) -> float {
+        const int col = nb * BN + c * 32 + lane;
+        return (p.bias && c < NCH && col < p.N) ? __ldg(p.bias + col) : 0.f;
+      };
+      float bias_cur = load_bias(0), bias_nxt = 0.f;
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c) {
         const int col0 = nb * BN + c * 32;
@@ -452,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col = col0 + lane;
         const bool col_ok = col < p.N;
         if (in_kind) load_in(c + 1, in_nxt);
+        if (p.bias) bias_nxt = load_bias(c + 1);
         // accumulator chunk, thread = row
         uint32_t r[32];
         tmem_ld32(tacc + c * 32, r);
@@ -503,20 +525,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                              p.vec_d, min(32, p.N - col0), v);
           } else {
             if (p.bias) {
-              const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
-              const bool bv_ok = col0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0;
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                float4 b = bv_ok ? __ldg(b4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (!bv_ok) {
-                  const int cc = col0 + 4 * k;
-                  b.x = cc < p.N ? p.bias[cc] : 0.f;
-                  b.y = cc + 1 < p.N ? p.bias[cc + 1] : 0.f;
-                  b.z = cc + 2 < p.N ? p.bias[cc + 2] : 0.f;
-                  b.w = cc + 3 < p.N ? p.bias[cc + 3] : 0.f;
-                }
-                v[4 * k] += b.x; v[4 * k + 1] += b.y; v[4 * k + 2] += b.z; v[4 * k + 3] += b.w;
-              }
+              for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bias_cur, j);
             }
             if (in_kind == 1) {
               float cv[32];
@@ -573,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) in_cur[i] = in_nxt[i];
         }
+        bias_cur = bias_nxt;
       }
     }
     if (lane == 0) bulk_wait_all();  // global writes complete before the CTA retires
@@ -743,6 +754,11 @@ static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p
   return launch_gemm<BN, true, true>(m, p, s, grid);
 }
 
+static double wave_eff(long long units, int sms) {
+  const long long waves = (units + sms - 1) / sms;
+  return (double)units / (double)(waves * sms);
+}
+
 static int pick_bn(long long M, long long N, long long batch, int sms, int mode) {
   if (mode != SG_EPI_NORMAL) {  // the whole row in one tile
     for (int bn : {64, 128, 256, 512})
@@ -751,19 +767,33 @@ static int pick_bn(long long M, long long N, long long batch, int sms, int mode)
   }
   if (N <= 64) return 64;
   if (N <= 128) return 128;
-  // Largest tile unless it leaves the last wave badly underfilled.
+  // 128 x 256 tiles read 96 B/clk of operands from smem per SM, 128 x 128 tiles
+  // 128 B/clk (the smem limit): take the wide tile unless its last wave is much
+  // emptier (measured: 256 wins by ~17% at equal wave counts).
   const long long mt = (M + kBM - 1) / kBM;
-  double best_eff = -1.0;
-  int best = 256;
-  for (int bn : {256, 128}) {
-    const long long tiles = mt * ((N + bn - 1) / bn) * batch;
-    const long long waves = (tiles + sms - 1) / sms;
-    const double work = (double)mt * kBM * ((N + bn - 1) / bn) * bn * batch;  // padded work
-    const double eff = (double)M * N * batch / work * (double)tiles / (double)(waves * sms);
-    if (eff > best_eff * 1.08) {
-      best_eff = eff;
-      best = bn;
+  auto eff = [&](int bn) {
+    const long long nt = (N + bn - 1) / bn;
+    return (double)N / (double)(nt * bn) * wave_eff(mt * nt * batch, sms);
+  };
+  return eff(128) > eff(256) * 1.15 ? 128 : 256;
+}
+
+// Split-K factor for tile-starved products (e.g. the weight gradients, M x N =
+// h x h with K = b*s tokens, under 3/4 of a wave): the smallest split count whose (split, tile) work
+// units fill the SMs to >= 90%, each split keeping >= 8 k-blocks.
+static int pick_splits(long long tiles, int k_blocks, int sms) {
+  if (4 * tiles >= 3LL * sms) return 1;  // (measured: splitting a ~0.9-wave product loses to the reduce traffic)
+  int best = 1;
+  double best_eff = wave_eff(tiles, sms);
+  for (int s = 2; s <= 16 && k_blocks / s >= 8; ++s) {
+    const int per = (k_blocks + s - 1) / s;
+    const int real = (k_blocks + per - 1) / per;
+    const double e = wave_eff(tiles * real, sms);
+    if (e > best_eff + 0.02) {
+      best = real;
+      best_eff = e;
     }
+    if (best_eff >= 0.9) break;
   }
   return best;
 }
@@ -813,12 +843,31 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.nb2 = (int)a->nb2;
   p.mode = a->mode;
   const long long batch = a->nb1 * a->nb2;
-  const int bn = pick_bn(a->M, a->N, batch, sms, a->mode);
+  int bn = pick_bn(a->M, a->N, batch, sms, a->mode);
+  static const int force_bn = [] {
+    const char* e = getenv("SG_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (force_bn && a->mode == SG_EPI_NORMAL && a->N > 128) bn = force_bn;
   p.m_tiles = (int)((a->M + kBM - 1) / kBM);
   p.n_tiles = (int)((a->N + bn - 1) / bn);
   p.k_blocks = (int)((a->K + kBK - 1) / kBK);
-  const long long tiles = (long long)p.m_tiles * p.n_tiles * batch;
-  if (tiles > INT32_MAX) return set_error(SG_ERR_SHAPE, "gemm: too many tiles");
+  long long tiles = (long long)p.m_tiles * p.n_tiles * batch;
+  if (tiles > INT32_MAX / 16) return set_error(SG_ERR_SHAPE, "gemm: too many tiles");
+  // split-K: only for plain fp32 products whose partials can be TMA-reduce-added
+  // (D zeroed first, or D == C accumulated in place); SG_DETERMINISTIC=1 disables it
+  static const bool deterministic = [] {
+    const char* e = getenv("SG_DETERMINISTIC");
+    return e && atoi(e) != 0;
+  }();
+  const bool in_place = a->C == a->D && a->c_dtype == SG_DTYPE_F32 && a->ldc == a->ldd;
+  const bool split_ok = !deterministic && a->mode == SG_EPI_NORMAL && a->d_dtype == SG_DTYPE_F32 && !a->bias &&
+                        a->act == SG_ACT_NONE && !a->D2 && !a->colsum && batch == 1 && (a->C == nullptr || in_place) &&
+                        a->alpha == 1.f;
+  p.k_splits = split_ok ? pick_splits(tiles, p.k_blocks, sms) : 1;
+  p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
+  p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+  tiles *= p.k_splits;
   p.num_tiles = (int)tiles;
   p.d_f32 = a->d_dtype == SG_DTYPE_F32;
   p.D = a->D; p.ldd = a->ldd; p.sd1 = a->sd1; p.sd2 = a->sd2;
@@ -832,6 +881,13 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
                   a->act == SG_ACT_NONE && !a->D2 && a->mode == SG_EPI_NORMAL)
                      ? 1
                      : 0;
+  if (p.k_splits > 1) {
+    p.reduce_add = 1;
+    if (a->C == nullptr &&
+        cudaMemset2DAsync(a->D, (size_t)a->ldd * 4, 0, (size_t)a->N * 4, (size_t)a->M,
+                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      return set_error(SG_ERR_CUDA, "gemm: split-K zero fill failed");
+  }
   p.bias = a->bias;
   p.aux_in = (a->act == SG_ACT_DGELU || a->mode == SG_EPI_SOFTMAX_BWD) ? static_cast<const __nv_bfloat16*>(a->aux)
                                                                       : nullptr;
