@@ -47,7 +47,7 @@ struct GemmParams {
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int k_splits, kb_per_split;   // split-K: work unit = (split, tile), partial sums reduce-added into D
-  int a_b2_first, b_b2_first, o_b2_first;
+  int a_b2_first, b_b2_first, o_b2_first, x_b2_first, c_b2_first;
   int mode;
   int d_f32;
   void* D;                      // direct stores of the row-softmax modes
@@ -72,14 +72,20 @@ struct GemmParams {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kEpiWarps = 4;            // one epilogue warp per TMEM lane quadrant
-constexpr int kThreads = 128 + 32 * kEpiWarps;
+// Epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
+// taking every other 32-column chunk) for epilogues without global inputs,
+// where the epilogue otherwise paces the tensor pipe at small K.
+template <int EW>
+struct EpiCfg {
+  static constexpr int kThreads = 128 + 32 * EW;
+  static constexpr int CSTEP = EW / 4;
+};
 // Per epilogue warp 8 KB of staging: two 4 KB slots (main tile up to 4 KB, or a
 // 2 KB bf16 main tile + 2 KB bf16 side tile) so chunk c+1 never waits for chunk
 // c's TMA store, or one 8 KB slot when an fp32 main tile needs a side tile.
 constexpr int kStgBytes = 8192;
 
-template <int BN>
+template <int BN, int EW>
 struct GemmCfg {
   static constexpr int MMA_N = BN > 256 ? 256 : BN;
   static constexpr int NSPLIT = BN / MMA_N;
@@ -87,8 +93,9 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = BN * kBK * 2;
-  static constexpr int STAGES = BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + kEpiWarps * kStgBytes + 256;
+  static constexpr int STAGES = EW == 8 ? (BN == 256 ? 3 : 4)
+                                        : (BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + EW * kStgBytes + 512;
 };
 
 __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer,
@@ -218,31 +225,13 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* d, bool vec, int n
   }
 }
 
-// Coalesced lane = column read of a 32 x 32 input sub-tile into registers
-// (x[i] = row0 + i of column col), rows >= nrows / cols >= N read as 0.
-// The 32 loads are all issued before any is consumed (bf16 values are widened
-// afterwards, outside the predicated loads).
-template <typename T>
-__device__ __forceinline__ void ld_cols(const T* base, long long ld, int nrows, bool col_ok, float (&x)[32]) {
-  if constexpr (sizeof(T) == 4) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = (col_ok && i < nrows) ? base[(long long)i * ld] : 0.f;
-  } else {
-    unsigned short raw[32];
-    const unsigned short* b = reinterpret_cast<const unsigned short*>(base);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) raw[i] = (col_ok && i < nrows) ? b[(long long)i * ld] : (unsigned short)0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(static_cast<uint32_t>(raw[i]) << 16);
-  }
-}
-
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, int EW>
+__global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
-                const __grid_constant__ CUtensorMap tmD2, const __grid_constant__ GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+                const __grid_constant__ CUtensorMap tmD2, const __grid_constant__ CUtensorMap tmC,
+                const __grid_constant__ GemmParams p) {
+  using Cfg = GemmCfg<BN, EW>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int ACC = Cfg::ACC_BUFS;
   constexpr uint32_t A_BYTES = Cfg::A_BYTES, B_BYTES = Cfg::B_BYTES;
@@ -251,12 +240,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint8_t* stg_all = sB + STAGES * B_BYTES;  // 1024-aligned
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + kEpiWarps * kStgBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + EW * kStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* inbar = bars + 2 * STAGES + 4;  // [EW][2]: epilogue input tiles (C / aux) landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + 2 * EW);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -265,14 +255,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmD);
+    if (p.C && !p.reduce_add) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], EW);
     }
+    for (int i = 0; i < 2 * EW; ++i) mbar_init(&inbar[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -366,10 +358,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    // warp w owns TMEM lane quadrant q = w % 4: tile rows 32q .. 32q+31.
-    const int q = warp & 3;
-    uint8_t* stg_w = stg_all + q * kStgBytes;
-    uint32_t it = 0, slot = 0;
+    // epilogue warp e owns TMEM lane quadrant q = e % 4 (tile rows 32q .. 32q+31,
+    // a hardware restriction: warp w reads lanes 32 (w % 4) ..) and the chunks
+    // c = e / 4, e / 4 + CSTEP, ...
+    const int e = warp - 4;
+    const int q = e & 3;
+    constexpr int CSTEP = EpiCfg<EW>::CSTEP;
+    const int c_first = e >> 2;
+    uint8_t* stg_w = stg_all + e * kStgBytes;
+    uint32_t it = 0, slot = 0, inph = 0;
     const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     constexpr int NCH = BN / 32;
@@ -379,15 +376,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t as = it % ACC, aph = (it / ACC) & 1;
       const int row0 = mb * kBM + q * 32;
       const int nrows = min(32, p.M - row0);
-      const size_t c_off = (size_t)z1 * p.sc1 + (size_t)z2 * p.sc2;
-      const size_t x_off = (size_t)z1 * p.sx1 + (size_t)z2 * p.sx2;
       float rv = 0.f;
       if (p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const uint32_t tacc = tmem_base + lane_base + as * BN;
 
-      if (p.mode == SG_EPI_SOFTMAX) {
+      if (EW == 4 && p.mode == SG_EPI_SOFTMAX) {
         // whole row in TMEM: max, sum of exponentials, then P chunks through smem + TMA
         const float sl2 = p.alpha * 1.4426950408889634f;
         float m = -INFINITY;
@@ -434,77 +429,82 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
 
-      // one global input per chunk at most (C, or the GELU' / softmax-backward aux);
-      // its lane = column loads for chunk c+1 are issued before chunk c is processed
+      // one global input per chunk at most (C, or the GELU' / softmax-backward aux),
+      // brought into the chunk's staging slot by TMA in the same swizzled layout the
+      // stores use (fp32 C -> main tile, bf16 aux / C -> side tile); with two slots
+      // the next chunk's tile is requested before this chunk is processed
       const int in_kind =
           (p.C && !p.reduce_add) ? 1 : ((p.act == SG_ACT_DGELU || p.mode == SG_EPI_SOFTMAX_BWD) ? 2 : 0);
-      auto load_in = [&](int c, float (&dst)[32]) {
+      const bool c_side = in_kind == 1 && !c_f32;  // bf16 C: side tile
+      // slot = main tile (fp32: 4 KB, bf16: 2 KB) [+ 2 KB bf16 side tile]; two 4 KB slots when it fits
+      const bool side = p.aux_out || p.has_d2 || in_kind == 2 || c_side;
+      const int main_bytes = (d_f32 || (in_kind == 1 && c_f32)) ? 4096 : 2048;
+      const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
+      auto issue_in = [&](int c, uint32_t si) {  // lane 0 only
+        uint8_t* base = stg_w + (dual ? si * 4096 : 0);
+        uint64_t* bar = &inbar[e * 2 + si];
         const int col0 = nb * BN + c * 32;
-        const int col = col0 + lane;
-        const bool ok = c < NCH && col0 < p.N && nrows > 0;
-        if (!ok) return;
-        if (in_kind == 1) {
-          if (c_f32)
-            ld_cols(static_cast<const float*>(p.C) + c_off + (size_t)row0 * p.ldc + col, p.ldc, nrows, col < p.N, dst);
-          else
-            ld_cols(static_cast<const __nv_bfloat16*>(p.C) + c_off + (size_t)row0 * p.ldc + col, p.ldc, nrows,
-                    col < p.N, dst);
-        } else if (in_kind == 2) {
-          ld_cols(p.aux_in + x_off + (size_t)row0 * p.ldx + col, p.ldx, nrows, col < p.N, dst);
+        if (in_kind == 1 && c_f32) {
+          mbar_arrive_expect_tx(bar, 4096);
+          load_box(&tmC, base, bar, col0, row0, z2, z1, p.c_b2_first);
+        } else if (in_kind == 1) {
+          mbar_arrive_expect_tx(bar, 2048);
+          load_box(&tmC, base + main_bytes, bar, col0, row0, z2, z1, p.c_b2_first);
+        } else {
+          mbar_arrive_expect_tx(bar, 2048);
+          load_box(&tmX, base + main_bytes, bar, col0, row0, z2, z1, p.x_b2_first);
         }
       };
-      // slot = main tile (fp32: 4 KB, bf16: 2 KB) [+ 2 KB bf16 side tile]; two 4 KB slots when it fits
-      const bool side = p.aux_out || p.has_d2 || in_kind == 2;
-      const int main_bytes = (d_f32 || in_kind == 1) ? 4096 : 2048;
-      const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
-      float in_cur[32], in_nxt[32];
-      if (in_kind) load_in(0, in_cur);
+      bool pref = false;  // the current chunk's input is already in flight
       // bias: lane j holds column j of the chunk (one coalesced load, prefetched a
       // chunk ahead) and the row-threads pick it up by shuffle
       auto load_bias = [&](int c) -> float {
         const int col = nb * BN + c * 32 + lane;
         return (p.bias && c < NCH && col < p.N) ? __ldg(p.bias + col) : 0.f;
       };
-      float bias_cur = load_bias(0), bias_nxt = 0.f;
+      float bias_cur = load_bias(c_first), bias_nxt = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = c_first; c < NCH; c += CSTEP) {
         const int col0 = nb * BN + c * 32;
         const bool active = col0 < p.N && nrows > 0;  // warp-uniform
         const int col = col0 + lane;
         const bool col_ok = col < p.N;
-        if (in_kind) load_in(c + 1, in_nxt);
-        if (p.bias) bias_nxt = load_bias(c + 1);
+        if (p.bias) bias_nxt = load_bias(c + CSTEP);
         // accumulator chunk, thread = row
         uint32_t r[32];
         tmem_ld32(tacc + c * 32, r);
         tmem_wait_ld();
-        if (c == NCH - 1) {
+        if (c + CSTEP >= NCH) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[as]);
         }
         if (active) {
-          uint8_t* s0 = stg_w + (dual ? slot * 4096 : 0);             // main tile: D, fp32 C input
+          const uint32_t si = dual ? slot : 0;
+          uint8_t* s0 = stg_w + si * 4096;                             // main tile: D, fp32 C input
           uint8_t* s1 = s0 + main_bytes;                               // bf16 side tile (SW64)
           if (dual) slot ^= 1;
-          // this slot's previous TMA stores have read it
           if (lane == 0) {
-            if (dual)
-              bulk_wait_read<1>();
-            else
+            if (in_kind && !pref) {  // not prefetched (first chunk of the tile / one slot)
               bulk_wait_read<0>();
+              issue_in(c, si);
+            }
+            const int cn = c + CSTEP;
+            if (in_kind && dual && cn < NCH && nb * BN + cn * 32 < p.N) {
+              bulk_wait_read<0>();  // the other slot's last store has read it
+              issue_in(cn, si ^ 1);
+            } else if (dual) {
+              bulk_wait_read<1>();  // this slot's previous TMA stores have read it
+            } else {
+              bulk_wait_read<0>();
+            }
           }
+          pref = in_kind && dual && c + CSTEP < NCH && nb * BN + (c + CSTEP) * 32 < p.N;
           __syncwarp();
-          // inputs: lane = column -> staging -> thread = row
-          if (in_kind == 1) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) *reinterpret_cast<float*>(s0 + swz_f32(i, lane)) = in_cur[i];
-          } else if (in_kind == 2) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              *reinterpret_cast<__nv_bfloat16*>(s1 + swz_bf16(i, lane)) = __float2bfloat16_rn(in_cur[i]);
+          if (in_kind) {
+            mbar_wait(&inbar[e * 2 + si], (inph >> si) & 1);
+            inph ^= 1u << si;
           }
-          __syncwarp();
           float v[32];
           if (p.alpha != 1.f) {
 #pragma unroll
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           }
-          if (p.mode == SG_EPI_SOFTMAX_BWD) {
+          if (EW == 4 && p.mode == SG_EPI_SOFTMAX_BWD) {
             float pv[32];
             ld_row_bf16(s1, lane, pv);
 #pragma unroll
@@ -530,7 +530,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (in_kind == 1) {
               float cv[32];
-              ld_row_f32(s0, lane, cv);
+              if (c_f32)
+                ld_row_f32(s0, lane, cv);
+              else
+                ld_row_bf16(s1, lane, cv);
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += cv[j];
             }
@@ -578,10 +581,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               bulk_commit();
             }
           }
-        }
-        if (in_kind) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) in_cur[i] = in_nxt[i];
         }
         bias_cur = bias_nxt;
       }
@@ -726,32 +725,32 @@ static int output_map(CUtensorMap* map, const void* ptr, bool f32, long long N, 
 }
 
 struct Maps {
-  CUtensorMap a, b, d, x, d2;
+  CUtensorMap a, b, d, x, d2, c;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int EW>
 static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, int grid) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  using Cfg = GemmCfg<BN, EW>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EW>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
       return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
     attr_set = true;
   }
-  kern<<<grid, kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, p);
+  kern<<<grid, EpiCfg<EW>::kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, m.c, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   return SG_OK;
 }
 
-template <int BN>
+template <int BN, int EW>
 static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p, cudaStream_t s, int grid) {
-  if (!amn && !bmn) return launch_gemm<BN, false, false>(m, p, s, grid);
-  if (!amn && bmn) return launch_gemm<BN, false, true>(m, p, s, grid);
-  if (amn && !bmn) return launch_gemm<BN, true, false>(m, p, s, grid);
-  return launch_gemm<BN, true, true>(m, p, s, grid);
+  if (!amn && !bmn) return launch_gemm<BN, false, false, EW>(m, p, s, grid);
+  if (!amn && bmn) return launch_gemm<BN, false, true, EW>(m, p, s, grid);
+  if (amn && !bmn) return launch_gemm<BN, true, false, EW>(m, p, s, grid);
+  return launch_gemm<BN, true, true, EW>(m, p, s, grid);
 }
 
 static double wave_eff(long long units, int sms) {
@@ -824,6 +823,8 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (a->d_dtype != SG_DTYPE_BF16 && a->d_dtype != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "gemm: d_dtype");
   if (a->D2 && a->act != SG_ACT_NONE) return set_error(SG_ERR_CONFIG, "gemm: D2 copy with GELU / GELU' epilogue");
   if (a->C && a->act == SG_ACT_DGELU) return set_error(SG_ERR_CONFIG, "gemm: C input together with GELU' input");
+  if (a->C && a->C != a->D && a->c_dtype != SG_DTYPE_F32 && (a->D2 || (a->act == SG_ACT_GELU && a->aux)))
+    return set_error(SG_ERR_CONFIG, "gemm: a bf16 C input shares the side tile with D2 / the GELU input copy");
   if (a->mode != SG_EPI_NORMAL) {
     if (a->mode != SG_EPI_SOFTMAX && a->mode != SG_EPI_SOFTMAX_BWD) return set_error(SG_ERR_CONFIG, "gemm: mode");
     if (a->N > 512) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need N <= 512");
@@ -918,7 +919,12 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (rc == SG_OK)
     rc = output_map(&m.d, a->D, p.d_f32, a->N, a->M, a->nb2, a->nb1, a->ldd, a->sd2, a->sd1, &p.o_b2_first);
   if (rc == SG_OK && p.aux_out)
-    rc = output_map(&m.x, a->aux, false, a->N, a->M, a->nb2, a->nb1, a->ldx, a->sx2, a->sx1, &tmp);
+    rc = output_map(&m.x, a->aux, false, a->N, a->M, a->nb2, a->nb1, a->ldx, a->sx2, a->sx1, &p.x_b2_first);
+  if (rc == SG_OK && !p.aux_out && p.aux_in)  // GELU' / softmax-backward input tile
+    rc = output_map(&m.x, a->aux, false, a->N, a->M, a->nb2, a->nb1, a->ldx, a->sx2, a->sx1, &p.x_b2_first);
+  if (rc == SG_OK && a->C && !p.reduce_add)
+    rc = output_map(&m.c, a->C, a->c_dtype == SG_DTYPE_F32, a->N, a->M, a->nb2, a->nb1, a->ldc, a->sc2, a->sc1,
+                    &p.c_b2_first);
   if (rc == SG_OK && p.has_d2)
     rc = output_map(&m.d2, a->D2, false, a->N, a->M, a->nb2, a->nb1, a->ld2, a->s22, a->s21, &tmp);
   if (rc != SG_OK) {
@@ -926,16 +932,28 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     clear_error();
     return launch_simt(a, sms, stream);
   }
-  if (!p.aux_out) m.x = m.d;  // unused maps still need a valid encoding
+  if (!p.aux_out && !p.aux_in) m.x = m.d;  // unused maps still need a valid encoding
+  if (!(a->C && !p.reduce_add)) m.c = m.d;
   if (!p.has_d2) m.d2 = m.d;
 
   const int grid = (int)std::min<long long>(tiles, sms);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
+  // 8 epilogue warps unless the epilogue needs whole rows (softmax modes)
+  static const int force_ew = [] {
+    const char* e = getenv("SG_GEMM_EPI_WARPS");
+    return e ? atoi(e) : 0;
+  }();
+  // (measured: at K > ~1.5k the mainloop hides a 4-warp epilogue and the 8-warp
+  // variant's shallower smem ring (3 stages at BN = 256) costs ~10%)
+  const bool ew8 = force_ew != 4 && a->mode == SG_EPI_NORMAL && (bn == 128 || bn == 256) &&
+                   (force_ew == 8 || p.kb_per_split <= 24);
   switch (bn) {
-    case 64: return dispatch_major<64>(amn, bmn, m, p, s, grid);
-    case 128: return dispatch_major<128>(amn, bmn, m, p, s, grid);
-    case 256: return dispatch_major<256>(amn, bmn, m, p, s, grid);
-    default: return dispatch_major<512>(amn, bmn, m, p, s, grid);
+    case 64: return dispatch_major<64, 4>(amn, bmn, m, p, s, grid);
+    case 128:
+      return ew8 ? dispatch_major<128, 8>(amn, bmn, m, p, s, grid) : dispatch_major<128, 4>(amn, bmn, m, p, s, grid);
+    case 256:
+      return ew8 ? dispatch_major<256, 8>(amn, bmn, m, p, s, grid) : dispatch_major<256, 4>(amn, bmn, m, p, s, grid);
+    default: return dispatch_major<512, 4>(amn, bmn, m, p, s, grid);
   }
 }

@@ -664,9 +664,10 @@ def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2
     dy16 = _bf16_of(out_grad, ws)
     _, b2_grad = bias_add_backward(out_grad, ws)
     b1_parts = new_colsum_parts(mesh, ws, ctx.mid.block_cols)
-    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16)
-    for dev in mesh.local_devs:  # GELU' and the b1 gradient in one bandwidth-bound pass, in place
-        K.dgelu(dmid.blocks[dev], ctx.mid.blocks[dev], dmid.blocks[dev], b1_parts[dev])
+    # GELU' (from the saved pre-activation, TMA-loaded per output tile) and the b1
+    # gradient column sums fused into the dAct product's epilogue (layers.py:502-504)
+    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
+                     colsum=b1_parts)
     dmid.colsum_parts = b1_parts
     w2_grad = summa_atb(ctx.act, dy16, ws, out_category="param_grad")
     _, b1_grad = bias_add_backward(dmid, ws)
