@@ -274,6 +274,77 @@ class Mesh:
         out[f] = buf
         return out
 
+    # ---- asynchronous forms (the SUMMA pipeline): the transfer is enqueued on the
+    # communicator's own stream, ordered after everything already enqueued on the
+    # current stream, and ``wait()`` makes the current stream wait for it; step
+    # l+1's panels are issued before step l's product so the two overlap.
+    def _bcast_async(self, axis: str, root: int, src: Sequence, recv, tag: str) -> "Pending":
+        self._count("broadcast", tag)
+        out: list = [None] * self.p
+        if self.is_local:
+            for f in self.local_devs:
+                i, j = divmod(f, self.c)
+                out[f] = src[self.flat(i, root) if axis == "row" else self.flat(root, j)]
+            return Pending(out, [])
+        import torch.distributed as dist
+
+        f = self.my_flat
+        i, j = divmod(f, self.c)
+        s = self.flat(i, root) if axis == "row" else self.flat(root, j)
+        group = self._dist_group(axis, i if axis == "row" else j)
+        if group is None:
+            out[f] = src[f]
+            return Pending(out, [])
+        buf = src[f] if f == s else recv
+        work = dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group, async_op=True)
+        out[f] = buf
+        return Pending(out, [work])
+
+    def bcast_row_async(self, root_col: int, src: Sequence, recv, tag: str = "misc") -> "Pending":
+        """Asynchronous bcast_row into the preallocated receive block ``recv`` (R1)."""
+        if not 0 <= root_col < self.c:
+            raise ConfigError(f"broadcast root column {root_col} out of range for c={self.c}")
+        return self._bcast_async("row", root_col, src, recv, tag)
+
+    def bcast_col_async(self, root_row: int, src: Sequence, recv, tag: str = "misc") -> "Pending":
+        """Asynchronous bcast_col into the preallocated receive block ``recv`` (R2)."""
+        if not 0 <= root_row < self.r:
+            raise ConfigError(f"broadcast root row {root_row} out of range for r={self.r}")
+        return self._bcast_async("col", root_row, src, recv, tag)
+
+    def _reduce_async(self, axis: str, dest: int, parts: Sequence, tag: str) -> "Pending":
+        """Start the group reduce of ``parts`` to group position ``dest``; ``finish``
+        folds the sum into the destination's output block."""
+        self._count("reduce", tag)
+        groups = self._row_groups if axis == "row" else self._col_groups
+        if self.is_local:
+            return Pending(list(parts), [], fold=[(g[dest], [parts[f] for f in g]) for g in groups])
+        import torch.distributed as dist
+
+        f = self.my_flat
+        i, j = divmod(f, self.c)
+        g = groups[i] if axis == "row" else groups[j]
+        d = g[dest]
+        group = self._dist_group(axis, i if axis == "row" else j)
+        works = []
+        if group is not None:
+            flat = K._flat_storage(parts[f])
+            if dist.get_backend(group) == "nccl":
+                works.append(dist.reduce(flat, dst=self._slot[d], group=group, async_op=True))
+            else:  # gloo reduce is CPU-only; all_reduce covers CUDA tensors
+                works.append(dist.all_reduce(flat, group=group, async_op=True))
+        return Pending(list(parts), works, fold=[(d, [parts[f]])] if f == d else [])
+
+    def reduce_row_async(self, dest_col: int, parts: Sequence, tag: str = "misc") -> "Pending":
+        if not 0 <= dest_col < self.c:
+            raise ConfigError(f"reduce destination column {dest_col} out of range for c={self.c}")
+        return self._reduce_async("row", dest_col, parts, tag)
+
+    def reduce_col_async(self, dest_row: int, parts: Sequence, tag: str = "misc") -> "Pending":
+        if not 0 <= dest_row < self.r:
+            raise ConfigError(f"reduce destination row {dest_row} out of range for r={self.r}")
+        return self._reduce_async("col", dest_row, parts, tag)
+
     def bcast_row(self, root_col: int, src: Sequence, shape=None, dtype=None, tag: str = "misc") -> list:
         """Position (i, j) gets src[(i, root_col)] (R1 panels, mesh.py:440-449)."""
         if not 0 <= root_col < self.c:
@@ -430,6 +501,31 @@ class Mesh:
             out = torch.empty(a.shape[0], b.shape[1], device=a.device, dtype=torch.float32)
         K.gemm(a.to(torch.bfloat16), b.to(torch.bfloat16), out, c=out if accumulate else None)
         return out
+
+
+class Pending:
+    """An issued (possibly asynchronous) collective: ``blocks`` is the per-position
+    result list, valid on the current stream after ``wait()``; for reduces,
+    ``finish(out)`` also folds the group sum into the destination block (in
+    group-position order on the local backend, mesh.py:464-466)."""
+
+    def __init__(self, blocks: list, works: list, fold: list | None = None) -> None:
+        self.blocks = blocks
+        self.works = works
+        self.fold = fold or []
+
+    def wait(self) -> list:
+        for w in self.works:
+            w.wait()
+        self.works = []
+        return self.blocks
+
+    def finish(self, out: Sequence, accumulate: bool = False) -> None:
+        self.wait()
+        for d, srcs in self.fold:
+            if out[d] is not None:
+                K.fold(out[d], srcs, accumulate=accumulate)
+        self.fold = []
 
 
 def _staged_copy(block: torch.Tensor, ws, dev: int, category: str) -> torch.Tensor:

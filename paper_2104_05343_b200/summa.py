@@ -226,14 +226,19 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
         elif steps > 1:
             K.zero(full_storage(acc[dev]))
     accumulate = (resid is not None and not direct_resid) or steps > 1
+    # panels of step l+1 are in flight (double-buffered receive slots) while step l's
+    # product runs; on the local backend the "broadcasts" alias the root's block
+    a_rx, b_rx = _rx_slots(mesh, ws, (m_b, k_b)), _rx_slots(mesh, ws, (k_b, n_b))
+
+    def issue(l):
+        return (mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag),
+                mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag))
+
+    pend = issue(0)
     for l in range(steps):
-        a_pan = mesh.bcast_row(l, a16.blocks, (m_b, k_b), BF16, tag=tag)
-        src = [None] * mesh.p
-        for j in range(mesh.c):
-            o = b16.owner(l, j)
-            if mesh.owns(o):
-                src[o] = b16.block(l, j)
-        b_pan = mesh.bcast_col(l % mesh.r, src, (k_b, n_b), BF16, tag=tag)
+        nxt = issue(l + 1) if l + 1 < steps else None
+        a_pan, b_pan = pend[0].wait(), pend[1].wait()
+        pend = nxt
         last = l == steps - 1
         for dev in mesh.local_devs:
             c_in = acc[dev] if accumulate else (resid.blocks[dev] if direct_resid else None)
@@ -297,19 +302,29 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                     if colsum is not None:
                         K.colsum(out[d], colsum[d], accumulate=True)
         return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
+    # dist pipeline: B(l+1, j) arrives while step l's partial product runs, and step
+    # l's row reduce overlaps step l+1's product (two partial-sum slots)
     acc = _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
+    b_rx = _rx_slots(mesh, ws, (n_b, k_b))
+    part_slots = _rx_slots(mesh, ws, (m_b, n_b), F32)
+    f = mesh.my_flat
+
+    def issue(l):
+        return mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag)
+
+    pend, red_prev = issue(0), None
     for l in range(mesh.c):
-        src = [None] * mesh.p
-        for j in range(mesh.c):
-            o = b16.owner(l, j)
-            if mesh.owns(o):
-                src[o] = b16.block(l, j)
-        b_pan = mesh.bcast_col(l % mesh.r, src, (n_b, k_b), BF16, tag=tag)
+        nxt = issue(l + 1) if l + 1 < mesh.c else None
+        b_pan = pend.wait()
+        pend = nxt
         parts = [None] * mesh.p
-        for dev in mesh.local_devs:
-            parts[dev] = ws_empty(ws, mesh, dev, (m_b, n_b))
-            K.gemm(a16.blocks[dev], b_pan[dev].t(), parts[dev])
-        mesh.reduce_row_into(l, parts, acc, tag=tag)
+        parts[f] = part_slots[l % 2]
+        K.gemm(a16.blocks[f], b_pan[f].t(), parts[f])
+        red = mesh.reduce_row_async(l, parts, tag=tag)
+        if red_prev is not None:
+            red_prev.finish(acc)
+        red_prev = red
+    red_prev.finish(acc)
     _finish(mesh, acc, out, None, res_b, act, aux_b)
     if colsum is not None:
         for dev in mesh.local_devs:
@@ -349,19 +364,54 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                     dst = out[k] if i == mesh.r - 1 else chain
                     K.gemm(a16.block(i, l).t(), b16.block(i, j), dst, c=prev)
         return out_mat
-    for l in range(mesh.c):
-        a_pan = mesh.bcast_row(l, a16.blocks, (t_b, m_b), BF16, tag=tag)
-        parts = [None] * mesh.p
-        for dev in mesh.local_devs:
-            parts[dev] = ws_empty(ws, mesh, dev, (m_b, n_b))
-            K.gemm(a_pan[dev].t(), b16.blocks[dev], parts[dev])
+    # dist pipeline: A(i, l+1) arrives while step l's partial product runs, and step
+    # l's column reduce overlaps step l+1's product
+    a_rx = _rx_slots(mesh, ws, (t_b, m_b))
+    part_slots = _rx_slots(mesh, ws, (m_b, n_b), F32)
+    f = mesh.my_flat
+
+    def issue(l):
+        return mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag)
+
+    def dest_of(l):
         dest = [None] * mesh.p
         for j in range(mesh.c):
             o = out_mat.owner(l, j)
             if mesh.owns(o):
                 dest[o] = out[l * mesh.c + j]
-        mesh.reduce_col_into(l % mesh.r, parts, dest, accumulate=acc_in, tag=tag)
+        return dest
+
+    pend, red_prev = issue(0), None
+    for l in range(mesh.c):
+        nxt = issue(l + 1) if l + 1 < mesh.c else None
+        a_pan = pend.wait()
+        pend = nxt
+        parts = [None] * mesh.p
+        parts[f] = part_slots[l % 2]
+        K.gemm(a_pan[f].t(), b16.blocks[f], parts[f])
+        red = (mesh.reduce_col_async(l % mesh.r, parts, tag=tag), dest_of(l))
+        if red_prev is not None:
+            red_prev[0].finish(red_prev[1], accumulate=acc_in)
+        red_prev = red
+    red_prev[0].finish(red_prev[1], accumulate=acc_in)
     return out_mat
+
+
+def _rx_slots(mesh: Mesh, ws, shape, dtype=BF16) -> list:
+    """Two receive blocks for the double-buffered panel pipeline (dist backend only)."""
+    if mesh.is_local:
+        return [None, None]
+    return [ws_empty(ws, mesh, mesh.my_flat, shape, dtype) for _ in range(2)]
+
+
+def _weight_row(mesh: Mesh, w: ShardedMatrix, l: int) -> list:
+    """Per-position list holding weight block (l, j) at its owner (l mod r, j)."""
+    src = [None] * mesh.p
+    for j in range(mesh.c):
+        o = w.owner(l, j)
+        if mesh.owns(o):
+            src[o] = w.block(l, j)
+    return src
 
 
 def ws_empty(ws, mesh, dev, shape, dtype=F32):

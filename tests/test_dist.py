@@ -73,6 +73,85 @@ def test_gloo_collectives_cpu(tmp_path, rows, cols):
         assert res["ar_col_max"] == (rows - 1) * cols + j + 1
 
 
+def _cpu_local_kernels():
+    """Test-only stand-ins for the per-position CUDA kernels (plain torch on CPU),
+    so the SPMD SUMMA schedule (double-buffered async panels, overlapped reduces)
+    can be checked over gloo without a GPU. The product path itself has no CPU
+    fallback; these are patched into the worker process only."""
+    from paper_2104_05343_b200 import kernels as K
+
+    def gemm(a, b, out, *, alpha=1.0, bias=None, c=None, act=0, aux=None, out2=None, colsum=None, mode=0,
+             rowvec=None):
+        assert act == 0 and mode == 0 and out2 is None
+        r = alpha * (a.double() @ b.double())
+        if bias is not None:
+            r = r + bias.double()
+        if c is not None:
+            r = r + c.double()
+        out.copy_(r.to(out.dtype))
+        if colsum is not None:
+            colsum += r.sum(dim=-2).to(colsum.dtype)
+        return out
+
+    def fold(dst, srcs, accumulate=False, op_max=False):
+        acc = dst.double().clone() if accumulate else srcs[0].double().clone()
+        for t in (srcs if accumulate else srcs[1:]):
+            acc = torch.maximum(acc, t.double()) if op_max else acc + t.double()
+        dst.copy_(acc.to(dst.dtype))
+
+    def epilogue(x, out, *, bias=None, c=None, act=0, aux=None, alpha=1.0):
+        assert act == 0
+        r = alpha * x.double() + (0 if bias is None else bias.double()) + (0 if c is None else c.double())
+        out.copy_(r.to(out.dtype))
+
+    K.gemm = gemm
+    K.fold = fold
+    K.epilogue = epilogue
+    K.zero = lambda t: t.zero_()
+    K.cast = lambda src, dst: dst.copy_(src.to(dst.dtype))
+    K.colsum = lambda x, out, accumulate=False: out.copy_((out if accumulate else 0) + x.double().sum(0))
+
+
+def _summa_cpu_worker(rank, world, port, rows, cols, out_dir):
+    import paper_2104_05343_b200 as sg
+
+    _init(rank, world, port)
+    try:
+        _cpu_local_kernels()
+        m = sg.create_mesh(sg.MeshConfig(rows=rows, cols=cols), backend="dist", device="cpu")
+        rng = np.random.default_rng(7)
+        ints = lambda *s: rng.integers(-4, 5, s).astype(np.float64)  # noqa: E731  (exact in bf16 / fp32)
+        a, b, bt, a2 = ints(8 * rows, 8 * cols), ints(8 * cols, 16 * cols), ints(16 * cols, 8 * cols), \
+            ints(8 * rows, 16 * cols)
+        ws = sg.Workspace(m.p)
+        A, A2 = sg.scatter(a, m), sg.scatter(a2, m)
+        B, BT = sg.scatter(b, m, layout="weight"), sg.scatter(bt, m, layout="weight")
+        res = {"ab": sg.gather(sg.summa_ab(A, B, ws)).tolist(),
+               "abt": sg.gather(sg.summa_abt(A, BT, ws)).tolist(),
+               "atb": sg.gather(sg.summa_atb(A, A2, ws)).tolist(),
+               "ref": [(a @ b).tolist(), (a @ bt.T).tolist(), (a.T @ a2).tolist()],
+               "collectives": m.collective_count()}
+        (out_dir / f"r{rank}.json").write_text(json.dumps(res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2), (2, 4)])
+def test_dist_summa_pipeline_cpu(tmp_path, rows, cols):
+    """The SPMD SUMMA forms (panel broadcasts of step l+1 in flight during step l,
+    reduces overlapped with the next product) give the exact products on
+    1x2, 2x2 and 2x4 meshes (summa.py:95-164)."""
+    world = rows * cols
+    mp.spawn(_summa_cpu_worker, args=(world, _free_port(), rows, cols, tmp_path), nprocs=world, join=True)
+    for rank in range(world):
+        res = json.loads((tmp_path / f"r{rank}.json").read_text())
+        for name, ref in zip(("ab", "abt", "atb"), res["ref"]):
+            np.testing.assert_array_equal(np.array(res[name]), np.array(ref), err_msg=name)
+        # c steps of (row bcast + column bcast) for AB, (column bcast + row reduce) for
+        # AB^T and (row bcast + column reduce) for A^T B
+        assert res["collectives"] == 6 * cols
+
+
 def _gpu_worker(rank, world, port, rows, cols, out_dir):
     import paper_2104_05343_b200 as sg
     from oracle import model_ref as M
