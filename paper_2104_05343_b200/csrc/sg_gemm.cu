@@ -85,17 +85,26 @@ struct EpiCfg {
 // c's TMA store, or one 8 KB slot when an fp32 main tile needs a side tile.
 constexpr int kStgBytes = 8192;
 
-template <int BN, int EW>
+// PAIR: a 2-CTA cluster computes a 256 x BN tile with tcgen05.mma.cta_group::2
+// (each CTA holds 128 rows of A, BN/2 rows of B and its 128 x BN accumulator),
+// halving the per-SM shared-memory operand traffic and B loads; the freed smem
+// buys deeper rings.
+template <int BN, int EW, bool PAIR = false>
 struct GemmCfg {
   static constexpr int MMA_N = BN > 256 ? 256 : BN;
   static constexpr int NSPLIT = BN / MMA_N;
   static constexpr int ACC_BUFS = 2 * BN <= 512 ? 2 : 1;
   static constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
+  static constexpr int TM = PAIR ? 2 * kBM : kBM;  // tile rows
+  static constexpr int BNL = PAIR ? BN / 2 : BN;   // B rows (N) loaded per CTA
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
-  static constexpr uint32_t B_BYTES = BN * kBK * 2;
-  static constexpr int STAGES = EW == 8 ? (BN == 256 ? 3 : 4)
-                                        : (BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
+  static constexpr uint32_t B_BYTES = BNL * kBK * 2;
+  static constexpr int STAGES =
+      PAIR ? (EW == 8 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 6 : 8))
+           : (EW == 8 ? (BN == 256 ? 3 : 4) : (BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8))));
   static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + EW * kStgBytes + 512;
+  static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(!PAIR || BN == 128 || BN == 256, "pair tiles are 256 x 128 or 256 x 256");
 };
 
 __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer,
@@ -104,6 +113,15 @@ __device__ __forceinline__ void load_box(const CUtensorMap* tm, void* dst, uint6
     tma_load_4d(dst, tm, bar, inner, z2, outer, z1);
   else
     tma_load_4d(dst, tm, bar, inner, outer, z2, z1);
+}
+
+// TMA load by either CTA of a pair, completing on the leader's barrier
+__device__ __forceinline__ void load_box_pair(const CUtensorMap* tm, void* dst, uint32_t bar_cluster, int inner,
+                                              int outer, int z2, int z1, int b2_first) {
+  if (b2_first)
+    tma_load_4d_pair(dst, tm, bar_cluster, inner, z2, outer, z1);
+  else
+    tma_load_4d_pair(dst, tm, bar_cluster, inner, outer, z2, z1);
 }
 
 __device__ __forceinline__ void store_box(const CUtensorMap* tm, const void* src, int inner, int outer, int z2, int z1,
@@ -225,16 +243,22 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* d, bool vec, int n
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EW>
+template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR>
 __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ CUtensorMap tmD2, const __grid_constant__ CUtensorMap tmC,
                 const __grid_constant__ GemmParams p) {
-  using Cfg = GemmCfg<BN, EW>;
+  using Cfg = GemmCfg<BN, EW, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int ACC = Cfg::ACC_BUFS;
+  constexpr int TM = Cfg::TM, BNL = Cfg::BNL;
   constexpr uint32_t A_BYTES = Cfg::A_BYTES, B_BYTES = Cfg::B_BYTES;
+  // pair mode: both CTAs of the cluster walk the same tile sequence; rank 0 (the
+  // leader) issues the MMAs and owns the smem-full / TMEM-empty barriers
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -262,14 +286,22 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EW);
+      mbar_init(&tempty[i], PAIR ? 2 * EW : EW);
     }
     for (int i = 0; i < 2 * EW; ++i) mbar_init(&inbar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if (PAIR)
+      tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // barrier inits and the pair's TMEM allocation visible cluster-wide
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -277,34 +309,54 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------------------ producer
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = unit0; t < p.num_tiles; t += nunits) {
         int mb, nb, z1, z2;
         decode_tile(p, t, mb, nb, z1, z2);
         int kb0, kb1;
         unit_k_range(p, t, kb0, kb1);
+        const int m0 = mb * TM + (int)rank * kBM;  // this CTA's A rows
+        const int n0 = nb * BN + (int)rank * BNL;  // this CTA's B rows (N)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
           uint8_t* a_dst = sA + stage * A_BYTES;
           uint8_t* b_dst = sB + stage * B_BYTES;
-          if (!A_MN) {
-            load_box(&tmA, a_dst, &full[stage], kb * kBK, mb * kBM, z2, z1, p.a_b2_first);
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            const uint32_t fb = mapa_smem(&full[stage], 0);
+            if (!A_MN) {
+              load_box_pair(&tmA, a_dst, fb, kb * kBK, m0, z2, z1, p.a_b2_first);
+            } else {
+#pragma unroll
+              for (int i = 0; i < kBM / 64; ++i)
+                load_box_pair(&tmA, a_dst + i * 64 * kBK * 2, fb, m0 + i * 64, kb * kBK, z2, z1, p.a_b2_first);
+            }
+            if (!B_MN) {
+              load_box_pair(&tmB, b_dst, fb, kb * kBK, n0, z2, z1, p.b_b2_first);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BNL / 64; ++i)
+                load_box_pair(&tmB, b_dst + i * 64 * kBK * 2, fb, n0 + i * 64, kb * kBK, z2, z1, p.b_b2_first);
+            }
           } else {
+            mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+            if (!A_MN) {
+              load_box(&tmA, a_dst, &full[stage], kb * kBK, m0, z2, z1, p.a_b2_first);
+            } else {
 #pragma unroll
-            for (int i = 0; i < kBM / 64; ++i)
-              load_box(&tmA, a_dst + i * 64 * kBK * 2, &full[stage], mb * kBM + i * 64, kb * kBK, z2, z1,
-                       p.a_b2_first);
-          }
-          if (!B_MN) {
+              for (int i = 0; i < kBM / 64; ++i)
+                load_box(&tmA, a_dst + i * 64 * kBK * 2, &full[stage], m0 + i * 64, kb * kBK, z2, z1, p.a_b2_first);
+            }
+            if (!B_MN) {
 #pragma unroll
-            for (int h = 0; h < Cfg::NSPLIT; ++h)
-              load_box(&tmB, b_dst + h * Cfg::MMA_N * kBK * 2, &full[stage], kb * kBK, nb * BN + h * Cfg::MMA_N, z2,
-                       z1, p.b_b2_first);
-          } else {
+              for (int h = 0; h < Cfg::NSPLIT; ++h)
+                load_box(&tmB, b_dst + h * Cfg::MMA_N * kBK * 2, &full[stage], kb * kBK, n0 + h * Cfg::MMA_N, z2, z1,
+                         p.b_b2_first);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              load_box(&tmB, b_dst + i * 64 * kBK * 2, &full[stage], nb * BN + i * 64, kb * kBK, z2, z1,
-                       p.b_b2_first);
+              for (int i = 0; i < BN / 64; ++i)
+                load_box(&tmB, b_dst + i * 64 * kBK * 2, &full[stage], n0 + i * 64, kb * kBK, z2, z1, p.b_b2_first);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -314,14 +366,17 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t IDESC = umma_idesc_bf16(kBM, Cfg::MMA_N, A_MN, B_MN);
+      constexpr uint32_t IDESC = umma_idesc_bf16(TM, Cfg::MMA_N, A_MN, B_MN);
       constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;  // second MMA_N-wide half of B
       uint32_t stage = 0, phase = 0, it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
         const uint32_t as = it % ACC, aph = (it / ACC) & 1;
-        mbar_wait(&tempty[as], aph ^ 1);
+        if (PAIR)
+          mbar_wait_cluster(&tempty[as], aph ^ 1);  // both CTAs' epilogues drained this buffer
+        else
+          mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         int kb0, kb1;
@@ -344,16 +399,25 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               const uint32_t bb = b_base + h * B_HALF;
               const uint64_t bd = B_MN ? umma_desc_sw128(bb + k * 2048, kBK * 128, 1024)
                                        : umma_desc_sw128(bb + k * 32, 0, 1024);
-              umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+              if (PAIR)
+                umma_bf16_pair(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+              else
+                umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty[stage]);
+          if (PAIR)
+            umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
+          else
+            umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[as]);
+        if (PAIR)
+          umma_commit_pair(&tfull[as], 0x3);
+        else
+          umma_commit(&tfull[as]);
       }
     }
   } else if (warp >= 4) {
@@ -370,11 +434,19 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     constexpr int NCH = BN / 32;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    const uint32_t tempty_leader = PAIR ? mapa_smem(&tempty[0], 0) : 0;
+    // release the accumulator buffer: to the leader's barrier in pair mode
+    auto release_acc = [&](uint32_t as) {
+      if (PAIR)
+        mbar_arrive_remote(tempty_leader + as * 8);
+      else
+        mbar_arrive(&tempty[as]);
+    };
+    for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
       int mb, nb, z1, z2;
       decode_tile(p, t, mb, nb, z1, z2);
       const uint32_t as = it % ACC, aph = (it / ACC) & 1;
-      const int row0 = mb * kBM + q * 32;
+      const int row0 = mb * TM + (int)rank * kBM + q * 32;
       const int nrows = min(32, p.M - row0);
       float rv = 0.f;
       if (p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
@@ -415,7 +487,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
           if (c == NCH - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[as]);
+            if (lane == 0) release_acc(as);
           }
           const int row = row0 + lane;
           if (c * 32 >= p.N || row >= p.M) continue;
@@ -477,7 +549,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         if (c + CSTEP >= NCH) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[as]);
+          if (lane == 0) release_acc(as);
         }
         if (active) {
           const uint32_t si = dual ? slot : 0;
@@ -589,8 +661,13 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  if (PAIR) {
+    cluster_sync_all();
+    if (warp == 2) tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+  } else {
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
 }
 
 // ------------------------------------------------------------------ SIMT path
@@ -728,29 +805,46 @@ struct Maps {
   CUtensorMap a, b, d, x, d2, c;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EW>
+template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR>
 static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, int grid) {
-  using Cfg = GemmCfg<BN, EW>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, EW>;
+  using Cfg = GemmCfg<BN, EW, PAIR>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EW, PAIR>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
       return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
     attr_set = true;
   }
-  kern<<<grid, EpiCfg<EW>::kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, m.c, p);
+  if (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(EpiCfg<EW>::kThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.d, m.x, m.d2, m.c, p);
+    if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+  } else {
+    kern<<<grid, EpiCfg<EW>::kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, m.c, p);
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   return SG_OK;
 }
 
-template <int BN, int EW>
+template <int BN, int EW, bool PAIR = false>
 static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p, cudaStream_t s, int grid) {
-  if (!amn && !bmn) return launch_gemm<BN, false, false, EW>(m, p, s, grid);
-  if (!amn && bmn) return launch_gemm<BN, false, true, EW>(m, p, s, grid);
-  if (amn && !bmn) return launch_gemm<BN, true, false, EW>(m, p, s, grid);
-  return launch_gemm<BN, true, true, EW>(m, p, s, grid);
+  if (!amn && !bmn) return launch_gemm<BN, false, false, EW, PAIR>(m, p, s, grid);
+  if (!amn && bmn) return launch_gemm<BN, false, true, EW, PAIR>(m, p, s, grid);
+  if (amn && !bmn) return launch_gemm<BN, true, false, EW, PAIR>(m, p, s, grid);
+  return launch_gemm<BN, true, true, EW, PAIR>(m, p, s, grid);
 }
 
 static double wave_eff(long long units, int sms) {
@@ -758,7 +852,7 @@ static double wave_eff(long long units, int sms) {
   return (double)units / (double)(waves * sms);
 }
 
-static int pick_bn(long long M, long long N, long long batch, int sms, int mode) {
+static int pick_bn(long long M, long long N, long long batch, int sms, int mode, int tm = kBM) {
   if (mode != SG_EPI_NORMAL) {  // the whole row in one tile
     for (int bn : {64, 128, 256, 512})
       if (N <= bn) return bn;
@@ -769,7 +863,7 @@ static int pick_bn(long long M, long long N, long long batch, int sms, int mode)
   // 128 x 256 tiles read 96 B/clk of operands from smem per SM, 128 x 128 tiles
   // 128 B/clk (the smem limit): take the wide tile unless its last wave is much
   // emptier (measured: 256 wins by ~17% at equal wave counts).
-  const long long mt = (M + kBM - 1) / kBM;
+  const long long mt = (M + tm - 1) / tm;
   auto eff = [&](int bn) {
     const long long nt = (N + bn - 1) / bn;
     return (double)N / (double)(nt * bn) * wave_eff(mt * nt * batch, sms);
@@ -844,13 +938,24 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.nb2 = (int)a->nb2;
   p.mode = a->mode;
   const long long batch = a->nb1 * a->nb2;
-  int bn = pick_bn(a->M, a->N, batch, sms, a->mode);
+  // 2-CTA pair tiles (256 x 128 / 256 x 256) for every plain product with more
+  // than one 128-row block; single-CTA tiles for the row-softmax modes, narrow
+  // N and M <= 128. SG_GEMM_PAIR=0 / SG_GEMM_BN=n override (experiments).
+  static const int env_pair = [] {
+    const char* e = getenv("SG_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
   static const int force_bn = [] {
     const char* e = getenv("SG_GEMM_BN");
     return e ? atoi(e) : 0;
   }();
-  if (force_bn && a->mode == SG_EPI_NORMAL && a->N > 128) bn = force_bn;
-  p.m_tiles = (int)((a->M + kBM - 1) / kBM);
+  const bool pair = env_pair != 0 && a->mode == SG_EPI_NORMAL && a->M > kBM && a->N > 64;
+  const int units = pair ? sms / 2 : sms;  // concurrent tile workers (CTA pairs or CTAs)
+  const int tm = pair ? 2 * kBM : kBM;
+  int bn = pick_bn(a->M, a->N, batch, units, a->mode, tm);
+  if (force_bn && a->mode == SG_EPI_NORMAL && a->N > 128 && (!pair || force_bn == 128 || force_bn == 256))
+    bn = force_bn;
+  p.m_tiles = (int)((a->M + tm - 1) / tm);
   p.n_tiles = (int)((a->N + bn - 1) / bn);
   p.k_blocks = (int)((a->K + kBK - 1) / kBK);
   long long tiles = (long long)p.m_tiles * p.n_tiles * batch;
@@ -865,7 +970,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   const bool split_ok = !deterministic && a->mode == SG_EPI_NORMAL && a->d_dtype == SG_DTYPE_F32 && !a->bias &&
                         a->act == SG_ACT_NONE && !a->D2 && !a->colsum && batch == 1 && (a->C == nullptr || in_place) &&
                         a->alpha == 1.f;
-  p.k_splits = split_ok ? pick_splits(tiles, p.k_blocks, sms) : 1;
+  p.k_splits = split_ok ? pick_splits(tiles, p.k_blocks, units) : 1;
   p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   tiles *= p.k_splits;
@@ -909,7 +1014,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     rc = operand_map(&m.a, a->A, a->K, a->M, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBM, &p.a_b2_first);
   else
     rc = operand_map(&m.a, a->A, a->M, a->K, a->nb2, a->nb1, a->lda, a->sa2, a->sa1, kBK, &p.a_b2_first);
-  const int b_box = std::min(bn, 256);
+  const int b_box = pair ? bn / 2 : std::min(bn, 256);
   if (rc == SG_OK) {
     if (!a->b_mn_major)
       rc = operand_map(&m.b, a->B, a->K, a->N, a->nb2, a->nb1, a->ldb, a->sb2, a->sb1, b_box, &p.b_b2_first);
@@ -936,7 +1041,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (!(a->C && !p.reduce_add)) m.c = m.d;
   if (!p.has_d2) m.d2 = m.d;
 
-  const int grid = (int)std::min<long long>(tiles, sms);
+  const int grid = (int)std::min<long long>(tiles, units) * (pair ? 2 : 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
   // 8 epilogue warps unless the epilogue needs whole rows (softmax modes)
@@ -948,6 +1053,13 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   // variant's shallower smem ring (3 stages at BN = 256) costs ~10%)
   const bool ew8 = force_ew != 4 && a->mode == SG_EPI_NORMAL && (bn == 128 || bn == 256) &&
                    (force_ew == 8 || p.kb_per_split <= 24);
+  if (pair) {
+    if (bn == 128)
+      return ew8 ? dispatch_major<128, 8, true>(amn, bmn, m, p, s, grid)
+                 : dispatch_major<128, 4, true>(amn, bmn, m, p, s, grid);
+    return ew8 ? dispatch_major<256, 8, true>(amn, bmn, m, p, s, grid)
+               : dispatch_major<256, 4, true>(amn, bmn, m, p, s, grid);
+  }
   switch (bn) {
     case 64: return dispatch_major<64, 4>(amn, bmn, m, p, s, grid);
     case 128:
