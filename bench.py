@@ -86,6 +86,17 @@ def peaks() -> dict:
     return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "src": "fallback (B200_PROFILING.md)"}
 
 
+def gemm_traffic():
+    """DRAM bytes per GEMM launch of one training step from the newest committed ncu
+    capture (profiles/*_gemm_traffic.json, written by tools/summarize_ncu.py)."""
+    files = sorted((ROOT / "profiles").glob("*_gemm_traffic.json"), key=lambda p: p.stat().st_mtime)
+    if not files:
+        return None
+    d = json.loads(files[-1].read_text())
+    d["file"] = f"profiles/{files[-1].name}"
+    return d
+
+
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -298,9 +309,12 @@ def main():
     gsum = prof.summary()
     inst_step_ms = s_ev0.elapsed_time(s_ev1)
     pk = peaks()
+    traffic = gemm_traffic()
     roof = {"kernel": "sg_gemm (tcgen05 persistent GEMM)", "bound": "tensor", "achieved": gsum["tflops"],
             "peak": pk["bf16_sustained"], "unit": "TFLOP/s", "frac": gsum["tflops"] / pk["bf16_sustained"],
-            "traffic": None, "peak_source": pk["src"] + " sustained bf16",
+            "traffic": None if traffic is None else traffic["traffic_bytes_per_launch"],
+            "traffic_source": None if traffic is None else traffic["file"],
+            "peak_source": pk["src"] + " sustained bf16",
             "launches_per_step": gsum["launches"], "gemm_ms_per_step": gsum["ms"],
             "gemm_share_of_step": gsum["ms"] / inst_step_ms if inst_step_ms > 0 else None,
             "algorithmic_flops_per_step": gsum["flops"]}
