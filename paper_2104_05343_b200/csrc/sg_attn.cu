@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sg.h"
@@ -263,6 +264,286 @@ __global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
   if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 
+// ============================================================================
+// Forward, d = 64, two query tiles per CTA ("ping-pong"): 384 threads
+//   warp 0      TMA: Q0, Q1 once; K_j / V_j blocks (three slots)
+//   warp 1      MMA issuer: S_i,j+1 = Q_i K_j+1^T is issued as soon as softmax i has
+//               pulled S_i,j into registers, PV_i,j = P_i,j V_j when P_i,j is in
+//               smem, so the tensor core works on one tile's products while the
+//               softmax warpgroups work on their exponentials
+//   warp 2      TMEM allocator: S0 | S1 | O0 | O1 (512 columns)
+//   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1 (thread = query row)
+// Each score block is read from TMEM once (the 128-key row in registers); O
+// accumulates in TMEM across key blocks; the row max used for the exponent only
+// advances (O and l rescaled through tcgen05.ld/st) when it grows by more than
+// 2^8, so most blocks need no correction. Scale/shift and the row sums use the
+// paired fp32 pipe (FFMA2 / FADD2).
+// ============================================================================
+constexpr int kQT = 2;  // query tiles per CTA
+
+struct Flash2Cfg {
+  static constexpr uint32_t T64 = 128 * 64 * 2;   // one 128 x 64 bf16 tile
+  static constexpr uint32_t P_BYTES = 2 * T64;     // 128 rows x 128 keys (2 atoms)
+  static constexpr int KV_SLOTS = 3;
+  static constexpr size_t SMEM = kQT * T64 + KV_SLOTS * 2 * T64 + kQT * P_BYTES + 256;
+};
+
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  return static_cast<uint64_t>(__float_as_uint(a)) | (static_cast<uint64_t>(__float_as_uint(b)) << 32);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t y, uint64_t z) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(y), "l"(z));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return r;
+}
+
+__global__ void __launch_bounds__(384, 1)
+    flash_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p) {
+  using Cfg = Flash2Cfg;
+  constexpr uint32_t T64 = Cfg::T64;
+  constexpr int NS = Cfg::KV_SLOTS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* sQ = smem;                 // [kQT] tiles
+  uint8_t* sK = sQ + kQT * T64;       // [NS]
+  uint8_t* sV = sK + NS * T64;        // [NS]
+  uint8_t* sP = sV + NS * T64;        // [kQT] x 2 atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kQT * Cfg::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;            // [NS]
+  uint64_t* v_full = bars + 1 + NS;       // [NS]
+  uint64_t* kv_empty = bars + 1 + 2 * NS; // [NS]
+  uint64_t* s_full = bars + 1 + 3 * NS;   // [kQT]
+  uint64_t* s_free = s_full + kQT;        // [kQT]
+  uint64_t* p_full = s_free + kQT;        // [kQT]
+  uint64_t* pv_done = p_full + kQT;       // [kQT]
+  uint64_t* o_full = pv_done + kQT;       // [kQT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + kQT);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int nkb = (p.s + kKB - 1) / kKB;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < kQT; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_full[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S_i at 128 i, O_i at 256 + 64 i
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, kQT * T64);
+#pragma unroll
+      for (int i = 0; i < kQT; ++i) tma4(&tmQ, sQ + i * T64, q_full, 0, (qb * kQT + i) * kQB, h, b, p.q_b2_first);
+      for (int j = 0; j < nkb; ++j) {
+        const int slot = j % NS;
+        mbar_wait(&kv_empty[slot], ((j / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[slot], T64);
+        tma4(&tmK, sK + slot * T64, &k_full[slot], 0, j * kKB, h, b, p.k_b2_first);
+        mbar_arrive_expect_tx(&v_full[slot], T64);
+        tma4(&tmV, sV + slot * T64, &v_full[slot], 0, j * kKB, h, b, p.v_b2_first);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
+      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P K-major, V MN-major
+      auto issue_s = [&](int i, int j) {
+        const uint32_t q_base = smem_u32(sQ + i * T64), k_base = smem_u32(sK + (j % NS) * T64);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem + i * 128, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
+                    IDESC_S, kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[i]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int i = 0; i < kQT; ++i) issue_s(i, 0);
+      for (int j = 0; j < nkb; ++j) {
+        const int slot = j % NS;
+        if (j + 1 < nkb) {
+          mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+          for (int i = 0; i < kQT; ++i) {
+            mbar_wait(&s_free[i], j & 1);  // softmax i holds S_i,j in registers
+            tc_fence_after();
+            issue_s(i, j + 1);
+          }
+        }
+        mbar_wait(&v_full[slot], (j / NS) & 1);
+        for (int i = 0; i < kQT; ++i) {
+          mbar_wait(&p_full[i], j & 1);  // P_i,j in smem, O_i corrected
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sP + i * Cfg::P_BYTES), v_base = smem_u32(sV + slot * T64);
+#pragma unroll
+          for (int kk = 0; kk < kKB / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * (kQB * 128) + (kk & 3) * 32, 0, 1024);
+            const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024);
+            umma_bf16(tmem + 256 + i * 64, ad, bd, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&pv_done[i]);
+          if (j + 1 == nkb) umma_commit(&o_full[i]);
+        }
+        umma_commit(&kv_empty[slot]);  // K_j, V_j no longer needed
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax tile i
+    const int i = (warp - 4) >> 2;
+    const int qd = warp & 3;                      // TMEM lane quadrant
+    const int r = qd * 32 + lane;                 // row inside the tile
+    const int qrow = (qb * kQT + i) * kQB + r;    // query position
+    const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
+    const uint32_t t_s = tmem + i * 128 + lane_base, t_o = tmem + 256 + i * 64 + lane_base;
+    uint8_t* prow_base = sP + i * Cfg::P_BYTES + r * 128;
+    const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
+    float m_use = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      const int kvalid = min(kKB, p.s - j * kKB);
+      mbar_wait(&s_full[i], j & 1);
+      tc_fence_after();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sv[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[i]);  // the MMA may overwrite S_i now
+      if (kvalid < kKB) {  // partial last block: keys past the end never contribute
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e >= kvalid) sv[c][e] = __float_as_uint(-INFINITY);
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(sv[c][e]));
+      const float m_cand = fmaxf(m_use, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2);
+      float alpha = 1.f;
+      bool correct = false;
+      if (j == 0) {
+        m_use = m_cand;
+      } else if (__any_sync(0xffffffffu, m_cand > m_use + 8.f)) {
+        alpha = ex2f_fast(m_use - m_cand);
+        m_use = m_cand;
+        correct = true;
+      }
+      const uint64_t neg2 = f2_pack(-m_use, -m_use);
+      // PV_i,j-1 has finished reading P_i (and writing O_i)
+      if (j > 0) mbar_wait(&pv_done[i], (j - 1) & 1);
+      uint64_t ps2 = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1])), scale2, neg2);
+          const float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
+          const float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
+          ps2 = fadd2(ps2, f2_pack(p0, p1));
+          __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+          pk[e] = *reinterpret_cast<uint32_t*>(&hv);
+        }
+        uint8_t* prow = prow_base + (c >> 1) * (kQB * 128);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
+          *reinterpret_cast<uint4*>(prow + (chunk << 4)) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        }
+      }
+      l = l * alpha + (__uint_as_float(static_cast<uint32_t>(ps2)) + __uint_as_float(static_cast<uint32_t>(ps2 >> 32)));
+      if (correct) {
+        // O_i row *= 2^(m_old - m_new) before PV_i,j accumulates into it
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(t_o + c * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st32(t_o + c * 32, ov);
+        }
+        tmem_wait_st();
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i]);
+    }
+    // O_i complete: normalise, bf16 row into the context block, lse
+    mbar_wait(&o_full[i], 0);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * 64;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(t_o + c * 32, ov);
+      tmem_wait_ld();
+      if (qrow < p.s) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 x;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv, __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
+        }
+      }
+    }
+    if (qrow < p.s && p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p, int b,
+                       cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(flash_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Flash2Cfg::SMEM) !=
+        cudaSuccess)
+      return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
+    attr = true;
+  }
+  dim3 grid((p.s + kQT * kQB - 1) / (kQT * kQB), p.nh, b);
+  flash_fwd2_kernel<<<grid, 384, Flash2Cfg::SMEM, stream>>>(q, k, v, p);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
 template <int HD>
 static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p,
                       int b, cudaStream_t stream) {
@@ -307,6 +588,11 @@ extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_
   if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, kKB, &p.v_b2_first);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static const int fwd_v1 = [] {
+    const char* e = getenv("SG_FLASH_FWD_V1");
+    return e ? atoi(e) : 0;
+  }();
+  if (d == 64 && !fwd_v1) return launch_fwd2(tq, tk, tv, p, (int)b, st);
   return d == 64 ? launch_fwd<64>(tq, tk, tv, p, (int)b, st) : launch_fwd<128>(tq, tk, tv, p, (int)b, st);
 }
 

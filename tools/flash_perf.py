@@ -33,3 +33,11 @@ t = timeit(lambda: K.flash_attn_bwd(qkv, dout, lse, drow, b, s, nh, d, dq, dqkv)
 print(f"flash bwd kernel: {t*1e3:.1f} us, {2.5*fl/t/1e9:.1f} TF/s")
 t = timeit(lambda: K.attn_rowdot(dout, out, nh, d, s, drow))
 print(f"rowdot: {t*1e3:.1f} us")
+# s = 2048 (GPT-shaped heads, d = 64 slice) for the forward
+b2, s2 = 4, 2048
+qkv2 = torch.randn(b2 * s2, 3 * hb, device="cuda").bfloat16()
+out2 = torch.empty(b2 * s2, hb, device="cuda", dtype=torch.bfloat16)
+lse2 = torch.empty(b2, nh, s2, device="cuda")
+fl2 = 4.0 * b2 * nh * s2 * s2 * d
+t = timeit(lambda: K.flash_attn_fwd(qkv2, b2, s2, nh, d, out2, lse2))
+print(f"flash fwd b={b2} s={s2} nh={nh} d={d}: {t*1e3:.1f} us, {fl2/t/1e9:.1f} TF/s")
