@@ -839,6 +839,265 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ----------------------------------------------------------------------------
+// Backward v2 (d = 64): same CTA decomposition, pipelined. Per query block i:
+//   MMA   S_i+1, dP_i+1 are issued right after P_i / dS_i land in smem, ahead of
+//         dV_i, dK_i, dQ_i, so block i+1's exponentials overlap block i's products;
+//         dQ alternates between two TMEM buffers
+//   warps 4-7 compute P_i+1 / dS_i+1 for the whole 128-key row in registers, wait
+//         only for the previous products to release the smem tiles, then drain
+//         dQ_i (TMEM -> smem -> TMA reduce-add) one block behind
+//   lse / D row statistics are prefetched a block ahead.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(384, 1)
+    flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* sK = smem;                 // 16 KB
+  uint8_t* sV = sK + kT64;            // 16 KB
+  uint8_t* sQ = sV + kT64;            // 2 slots
+  uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
+  uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
+  uint8_t* sDS = sP + 2 * kT64;       // 32 KB
+  uint8_t* sStg = sDS + 2 * kT64;     // 8 warps x 4 KB dQ staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;    // [2]
+  uint64_t* qd_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* bufs_free = bars + 7;
+  uint64_t* dq_full = bars + 8;    // [2]
+  uint64_t* dq_empty = bars + 10;  // [2]
+  uint64_t* acc_full = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int nqb = (p.s + 127) / 128;
+  const int kvalid = min(128, p.s - kb * 128);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmDQ);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_empty[i], 8);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(bufs_free, 1);
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * kT64);
+      tma4(&tmK, sK, kv_full, 0, kb * 128, h, b, p.k_b2_first);
+      tma4(&tmV, sV, kv_full, 0, kb * 128, h, b, p.v_b2_first);
+      for (int i = 0; i < nqb; ++i) {
+        const int slot = i & 1;
+        mbar_wait(&qd_empty[slot], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
+        tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
+        tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
+      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
+      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, false, true);    // dQ: A = dS, B = K
+      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+      auto issue_sdp = [&](int i) {
+        const int slot = i & 1;
+        mbar_wait(&qd_full[slot], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
+          umma_bf16(t_s, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
+                    ID_SQ, kk > 0 ? 1u : 0u);
+          umma_bf16(t_dp, umma_desc_sw128(do_base + kk * 32, 0, 1024), umma_desc_sw128(v_base + kk * 32, 0, 1024),
+                    ID_SQ, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_sdp(0);
+      for (int i = 0; i < nqb; ++i) {
+        const int slot = i & 1;
+        mbar_wait(ds_full, i & 1);  // P_i, dS_i in smem; S_i / dP_i read
+        tc_fence_after();
+        if (i + 1 < nqb) issue_sdp(i + 1);
+        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
+          const uint32_t acc = (i | kq) != 0 ? 1u : 0u;
+          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, 2 * 8192, 1024),
+                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
+          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, 2 * 8192, 1024),
+                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
+        }
+        umma_commit(&qd_empty[slot]);
+        if (i >= 2) mbar_wait(&dq_empty[slot], ((i - 2) >> 1) & 1);  // dQ_i-2 drained from this buffer
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
+          umma_bf16(t_dq + slot * 64, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
+                    umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&dq_full[slot]);
+        umma_commit(bufs_free);  // P_i / dS_i no longer read
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    // 8 warps: warp e owns TMEM lane quadrant e % 4 (32 query rows) and key half
+    // e / 4 (64 of the 128 key columns = one 64-key atom of P / dS)
+    const int e = warp - 4;
+    const int q = e & 3, half = e >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sStg + e * 4096;
+    const size_t head_off = ((size_t)b * p.nh + h) * p.s;
+    const float scale = p.scale, scale_log2 = p.scale_log2;
+    const bool full_keys = kvalid == 128;
+    // raw loads only: converting here would make the prefetch wait for the load
+    auto row_stats = [&](int i, float& lse, float& dd) {
+      const int qrow = i * 128 + r;
+      const bool ok = i < nqb && qrow < p.s;
+      lse = ok ? __ldg(p.lse + head_off + qrow) : 0.f;
+      dd = ok ? __ldg(p.drow + head_off + qrow) : 0.f;
+    };
+    // dQ columns [32 half, 32 half + 32) of query block i: TMEM -> fp32 staging ->
+    // TMA reduce-add, then release the buffer
+    auto drain_dq = [&](int i) {
+      const int slot = i & 1;
+      mbar_wait(&dq_full[slot], (i >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+      uint32_t v[32];
+      tmem_ld32(t_dq + slot * 64 + lane_base + half * 32, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+            make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
+                        __uint_as_float(v[4 * k + 3]));
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&dq_empty[slot]);
+        if (p.dq_b2_first)
+          tma_reduce_add_4d(&tmDQ, stg, half * 32, h, i * 128 + q * 32, b);
+        else
+          tma_reduce_add_4d(&tmDQ, stg, half * 32, i * 128 + q * 32, h, b);
+        bulk_commit();
+      }
+    };
+    float lse2_n, dd_n;
+    row_stats(0, lse2_n, dd_n);
+    for (int i = 0; i < nqb; ++i) {
+      const float lse_c = lse2_n, dd = dd_n;
+      row_stats(i + 1, lse2_n, dd_n);  // prefetch
+      const bool qok = i * 128 + r < p.s;
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+      const float lse2 = lse_c * 1.4426950408889634f;
+      uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;  // 32-key chunk
+        uint32_t sv[32], dv[32];
+        tmem_ld32(t_s + lane_base + c * 32, sv);
+        tmem_ld32(t_dp + lane_base + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2) {
+          float p0 = ex2f_fast(fmaf(__uint_as_float(sv[2 * e2]), scale_log2, -lse2));
+          float p1 = ex2f_fast(fmaf(__uint_as_float(sv[2 * e2 + 1]), scale_log2, -lse2));
+          if (!full_keys || !qok) {
+            if (!qok || c * 32 + 2 * e2 >= kvalid) p0 = 0.f;
+            if (!qok || c * 32 + 2 * e2 + 1 >= kvalid) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dv[2 * e2]) - dd) * scale;
+          const float d1 = p1 * (__uint_as_float(dv[2 * e2 + 1]) - dd) * scale;
+          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
+          pk[cc][e2] = *reinterpret_cast<uint32_t*>(&hp);
+          dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
+        }
+      }
+      // the previous block's dV / dK / dQ products have finished reading P / dS
+      if (i > 0) mbar_wait(bufs_free, (i - 1) & 1);
+      uint8_t* prow = sP + half * kT64 + r * 128;
+      uint8_t* drow_ = sDS + half * kT64 + r * 128;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int chunk = (cc * 4 + k) ^ (r & 7);
+          *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
+              make_uint4(pk[cc][4 * k], pk[cc][4 * k + 1], pk[cc][4 * k + 2], pk[cc][4 * k + 3]);
+          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
+              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (i > 0) drain_dq(i - 1);
+    }
+    drain_dq(nqb - 1);
+    // dK, dV of this key block: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int key = kb * 128 + r;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tsrc = (which == 0 ? t_dk : t_dv) + lane_base + half * 32;
+      __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64 + half * 32;
+      uint32_t v[32];
+      tmem_ld32(tsrc, v);
+      tmem_wait_ld();
+      if (key < p.s) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 x;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2)
+            hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e2]), __uint_as_float(v[8 * k + 2 * e2 + 1]));
+          *reinterpret_cast<uint4*>(dst + 8 * k) = x;
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace sg
 
 extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
@@ -872,12 +1131,20 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(flash_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
       return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
     attr = true;
   }
+  static const int bwd_v1 = [] {
+    const char* e = getenv("SG_FLASH_BWD_V1");
+    return e ? atoi(e) : 0;
+  }();
   dim3 grid((unsigned)((s + 127) / 128), (unsigned)nh, (unsigned)b);
-  flash_bwd_kernel<<<grid, 256, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
+  if (bwd_v1)
+    flash_bwd_kernel<<<grid, 256, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
+  else
+    flash_bwd2_kernel<<<grid, 384, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
