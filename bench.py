@@ -58,11 +58,17 @@ def parse():
     ap.add_argument("--checkpointing", action="store_true", help="activation checkpointing (recompute)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--summa-n", type=int, default=8192)
+    ap.add_argument("--mode", choices=("train", "infer"), default="train",
+                    help="train: fwd+bwd+SGD step; infer: forward (with the CE loss, as the reference) only")
+    ap.add_argument("--max-batch", action="store_true",
+                    help="after the timed run, find the largest global batch that fits (doubling, then bisection)")
     return ap.parse_args()
 
 
 def workload(args) -> dict:
     w = dict(WORKLOADS[args.workload])
+    if args.mode == "infer":
+        w["name"] = w["name"].replace("-train", "-infer")
     if args.batch:
         w["b"] = args.batch
     if args.layers:
@@ -70,11 +76,20 @@ def workload(args) -> dict:
     return w
 
 
-def model_flops(w: dict) -> float:
-    """Algorithmic FLOPs of one fwd+bwd step (costmodel.py:63-65 x3, + lm-head 2bsvh x3)."""
+def model_flops(w: dict, mode: str = "train") -> float:
+    """Algorithmic FLOPs of one fwd+bwd step (costmodel.py:63-65 x3, + lm-head 2bsvh x3), or of
+    the forward alone in inference mode."""
     b, s, h, v, L = w["b"], w["s"], w["h"], w["v"], w["layers"]
     per_layer_fwd = 2.0 * (12 * b * s * h * h + 2 * b * s * s * h)
-    return 3.0 * (L * per_layer_fwd + 2.0 * b * s * v * h)
+    return (1.0 if mode == "infer" else 3.0) * (L * per_layer_fwd + 2.0 * b * s * v * h)
+
+
+def cpu_sample(w: dict, mode: str) -> dict:
+    from oracle import cpu_bench
+
+    if mode == "infer":
+        return cpu_bench.inference_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=1)
+    return cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
 
 
 def peaks() -> dict:
@@ -157,7 +172,7 @@ def run_reference(args):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
+        r = cpu_sample(w, args.mode)
         if i >= args.warmup:
             vals.append(r["samples_per_s"])
     v = statistics.mean(vals)
@@ -178,7 +193,7 @@ def _config(w, n_gpus, args, extra=None) -> dict:
            "global_batch": w["b"], "seq_len": w["s"], "hidden": w["h"], "heads": w["n"], "layers": w["layers"],
            "vocab": w["v"], "mesh": f"{mc.rows}x{mc.cols}", "parallelism": f"2d-summa r{mc.rows}xc{mc.cols}",
            "checkpointing": bool(args.checkpointing), "cuda_graph": (not args.no_graph) and n_gpus == 1,
-           "optimizer": "sgd", "l2": "working set (weights fp32+bf16, >10 GB activations) larger than the 126 MB L2"}
+           "mode": args.mode, "optimizer": "sgd" if args.mode == "train" else None, "l2": "working set (weights fp32+bf16, >10 GB activations) larger than the 126 MB L2"}
     if extra:
         cfg.update(extra)
     return cfg
@@ -219,6 +234,8 @@ def main():
     lr = 1e-4
 
     def step():
+        if args.mode == "infer":
+            return model.infer(tok_d, lab_d, ws)
         return model.train_step(tok_d, lab_d, ws, lr, checkpointing=args.checkpointing)
 
     def barrier():
@@ -330,12 +347,21 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_bench
 
-        r = cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
+        r = cpu_sample(w, args.mode)
         cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": cpu_bench.host_cores(), "kind": "port",
                "sample": r["sample"]}
 
+    maxb = None
+    if args.max_batch:
+        import gc
+
+        # free the timed model (and the captured graph's pool) before probing
+        run = step = graph = model = ws = None
+        gc.collect()
+        torch.cuda.empty_cache()
+        maxb = max_batch_sweep(sg, mesh, w, args, world)
     if rank == 0:
-        flops = model_flops(w)
+        flops = model_flops(w, args.mode)
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids)",
@@ -344,9 +370,69 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches), "roofline": roof, "summa": summa, "cpu_baseline": cpu,
                 "clocks": clocks.summary(), "final_loss": final_loss}
+        if maxb is not None:
+            line["max_batch"] = maxb
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def max_batch_sweep(sg, mesh, w, args, world) -> dict:
+    """Largest global batch whose step (train or infer) runs without running out of HBM:
+    double from the bench batch, then bisect. Same mesh and
+    model size; a fresh random-init model per probe."""
+    import gc
+
+    import numpy as np
+    import torch
+
+    r = mesh.r
+
+    def fits(b: int) -> bool:
+        model = ws = tok = lab = None
+        ok = True
+        try:
+            cfg = sg.ModelConfig(b=b, s=w["s"], h=w["h"], n=w["n"], v=w["v"], num_layers=w["layers"])
+            model = sg.MeshModel(mesh, cfg, None, seed=1234)
+            ws = model.make_workspace()
+            rng = np.random.default_rng(1)
+            tok = torch.from_numpy(rng.integers(0, cfg.v, (b, cfg.s))).cuda()
+            lab = torch.from_numpy(rng.integers(0, cfg.v, (b, cfg.s))).cuda()
+            if args.mode == "infer":
+                model.infer(tok, lab, ws)
+            else:
+                model.train_step(tok, lab, ws, 1e-4, checkpointing=args.checkpointing)
+            torch.cuda.synchronize()
+        except torch.cuda.OutOfMemoryError:
+            ok = False
+        del model, ws, tok, lab
+        gc.collect()
+        torch.cuda.empty_cache()
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([1.0 if ok else 0.0], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            ok = bool(t.item() > 0.5)
+        return ok
+
+    tried = {}
+    lo, hi = 0, None
+    b = max(w["b"], r)
+    while hi is None and b <= 1 << 16:
+        tried[b] = fits(b)
+        if tried[b]:
+            lo, b = b, 2 * b
+        else:
+            hi = b
+    while hi is not None and hi - lo > max(r, lo // 8):
+        mid = (lo + hi) // 2 // r * r
+        if mid <= lo:
+            break
+        tried[mid] = fits(mid)
+        lo, hi = (mid, hi) if tried[mid] else (lo, mid)
+    return {"max_batch": lo, "first_oom": hi, "probes": {str(k): v for k, v in sorted(tried.items())},
+            "mode": args.mode, "hbm_gb": torch.cuda.get_device_properties(0).total_memory / 1e9}
 
 
 def summa_point(sg, K, mesh, n, pk, barrier, world) -> dict:

@@ -95,6 +95,44 @@ def training_samples_per_sec(h: int, n: int, s: int, v: int, layers: int, b_samp
                       f"n={n}, v={v}; step time = head + {layers} x layer (extrapolated)"}
 
 
+def time_layer_forward(cfg: M.RefConfig, seed: int = 0) -> float:
+    """Seconds for one pre-norm layer forward at cfg.b (layers.py:700-725)."""
+    rng = np.random.default_rng(seed)
+    p = _layer_params(cfg, rng)
+    x = rng.standard_normal((cfg.b * cfg.s, cfg.h))
+    t0 = time.perf_counter()
+    a1, _ = M.layernorm(x, p["ln1_gamma"], p["ln1_beta"], cfg.eps)
+    att, _ = M.attention(a1, p["w_qkv"], p["b_qkv"], p["w_dense"], p["b_dense"], cfg)
+    y1 = x + att
+    a2, _ = M.layernorm(y1, p["ln2_gamma"], p["ln2_beta"], cfg.eps)
+    _ = y1 + M.gelu(a2 @ p["w1"] + p["b1"]) @ p["w2"] + p["b2"]
+    return time.perf_counter() - t0
+
+
+def time_head_forward(cfg: M.RefConfig, seed: int = 0) -> float:
+    """Seconds for embedding + tied lm-head + mean cross entropy, forward only."""
+    rng = np.random.default_rng(seed)
+    table = rng.uniform(-1 / np.sqrt(cfg.h), 1 / np.sqrt(cfg.h), (cfg.v, cfg.h))
+    tokens = rng.integers(0, cfg.v, (cfg.b, cfg.s)).reshape(-1)
+    labels = rng.integers(0, cfg.v, (cfg.b, cfg.s)).reshape(-1)
+    x = rng.standard_normal((cfg.b * cfg.s, cfg.h))
+    t0 = time.perf_counter()
+    _ = table[tokens]
+    M.cross_entropy(x @ table.T, labels)
+    return time.perf_counter() - t0
+
+
+def inference_samples_per_sec(h: int, n: int, s: int, v: int, layers: int, b_sample: int = 1) -> dict:
+    """Extrapolated CPU forward (inference) throughput of the full stack from a bounded sample."""
+    cfg = M.RefConfig(b=b_sample, s=s, h=h, n=n, v=v, num_layers=1)
+    t_layer = time_layer_forward(cfg)
+    t_head = time_head_forward(cfg)
+    t_step = t_head + layers * t_layer
+    return {"samples_per_s": b_sample / t_step, "t_layer_s": t_layer, "t_head_s": t_head,
+            "sample": f"oracle fp64 forward of 1 layer + embedding/lm-head/CE at b={b_sample}, s={s}, h={h}, "
+                      f"n={n}, v={v}; forward time = head + {layers} x layer (extrapolated)"}
+
+
 def summa_tflops(n: int = 4096) -> dict:
     """fp64 numpy product at N^3 (the reference's local_matmul, mesh.py:354-361)."""
     rng = np.random.default_rng(0)

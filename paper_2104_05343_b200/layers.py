@@ -494,7 +494,12 @@ def fused_softmax_ok(cfg: ModelConfig) -> bool:
 
 
 def flash_ok(cfg: ModelConfig) -> bool:
-    """The tcgen05 flash kernels (sg_attn.cu) cover head_dim 64 at any sequence length."""
+    """The tcgen05 flash forward (sg_attn.cu) covers head_dim 64 and 128 at any sequence length."""
+    return FLASH_ATTENTION and cfg.head_dim in (64, 128)
+
+
+def flash_bwd_ok(cfg: ModelConfig) -> bool:
+    """The flash backward covers head_dim 64; otherwise P is rebuilt from Q, K (AttentionContext.probs)."""
     return FLASH_ATTENTION and cfg.head_dim == 64
 
 
@@ -593,7 +598,7 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
         v = _heads_view(blk[:, 2 * hb:], b_loc, s, n_loc, d)
         dq_blk = ws.empty(dev, (bs_loc, 3 * hb), "free", dtype=BF16)
         dqkv_blocks[dev] = dq_blk
-        if ctx.lse is not None:
+        if ctx.lse is not None and flash_bwd_ok(cfg):
             # flash backward: P rebuilt per tile from lse, never in HBM; D = rowsum(dO O)
             drow = ws.empty(dev, (b_loc, n_loc, s), "free", dtype=F32, pad=False)
             K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)

@@ -233,6 +233,21 @@ class MeshModel:
         sgd_matrix(self.table, grads.table, lr)
         return loss
 
+    def infer(self, tokens, labels, ws: Workspace) -> torch.Tensor:
+        """Forward-only pass (the paper's inference = b / forward time): the
+        reference always computes the CE loss (model.py:296-324); no layer state is kept,
+        so memory is one layer's activations plus the logits."""
+        cfg = self.cfg
+        if tuple(tokens.shape) != (cfg.b, cfg.s):
+            raise ShapeError(f"tokens must be [{cfg.b}, {cfg.s}], got {tuple(tokens.shape)}")
+        ids = _device_ids(self.mesh, tokens)
+        x = embedding_forward(tokens, self.table, cfg, ws, out_category="forward", ids=ids)
+        for layer in self.layers:
+            x, _ = layer.forward(x, ws)
+        logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
+        loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True)
+        return loss
+
     # ------------------------------------------------------------------ gather for parity
     def gather_params(self) -> dict[str, np.ndarray]:
         c, cfg = self.mesh.c, self.cfg

@@ -127,3 +127,41 @@ def test_sgd_step_reduces_loss_and_train_step():
     p_got = model2.gather_params()
     for k in p_ref:
         assert rel(p_got[k], p_ref[k]) < 1e-5, k
+
+
+@pytest.mark.parametrize("rc", [(1, 1), (2, 2)])
+@pytest.mark.parametrize("d", [64, 128])
+def test_infer_matches_oracle_loss(rc, d):
+    """Forward-only inference (MeshModel.infer, no saved state) gives the oracle loss;
+    head_dim 128 runs the d=128 flash forward (model.py:296-324)."""
+    import torch
+
+    sg = _sg()
+    m = mesh(*rc)
+    n = 2 * rc[1]
+    h = n * d
+    cfg = sg.ModelConfig(b=4, s=128, h=h, n=n, v=64, num_layers=1)
+    rcfg = M.RefConfig(cfg.b, cfg.s, cfg.h, cfg.n, cfg.v, cfg.num_layers)
+    params = {k: bf16_round(v) for k, v in M.init_params(rcfg, 5).items()}
+    tokens, labels = M.sample_data(rcfg, 5)
+    model = sg.MeshModel(m, cfg, params)
+    ws = model.make_workspace()
+    loss = float(model.infer(torch.as_tensor(tokens), torch.as_tensor(labels), ws).item())
+    ref_loss, _ = M.serial_forward(rcfg, params, tokens, labels)
+    assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3
+
+
+def test_head_dim_128_training_vs_oracle():
+    """d = 128: flash forward, backward through the rebuilt probabilities."""
+    sg = _sg()
+    m = mesh(1, 2)
+    cfg = sg.ModelConfig(b=2, s=128, h=512, n=4, v=64, num_layers=1)
+    rcfg = M.RefConfig(cfg.b, cfg.s, cfg.h, cfg.n, cfg.v, cfg.num_layers)
+    params = {k: bf16_round(v) for k, v in M.init_params(rcfg, 9).items()}
+    tokens, labels = M.sample_data(rcfg, 9)
+    model = sg.MeshModel(m, cfg, params)
+    loss, grads, _, _ = sg.run_loss_and_grads(model, tokens, labels, checkpointing=False)
+    ref_loss, saved = M.serial_forward(rcfg, params, tokens, labels)
+    ref = M.serial_backward(rcfg, params, saved)
+    assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3
+    _compare_grads(sg, model.gather_grads(grads), {k: v for k, v in ref.items() if not k.startswith("_")})
