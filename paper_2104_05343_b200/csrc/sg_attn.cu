@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -285,7 +286,8 @@ struct Flash2Cfg {
   static constexpr uint32_t T64 = 128 * 64 * 2;   // one 128 x 64 bf16 tile
   static constexpr uint32_t P_BYTES = 2 * T64;     // 128 rows x 128 keys (2 atoms)
   static constexpr int KV_SLOTS = 3;
-  static constexpr size_t SMEM = kQT * T64 + KV_SLOTS * 2 * T64 + kQT * P_BYTES + 256;
+  static constexpr int Q_SLOTS = 2;                // Q of the next item prefetched
+  static constexpr size_t SMEM = Q_SLOTS * kQT * T64 + KV_SLOTS * 2 * T64 + kQT * P_BYTES + 256;
 };
 
 __device__ __forceinline__ uint64_t f2_pack(float a, float b) {
@@ -302,25 +304,31 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
   return r;
 }
 
+// Persistent: CTA c processes work items t = c, c + grid, ... with t = (query-tile
+// pair, head, batch), pair index fastest (neighbouring CTAs share K / V in L2).
+// All per-block barriers run on a CTA-wide block counter G across items, so the
+// next item's Q, first K / V block and first score products are in flight while
+// the current item finishes.
 __global__ void __launch_bounds__(384, 1)
     flash_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p) {
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p, int bsz) {
   using Cfg = Flash2Cfg;
   constexpr uint32_t T64 = Cfg::T64;
   constexpr int NS = Cfg::KV_SLOTS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
-  uint8_t* sQ = smem;                 // [kQT] tiles
-  uint8_t* sK = sQ + kQT * T64;       // [NS]
-  uint8_t* sV = sK + NS * T64;        // [NS]
-  uint8_t* sP = sV + NS * T64;        // [kQT] x 2 atoms
+  uint8_t* sQ = smem;                             // [Q_SLOTS][kQT] tiles
+  uint8_t* sK = sQ + Cfg::Q_SLOTS * kQT * T64;    // [NS]
+  uint8_t* sV = sK + NS * T64;                    // [NS]
+  uint8_t* sP = sV + NS * T64;                    // [kQT] x 2 atoms
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kQT * Cfg::P_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;            // [NS]
-  uint64_t* v_full = bars + 1 + NS;       // [NS]
-  uint64_t* kv_empty = bars + 1 + 2 * NS; // [NS]
-  uint64_t* s_full = bars + 1 + 3 * NS;   // [kQT]
+  uint64_t* q_full = bars;                // [2]
+  uint64_t* q_empty = bars + 2;           // [2]
+  uint64_t* k_full = bars + 4;            // [NS]
+  uint64_t* v_full = k_full + NS;         // [NS]
+  uint64_t* kv_empty = v_full + NS;       // [NS]
+  uint64_t* s_full = kv_empty + NS;       // [kQT]
   uint64_t* s_free = s_full + kQT;        // [kQT]
   uint64_t* p_full = s_free + kQT;        // [kQT]
   uint64_t* pv_done = p_full + kQT;       // [kQT]
@@ -328,14 +336,24 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + kQT);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int nkb = (p.s + kKB - 1) / kKB;
+  const int npairs = (p.s + kQT * kQB - 1) / (kQT * kQB);
+  const int n_items = npairs * p.nh * bsz;
+  auto decode = [&](int t, int& qb, int& h, int& b) {
+    qb = t % npairs;
+    const int r = t / npairs;
+    h = r % p.nh;
+    b = r / p.nh;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -358,47 +376,65 @@ __global__ void __launch_bounds__(384, 1)
   // TMEM columns: S_i at 128 i, O_i at 256 + 64 i
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, kQT * T64);
+      int g = 0;
+      for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
+        int qb, h, b;
+        decode(t, qb, h, b);
+        const int qs = it & 1;
+        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], kQT * T64);
 #pragma unroll
-      for (int i = 0; i < kQT; ++i) tma4(&tmQ, sQ + i * T64, q_full, 0, (qb * kQT + i) * kQB, h, b, p.q_b2_first);
-      for (int j = 0; j < nkb; ++j) {
-        const int slot = j % NS;
-        mbar_wait(&kv_empty[slot], ((j / NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[slot], T64);
-        tma4(&tmK, sK + slot * T64, &k_full[slot], 0, j * kKB, h, b, p.k_b2_first);
-        mbar_arrive_expect_tx(&v_full[slot], T64);
-        tma4(&tmV, sV + slot * T64, &v_full[slot], 0, j * kKB, h, b, p.v_b2_first);
+        for (int i = 0; i < kQT; ++i)
+          tma4(&tmQ, sQ + (qs * kQT + i) * T64, &q_full[qs], 0, (qb * kQT + i) * kQB, h, b, p.q_b2_first);
+        for (int j = 0; j < nkb; ++j, ++g) {
+          const int slot = g % NS;
+          mbar_wait(&kv_empty[slot], ((g / NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[slot], T64);
+          tma4(&tmK, sK + slot * T64, &k_full[slot], 0, j * kKB, h, b, p.k_b2_first);
+          mbar_arrive_expect_tx(&v_full[slot], T64);
+          tma4(&tmV, sV + slot * T64, &v_full[slot], 0, j * kKB, h, b, p.v_b2_first);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
       constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P K-major, V MN-major
-      auto issue_s = [&](int i, int j) {
-        const uint32_t q_base = smem_u32(sQ + i * T64), k_base = smem_u32(sK + (j % NS) * T64);
+      const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+      const int total = my_items * nkb;  // this CTA's key blocks over all its items
+      // S_i for global block G (item G / nkb, key block G % nkb)
+      auto issue_s = [&](int i, int G) {
+        const int it = G / nkb;
+        const uint32_t q_base = smem_u32(sQ + ((it & 1) * kQT + i) * T64), k_base = smem_u32(sK + (G % NS) * T64);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16(tmem + i * 128, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
                     IDESC_S, kk > 0 ? 1u : 0u);
         umma_commit(&s_full[i]);
       };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      for (int i = 0; i < kQT; ++i) issue_s(i, 0);
-      for (int j = 0; j < nkb; ++j) {
-        const int slot = j % NS;
-        if (j + 1 < nkb) {
-          mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+      auto ready_s = [&](int G) {  // Q of G's item (at its first block) and K_G landed
+        if (G % nkb == 0) mbar_wait(&q_full[(G / nkb) & 1], ((G / nkb) >> 1) & 1);
+        mbar_wait(&k_full[G % NS], (G / NS) & 1);
+        tc_fence_after();
+      };
+      if (total > 0) {
+        ready_s(0);
+        for (int i = 0; i < kQT; ++i) issue_s(i, 0);
+      }
+      for (int G = 0; G < total; ++G) {
+        const int slot = G % NS, j = G % nkb;
+        if (G + 1 < total) {
+          ready_s(G + 1);
           for (int i = 0; i < kQT; ++i) {
-            mbar_wait(&s_free[i], j & 1);  // softmax i holds S_i,j in registers
+            mbar_wait(&s_free[i], G & 1);  // softmax i holds S_i,G in registers
             tc_fence_after();
-            issue_s(i, j + 1);
+            issue_s(i, G + 1);
           }
         }
-        mbar_wait(&v_full[slot], (j / NS) & 1);
+        if (j == nkb - 1) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score products issued
+        mbar_wait(&v_full[slot], (G / NS) & 1);
         for (int i = 0; i < kQT; ++i) {
-          mbar_wait(&p_full[i], j & 1);  // P_i,j in smem, O_i corrected
+          mbar_wait(&p_full[i], G & 1);  // P_i,G in smem, O_i corrected (or read out, first block)
           tc_fence_after();
           const uint32_t p_base = smem_u32(sP + i * Cfg::P_BYTES), v_base = smem_u32(sV + slot * T64);
 #pragma unroll
@@ -408,9 +444,9 @@ __global__ void __launch_bounds__(384, 1)
             umma_bf16(tmem + 256 + i * 64, ad, bd, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
           }
           umma_commit(&pv_done[i]);
-          if (j + 1 == nkb) umma_commit(&o_full[i]);
+          if (j == nkb - 1) umma_commit(&o_full[i]);
         }
-        umma_commit(&kv_empty[slot]);  // K_j, V_j no longer needed
+        umma_commit(&kv_empty[slot]);  // K_G, V_G no longer needed
       }
     }
   } else if (warp >= 4) {
@@ -418,110 +454,120 @@ __global__ void __launch_bounds__(384, 1)
     const int i = (warp - 4) >> 2;
     const int qd = warp & 3;                      // TMEM lane quadrant
     const int r = qd * 32 + lane;                 // row inside the tile
-    const int qrow = (qb * kQT + i) * kQB + r;    // query position
     const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
     const uint32_t t_s = tmem + i * 128 + lane_base, t_o = tmem + 256 + i * 64 + lane_base;
     uint8_t* prow_base = sP + i * Cfg::P_BYTES + r * 128;
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
-    float m_use = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkb; ++j) {
-      const int kvalid = min(kKB, p.s - j * kKB);
-      mbar_wait(&s_full[i], j & 1);
-      tc_fence_after();
-      uint32_t sv[4][32];
+    int G = 0;
+    for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
+      int qb, h, b;
+      decode(t, qb, h, b);
+      const int qrow = (qb * kQT + i) * kQB + r;  // query position
+      float m_use = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkb; ++j, ++G) {
+        const int kvalid = min(kKB, p.s - j * kKB);
+        mbar_wait(&s_full[i], G & 1);
+        tc_fence_after();
+        uint32_t sv[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sv[c]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[i]);  // the MMA may overwrite S_i now
-      if (kvalid < kKB) {  // partial last block: keys past the end never contribute
+        for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sv[c]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[i]);  // the MMA may overwrite S_i now
+        if (kvalid < kKB) {  // partial last block: keys past the end never contribute
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e >= kvalid) sv[c][e] = __float_as_uint(-INFINITY);
+        }
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c * 32 + e >= kvalid) sv[c][e] = __float_as_uint(-INFINITY);
-      }
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(sv[c][e]));
-      const float m_cand = fmaxf(m_use, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2);
-      float alpha = 1.f;
-      bool correct = false;
-      if (j == 0) {
-        m_use = m_cand;
-      } else if (__any_sync(0xffffffffu, m_cand > m_use + 8.f)) {
-        alpha = ex2f_fast(m_use - m_cand);
-        m_use = m_cand;
-        correct = true;
-      }
-      const uint64_t neg2 = f2_pack(-m_use, -m_use);
-      // PV_i,j-1 has finished reading P_i (and writing O_i)
-      if (j > 0) mbar_wait(&pv_done[i], (j - 1) & 1);
-      uint64_t ps2 = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1])), scale2, neg2);
-          const float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
-          const float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
-          ps2 = fadd2(ps2, f2_pack(p0, p1));
-          __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-          pk[e] = *reinterpret_cast<uint32_t*>(&hv);
+          for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(sv[c][e]));
+        const float m_cand = fmaxf(m_use, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2);
+        float alpha = 1.f;
+        bool correct = false;
+        if (j == 0) {
+          m_use = m_cand;
+        } else if (__any_sync(0xffffffffu, m_cand > m_use + 8.f)) {
+          alpha = ex2f_fast(m_use - m_cand);
+          m_use = m_cand;
+          correct = true;
         }
-        uint8_t* prow = prow_base + (c >> 1) * (kQB * 128);
+        const uint64_t neg2 = f2_pack(-m_use, -m_use);
+        // PV_i,G-1 has finished reading P_i (and writing O_i)
+        if (G > 0) mbar_wait(&pv_done[i], (G - 1) & 1);
+        uint64_t ps2 = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
-          *reinterpret_cast<uint4*>(prow + (chunk << 4)) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint64_t y =
+                ffma2(f2_pack(__uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1])), scale2, neg2);
+            const float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
+            const float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
+            ps2 = fadd2(ps2, f2_pack(p0, p1));
+            __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+            pk[e] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          uint8_t* prow = prow_base + (c >> 1) * (kQB * 128);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
+            *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
+                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+          }
+        }
+        l = l * alpha + (__uint_as_float(static_cast<uint32_t>(ps2)) + __uint_as_float(static_cast<uint32_t>(ps2 >> 32)));
+        if (correct) {
+          // O_i row *= 2^(m_old - m_new) before PV_i,G accumulates into it
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(t_o + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st32(t_o + c * 32, ov);
+          }
+          tmem_wait_st();
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
+      }
+      // O_i of this item complete: normalise, bf16 row into the context block, lse.
+      // The next item's first PV overwrites O_i only after this warpgroup's next p_full.
+      mbar_wait(&o_full[i], it & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(t_o + c * 32, ov);
+        tmem_wait_ld();
+        if (qrow < p.s) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 x;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv,
+                                            __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
+            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
+          }
         }
       }
-      l = l * alpha + (__uint_as_float(static_cast<uint32_t>(ps2)) + __uint_as_float(static_cast<uint32_t>(ps2 >> 32)));
-      if (correct) {
-        // O_i row *= 2^(m_old - m_new) before PV_i,j accumulates into it
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t ov[32];
-          tmem_ld32(t_o + c * 32, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-          tmem_st32(t_o + c * 32, ov);
-        }
-        tmem_wait_st();
-      }
-      fence_proxy_async_smem();
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[i]);
+      if (qrow < p.s && p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
     }
-    // O_i complete: normalise, bf16 row into the context block, lse
-    mbar_wait(&o_full[i], 0);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * 64;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t ov[32];
-      tmem_ld32(t_o + c * 32, ov);
-      tmem_wait_ld();
-      if (qrow < p.s) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 x;
-          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv, __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
-        }
-      }
-    }
-    if (qrow < p.s && p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
   }
   tc_fence_before();
   __syncthreads();
@@ -537,8 +583,9 @@ static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
       return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
     attr = true;
   }
-  dim3 grid((p.s + kQT * kQB - 1) / (kQT * kQB), p.nh, b);
-  flash_fwd2_kernel<<<grid, 384, Flash2Cfg::SMEM, stream>>>(q, k, v, p);
+  const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
+  const int sms = sg_device_sm_count();
+  flash_fwd2_kernel<<<std::min(items, sms > 0 ? sms : 148), 384, Flash2Cfg::SMEM, stream>>>(q, k, v, p, b);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -840,45 +887,59 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ----------------------------------------------------------------------------
-// Backward v2 (d = 64): same CTA decomposition, pipelined. Per query block i:
-//   MMA   S_i+1, dP_i+1 are issued right after P_i / dS_i land in smem, ahead of
-//         dV_i, dK_i, dQ_i, so block i+1's exponentials overlap block i's products;
+// Backward v2 (d = 64), persistent: CTA c walks work items t = c, c + grid, ...
+// with t = (key block, head, batch), key block fastest. Per query block:
+//   MMA   S_G+1, dP_G+1 are issued right after P_G / dS_G land in smem, ahead of
+//         dV_G, dK_G, dQ_G, so the next block's exponentials overlap this block's
+//         products — across item boundaries too (K / V double-buffered per item);
 //         dQ alternates between two TMEM buffers
-//   warps 4-7 compute P_i+1 / dS_i+1 for the whole 128-key row in registers, wait
-//         only for the previous products to release the smem tiles, then drain
-//         dQ_i (TMEM -> smem -> TMA reduce-add) one block behind
+//   warps 4-11 (lane quadrant x key half) compute P / dS for their 64 keys in
+//         registers, wait only for the previous products to release the smem
+//         tiles, drain dQ (TMEM -> smem -> TMA reduce-add) one block behind, and
+//         at an item's end write its dK / dV and release the TMEM accumulators
 //   lse / D row statistics are prefetched a block ahead.
+// G counts query blocks over all of the CTA's items (barrier phases).
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(384, 1)
     flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p) {
+                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p, int bsz) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
-  uint8_t* sK = smem;                 // 16 KB
-  uint8_t* sV = sK + kT64;            // 16 KB
-  uint8_t* sQ = sV + kT64;            // 2 slots
+  uint8_t* sK = smem;                 // 2 slots (items)
+  uint8_t* sV = sK + 2 * kT64;        // 2 slots
+  uint8_t* sQ = sV + 2 * kT64;        // 2 slots (query blocks)
   uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
   uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
   uint8_t* sDS = sP + 2 * kT64;       // 32 KB
   uint8_t* sStg = sDS + 2 * kT64;     // 8 warps x 4 KB dQ staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
-  uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;    // [2]
-  uint64_t* qd_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* bufs_free = bars + 7;
-  uint64_t* dq_full = bars + 8;    // [2]
-  uint64_t* dq_empty = bars + 10;  // [2]
-  uint64_t* acc_full = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 4096);
+  uint64_t* kv_full = bars;        // [2]
+  uint64_t* kv_empty = bars + 2;   // [2]
+  uint64_t* qd_full = bars + 4;    // [2]
+  uint64_t* qd_empty = bars + 6;   // [2]
+  uint64_t* s_full = bars + 8;
+  uint64_t* ds_full = bars + 9;
+  uint64_t* bufs_free = bars + 10;
+  uint64_t* dq_full = bars + 11;   // [2]
+  uint64_t* dq_empty = bars + 13;  // [2]
+  uint64_t* acc_full = bars + 15;
+  uint64_t* acc_empty = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int nqb = (p.s + 127) / 128;
-  const int kvalid = min(128, p.s - kb * 128);
+  const int nkb = nqb;
+  const int n_items = nkb * p.nh * bsz;
+  auto decode = [&](int t, int& kb, int& h, int& b) {
+    kb = t % nkb;
+    const int r = t / nkb;
+    h = r % p.nh;
+    b = r / p.nh;
+  };
+  const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_items * nqb;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -886,8 +947,9 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
     tma_prefetch_desc(&tmDQ);
-    mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
       mbar_init(&dq_full[i], 1);
@@ -897,6 +959,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(ds_full, 8);
     mbar_init(bufs_free, 1);
     mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -908,15 +971,22 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * kT64);
-      tma4(&tmK, sK, kv_full, 0, kb * 128, h, b, p.k_b2_first);
-      tma4(&tmV, sV, kv_full, 0, kb * 128, h, b, p.v_b2_first);
-      for (int i = 0; i < nqb; ++i) {
-        const int slot = i & 1;
-        mbar_wait(&qd_empty[slot], ((i >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
-        tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
-        tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
+      int G = 0;
+      for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
+        int kb, h, b;
+        decode(t, kb, h, b);
+        const int ks = it & 1;
+        mbar_wait(&kv_empty[ks], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[ks], 2 * kT64);
+        tma4(&tmK, sK + ks * kT64, &kv_full[ks], 0, kb * 128, h, b, p.k_b2_first);
+        tma4(&tmV, sV + ks * kT64, &kv_full[ks], 0, kb * 128, h, b, p.v_b2_first);
+        for (int i = 0; i < nqb; ++i, ++G) {
+          const int slot = G & 1;
+          mbar_wait(&qd_empty[slot], ((G >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
+          tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
+          tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
+        }
       }
     }
   } else if (warp == 1) {
@@ -924,11 +994,13 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
       constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
       constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, false, true);    // dQ: A = dS, B = K
-      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), p_base = smem_u32(sP), ds_base = smem_u32(sDS);
-      auto issue_sdp = [&](int i) {
-        const int slot = i & 1;
-        mbar_wait(&qd_full[slot], (i >> 1) & 1);
+      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+      auto issue_sdp = [&](int G) {
+        const int it = G / nqb, slot = G & 1;
+        if (G % nqb == 0) mbar_wait(&kv_full[it & 1], (it >> 1) & 1);
+        mbar_wait(&qd_full[slot], (G >> 1) & 1);
         tc_fence_after();
+        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64), v_base = smem_u32(sV + (it & 1) * kT64);
         const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
@@ -939,13 +1011,18 @@ __global__ void __launch_bounds__(384, 1)
         }
         umma_commit(s_full);
       };
-      mbar_wait(kv_full, 0);
-      issue_sdp(0);
-      for (int i = 0; i < nqb; ++i) {
-        const int slot = i & 1;
-        mbar_wait(ds_full, i & 1);  // P_i, dS_i in smem; S_i / dP_i read
+      if (total > 0) issue_sdp(0);
+      for (int G = 0; G < total; ++G) {
+        const int slot = G & 1, it = G / nqb, i = G % nqb;
+        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem; S_G / dP_G read
         tc_fence_after();
-        if (i + 1 < nqb) issue_sdp(i + 1);
+        if (G + 1 < total) issue_sdp(G + 1);
+        // the previous item's dK / dV have been read out before this item's first products
+        if (i == 0 && it > 0) {
+          mbar_wait(acc_empty, (it - 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64);
         const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
@@ -956,7 +1033,7 @@ __global__ void __launch_bounds__(384, 1)
                     umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
         }
         umma_commit(&qd_empty[slot]);
-        if (i >= 2) mbar_wait(&dq_empty[slot], ((i - 2) >> 1) & 1);  // dQ_i-2 drained from this buffer
+        if (G >= 2) mbar_wait(&dq_empty[slot], ((G - 2) >> 1) & 1);  // dQ_G-2 drained from this buffer
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
@@ -964,9 +1041,12 @@ __global__ void __launch_bounds__(384, 1)
                     umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
         }
         umma_commit(&dq_full[slot]);
-        umma_commit(bufs_free);  // P_i / dS_i no longer read
+        umma_commit(bufs_free);  // P_G / dS_G no longer read
+        if (i == nqb - 1) {
+          umma_commit(acc_full);          // this item's dK / dV complete
+          umma_commit(&kv_empty[it & 1]);  // and its K / V no longer needed
+        }
       }
-      umma_commit(acc_full);
     }
   } else if (warp >= 4) {
     // 8 warps: warp e owns TMEM lane quadrant e % 4 (32 query rows) and key half
@@ -976,21 +1056,27 @@ __global__ void __launch_bounds__(384, 1)
     const int r = q * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     uint8_t* stg = sStg + e * 4096;
-    const size_t head_off = ((size_t)b * p.nh + h) * p.s;
     const float scale = p.scale, scale_log2 = p.scale_log2;
-    const bool full_keys = kvalid == 128;
     // raw loads only: converting here would make the prefetch wait for the load
-    auto row_stats = [&](int i, float& lse, float& dd) {
-      const int qrow = i * 128 + r;
-      const bool ok = i < nqb && qrow < p.s;
-      lse = ok ? __ldg(p.lse + head_off + qrow) : 0.f;
-      dd = ok ? __ldg(p.drow + head_off + qrow) : 0.f;
+    auto row_stats = [&](int G, float& lse, float& dd) {
+      lse = dd = 0.f;
+      if (G >= total) return;
+      int kb, h, b;
+      decode((int)blockIdx.x + (G / nqb) * (int)gridDim.x, kb, h, b);
+      const int qrow = (G % nqb) * 128 + r;
+      if (qrow >= p.s) return;
+      const size_t off = ((size_t)b * p.nh + h) * p.s + qrow;
+      lse = __ldg(p.lse + off);
+      dd = __ldg(p.drow + off);
     };
-    // dQ columns [32 half, 32 half + 32) of query block i: TMEM -> fp32 staging ->
-    // TMA reduce-add, then release the buffer
-    auto drain_dq = [&](int i) {
-      const int slot = i & 1;
-      mbar_wait(&dq_full[slot], (i >> 1) & 1);
+    // dQ columns [32 half, 32 half + 32) of global query block G: TMEM -> fp32
+    // staging -> TMA reduce-add, then release the buffer
+    auto drain_dq = [&](int G) {
+      const int slot = G & 1;
+      int kb, h, b;
+      decode((int)blockIdx.x + (G / nqb) * (int)gridDim.x, kb, h, b);
+      const int i = G % nqb;
+      mbar_wait(&dq_full[slot], (G >> 1) & 1);
       tc_fence_after();
       if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
@@ -1014,13 +1100,18 @@ __global__ void __launch_bounds__(384, 1)
         bulk_commit();
       }
     };
-    float lse2_n, dd_n;
-    row_stats(0, lse2_n, dd_n);
-    for (int i = 0; i < nqb; ++i) {
-      const float lse_c = lse2_n, dd = dd_n;
-      row_stats(i + 1, lse2_n, dd_n);  // prefetch
+    float lse_n, dd_n;
+    row_stats(0, lse_n, dd_n);
+    for (int G = 0; G < total; ++G) {
+      const int it = G / nqb, i = G % nqb;
+      int kb, h, b;
+      decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
+      const int kvalid = min(128, p.s - kb * 128);
+      const bool full_keys = kvalid == 128;
+      const float lse_c = lse_n, dd = dd_n;
+      row_stats(G + 1, lse_n, dd_n);  // prefetch
       const bool qok = i * 128 + r < p.s;
-      mbar_wait(s_full, i & 1);
+      mbar_wait(s_full, G & 1);
       tc_fence_after();
       const float lse2 = lse_c * 1.4426950408889634f;
       uint32_t pk[2][16], dk[2][16];
@@ -1047,7 +1138,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
       // the previous block's dV / dK / dQ products have finished reading P / dS
-      if (i > 0) mbar_wait(bufs_free, (i - 1) & 1);
+      if (G > 0) mbar_wait(bufs_free, (G - 1) & 1);
       uint8_t* prow = sP + half * kT64 + r * 128;
       uint8_t* drow_ = sDS + half * kT64 + r * 128;
 #pragma unroll
@@ -1065,32 +1156,38 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      if (i > 0) drain_dq(i - 1);
-    }
-    drain_dq(nqb - 1);
-    // dK, dV of this key block: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const int key = kb * 128 + r;
+      if (G > 0) drain_dq(G - 1);
+      if (i == nqb - 1) {
+        // this item's dK, dV: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
+        mbar_wait(acc_full, it & 1);
+        tc_fence_after();
+        const int key = kb * 128 + r;
+        uint32_t vk[32], vv[32];
+        tmem_ld32(t_dk + lane_base + half * 32, vk);
+        tmem_ld32(t_dv + lane_base + half * 32, vv);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
+        if (key < p.s) {
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = (which == 0 ? t_dk : t_dv) + lane_base + half * 32;
-      __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64 + half * 32;
-      uint32_t v[32];
-      tmem_ld32(tsrc, v);
-      tmem_wait_ld();
-      if (key < p.s) {
+          for (int which = 0; which < 2; ++which) {
+            const uint32_t* v = which == 0 ? vk : vv;
+            __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64 + half * 32;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 x;
-          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+            for (int k = 0; k < 4; ++k) {
+              uint4 x;
+              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
-          for (int e2 = 0; e2 < 4; ++e2)
-            hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e2]), __uint_as_float(v[8 * k + 2 * e2 + 1]));
-          *reinterpret_cast<uint4*>(dst + 8 * k) = x;
+              for (int e2 = 0; e2 < 4; ++e2)
+                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e2]), __uint_as_float(v[8 * k + 2 * e2 + 1]));
+              *reinterpret_cast<uint4*>(dst + 8 * k) = x;
+            }
+          }
         }
       }
     }
+    if (total > 0) drain_dq(total - 1);
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
@@ -1129,10 +1226,11 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_f32_tile_4d(&tdq, dq_acc, d, s, nh, b, lddq, d, s * lddq, &p.dq_b2_first);
   if (rc) return rc;
   constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
+  constexpr size_t SMEM2 = 12 * kT64 + 8 * 4096 + 256;  // v2: K, V double-buffered per item
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(flash_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)
+        cudaFuncSetAttribute(flash_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2) != cudaSuccess)
       return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
     attr = true;
   }
@@ -1144,7 +1242,12 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (bwd_v1)
     flash_bwd_kernel<<<grid, 256, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
   else
-    flash_bwd2_kernel<<<grid, 384, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
+  {
+    const int items = (int)grid.x * (int)grid.y * (int)grid.z;
+    const int sms = sg_device_sm_count();
+    flash_bwd2_kernel<<<std::min(items, sms > 0 ? sms : 148), 384, SMEM2, static_cast<cudaStream_t>(stream)>>>(
+        tq, tk, tv, tdo, tdq, p, (int)b);
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));

@@ -41,3 +41,10 @@ lse2 = torch.empty(b2, nh, s2, device="cuda")
 fl2 = 4.0 * b2 * nh * s2 * s2 * d
 t = timeit(lambda: K.flash_attn_fwd(qkv2, b2, s2, nh, d, out2, lse2))
 print(f"flash fwd b={b2} s={s2} nh={nh} d={d}: {t*1e3:.1f} us, {fl2/t/1e9:.1f} TF/s")
+dout2 = torch.randn(b2 * s2, hb, device="cuda").bfloat16()
+drow2 = torch.empty(b2, nh, s2, device="cuda")
+dq2 = torch.zeros(b2 * s2, hb, device="cuda")
+dqkv2 = torch.empty(b2 * s2, 3 * hb, device="cuda", dtype=torch.bfloat16)
+K.flash_attn_fwd(qkv2, b2, s2, nh, d, out2, lse2)
+t = timeit(lambda: K.flash_attn_bwd(qkv2, dout2, lse2, drow2, b2, s2, nh, d, dq2, dqkv2))
+print(f"flash bwd b={b2} s={s2}: {t*1e3:.1f} us, {2.5*fl2/t/1e9:.1f} TF/s")
