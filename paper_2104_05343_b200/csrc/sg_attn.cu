@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_begin();
   const uint32_t t_s = tmem, t_pv = tmem + 128;
 
   if (warp == 0) {
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_begin();
   // TMEM columns: S_i at 128 i, O_i at 256 + 64 i
   if (warp == 0) {
     if (lane == 0) {
@@ -585,7 +587,7 @@ static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
   }
   const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
   const int sms = sg_device_sm_count();
-  flash_fwd2_kernel<<<std::min(items, sms > 0 ? sms : 148), 384, Flash2Cfg::SMEM, stream>>>(q, k, v, p, b);
+  launch_k(flash_fwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), Flash2Cfg::SMEM, stream, q, k, v, p, b);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -603,7 +605,7 @@ static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensor
     attr = true;
   }
   dim3 grid((p.s + kQB - 1) / kQB, p.nh, b);
-  flash_fwd_kernel<HD><<<grid, 256, Cfg::SMEM, stream>>>(q, k, v, p);
+  launch_k(flash_fwd_kernel<HD>, grid, dim3(256), Cfg::SMEM, stream, q, k, v, p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -720,6 +722,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_begin();
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
 
   if (warp == 0) {
@@ -967,6 +970,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_begin();
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
 
   if (warp == 0) {
@@ -1240,13 +1244,13 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   }();
   dim3 grid((unsigned)((s + 127) / 128), (unsigned)nh, (unsigned)b);
   if (bwd_v1)
-    flash_bwd_kernel<<<grid, 256, SMEM, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo, tdq, p);
+    launch_k(flash_bwd_kernel, grid, dim3(256), SMEM, static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, p);
   else
   {
     const int items = (int)grid.x * (int)grid.y * (int)grid.z;
     const int sms = sg_device_sm_count();
-    flash_bwd2_kernel<<<std::min(items, sms > 0 ? sms : 148), 384, SMEM2, static_cast<cudaStream_t>(stream)>>>(
-        tq, tk, tv, tdo, tdq, p, (int)b);
+    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), SMEM2,
+             static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, p, (int)b);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();  // prologue above overlaps the previous kernel; inputs are read below
 
   if (warp == 0) {
     if (lane == 0) {
@@ -675,6 +676,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
 // pitches or batch strides that are not 16-byte multiples, e.g. head_dim 4 in
 // the reference's unit-test configurations). NORMAL-mode semantics.
 __global__ void gemm_simt_kernel(const __grid_constant__ sg_gemm_args a) {
+  pdl_begin();
   const long long total = a.nb1 * a.nb2 * a.M * a.N;
   const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A);
   const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B);
@@ -821,17 +823,21 @@ static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, 
     cfg.blockDim = dim3(EpiCfg<EW>::kThreads);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.d, m.x, m.d2, m.c, p);
     if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   } else {
-    kern<<<grid, EpiCfg<EW>::kThreads, Cfg::SMEM, stream>>>(m.a, m.b, m.d, m.x, m.d2, m.c, p);
+    cudaError_t e = launch_k(kern, dim3(grid), dim3(EpiCfg<EW>::kThreads), Cfg::SMEM, stream, m.a, m.b, m.d, m.x, m.d2,
+                             m.c, p);
+    if (e != cudaSuccess) return set_error(SG_ERR_CUDA, cudaGetErrorString(e));
   }
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -895,7 +901,7 @@ static int launch_simt(const sg_gemm_args* a, int sms, void* stream) {
   if (a->mode != SG_EPI_NORMAL) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need TMA-aligned operands");
   const long long total = a->nb1 * a->nb2 * a->M * a->N;
   const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
-  gemm_simt_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(*a);
+  launch_k(gemm_simt_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), *a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));

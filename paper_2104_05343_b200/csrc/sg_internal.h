@@ -9,3 +9,37 @@ void count_launch();  // every kernel this library launches (bench gpu_launches)
 }  // namespace sg
 
 extern "C" int sg_device_sm_count(void);
+
+#include <cstdlib>
+#include <utility>
+
+namespace sg {
+// Programmatic dependent launch: every libsg kernel is launched with programmatic
+// stream serialisation, triggers its dependents at entry and waits for its
+// predecessor (griddepcontrol) before touching memory, so a kernel's launch and
+// prologue overlap the tail of the previous one (also inside CUDA graphs).
+// SG_PDL=0 launches plainly (A/B measurements).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SG_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+}  // namespace sg

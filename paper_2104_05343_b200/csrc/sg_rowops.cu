@@ -18,6 +18,7 @@
 
 #include "sg.h"
 #include "sg_internal.h"
+#include "sg_ptx.cuh"
 
 namespace sg {
 
@@ -156,6 +157,7 @@ static bool aligned16(const void* p, long long ld, int esz) {
 template <typename TX>
 __global__ void ln_stats_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
                                 float* __restrict__ stats) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -187,6 +189,7 @@ __global__ void ln_fwd_kernel(const TX* __restrict__ x, long long rows, int cols
                               const float* __restrict__ stats, float inv_h, float eps,
                               const float* __restrict__ gamma, const float* __restrict__ beta, TY* __restrict__ y,
                               long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -237,6 +240,7 @@ __global__ void ln_bwd_stats_kernel(const TD* __restrict__ dy, long long lddy, c
                                     long long ldx, const float* __restrict__ mean, const float* __restrict__ rstd,
                                     const float* __restrict__ gamma, long long rows, int cols,
                                     float* __restrict__ stats) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     int cols, const float* __restrict__ stats, float inv_h, const TR* __restrict__ resid, long long ldr,
     float* __restrict__ dx, long long lddx, bf16* __restrict__ dx2, long long lddx2, float* __restrict__ dgamma,
     float* __restrict__ dbeta, float* __restrict__ dsum) {
+  pdl_begin();
   __shared__ __align__(16) float sm[3 * kSegWarps * kSegCols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * kSegCols;
@@ -409,6 +414,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
 template <typename TX, int RU, bool FULL>
 __global__ void __launch_bounds__(256) colsum_kernel(const TX* __restrict__ x, long long rows, int cols, long long ldx,
                                                      float* __restrict__ out) {
+  pdl_begin();
   __shared__ __align__(16) float sm[kSegWarps * kSegCols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * kSegCols;
@@ -457,6 +463,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const TX* __restrict__ x, l
 template <typename TX>
 __global__ void bias_add_kernel(TX* __restrict__ x, long long rows, int cols, long long ldx,
                                 const float* __restrict__ bias) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -477,6 +484,7 @@ __global__ void bias_add_kernel(TX* __restrict__ x, long long rows, int cols, lo
 template <typename TS, typename TP>
 __global__ void softmax_kernel(const TS* __restrict__ S, long long rows, int cols, long long lds, TP* __restrict__ P,
                                long long ldp) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -517,6 +525,7 @@ __global__ void softmax_kernel(const TS* __restrict__ S, long long rows, int col
 template <typename TD, typename TP, typename TO>
 __global__ void softmax_bwd_kernel(const TD* __restrict__ dP, long long lddp, const TP* __restrict__ P, long long ldp,
                                    long long rows, int cols, float scale, TO* __restrict__ dS, long long ldds) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -552,6 +561,7 @@ template <typename TL>
 __global__ void xent_local_kernel(const TL* __restrict__ logits, long long rows, long long ldl, int n_real,
                                   const int64_t* __restrict__ labels, long long col_lo, float* __restrict__ lmax,
                                   float* __restrict__ gmax, float* __restrict__ packed) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -619,6 +629,7 @@ __global__ void xent_local_kernel(const TL* __restrict__ logits, long long rows,
 // packed[r].sum *= e^{lmax - gmax} so the row all-reduce sums share one max.
 __global__ void xent_rescale_kernel(long long rows, const float* __restrict__ lmax, const float* __restrict__ gmax,
                                     float* __restrict__ packed) {
+  pdl_begin();
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += gridDim.x * (long long)blockDim.x) {
     const float lm = lmax[r];
     packed[2 * r] = lm == -INFINITY ? 0.f : packed[2 * r] * __expf(lm - gmax[r]);
@@ -628,6 +639,7 @@ __global__ void xent_rescale_kernel(long long rows, const float* __restrict__ lm
 // loss[r] = log(sum) + max - x_label; *partial (+)= sum_r loss[r]  (layers.py:597-599)
 __global__ void xent_loss_kernel(long long rows, const float* __restrict__ gmax, const float* __restrict__ packed,
                                  float* __restrict__ loss_rows, float* __restrict__ partial) {
+  pdl_begin();
   float acc = 0.f;
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += gridDim.x * (long long)blockDim.x) {
     const float l = logf(packed[2 * r]) + gmax[r] - packed[2 * r + 1];
@@ -651,6 +663,7 @@ template <typename TL, typename TO>
 __global__ void xent_bwd_kernel(const TL* logits, long long rows, long long ldl, int n_real, int ncols,
                                 const int64_t* __restrict__ labels, long long col_lo, const float* __restrict__ gmax,
                                 const float* __restrict__ packed, float scale, TO* dl, long long lddl) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -699,6 +712,7 @@ template <typename TT, typename TO>
 __global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, long long n, long long lo, long long vb,
                                  const TT* __restrict__ table, long long ldt, int hc, TO* __restrict__ out,
                                  long long ldo) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -719,6 +733,7 @@ template <typename TD>
 __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, long long lo, long long vb,
                                  const TD* __restrict__ dout, long long ldd, int hc, float* __restrict__ grad,
                                  long long ldg) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -739,6 +754,7 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, l
 // ============================================================ element-wise
 template <typename TS, typename TD>
 __global__ void cast_kernel(const TS* __restrict__ s, TD* __restrict__ d, long long n) {
+  pdl_begin();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
     if constexpr (sizeof(TD) == 4)
       d[i] = ld1(s + i);
@@ -754,6 +770,7 @@ struct SrcList {
 // the reference's reduce / all-reduce (mesh.py:464-466, 490-497).
 template <typename T>
 __global__ void fold_kernel(T* __restrict__ dst, SrcList srcs, int nsrc, long long n, int accumulate, int op_max) {
+  pdl_begin();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
     float acc = accumulate ? ld1(dst + i) : ld1(static_cast<const T*>(srcs.p[0]) + i);
     for (int k = accumulate ? 0 : 1; k < nsrc; ++k) {
@@ -783,6 +800,7 @@ template <typename TC, typename TO>
 __global__ void epilogue_kernel(const float* __restrict__ x, long long rows, int cols, long long ldx, float alpha,
                                 const float* __restrict__ bias, const TC* __restrict__ cin, long long ldc, int act,
                                 bf16* __restrict__ aux, long long ldaux, TO* __restrict__ out, long long ldo) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -822,6 +840,7 @@ __global__ void epilogue_kernel(const float* __restrict__ x, long long rows, int
 template <typename T>
 __global__ void attn_rowdot_kernel(const T* __restrict__ dO, long long ldo, const T* __restrict__ O, long long ldO,
                                    long long rows, int nh, int d, int s, float* __restrict__ out) {
+  pdl_begin();
   const long long total = rows * nh;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += gridDim.x * (long long)blockDim.x) {
     const long long row = i / nh;
@@ -855,6 +874,7 @@ template <typename TO, int RU, bool FULL>
 __global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long lda, const bf16* __restrict__ mid,
                                                     long long ldm, long long rows, int cols, TO* out, long long ldo,
                                                     float* __restrict__ colsum) {
+  pdl_begin();
   __shared__ __align__(16) float sm[kSegWarps * kSegCols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c0 = blockIdx.y * kSegCols;
@@ -906,6 +926,149 @@ __global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long 
   }
 }
 
+// y = LayerNorm(x) with the whole row held in registers (cols = 256 * NV): one HBM
+// read of x; the (sum, sumsq) row statistics come from the mesh all-reduce
+// (stats != nullptr) or, on a 1-column mesh, from the registers themselves.
+template <typename TX, typename TY, int NV>
+__global__ void __launch_bounds__(256) ln_fwd_rows_kernel(
+    const TX* __restrict__ x, long long rows, long long ldx, const float* __restrict__ stats, float inv_h, float eps,
+    const float* __restrict__ gamma, const float* __restrict__ beta, TY* __restrict__ y, long long ldy,
+    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = wid; r < rows; r += nw) {
+    Vec8<TX> raw[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) raw[k].load(x + r * ldx + k * 256 + lane * 8);
+    float s1, s2;
+    if (stats) {
+      s1 = stats[2 * r];
+      s2 = stats[2 * r + 1];
+    }
+    float v[NV][8];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) raw[k].to(v[k]);
+    if (!stats) {
+      s1 = 0.f;
+      s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          s1 += v[k][i];
+          s2 += v[k][i] * v[k][i];
+        }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+    }
+    const float mu = s1 * inv_h;
+    const float var = s2 * inv_h - mu * mu;  // one-pass variance, layers.py:296-297
+    const float rs = 1.0f / sqrtf(var + eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int c = k * 256 + lane * 8;
+      float g[8], bb[8];
+      Vec8<float> gv, bv;
+      gv.load(gamma + c);
+      bv.load(beta + c);
+      gv.to(g);
+      bv.to(bb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[k][i] = (v[k][i] - mu) * rs * g[i] + bb[i];
+      st8(y + r * ldy + c, 8, v[k]);
+    }
+    if (lane == 0) {
+      if (mean_out) mean_out[r] = mu;
+      if (rstd_out) rstd_out[r] = rs;
+    }
+  }
+}
+
+// The dQKV block after the flash backward: dq (fp32 accumulator) -> bf16 columns
+// [0, hb) of dqkv, and colsum += column sums of the whole [rows, 3 hb] gradient
+// (the b_qkv gradient, layers.py:238) in the same pass. Column-segment layout;
+// hb % 256 == 0 so every 256-column segment is all dQ or all dK / dV.
+template <int RU>
+__global__ void __launch_bounds__(256) qkv_grad_finish_kernel(const float* __restrict__ dq, long long lddq,
+                                                              bf16* __restrict__ dqkv, long long ldg, long long rows,
+                                                              int hb, float* __restrict__ colsum) {
+  pdl_begin();
+  __shared__ __align__(16) float sm[kSegWarps * kSegCols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * kSegCols;
+  const int c = c0 + lane * 8;
+  const bool is_q = c0 < hb;
+  float acc[1][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[0][i] = 0.f;
+  const long long step = (long long)gridDim.x * kSegWarps * RU;
+  for (long long r0 = ((long long)blockIdx.x * kSegWarps + warp) * RU; r0 < rows; r0 += step) {
+    float v[RU][8];
+    if (is_q) {
+      Vec8<float> raw[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) raw[u].load(dq + min(r0 + u, rows - 1) * lddq + c);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        raw[u].to(v[u]);
+        if (r0 + u < rows) st8(dqkv + (r0 + u) * ldg + c, 8, v[u]);
+      }
+    } else {
+      Vec8<bf16> raw[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) raw[u].load(dqkv + min(r0 + u, rows - 1) * ldg + c);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) raw[u].to(v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u)
+      if (r0 + u < rows)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
+  }
+  if (colsum) {
+    float* const dst[1] = {colsum};
+    seg_flush<1>(acc, dst, c0, 3 * hb, sm);
+  }
+}
+
+// D[b, h, t] = rowsum(dO * O) over each 64-wide head, a warp per token row: lane
+// l holds elements 8l .. 8l+7 of each 256-column chunk, 8 lanes make a head.
+template <int NV>
+__global__ void __launch_bounds__(256) attn_rowdot64_kernel(const bf16* __restrict__ dO, long long ldo,
+                                                            const bf16* __restrict__ O, long long ldO, long long rows,
+                                                            int nh, int s, float* __restrict__ out) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long row = wid; row < rows; row += nw) {
+    Vec8<bf16> a[NV], b[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      a[k].load(dO + row * ldo + k * 256 + lane * 8);
+      b[k].load(O + row * ldO + k * 256 + lane * 8);
+    }
+    const long long bb = row / s, t = row - bb * s;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float x[8], y[8];
+      a[k].to(x);
+      b[k].to(y);
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(x[e], y[e], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      const int h = k * 4 + (lane >> 3);
+      if ((lane & 7) == 0) out[(bb * nh + h) * (long long)s + t] = acc;
+    }
+  }
+}
+
 // Multi-tensor SGD: w -= lr * g on fp32 masters (2-D, own row pitches) with the
 // bf16 GEMM twin refreshed in the same pass (layers.py:761-772, model.py:356-364).
 // Blocks are dealt out over fixed 4096-element chunks of all tensors.
@@ -923,6 +1086,7 @@ struct SgdBatch {
   float lr;
 };
 __global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ SgdBatch b) {
+  pdl_begin();
   for (long long ch = blockIdx.x; ch < b.first_chunk[b.n]; ch += gridDim.x) {
     int t = 0;
     while (t + 1 < b.n && b.first_chunk[t + 1] <= ch) ++t;
@@ -980,7 +1144,7 @@ extern "C" int sg_ln_stats(const void* x, int xdt, int64_t rows, int64_t cols, i
   if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "ln_stats: unaligned");
   if (rows == 0) return SG_OK;
   const int grid = grid_for(rows, 8);
-  SG_DISPATCH_T(xdt, TX, (ln_stats_kernel<TX><<<grid, 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, stats)));
+  SG_DISPATCH_T(xdt, TX, (launch_k(ln_stats_kernel<TX>, dim3(grid), dim3(256), 0, S(stream), static_cast<const TX*>(x), rows, (int)cols, ldx, stats)));
   return launch_check();
 }
 
@@ -996,7 +1160,21 @@ extern "C" int sg_ln_fwd(const void* x, int xdt, int64_t rows, int64_t cols, int
   if (rows == 0) return SG_OK;
   const int grid = grid_for(rows, 8);
   const float inv_h = 1.0f / (float)h_total;
-  SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(ydt, TY, (ln_fwd_kernel<TX, TY><<<grid, 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, stats, inv_h, eps, gamma, beta, static_cast<TY*>(y), ldy, mean, rstd))));
+  const int nv = cols % 256 == 0 ? (int)(cols / 256) : 0;
+  if (nv == 1 || nv == 2 || nv == 4 || nv == 8) {
+    // whole row in registers: a warp per row, grid = one wave of resident warps
+    const int g2 = grid_for(rows, 8, nv <= 4 ? 8 : 4);
+#define SG_LN_ROWS(NV) SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(ydt, TY, (launch_k(ln_fwd_rows_kernel<TX, TY, NV>, dim3(g2), dim3(256), 0, S(stream), static_cast<const TX*>(x), rows, ldx, stats, inv_h, eps, gamma, beta, static_cast<TY*>(y), ldy, mean, rstd))))
+    switch (nv) {
+      case 1: SG_LN_ROWS(1); break;
+      case 2: SG_LN_ROWS(2); break;
+      case 4: SG_LN_ROWS(4); break;
+      default: SG_LN_ROWS(8); break;
+    }
+#undef SG_LN_ROWS
+    return launch_check();
+  }
+  SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(ydt, TY, (launch_k(ln_fwd_kernel<TX, TY>, dim3(grid), dim3(256), 0, S(stream), static_cast<const TX*>(x), rows, (int)cols, ldx, stats, inv_h, eps, gamma, beta, static_cast<TY*>(y), ldy, mean, rstd))));
   return launch_check();
 }
 
@@ -1009,7 +1187,7 @@ extern "C" int sg_ln_bwd_stats(const void* dy, int dydt, int64_t lddy, const voi
     return set_error(SG_ERR_SHAPE, "ln_bwd_stats: unaligned");
   if (rows == 0) return SG_OK;
   const int grid = grid_for(rows, 8);
-  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, (ln_bwd_stats_kernel<TD, TX><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats))));
+  SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, (launch_k(ln_bwd_stats_kernel<TD, TX>, dim3(grid), dim3(256), 0, S(stream), static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats))));
   return launch_check();
 }
 
@@ -1031,7 +1209,7 @@ extern "C" int sg_ln_bwd(const void* dy, int dydt, int64_t lddy, const void* x, 
   if (rdt != SG_DTYPE_BF16) rdt = SG_DTYPE_F32;
   // dx is fp32 (residual-stream gradient); the optional dx2 is its bf16 GEMM operand copy
   if (dxdt != SG_DTYPE_F32) return set_error(SG_ERR_CONFIG, "ln_bwd: dx must be fp32");
-#define SG_LN_BWD(FULL) SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (ln_bwd_kernel<TD, TX, TR, 2, FULL><<<grid, 256, 0, S(stream)>>>(static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta, dsum)))))
+#define SG_LN_BWD(FULL) SG_DISPATCH_T(dydt, TD, SG_DISPATCH_T(xdt, TX, SG_DISPATCH_T(rdt, TR, (launch_k(ln_bwd_kernel<TD, TX, TR, 2, FULL>, dim3(grid), dim3(256), 0, S(stream), static_cast<const TD*>(dy), lddy, static_cast<const TX*>(x), ldx, mean, rstd, gamma, rows, (int)cols, stats, inv_h, static_cast<const TR*>(resid), ldr, static_cast<float*>(dx), lddx, static_cast<bf16*>(dx2), lddx2, dgamma, dbeta, dsum)))))
   if (cols % 8 == 0)
     SG_LN_BWD(true);
   else
@@ -1049,9 +1227,9 @@ extern "C" int sg_colsum(const void* x, int xdt, int64_t rows, int64_t cols, int
     return set_error(SG_ERR_CUDA, "memset");
   if (rows == 0) return SG_OK;
   if (cols % 8 == 0)
-    SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX, 4, true><<<seg_grid(rows, cols, 4, 4), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
+    SG_DISPATCH_T(xdt, TX, (launch_k(colsum_kernel<TX, 4, true>, dim3(seg_grid(rows, cols, 4, 4)), dim3(256), 0, S(stream), static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
   else
-    SG_DISPATCH_T(xdt, TX, (colsum_kernel<TX, 4, false><<<seg_grid(rows, cols, 4, 2), 256, 0, S(stream)>>>(static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
+    SG_DISPATCH_T(xdt, TX, (launch_k(colsum_kernel<TX, 4, false>, dim3(seg_grid(rows, cols, 4, 2)), dim3(256), 0, S(stream), static_cast<const TX*>(x), rows, (int)cols, ldx, out)));
   return launch_check();
 }
 
@@ -1062,7 +1240,7 @@ extern "C" int sg_bias_add(void* x, int xdt, int64_t rows, int64_t cols, int64_t
   if (!aligned16(x, ldx, xdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(bias, 0, 4))
     return set_error(SG_ERR_SHAPE, "bias_add: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(xdt, TX, (bias_add_kernel<TX><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<TX*>(x), rows, (int)cols, ldx, bias)));
+  SG_DISPATCH_T(xdt, TX, (launch_k(bias_add_kernel<TX>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), static_cast<TX*>(x), rows, (int)cols, ldx, bias)));
   return launch_check();
 }
 
@@ -1073,7 +1251,7 @@ extern "C" int sg_softmax_rows(const void* s, int sdt, int64_t rows, int64_t col
   if (!aligned16(s, lds, sdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(p, ldp, pdt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "softmax: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(pdt, TP, (softmax_kernel<TS, TP><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TS*>(s), rows, (int)cols, lds, static_cast<TP*>(p), ldp))));
+  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(pdt, TP, (launch_k(softmax_kernel<TS, TP>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), static_cast<const TS*>(s), rows, (int)cols, lds, static_cast<TP*>(p), ldp))));
   return launch_check();
 }
 
@@ -1086,7 +1264,7 @@ extern "C" int sg_softmax_bwd(const void* dp, int dpdt, int64_t lddp, const void
       !aligned16(ds, ldds, dsdt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "softmax_bwd: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(dpdt, TD, SG_DISPATCH_T(pdt, TP, SG_DISPATCH_T(dsdt, TO, (softmax_bwd_kernel<TD, TP, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TD*>(dp), lddp, static_cast<const TP*>(p), ldp, rows, (int)cols, scale, static_cast<TO*>(ds), ldds)))));
+  SG_DISPATCH_T(dpdt, TD, SG_DISPATCH_T(pdt, TP, SG_DISPATCH_T(dsdt, TO, (launch_k(softmax_bwd_kernel<TD, TP, TO>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), static_cast<const TD*>(dp), lddp, static_cast<const TP*>(p), ldp, rows, (int)cols, scale, static_cast<TO*>(ds), ldds)))));
   return launch_check();
 }
 
@@ -1097,14 +1275,14 @@ extern "C" int sg_xent_local(const void* logits, int ldt, int64_t rows, int64_t 
   if (rows < 0 || n_real < 0) return set_error(SG_ERR_SHAPE, "xent_local: bad extents");
   if (!aligned16(logits, ldl, ldt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "xent_local: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(ldt, TL, (xent_local_kernel<TL><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TL*>(logits), rows, ldl, (int)n_real, labels, col_lo, lmax, gmax, packed)));
+  SG_DISPATCH_T(ldt, TL, (launch_k(xent_local_kernel<TL>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), static_cast<const TL*>(logits), rows, ldl, (int)n_real, labels, col_lo, lmax, gmax, packed)));
   return launch_check();
 }
 
 extern "C" int sg_xent_rescale(int64_t rows, const float* lmax, const float* gmax, float* packed, void* stream) {
   clear_error();
   if (rows <= 0) return SG_OK;
-  xent_rescale_kernel<<<grid_for(rows, 256), 256, 0, S(stream)>>>(rows, lmax, gmax, packed);
+  launch_k(xent_rescale_kernel, dim3(grid_for(rows, 256)), dim3(256), 0, S(stream), rows, lmax, gmax, packed);
   return launch_check();
 }
 
@@ -1113,7 +1291,7 @@ extern "C" int sg_xent_loss(int64_t rows, const float* gmax, const float* packed
   clear_error();
   if (cudaMemsetAsync(partial, 0, sizeof(float), S(stream)) != cudaSuccess) return set_error(SG_ERR_CUDA, "memset");
   if (rows <= 0) return SG_OK;
-  xent_loss_kernel<<<grid_for(rows, 256, 2), 256, 0, S(stream)>>>(rows, gmax, packed, loss_rows, partial);
+  launch_k(xent_loss_kernel, dim3(grid_for(rows, 256, 2)), dim3(256), 0, S(stream), rows, gmax, packed, loss_rows, partial);
   return launch_check();
 }
 
@@ -1125,7 +1303,7 @@ extern "C" int sg_xent_bwd(const void* logits, int ldt, int64_t rows, int64_t ld
   if (!aligned16(logits, ldl, ldt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(dl, lddl, dldt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "xent_bwd: unaligned");
   if (rows == 0 || ncols == 0) return SG_OK;
-  SG_DISPATCH_T(ldt, TL, SG_DISPATCH_T(dldt, TO, (xent_bwd_kernel<TL, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(static_cast<const TL*>(logits), rows, ldl, (int)n_real, (int)ncols, labels, col_lo, gmax, packed, scale, static_cast<TO*>(dl), lddl))));
+  SG_DISPATCH_T(ldt, TL, SG_DISPATCH_T(dldt, TO, (launch_k(xent_bwd_kernel<TL, TO>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), static_cast<const TL*>(logits), rows, ldl, (int)n_real, (int)ncols, labels, col_lo, gmax, packed, scale, static_cast<TO*>(dl), lddl))));
   return launch_check();
 }
 
@@ -1136,7 +1314,7 @@ extern "C" int sg_embed_fwd(const int64_t* ids, int64_t n, int64_t lo, int64_t v
   if (!aligned16(table, ldt, tdt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "embed_fwd: unaligned");
   if (n == 0) return SG_OK;
-  SG_DISPATCH_T(tdt, TT, SG_DISPATCH_T(odt, TO, (embed_fwd_kernel<TT, TO><<<grid_for(n, 8), 256, 0, S(stream)>>>(ids, n, lo, vb, static_cast<const TT*>(table), ldt, (int)hc, static_cast<TO*>(out), ldo))));
+  SG_DISPATCH_T(tdt, TT, SG_DISPATCH_T(odt, TO, (launch_k(embed_fwd_kernel<TT, TO>, dim3(grid_for(n, 8)), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TT*>(table), ldt, (int)hc, static_cast<TO*>(out), ldo))));
   return launch_check();
 }
 
@@ -1146,7 +1324,7 @@ extern "C" int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t v
   if (n < 0 || hc < 1 || vb < 0) return set_error(SG_ERR_SHAPE, "embed_bwd: bad extents");
   if (!aligned16(dout, ldd, ddt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "embed_bwd: unaligned");
   if (n == 0) return SG_OK;
-  SG_DISPATCH_T(ddt, TD, (embed_bwd_kernel<TD><<<grid_for(n, 8), 256, 0, S(stream)>>>(ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
+  SG_DISPATCH_T(ddt, TD, (launch_k(embed_bwd_kernel<TD>, dim3(grid_for(n, 8)), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
   return launch_check();
 }
 
@@ -1177,7 +1355,7 @@ extern "C" int sg_sgd_multi(const sg_sgd_item* items, int n, float lr, void* str
     if (chunks == 0) continue;
     if (g_sms <= 0) g_sms = sg_device_sm_count();
     const long long grid = std::min<long long>(chunks, (long long)(g_sms > 0 ? g_sms : 148) * 8);
-    sgd_multi_kernel<<<(int)grid, 256, 0, S(stream)>>>(bt);
+    launch_k(sgd_multi_kernel, dim3((int)grid), dim3(256), 0, S(stream), bt);
     const int rc = launch_check();
     if (rc != SG_OK) return rc;
   }
@@ -1193,7 +1371,7 @@ extern "C" int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const fl
 extern "C" int sg_cast(const void* src, int sdt, void* dst, int ddt, int64_t n, void* stream) {
   clear_error();
   if (n <= 0) return SG_OK;
-  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(ddt, TD, (cast_kernel<TS, TD><<<grid_for(n, 256, 4), 256, 0, S(stream)>>>(static_cast<const TS*>(src), static_cast<TD*>(dst), n))));
+  SG_DISPATCH_T(sdt, TS, SG_DISPATCH_T(ddt, TD, (launch_k(cast_kernel<TS, TD>, dim3(grid_for(n, 256, 4)), dim3(256), 0, S(stream), static_cast<const TS*>(src), static_cast<TD*>(dst), n))));
   return launch_check();
 }
 
@@ -1204,7 +1382,7 @@ extern "C" int sg_fold(void* dst, int dt, const void* const* srcs, int nsrc, int
   if (n <= 0 || nsrc == 0) return SG_OK;
   SrcList l{};
   for (int i = 0; i < nsrc; ++i) l.p[i] = srcs[i];
-  SG_DISPATCH_T(dt, T, (fold_kernel<T><<<grid_for(n, 256, 4), 256, 0, S(stream)>>>(static_cast<T*>(dst), l, nsrc, n, accumulate, op_max)));
+  SG_DISPATCH_T(dt, T, (launch_k(fold_kernel<T>, dim3(grid_for(n, 256, 4)), dim3(256), 0, S(stream), static_cast<T*>(dst), l, nsrc, n, accumulate, op_max)));
   return launch_check();
 }
 
@@ -1218,7 +1396,7 @@ extern "C" int sg_epilogue(const float* x, int64_t rows, int64_t cols, int64_t l
       !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2) || !aligned16(bias, 0, 4))
     return set_error(SG_ERR_SHAPE, "epilogue: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(cdt, TC, SG_DISPATCH_T(odt, TO, (epilogue_kernel<TC, TO><<<grid_for(rows, 8), 256, 0, S(stream)>>>(x, rows, (int)cols, ldx, alpha, bias, static_cast<const TC*>(cin), ldc, act, static_cast<bf16*>(aux), ldaux, static_cast<TO*>(out), ldo))));
+  SG_DISPATCH_T(cdt, TC, SG_DISPATCH_T(odt, TO, (launch_k(epilogue_kernel<TC, TO>, dim3(grid_for(rows, 8)), dim3(256), 0, S(stream), x, rows, (int)cols, ldx, alpha, bias, static_cast<const TC*>(cin), ldc, act, static_cast<bf16*>(aux), ldaux, static_cast<TO*>(out), ldo))));
   return launch_check();
 }
 
@@ -1230,7 +1408,22 @@ extern "C" int sg_attn_rowdot(const void* dO, int dt, int64_t ldo, const void* O
       (d * (dt == SG_DTYPE_F32 ? 4 : 2)) % 16)
     return set_error(SG_ERR_SHAPE, "attn_rowdot: unaligned");
   if (rows == 0) return SG_OK;
-  SG_DISPATCH_T(dt, T, (attn_rowdot_kernel<T><<<grid_for(rows * nh, 256, 8), 256, 0, S(stream)>>>(static_cast<const T*>(dO), ldo, static_cast<const T*>(O), ldO, rows, (int)nh, (int)d, (int)s, out)));
+  const int64_t nv_rd = nh * 64 / 256;
+  if (dt == SG_DTYPE_BF16 && d == 64 && (nh * 64) % 256 == 0 && (nv_rd <= 4 || nv_rd == 8)) {
+    const int nv = (int)(nh * 64 / 256);
+    const dim3 g2(grid_for(rows, 8, 8));
+#define SG_ROWDOT(NV) launch_k(attn_rowdot64_kernel<NV>, g2, dim3(256), 0, S(stream), static_cast<const bf16*>(dO), ldo, static_cast<const bf16*>(O), ldO, rows, (int)nh, (int)s, out)
+    switch (nv) {
+      case 1: SG_ROWDOT(1); break;
+      case 2: SG_ROWDOT(2); break;
+      case 3: SG_ROWDOT(3); break;
+      case 4: SG_ROWDOT(4); break;
+      default: SG_ROWDOT(8); break;
+    }
+#undef SG_ROWDOT
+    return launch_check();
+  }
+  SG_DISPATCH_T(dt, T, (launch_k(attn_rowdot_kernel<T>, dim3(grid_for(rows * nh, 256, 8)), dim3(256), 0, S(stream), static_cast<const T*>(dO), ldo, static_cast<const T*>(O), ldO, rows, (int)nh, (int)d, (int)s, out)));
   return launch_check();
 }
 
@@ -1241,11 +1434,22 @@ extern "C" int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t 
   if (!aligned16(dact, lda, 2) || !aligned16(mid, ldm, 2) || !aligned16(out, ldo, odt == SG_DTYPE_F32 ? 4 : 2))
     return set_error(SG_ERR_SHAPE, "dgelu: unaligned");
   if (rows == 0) return SG_OK;
-#define SG_DGELU(FULL) SG_DISPATCH_T(odt, TO, (dgelu_kernel<TO, 4, FULL><<<seg_grid(rows, cols, 4, 2), 256, 0, S(stream)>>>(static_cast<const bf16*>(dact), lda, static_cast<const bf16*>(mid), ldm, rows, (int)cols, static_cast<TO*>(out), ldo, colsum)))
+#define SG_DGELU(FULL) SG_DISPATCH_T(odt, TO, (launch_k(dgelu_kernel<TO, 4, FULL>, dim3(seg_grid(rows, cols, 4, 2)), dim3(256), 0, S(stream), static_cast<const bf16*>(dact), lda, static_cast<const bf16*>(mid), ldm, rows, (int)cols, static_cast<TO*>(out), ldo, colsum)))
   if (cols % 8 == 0)
     SG_DGELU(true);
   else
     SG_DGELU(false);
 #undef SG_DGELU
+  return launch_check();
+}
+
+extern "C" int sg_qkv_grad_finish(const float* dq, int64_t lddq, void* dqkv, int64_t ldg, int64_t rows, int64_t hb,
+                                  float* colsum, void* stream) {
+  clear_error();
+  if (rows < 0 || hb < 1 || hb % 256 != 0) return set_error(SG_ERR_SHAPE, "qkv_grad_finish: hb must be a multiple of 256");
+  if (!aligned16(dq, lddq, 4) || !aligned16(dqkv, ldg, 2)) return set_error(SG_ERR_SHAPE, "qkv_grad_finish: unaligned");
+  if (rows == 0) return SG_OK;
+  launch_k(qkv_grad_finish_kernel<2>, seg_grid(rows, 3 * hb, 2, 3), dim3(256), 0, S(stream), dq, lddq,
+           static_cast<bf16*>(dqkv), ldg, rows, (int)hb, colsum);
   return launch_check();
 }

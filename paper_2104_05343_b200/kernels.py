@@ -403,6 +403,13 @@ def dgelu(dact, mid, out, colsum=None):
     _call("sg_dgelu", _p(dact), lda, _p(mid), ldm, rows, cols, _p(out), _dt(out), ldo, _p(colsum), _stream(dact))
 
 
+def qkv_grad_finish(dq_acc, dqkv, hb, colsum):
+    """dqkv[:, :hb] = bf16(dq_acc); colsum += column sums of dqkv (fused; hb % 256 == 0)."""
+    rows, _, lddq = _rows2d(dq_acc)
+    _, _, ldg = _rows2d(dqkv)
+    _call("sg_qkv_grad_finish", _p(dq_acc), lddq, _p(dqkv), ldg, rows, hb, _p(colsum), _stream(dqkv))
+
+
 def flash_attn_fwd(qkv, b, s, n_heads, d, out, lse=None):
     """Flash-style attention forward: qkv [b*s, 3*nh*d] block -> out [b*s, nh*d], lse [b, nh, s]."""
     _, _, ldq = _rows2d(qkv)

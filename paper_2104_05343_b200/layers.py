@@ -604,8 +604,11 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
             K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)
             dq_acc = ws.alloc(dev, (bs_loc, hb), "free", dtype=F32)
             K.flash_attn_bwd(blk, dctx.blocks[dev], ctx.lse[dev], drow, b_loc, s, n_loc, d, dq_acc, dq_blk)
-            K.epilogue(dq_acc, dq_blk[:, :hb])
-            K.colsum(dq_blk, bq_parts[dev])
+            if hb % 256 == 0:  # dQ to bf16 and the b_qkv gradient in one pass
+                K.qkv_grad_finish(dq_acc, dq_blk, hb, bq_parts[dev])
+            else:
+                K.epilogue(dq_acc, dq_blk[:, :hb])
+                K.colsum(dq_blk, bq_parts[dev], accumulate=True)
             continue
         dheads = _heads_view(dctx.blocks[dev], b_loc, s, n_loc, d)
         p_mat = ctx.probs[dev]
