@@ -198,9 +198,22 @@ def gen_layers(sg) -> dict:
     return arrays
 
 
+def gen_checkpoint(sg) -> None:
+    """A model checkpoint file written by the reference's save_checkpoint (model.py:431-445)."""
+    from summagrid import model
+
+    cfg = sg.ModelConfig(b=2, s=4, h=8, n=2, v=10, num_layers=1)
+    params = model.init_global_params(cfg, 3)
+    model.save_checkpoint(OUT / "ckpt_small.bin", cfg, params)
+
+
 def main() -> None:
     sg = _ref()
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--only-checkpoint" in sys.argv:
+        gen_checkpoint(sg)
+        return
+    gen_checkpoint(sg)
     book = gen_bookkeeping(sg)
     (OUT / "bookkeeping.json").write_text(json.dumps(book, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "summa.npz", **gen_summa(sg))

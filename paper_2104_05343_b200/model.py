@@ -15,6 +15,7 @@ the reference's signatures.
 from __future__ import annotations
 
 import math
+import struct
 from dataclasses import dataclass
 from typing import Optional
 
@@ -62,6 +63,61 @@ def param_shape(cfg: ModelConfig, name: str) -> tuple[int, ...]:
     base = name.rsplit(".", 1)[-1]
     return {"table": (cfg.v, h), "w_qkv": (h, 3 * h), "b_qkv": (3 * h,), "w_dense": (h, h), "w1": (h, 4 * h),
             "b1": (4 * h,), "w2": (4 * h, h)}.get(base, (h,))
+
+
+# ---------------------------------------------------------------- checkpoint file
+# The reference's on-disk model format (model.py:64-79, 431-462): little-endian
+# header of eight u64 (magic, version, b, s, h, n, v, num_layers), u64 classifier
+# flag, f64 eps, then every parameter as f64 row-major in declaration order.
+CKPT_MAGIC = 0x5347524944434B50
+CKPT_VERSION = 1
+_CKPT_HEADER = struct.Struct("<8QQd")
+
+
+def _ckpt_names(cfg: ModelConfig, classifier: bool) -> list[str]:
+    return param_declaration_order(cfg) + (["cls_w"] if classifier else [])
+
+
+def _ckpt_shape(cfg: ModelConfig, name: str) -> tuple[int, ...]:
+    return (cfg.h, 2) if name == "cls_w" else param_shape(cfg, name)
+
+
+def save_checkpoint(path, cfg: ModelConfig, global_params: dict, classifier: bool = False) -> None:
+    """Write ``global_params`` (host arrays, standard layout) in the reference's
+    binary checkpoint format (model.py:431-445); ShapeError on a wrong shape."""
+    with open(path, "wb") as f:
+        f.write(_CKPT_HEADER.pack(CKPT_MAGIC, CKPT_VERSION, cfg.b, cfg.s, cfg.h, cfg.n, cfg.v, cfg.num_layers,
+                                  1 if classifier else 0, float(cfg.eps)))
+        for name in _ckpt_names(cfg, classifier):
+            arr = np.ascontiguousarray(np.asarray(global_params[name]), dtype="<f8")
+            if arr.shape != _ckpt_shape(cfg, name):
+                raise ShapeError(f"{name}: expected {_ckpt_shape(cfg, name)}, got {arr.shape}")
+            f.write(arr.tobytes())
+
+
+def load_checkpoint(path) -> tuple[ModelConfig, dict, bool]:
+    """(cfg, host f64 parameters, classifier flag) of a reference checkpoint file
+    (model.py:448-462); ConfigError on a bad magic / version or a truncated file."""
+    with open(path, "rb") as f:
+        head = f.read(_CKPT_HEADER.size)
+        if len(head) != _CKPT_HEADER.size:
+            raise ConfigError("checkpoint file truncated (header)")
+        magic, version, b, s, h, n, v, layers, cls_flag, eps = _CKPT_HEADER.unpack(head)
+        if magic != CKPT_MAGIC:
+            raise ConfigError(f"not a model checkpoint (bad magic {magic:#x})")
+        if version != CKPT_VERSION:
+            raise ConfigError(f"unsupported checkpoint version {version}")
+        cfg = ModelConfig(b=b, s=s, h=h, n=n, v=v, num_layers=layers, eps=eps)
+        classifier = bool(cls_flag)
+        params = {}
+        for name in _ckpt_names(cfg, classifier):
+            shape = _ckpt_shape(cfg, name)
+            count = int(np.prod(shape))
+            raw = f.read(8 * count)
+            if len(raw) != 8 * count:
+                raise ConfigError(f"checkpoint file truncated at {name}")
+            params[name] = np.frombuffer(raw, dtype="<f8").reshape(shape).copy()
+    return cfg, params, classifier
 
 
 def init_global_params(cfg: ModelConfig, seed: int, classifier: bool = False) -> dict[str, np.ndarray]:
@@ -247,6 +303,19 @@ class MeshModel:
         logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True)
         return loss
+
+    # ------------------------------------------------------------------ checkpoint file
+    def save(self, path) -> None:
+        """Gather the parameters and write them in the reference checkpoint format."""
+        save_checkpoint(path, self.cfg, self.gather_params())
+
+    @classmethod
+    def load(cls, path, mesh: Mesh, **kw) -> "MeshModel":
+        """A model on ``mesh`` (any shape the dimensions divide) from a checkpoint file."""
+        cfg, params, classifier = load_checkpoint(path)
+        if classifier:
+            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
+        return cls(mesh, cfg, params, **kw)
 
     # ------------------------------------------------------------------ gather for parity
     def gather_params(self) -> dict[str, np.ndarray]:

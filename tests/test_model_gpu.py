@@ -165,3 +165,24 @@ def test_head_dim_128_training_vs_oracle():
     ref = M.serial_backward(rcfg, params, saved)
     assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3
     _compare_grads(sg, model.gather_grads(grads), {k: v for k, v in ref.items() if not k.startswith("_")})
+
+
+def test_checkpoint_file_across_meshes(tmp_path):
+    """A model saved from a 2x2 mesh and reloaded on 1x2 keeps its parameters and loss."""
+    import torch
+
+    sg = _sg()
+    cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=61, num_layers=2)
+    rcfg = M.RefConfig(cfg.b, cfg.s, cfg.h, cfg.n, cfg.v, cfg.num_layers)
+    params = {k: bf16_round(v) for k, v in M.init_params(rcfg, 4).items()}
+    tokens, labels = M.sample_data(rcfg, 4)
+    a = sg.MeshModel(mesh(2, 2), cfg, params)
+    path = tmp_path / "m.bin"
+    a.save(path)
+    b = sg.MeshModel.load(path, mesh(1, 2))
+    pa, pb = a.gather_params(), b.gather_params()
+    for k in pa:
+        np.testing.assert_array_equal(pa[k], pb[k])
+    la = float(a.infer(torch.as_tensor(tokens), torch.as_tensor(labels), a.make_workspace()).item())
+    lb = float(b.infer(torch.as_tensor(tokens), torch.as_tensor(labels), b.make_workspace()).item())
+    assert abs(la - lb) / abs(la) < 1e-3
