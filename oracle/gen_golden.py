@@ -207,13 +207,45 @@ def gen_checkpoint(sg) -> None:
     model.save_checkpoint(OUT / "ckpt_small.bin", cfg, params)
 
 
+def gen_baseline(sg) -> dict:
+    """The reference's Megatron 1D layer (baseline.py:40-224) on q = 1 and 2 meshes."""
+    from summagrid import model
+    from summagrid.baseline import Baseline1DLayer
+
+    arrays = {}
+    cfg = sg.ModelConfig(b=2, s=16, h=64, n=4, v=16, num_layers=1)
+    g = model.init_global_params(cfg, 5)
+    lp = {k.split(".", 2)[2]: v for k, v in g.items() if k.startswith("layers.0.")}
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((cfg.b * cfg.s, cfg.h))
+    dy = rng.standard_normal((cfg.b * cfg.s, cfg.h))
+    for k, v in lp.items():
+        arrays[f"param.{k}"] = v
+    arrays["x"], arrays["dy"] = x, dy
+    for q in (1, 2):
+        mesh = sg.create_mesh(sg.MeshConfig(q=q))
+        layer = Baseline1DLayer(mesh, cfg, lp)
+        ws = sg.Workspace(mesh.p)
+        out, saved = layer.forward(x, ws)
+        dx, grads = layer.backward(dy, saved, ws)
+        arrays[f"q{q}.out"] = np.asarray(out)
+        arrays[f"q{q}.dx"] = np.asarray(dx)
+        for k, v in grads.items():
+            arrays[f"q{q}.grad.{k}"] = np.asarray(v)
+    return arrays
+
+
 def main() -> None:
     sg = _ref()
     OUT.mkdir(parents=True, exist_ok=True)
     if "--only-checkpoint" in sys.argv:
         gen_checkpoint(sg)
         return
+    if "--only-baseline" in sys.argv:
+        np.savez_compressed(OUT / "baseline1d.npz", **gen_baseline(sg))
+        return
     gen_checkpoint(sg)
+    np.savez_compressed(OUT / "baseline1d.npz", **gen_baseline(sg))
     book = gen_bookkeeping(sg)
     (OUT / "bookkeeping.json").write_text(json.dumps(book, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "summa.npz", **gen_summa(sg))

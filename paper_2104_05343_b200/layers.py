@@ -508,16 +508,20 @@ FLASH_ATTENTION = True
 
 def _probs(cfg: ModelConfig, mesh: Mesh, qkv_blk, dev):
     """P = softmax(Q K^T / sqrt(d)) as bf16 [b, n, s, s] (the reference's saved ``probs``)."""
-    b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
-    hb = cfg.h // mesh.c
+    return _probs_core(cfg, cfg.b // mesh.r, cfg.n // mesh.c, qkv_blk, mesh.device(dev))
+
+
+def _probs_core(cfg: ModelConfig, b_loc: int, n_loc: int, qkv_blk, device):
+    d, s = cfg.head_dim, cfg.s
+    hb = n_loc * d
     q = _heads_view(qkv_blk[:, :hb], b_loc, s, n_loc, d)
     k = _heads_view(qkv_blk[:, hb:2 * hb], b_loc, s, n_loc, d)
-    probs = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
+    probs = padded_empty((b_loc, n_loc, s, s), BF16, device)
     if fused_softmax_ok(cfg):
         # P straight out of TMEM: no fp32 score matrix in HBM
         K.gemm(q, k.transpose(-1, -2), probs, alpha=1.0 / math.sqrt(d), mode=K.EPI_SOFTMAX)
     else:
-        scores = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
+        scores = padded_empty((b_loc, n_loc, s, s), F32, device)
         K.gemm(q, k.transpose(-1, -2), scores, alpha=1.0 / math.sqrt(d))
         K.softmax_rows(_rows_view(scores), _rows_view(probs))
     return probs
@@ -525,13 +529,20 @@ def _probs(cfg: ModelConfig, mesh: Mesh, qkv_blk, dev):
 
 def _local_attention(cfg: ModelConfig, mesh: Mesh, qkv_blk, ctx_blk, ws, dev):
     """Per-position multi-head attention on one block; returns (probs | None, lse | None)."""
-    b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
-    hb = cfg.h // mesh.c
+    return attention_core_forward(cfg, cfg.b // mesh.r, cfg.n // mesh.c, qkv_blk, ctx_blk, ws, dev, mesh.device(dev))
+
+
+def attention_core_forward(cfg: ModelConfig, b_loc: int, n_loc: int, qkv_blk, ctx_blk, ws, dev, device):
+    """softmax(Q K^T / sqrt(d)) V for the b_loc sequences x n_loc heads of one
+    position's [b_loc*s, 3*n_loc*d] QKV block (layers.py:404-416); returns
+    (probs | None, lse | None)."""
+    d, s = cfg.head_dim, cfg.s
+    hb = n_loc * d
     if flash_ok(cfg):
         lse = ws.empty(dev, (b_loc, n_loc, s), "forward", dtype=F32, pad=False)
         K.flash_attn_fwd(qkv_blk, b_loc, s, n_loc, d, ctx_blk, lse)
         return None, lse
-    probs = _probs(cfg, mesh, qkv_blk, dev)
+    probs = _probs_core(cfg, b_loc, n_loc, qkv_blk, device)
     v = _heads_view(qkv_blk[:, 2 * hb:], b_loc, s, n_loc, d)
     K.gemm(probs, v, _heads_view(ctx_blk, b_loc, s, n_loc, d))
     return probs, None
@@ -567,6 +578,54 @@ def attention_forward(x: ShardedMatrix, w_qkv: ShardedMatrix, b_qkv: RowHostedVe
                                  lse=lse if flash_ok(cfg) else None)
 
 
+def attention_core_backward(cfg: ModelConfig, b_loc: int, n_loc: int, qkv_blk, ctx_blk, dctx_blk, lse, probs_fn, ws,
+                            dev, device, bq_part):
+    """dQKV [b_loc*s, 3*n_loc*d] (bf16) of one position's attention core from dO = dctx
+    (layers.py:444-459); ``bq_part`` (fp32 [3*n_loc*d]) accumulates its column sums
+    (the b_qkv gradient). Flash path from the saved lse, otherwise through P
+    (``probs_fn()`` returns it, rebuilt if it was not kept)."""
+    d, s = cfg.head_dim, cfg.s
+    hb = n_loc * d
+    bs_loc = b_loc * s
+    scale = 1.0 / math.sqrt(d)
+    q = _heads_view(qkv_blk[:, :hb], b_loc, s, n_loc, d)
+    k = _heads_view(qkv_blk[:, hb:2 * hb], b_loc, s, n_loc, d)
+    v = _heads_view(qkv_blk[:, 2 * hb:], b_loc, s, n_loc, d)
+    dq_blk = ws.empty(dev, (bs_loc, 3 * hb), "free", dtype=BF16)
+    if lse is not None and flash_bwd_ok(cfg):
+        # flash backward: P rebuilt per tile from lse, never in HBM; D = rowsum(dO O)
+        drow = ws.empty(dev, (b_loc, n_loc, s), "free", dtype=F32, pad=False)
+        K.attn_rowdot(dctx_blk, ctx_blk, n_loc, d, s, drow)
+        dq_acc = ws.alloc(dev, (bs_loc, hb), "free", dtype=F32)
+        K.flash_attn_bwd(qkv_blk, dctx_blk, lse, drow, b_loc, s, n_loc, d, dq_acc, dq_blk)
+        if hb % 256 == 0:  # dQ to bf16 and the b_qkv gradient in one pass
+            K.qkv_grad_finish(dq_acc, dq_blk, hb, bq_part)
+        else:
+            K.epilogue(dq_acc, dq_blk[:, :hb])
+            K.colsum(dq_blk, bq_part, accumulate=True)
+        return dq_blk
+    dheads = _heads_view(dctx_blk, b_loc, s, n_loc, d)
+    p_mat = probs_fn()
+    cs = [bq_part[i * hb:(i + 1) * hb].view(1, n_loc, d) for i in range(3)]
+    ds = padded_empty((b_loc, n_loc, s, s), BF16, device)
+    if fused_softmax_ok(cfg) and FUSED_SOFTMAX_BWD:
+        # dS = P (dP - D) / sqrt(d) straight out of the dP = dO V^T accumulator, with
+        # D = rowsum(dP P) = rowsum(dO O) computed from the saved context
+        drow = padded_empty((b_loc, n_loc, s), F32, device)
+        K.attn_rowdot(dctx_blk, ctx_blk, n_loc, d, s, drow)
+        K.gemm(dheads, v.transpose(-1, -2), ds, alpha=scale, mode=K.EPI_SOFTMAX_BWD, aux=p_mat, rowvec=drow)
+    else:
+        dp = padded_empty((b_loc, n_loc, s, s), F32, device)
+        K.gemm(dheads, v.transpose(-1, -2), dp)                              # dP = dO V^T
+        K.softmax_bwd(_rows_view(dp), _rows_view(p_mat), scale, _rows_view(ds))
+    K.gemm(p_mat.transpose(-1, -2), dheads, _heads_view(dq_blk[:, 2 * hb:], b_loc, s, n_loc, d),
+           colsum=cs[2])                                                     # dV = P^T dO
+    K.gemm(ds, k, _heads_view(dq_blk[:, :hb], b_loc, s, n_loc, d), colsum=cs[0])          # dQ = dS K
+    K.gemm(ds.transpose(-1, -2), q, _heads_view(dq_blk[:, hb:2 * hb], b_loc, s, n_loc, d),
+           colsum=cs[1])                                                     # dK = dS^T Q
+    return dq_blk
+
+
 def _all(mesh: Mesh) -> list:
     return [d if mesh.owns(d) else None for d in range(mesh.p)]
 
@@ -580,55 +639,19 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
                        w_dense: ShardedMatrix, cfg: ModelConfig, ws: Workspace):
     """(dx, dW_qkv, db_qkv, dW_dense, db_dense) (layers.py:424-465)."""
     mesh = out_grad.mesh
-    b_loc, n_loc, d, s = cfg.b // mesh.r, cfg.n // mesh.c, cfg.head_dim, cfg.s
+    b_loc, n_loc = cfg.b // mesh.r, cfg.n // mesh.c
     hb = cfg.h // mesh.c
-    bs_loc = b_loc * s
-    scale = 1.0 / math.sqrt(d)
     dy16 = _bf16_of(out_grad, ws)
     _, b_dense_grad = bias_add_backward(out_grad, ws)
     dctx = summa_abt(dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
     w_dense_grad = summa_atb(ctx.ctx_mat, dy16, ws, out_category="param_grad")
-    fused = fused_softmax_ok(cfg)
     bq_parts = new_colsum_parts(mesh, ws, 3 * hb)  # b_qkv gradient fused into dQ / dK / dV epilogues
     dqkv_blocks = [None] * mesh.p
     for dev in mesh.local_devs:
-        blk = ctx.qkv.blocks[dev]
-        q = _heads_view(blk[:, :hb], b_loc, s, n_loc, d)
-        k = _heads_view(blk[:, hb:2 * hb], b_loc, s, n_loc, d)
-        v = _heads_view(blk[:, 2 * hb:], b_loc, s, n_loc, d)
-        dq_blk = ws.empty(dev, (bs_loc, 3 * hb), "free", dtype=BF16)
-        dqkv_blocks[dev] = dq_blk
-        if ctx.lse is not None and flash_bwd_ok(cfg):
-            # flash backward: P rebuilt per tile from lse, never in HBM; D = rowsum(dO O)
-            drow = ws.empty(dev, (b_loc, n_loc, s), "free", dtype=F32, pad=False)
-            K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)
-            dq_acc = ws.alloc(dev, (bs_loc, hb), "free", dtype=F32)
-            K.flash_attn_bwd(blk, dctx.blocks[dev], ctx.lse[dev], drow, b_loc, s, n_loc, d, dq_acc, dq_blk)
-            if hb % 256 == 0:  # dQ to bf16 and the b_qkv gradient in one pass
-                K.qkv_grad_finish(dq_acc, dq_blk, hb, bq_parts[dev])
-            else:
-                K.epilogue(dq_acc, dq_blk[:, :hb])
-                K.colsum(dq_blk, bq_parts[dev], accumulate=True)
-            continue
-        dheads = _heads_view(dctx.blocks[dev], b_loc, s, n_loc, d)
-        p_mat = ctx.probs[dev]
-        cs = [bq_parts[dev][i * hb:(i + 1) * hb].view(1, n_loc, d) for i in range(3)]
-        ds = padded_empty((b_loc, n_loc, s, s), BF16, mesh.device(dev))
-        if fused and FUSED_SOFTMAX_BWD:
-            # dS = P (dP - D) / sqrt(d) straight out of the dP = dO V^T accumulator, with
-            # D = rowsum(dP P) = rowsum(dO O) computed from the saved context
-            drow = padded_empty((b_loc, n_loc, s), F32, mesh.device(dev))
-            K.attn_rowdot(dctx.blocks[dev], ctx.ctx_mat.blocks[dev], n_loc, d, s, drow)
-            K.gemm(dheads, v.transpose(-1, -2), ds, alpha=scale, mode=K.EPI_SOFTMAX_BWD, aux=p_mat, rowvec=drow)
-        else:
-            dp = padded_empty((b_loc, n_loc, s, s), F32, mesh.device(dev))
-            K.gemm(dheads, v.transpose(-1, -2), dp)                              # dP = dO V^T
-            K.softmax_bwd(_rows_view(dp), _rows_view(p_mat), scale, _rows_view(ds))
-        K.gemm(p_mat.transpose(-1, -2), dheads, _heads_view(dq_blk[:, 2 * hb:], b_loc, s, n_loc, d),
-               colsum=cs[2])                                                     # dV = P^T dO
-        K.gemm(ds, k, _heads_view(dq_blk[:, :hb], b_loc, s, n_loc, d), colsum=cs[0])          # dQ = dS K
-        K.gemm(ds.transpose(-1, -2), q, _heads_view(dq_blk[:, hb:2 * hb], b_loc, s, n_loc, d),
-               colsum=cs[1])                                                     # dK = dS^T Q
+        dqkv_blocks[dev] = attention_core_backward(
+            cfg, b_loc, n_loc, ctx.qkv.blocks[dev], ctx.ctx_mat.blocks[dev], dctx.blocks[dev],
+            None if ctx.lse is None else ctx.lse[dev], lambda dev=dev: ctx.probs[dev], ws, dev, mesh.device(dev),
+            bq_parts[dev])
     dqkv = ShardedMatrix(mesh, cfg.b * cfg.s, 3 * cfg.h, dqkv_blocks)
     dqkv.colsum_parts = bq_parts
     _, b_qkv_grad = bias_add_backward(dqkv, ws)

@@ -428,6 +428,24 @@ class Mesh:
         """In place along columns (R8, mesh.py:506-508)."""
         self._allreduce("col", bufs, op, tag)
 
+    def allreduce_all(self, bufs: Sequence, op: str = "sum", tag: str = "misc") -> None:
+        """In place over every position of the mesh (the 1D baseline's ring all-reduce,
+        baseline.py:128-202, mesh.py:510-513); position order on the local backend."""
+        if op not in ("sum", "max"):
+            raise ConfigError(f"unknown all_reduce op {op!r}")
+        self._count("allreduce", tag)
+        if self.is_local:
+            first = bufs[0]
+            K.fold(first, list(bufs), op_max=(op == "max"))
+            for f in range(1, self.p):
+                K.fold(bufs[f], [first])
+            return
+        import torch.distributed as dist
+
+        if self.p > 1:
+            dist.all_reduce(K._flat_storage(bufs[self.my_flat]),
+                            op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+
     # ------------------------------------------------ reference single-controller API
     # (local backend only: the caller holds every position's block, as in the reference)
     def _need_local(self) -> None:
