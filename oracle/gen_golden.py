@@ -235,17 +235,48 @@ def gen_baseline(sg) -> dict:
     return arrays
 
 
+def gen_ledger(sg) -> dict:
+    """Reference ledgers (mesh.py:102-200) after each SUMMA form and the 1D baseline layer."""
+    from summagrid.summa import scatter, summa_ab, summa_abt, summa_atb
+
+    out = {}
+    rng = np.random.default_rng(11)
+    for q, ns, pl in ((1, 1, "natural"), (2, 1, "natural"), (2, 2, "natural"), (3, 3, "natural"),
+                      (2, 2, "bunched")):
+        for form in ("ab", "abt", "atb"):
+            mesh = sg.create_mesh(sg.MeshConfig(q=q, node_size=ns, placement=sg.Placement(pl)),
+                                  cost=sg.CostParams(beta=1.5))
+            ws = sg.Workspace(mesh.p)
+            a = rng.standard_normal((6 * q, 4 * q))
+            if form == "ab":
+                summa_ab(scatter(a, mesh), scatter(rng.standard_normal((4 * q, 8 * q)), mesh), ws, tag="t")
+            elif form == "abt":
+                summa_abt(scatter(a, mesh), scatter(rng.standard_normal((8 * q, 4 * q)), mesh), ws, tag="t")
+            else:
+                summa_atb(scatter(a, mesh), scatter(rng.standard_normal((6 * q, 8 * q)), mesh), ws, tag="t")
+            rep = sg.ledger_report(mesh)
+            out[f"q{q}_ns{ns}_{pl}_{form}"] = {c: getattr(rep, c).tolist() for c in (
+                "broadcast_cost", "reduce_cost", "allreduce_cost", "scalars_sent_internode",
+                "scalars_sent_intranode", "macs", "messages_sent")}
+            out[f"q{q}_ns{ns}_{pl}_{form}"]["csv"] = sg.ledger_csv(rep)
+    return out
+
+
 def main() -> None:
     sg = _ref()
     OUT.mkdir(parents=True, exist_ok=True)
     if "--only-checkpoint" in sys.argv:
         gen_checkpoint(sg)
         return
+    if "--only-ledger" in sys.argv:
+        (OUT / "ledger.json").write_text(json.dumps(gen_ledger(sg), indent=1, sort_keys=True))
+        return
     if "--only-baseline" in sys.argv:
         np.savez_compressed(OUT / "baseline1d.npz", **gen_baseline(sg))
         return
     gen_checkpoint(sg)
     np.savez_compressed(OUT / "baseline1d.npz", **gen_baseline(sg))
+    (OUT / "ledger.json").write_text(json.dumps(gen_ledger(sg), indent=1, sort_keys=True))
     book = gen_bookkeeping(sg)
     (OUT / "bookkeeping.json").write_text(json.dumps(book, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "summa.npz", **gen_summa(sg))

@@ -103,6 +103,9 @@ class Baseline1DLayer:
         xr.copy_(x)
         a1, ln1 = self._ln(xr, self.rep["ln1_gamma"], self.rep["ln1_beta"], ws, dev0)
         n_loc, hp = cfg.n // p, cfg.h // p
+        h, att_macs = cfg.h, cfg.b * n_loc * cfg.s * cfg.s * cfg.head_dim
+        # per-position multiply-accumulates, as the reference's local_matmul / add_macs charge them
+        mesh.add_macs_all(bs * h * 3 * hp + 2 * att_macs + bs * hp * h + bs * h * 4 * hp + bs * 4 * hp * h)
         saved = {"ln1": ln1, "a1": a1, "dev": [None] * p}
         parts = [None] * p
         for d in mesh.local_devs:
@@ -145,6 +148,8 @@ class Baseline1DLayer:
         dyf.copy_(torch.as_tensor(np.asarray(dy) if not isinstance(dy, torch.Tensor) else dy).to(device, F32))
         dy16 = ws.empty(dev0, (bs, cfg.h), "free", dtype=BF16)
         dy16.copy_(dyf)
+        h, att_macs = cfg.h, cfg.b * n_loc * cfg.s * cfg.s * cfg.head_dim
+        mesh.add_macs_all(4 * bs * h * 4 * hp + 2 * bs * hp * h + 4 * att_macs + 2 * bs * 3 * hp * h)
         b2_grad = torch.zeros(cfg.h, device=device)
         K.colsum(dyf, b2_grad, accumulate=True)
         dw1, db1, dw2 = [None] * p, [None] * p, [None] * p

@@ -269,7 +269,7 @@ def embedding_backward(out_grad: ShardedMatrix, tokens, table: ShardedMatrix, cf
     for l in range(c):
         if mesh.is_local:
             # the column reduce collapses into atomics on the owner's block
-            mesh._count("reduce", tag)
+            mesh.charge("reduce", "col", l % r, vb * hb, tag)
             for j in range(c):
                 dst = res.block(l, j)
                 for i in range(r):
@@ -568,6 +568,8 @@ def attention_forward(x: ShardedMatrix, w_qkv: ShardedMatrix, b_qkv: RowHostedVe
     qkv = summa_ab(x, w_qkv, ws, out_category="forward", tag="summa", out_dtype=BF16,
                    bias=[None if d is None else b_qkv.for_position(mesh, d) for d in _all(mesh)])
     ctx_blocks, probs, lse = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
+    mac_per_dev = (cfg.b // mesh.r) * (cfg.n // mesh.c) * cfg.s * cfg.s * cfg.head_dim
+    mesh.add_macs_all(2 * mac_per_dev)  # QK^T, PV (layers.py:414)
     for dev in mesh.local_devs:
         ctx_blocks[dev] = ws.empty(dev, (bs_loc, hb), "free", dtype=BF16)
         probs[dev], lse[dev] = _local_attention(cfg, mesh, qkv.blocks[dev], ctx_blocks[dev], ws, dev)
@@ -646,6 +648,7 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     dctx = summa_abt(dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
     w_dense_grad = summa_atb(ctx.ctx_mat, dy16, ws, out_category="param_grad")
     bq_parts = new_colsum_parts(mesh, ws, 3 * hb)  # b_qkv gradient fused into dQ / dK / dV epilogues
+    mesh.add_macs_all(4 * b_loc * n_loc * cfg.s * cfg.s * cfg.head_dim)  # dP, dV, dQ, dK (layers.py:457)
     dqkv_blocks = [None] * mesh.p
     for dev in mesh.local_devs:
         dqkv_blocks[dev] = attention_core_backward(

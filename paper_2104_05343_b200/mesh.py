@@ -33,6 +33,7 @@ import torch
 
 from . import kernels as K
 from .errors import ConfigError, MeshMismatchError, ShapeError
+from .ledger import CommLedger
 
 
 class Placement(enum.Enum):
@@ -155,6 +156,7 @@ class Mesh:
             self._slot.append(n * cfg.node_size + seen[n])
             seen[n] += 1
         self.stats: Counter = Counter()
+        self.ledger = CommLedger(self.p)
         self._closed = False
         if backend == "local":
             if device is None:
@@ -240,6 +242,34 @@ class Mesh:
     def _count(self, kind: str, tag: str) -> None:
         self.stats[(kind, tag)] += 1
 
+    # ---- ledger (accounting only, ledger.py): the reference's cost model per collective
+    @staticmethod
+    def _numel(blocks) -> int:
+        for b in blocks:
+            if b is not None:
+                return int(b.numel())
+        return 0
+
+    def _charge_group(self, kind: str, group: Sequence[int], root_pos: int, n: int, tag: str) -> None:
+        if kind == "allreduce":
+            self.ledger.charge_ring(group, n, self.cost.beta, tag, self.node_of)
+        else:
+            self.ledger.charge_tree(group, root_pos, n, self.cost.beta, tag, kind, self.node_of)
+
+    def charge(self, kind: str, axis: str, root_pos: int, n: int, tag: str) -> None:
+        """Count one collective call and charge it on every group of ``axis`` (row / col / all)."""
+        self._count(kind, tag)
+        groups = self._row_groups if axis == "row" else self._col_groups if axis == "col" else [self.all_group()]
+        for g in groups:
+            self._charge_group(kind, g, root_pos, n, tag)
+
+    def add_macs(self, dev: int, count: int) -> None:
+        self.ledger.macs[dev] += count
+
+    def add_macs_all(self, count: int) -> None:
+        """The same local product on every position (SUMMA steps)."""
+        self.ledger.macs += count
+
     def collective_count(self, kind: str | None = None, tag: str | None = None) -> int:
         return sum(v for (k, t), v in self.stats.items() if (kind is None or k == kind) and (tag is None or t == tag))
 
@@ -250,7 +280,7 @@ class Mesh:
 
     def _bcast(self, axis: str, root: int, src: Sequence, shape, dtype, tag: str) -> list:
         """Each owned position receives the block of the group member at ``root``."""
-        self._count("broadcast", tag)
+        self.charge("broadcast", axis, root, int(math.prod(shape)) if shape else self._numel(src), tag)
         out: list = [None] * self.p
         if self.is_local:
             for f in self.local_devs:
@@ -279,7 +309,7 @@ class Mesh:
     # current stream, and ``wait()`` makes the current stream wait for it; step
     # l+1's panels are issued before step l's product so the two overlap.
     def _bcast_async(self, axis: str, root: int, src: Sequence, recv, tag: str) -> "Pending":
-        self._count("broadcast", tag)
+        self.charge("broadcast", axis, root, self._numel(src), tag)
         out: list = [None] * self.p
         if self.is_local:
             for f in self.local_devs:
@@ -315,7 +345,7 @@ class Mesh:
     def _reduce_async(self, axis: str, dest: int, parts: Sequence, tag: str) -> "Pending":
         """Start the group reduce of ``parts`` to group position ``dest``; ``finish``
         folds the sum into the destination's output block."""
-        self._count("reduce", tag)
+        self.charge("reduce", axis, dest, self._numel(parts), tag)
         groups = self._row_groups if axis == "row" else self._col_groups
         if self.is_local:
             return Pending(list(parts), [], fold=[(g[dest], [parts[f] for f in g]) for g in groups])
@@ -358,7 +388,7 @@ class Mesh:
         return self._bcast("col", root_row, src, shape, dtype, tag)
 
     def _reduce_into(self, axis: str, dest: int, parts: Sequence, out: Sequence, accumulate: bool, tag: str) -> None:
-        self._count("reduce", tag)
+        self.charge("reduce", axis, dest, self._numel(parts), tag)
         if self.is_local:
             groups = self._row_groups if axis == "row" else self._col_groups
             for g in groups:
@@ -399,7 +429,7 @@ class Mesh:
     def _allreduce(self, axis: str, bufs: Sequence, op: str, tag: str) -> None:
         if op not in ("sum", "max"):
             raise ConfigError(f"unknown all_reduce op {op!r}")
-        self._count("allreduce", tag)
+        self.charge("allreduce", axis, 0, self._numel(bufs), tag)
         if self.is_local:
             groups = self._row_groups if axis == "row" else self._col_groups
             for g in groups:
@@ -433,7 +463,7 @@ class Mesh:
         baseline.py:128-202, mesh.py:510-513); position order on the local backend."""
         if op not in ("sum", "max"):
             raise ConfigError(f"unknown all_reduce op {op!r}")
-        self._count("allreduce", tag)
+        self.charge("allreduce", "all", 0, self._numel(bufs), tag)
         if self.is_local:
             first = bufs[0]
             K.fold(first, list(bufs), op_max=(op == "max"))
@@ -459,6 +489,7 @@ class Mesh:
         if not 0 <= root_col < self.c:
             raise ConfigError(f"broadcast root column {root_col} out of range for c={self.c}")
         self._count("broadcast", tag)
+        self._charge_group("broadcast", self._row_groups[row], root_col, int(block.numel()), tag)
         return [_staged_copy(block, ws, f, category) for f in self._row_groups[row]]
 
     def broadcast_col(self, col: int, root_row: int, block: torch.Tensor, tag: str = "misc", ws=None,
@@ -467,6 +498,7 @@ class Mesh:
         if not 0 <= root_row < self.r:
             raise ConfigError(f"broadcast root row {root_row} out of range for r={self.r}")
         self._count("broadcast", tag)
+        self._charge_group("broadcast", self._col_groups[col], root_row, int(block.numel()), tag)
         return [_staged_copy(block, ws, f, category) for f in self._col_groups[col]]
 
     def _fold_blocks(self, blocks: Sequence[torch.Tensor], op: str) -> torch.Tensor:
@@ -484,6 +516,7 @@ class Mesh:
         if not 0 <= dest_col < self.c:
             raise ConfigError(f"reduce destination column {dest_col} out of range for c={self.c}")
         self._count("reduce", tag)
+        self._charge_group("reduce", self._row_groups[row], dest_col, int(blocks[0].numel()), tag)
         return self._fold_blocks(blocks, "sum")
 
     def reduce_col(self, col: int, dest_row: int, blocks: Sequence[torch.Tensor], tag: str = "misc") -> torch.Tensor:
@@ -491,24 +524,26 @@ class Mesh:
         if not 0 <= dest_row < self.r:
             raise ConfigError(f"reduce destination row {dest_row} out of range for r={self.r}")
         self._count("reduce", tag)
+        self._charge_group("reduce", self._col_groups[col], dest_row, int(blocks[0].numel()), tag)
         return self._fold_blocks(blocks, "sum")
 
-    def _all_reduce_blocks(self, blocks, op, tag):
+    def _all_reduce_blocks(self, group, blocks, op, tag):
         self._need_local()
         if op not in ("sum", "max"):
             raise ConfigError(f"unknown all_reduce op {op!r}")
         self._count("allreduce", tag)
+        self._charge_group("allreduce", group, 0, int(blocks[0].numel()), tag)
         acc = self._fold_blocks(blocks, op)
         return [acc.clone() for _ in blocks]
 
     def all_reduce_row(self, row: int, blocks, op: str = "sum", tag: str = "misc"):
-        return self._all_reduce_blocks(blocks, op, tag)
+        return self._all_reduce_blocks(self._row_groups[row], blocks, op, tag)
 
     def all_reduce_col(self, col: int, blocks, op: str = "sum", tag: str = "misc"):
-        return self._all_reduce_blocks(blocks, op, tag)
+        return self._all_reduce_blocks(self._col_groups[col], blocks, op, tag)
 
     def all_reduce_all(self, blocks, op: str = "sum", tag: str = "misc"):
-        return self._all_reduce_blocks(blocks, op, tag)
+        return self._all_reduce_blocks(self.all_group(), blocks, op, tag)
 
     def local_matmul(self, dev: int, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
                      accumulate: bool = False) -> torch.Tensor:
@@ -517,6 +552,7 @@ class Mesh:
             raise ShapeError(f"local matmul inner dims differ: {tuple(a.shape)} x {tuple(b.shape)}")
         if out is None:
             out = torch.empty(a.shape[0], b.shape[1], device=a.device, dtype=torch.float32)
+        self.ledger.macs[dev] += int(a.shape[0]) * int(a.shape[1]) * int(b.shape[1])
         K.gemm(a.to(torch.bfloat16), b.to(torch.bfloat16), out, c=out if accumulate else None)
         return out
 

@@ -239,6 +239,7 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
         nxt = issue(l + 1) if l + 1 < steps else None
         a_pan, b_pan = pend[0].wait(), pend[1].wait()
         pend = nxt
+        mesh.add_macs_all(m_b * k_b * n_b)
         last = l == steps - 1
         for dev in mesh.local_devs:
             c_in = acc[dev] if accumulate else (resid.blocks[dev] if direct_resid else None)
@@ -281,8 +282,9 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
         # (the GEMM takes one global epilogue input at a time)
         split_epi = mesh.c > 1 and act != K.ACT_NONE
         for l in range(mesh.c):
-            mesh._count("broadcast", tag)
-            mesh._count("reduce", tag)
+            mesh.charge("broadcast", "col", l % mesh.r, n_b * k_b, tag)  # B(l, j) down column j
+            mesh.charge("reduce", "row", l, m_b * n_b, tag)             # partials to (i, l)
+            mesh.add_macs_all(m_b * k_b * n_b)
             for i in range(mesh.r):
                 d = mesh.flat(i, l)
                 chain = out[d] if mesh.c == 1 or (out_dtype == F32 and act == K.ACT_NONE) else \
@@ -319,6 +321,7 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
         pend = nxt
         parts = [None] * mesh.p
         parts[f] = part_slots[l % 2]
+        mesh.add_macs_all(m_b * k_b * n_b)
         K.gemm(a16.blocks[f], b_pan[f].t(), parts[f])
         red = mesh.reduce_row_async(l, parts, tag=tag)
         if red_prev is not None:
@@ -354,8 +357,9 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
     acc_in = accumulate_into is not None
     if mesh.is_local:
         for l in range(mesh.c):
-            mesh._count("broadcast", tag)
-            mesh._count("reduce", tag)
+            mesh.charge("broadcast", "row", l, t_b * m_b, tag)      # A(i, l) along row i
+            mesh.charge("reduce", "col", l % mesh.r, m_b * n_b, tag)  # partials to (l mod r, j)
+            mesh.add_macs_all(m_b * t_b * n_b)
             for j in range(mesh.c):
                 k = l * mesh.c + j
                 chain = out[k] if out[k].dtype == F32 else ws_empty(ws, mesh, mesh.flat(l % mesh.r, j), (m_b, n_b))
@@ -388,6 +392,7 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
         pend = nxt
         parts = [None] * mesh.p
         parts[f] = part_slots[l % 2]
+        mesh.add_macs_all(m_b * t_b * n_b)
         K.gemm(a_pan[f].t(), b16.blocks[f], parts[f])
         red = (mesh.reduce_col_async(l % mesh.r, parts, tag=tag), dest_of(l))
         if red_prev is not None:
