@@ -262,11 +262,34 @@ def gen_ledger(sg) -> dict:
     return out
 
 
+def gen_classifier(sg) -> dict:
+    """Loss and every gradient (cls_w included) of a model with the position-0
+    classifier head (model.py:238-292), reference mesh q = 2."""
+    from summagrid import dense, model
+
+    cfg = sg.ModelConfig(b=4, s=8, h=32, n=4, v=24, num_layers=1)
+    params = model.init_global_params(cfg, 13, classifier=True)
+    rng = dense.make_rng(14)
+    tokens = rng.integers(0, cfg.v, (cfg.b, cfg.s))
+    labels = rng.integers(0, cfg.v, (cfg.b, cfg.s))
+    cls_labels = np.array([0, 1, 1, 0])
+    mesh = sg.create_mesh(sg.MeshConfig(q=2))
+    m = model.MeshModel(mesh, cfg, params, classifier=True)
+    loss, grads, _, _ = model.run_loss_and_grads(m, tokens, labels, checkpointing=False, cls_labels=cls_labels)
+    out = {f"grad.{k}": v for k, v in m.gather_grads(grads).items()}
+    out.update({f"param.{k}": v for k, v in params.items()})
+    out.update(loss=np.array(float(loss)), tokens=tokens, labels=labels, cls_labels=cls_labels)
+    return out
+
+
 def main() -> None:
     sg = _ref()
     OUT.mkdir(parents=True, exist_ok=True)
     if "--only-checkpoint" in sys.argv:
         gen_checkpoint(sg)
+        return
+    if "--only-classifier" in sys.argv:
+        np.savez_compressed(OUT / "model_cls.npz", **gen_classifier(sg))
         return
     if "--only-ledger" in sys.argv:
         (OUT / "ledger.json").write_text(json.dumps(gen_ledger(sg), indent=1, sort_keys=True))
@@ -277,6 +300,7 @@ def main() -> None:
     gen_checkpoint(sg)
     np.savez_compressed(OUT / "baseline1d.npz", **gen_baseline(sg))
     (OUT / "ledger.json").write_text(json.dumps(gen_ledger(sg), indent=1, sort_keys=True))
+    np.savez_compressed(OUT / "model_cls.npz", **gen_classifier(sg))
     book = gen_bookkeeping(sg)
     (OUT / "bookkeeping.json").write_text(json.dumps(book, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "summa.npz", **gen_summa(sg))

@@ -126,8 +126,6 @@ def init_global_params(cfg: ModelConfig, seed: int, classifier: bool = False) ->
     PCG64(seed) draws U[-1/sqrt(h), 1/sqrt(h)) in the order table, then per
     layer w_qkv, w_dense, w1, w2; vectors start at identity (gamma=1, rest 0).
     """
-    if classifier:
-        raise ConfigError("the sequence-classifier branch is outside this build's hot path")
     rng = np.random.Generator(np.random.PCG64(seed))
     lim = 1.0 / math.sqrt(cfg.h)
     out = {"table": rng.uniform(-lim, lim, size=(cfg.v, cfg.h))}
@@ -139,6 +137,8 @@ def init_global_params(cfg: ModelConfig, seed: int, classifier: bool = False) ->
                 out[pre + name] = rng.uniform(-lim, lim, size=shape)
             else:
                 out[pre + name] = (np.ones if name.endswith("gamma") else np.zeros)(shape)
+    if classifier:  # drawn after every layer (model.py:116-117)
+        out["cls_w"] = rng.uniform(-lim, lim, size=(cfg.h, 2))
     return out
 
 
@@ -158,6 +158,7 @@ class ModelSaved:
     layer_saves: Optional[list] = None
     store: Optional[CheckpointStore] = None
     ids: Optional[list] = None
+    cls_ctx: Optional[dict] = None
 
 
 def _with_twin(m: ShardedMatrix) -> ShardedMatrix:
@@ -172,12 +173,10 @@ class MeshModel:
 
     def __init__(self, mesh: Mesh, cfg: ModelConfig, global_params: dict | None = None, classifier: bool = False,
                  skip_dead_recompute: bool = False, *, seed: int = 0, logits_dtype: torch.dtype = BF16) -> None:
-        if classifier:
-            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
         cfg.validate_mesh(mesh)
         self.mesh = mesh
         self.cfg = cfg
-        self.classifier = False
+        self.classifier = classifier
         self.logits_dtype = logits_dtype
         c = mesh.c
         v_pad = cfg.v_padded(mesh)
@@ -210,6 +209,22 @@ class MeshModel:
                     for name in _LAYER_KEYS if name not in _MATS}
             params = LayerParams(**kw, **vec)
             self.layers.append(TransformerLayer(mesh, cfg, params, skip_dead_recompute=skip_dead_recompute))
+        # position-0 binary classifier head (model.py:123-131, 185-188): the [h, 2]
+        # weight split by rows over the mesh columns, a replica per column
+        self.cls_w: list | None = None
+        self.cls_w16: list | None = None
+        if classifier:
+            w = (np.asarray(global_params["cls_w"], dtype=np.float64) if global_params is not None
+                 else np.random.default_rng(seed + 7).uniform(-1 / math.sqrt(cfg.h), 1 / math.sqrt(cfg.h), (cfg.h, 2)))
+            hb = cfg.h // c
+            self.cls_w, self.cls_w16 = [None] * c, [None] * c
+            for j in range(c):
+                if not mesh.is_local and mesh.my_flat % c != j:
+                    continue
+                self.cls_w[j] = padded_empty((hb, 2), F32, mesh.device())
+                self.cls_w[j].copy_(torch.as_tensor(w[j * hb:(j + 1) * hb], dtype=F32))
+                self.cls_w16[j] = padded_empty((hb, 2), BF16, mesh.device())
+                self.cls_w16[j].copy_(self.cls_w[j])
 
     # ------------------------------------------------------------------ workspace
     def make_workspace(self, checkpointing: bool = True, eager_update: bool = False, merge_fwd_bwd: bool = False,
@@ -225,8 +240,8 @@ class MeshModel:
         cfg = self.cfg
         if tuple(tokens.shape) != (cfg.b, cfg.s):
             raise ShapeError(f"tokens must be [{cfg.b}, {cfg.s}], got {tuple(tokens.shape)}")
-        if cls_labels is not None:
-            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
+        if self.classifier and cls_labels is None:
+            raise ConfigError("classifier enabled but cls_labels missing")
         ws.reset_all("forward")
         ws.reset_all("free")
         ids = _device_ids(self.mesh, tokens)
@@ -241,8 +256,12 @@ class MeshModel:
                 layer_saves.append(saved)
         logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor)
+        cls_ctx = None
+        if self.classifier:
+            cls_loss, cls_ctx = self._cls_forward(x, cls_labels, ws)
+            loss = loss + (cls_loss if return_tensor else float(cls_loss.item()))
         return loss, ModelSaved(tokens=tokens, labels=labels, x_final=x, ce_ctx=ce_ctx, layer_saves=layer_saves,
-                                store=store, ids=ids)
+                                store=store, ids=ids, cls_ctx=cls_ctx)
 
     def backward(self, saved: ModelSaved, ws: Workspace, upstream: float = 1.0, eager_update: bool = False,
                  lr: float = 0.0) -> ModelGrads:
@@ -253,11 +272,17 @@ class MeshModel:
         dlogits = ShardedMatrix(mesh, cfg.b * cfg.s, cfg.v_padded(mesh), dl)
         from .layers import new_colsum_parts
 
-        parts = new_colsum_parts(mesh, ws, cfg.h // mesh.c)  # last layer's b2 gradient, fused
-        dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32,
-                      want_bf16=True, colsum=parts)
-        dx.colsum_parts = parts
+        if self.classifier:
+            # the head adds into dx after the product: its bf16 twin and column sums are
+            # formed later, by the layer (_bf16_of / bias_add_backward)
+            dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32)
+        else:
+            parts = new_colsum_parts(mesh, ws, cfg.h // mesh.c)  # last layer's b2 gradient, fused
+            dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32,
+                          want_bf16=True, colsum=parts)
+            dx.colsum_parts = parts
         table_grad = summa_atb(dlogits, saved.x_final, ws, out_category="param_grad_tied", tag="lmhead")
+        cls_w_grad = self._cls_backward(saved.cls_ctx, dx, ws, upstream) if self.classifier else None
         if saved.store is not None:
             dx0, layer_grads = checkpointed_backward(self.layers, dx, saved.store, ws, eager_update=eager_update,
                                                      lr=lr)
@@ -273,20 +298,90 @@ class MeshModel:
                     layer_grads[li] = g
             dx0 = dy
         embedding_backward(dx0, saved.tokens, self.table, cfg, ws, ids=saved.ids, accumulate_into=table_grad)
-        return ModelGrads(table=table_grad, layers=layer_grads)
+        return ModelGrads(table=table_grad, layers=layer_grads, cls_w=cls_w_grad)
+
+    # ------------------------------------------------------------------ classifier branch
+    def _cls_x0(self, x: ShardedMatrix, dev: int) -> torch.Tensor:
+        """Rows at sequence position 0 of a position's [b_loc*s, h/c] block (a strided view)."""
+        blk = x.blocks[dev]
+        b_loc = self.cfg.b // self.mesh.r
+        return torch.as_strided(blk, (b_loc, blk.shape[1]), (self.cfg.s * blk.stride(0), 1))
+
+    def _cls_forward(self, x_final: ShardedMatrix, cls_labels, ws: Workspace):
+        """Position-0 binary classifier loss (model.py:238-276): partial logits x0 W_j
+        row-all-reduced, softmax cross entropy, mean over the b sequences."""
+        mesh, cfg = self.mesh, self.cfg
+        b_loc, hb, c = cfg.b // mesh.r, cfg.h // mesh.c, mesh.c
+        labels = torch.as_tensor(np.asarray(cls_labels.cpu() if isinstance(cls_labels, torch.Tensor) else cls_labels),
+                                 dtype=torch.int64)
+        if labels.shape != (cfg.b,):
+            raise ShapeError(f"cls_labels must be [{cfg.b}], got {tuple(labels.shape)}")
+        if labels.numel() and (int(labels.min()) < 0 or int(labels.max()) > 1):
+            raise ConfigError("cls_labels must lie in [0, 2)")
+        x0, logits, labs = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
+        for dev in mesh.local_devs:
+            x0[dev] = ws.empty(dev, (b_loc, hb), "free", dtype=BF16)
+            K.epilogue(self._cls_x0(x_final, dev), x0[dev])
+            logits[dev] = ws.empty(dev, (b_loc, 2), "free", dtype=F32)
+            K.gemm(x0[dev], self.cls_w16[dev % c], logits[dev])
+            i = dev // c
+            labs[dev] = labels[i * b_loc:(i + 1) * b_loc].to(mesh.device())
+        mesh.allreduce_row(logits, tag="classifier")
+        gmax, packed, part = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
+        for dev in mesh.local_devs:
+            lmax = ws.empty(dev, (b_loc,), "free", dtype=F32)
+            gmax[dev] = ws.empty(dev, (b_loc,), "free", dtype=F32)
+            packed[dev] = ws.empty(dev, (b_loc, 2), "free", dtype=F32, pad=False)
+            K.xent_local(logits[dev], 2, labs[dev], 0, lmax, gmax[dev], packed[dev])
+            rows = ws.empty(dev, (b_loc,), "free", dtype=F32)
+            part[dev] = ws.empty(dev, (1,), "free", dtype=F32)
+            K.xent_loss(gmax[dev], packed[dev], rows, part[dev])
+        mesh.allreduce_col(part, tag="classifier")
+        loss = part[mesh.local_devs[0]] / cfg.b
+        return loss, {"x0": x0, "logits": logits, "labels": labs, "gmax": gmax, "packed": packed}
+
+    def _cls_backward(self, ctx: dict, dx_final: ShardedMatrix, ws: Workspace, upstream: float = 1.0) -> list:
+        """dW_j = x0^T dlogits (column-reduced to each column's shard) and dx0 =
+        dlogits W_j^T added into dx at sequence position 0 (model.py:278-292)."""
+        mesh, cfg = self.mesh, self.cfg
+        b_loc, hb, c = cfg.b // mesh.r, cfg.h // mesh.c, mesh.c
+        dw = [None] * mesh.p
+        for dev in mesh.local_devs:
+            dl = ws.empty(dev, (b_loc, 2), "free", dtype=F32)
+            K.xent_bwd(ctx["logits"][dev], 2, ctx["labels"][dev], 0, ctx["gmax"][dev], ctx["packed"][dev],
+                       upstream / cfg.b, dl)
+            dl16 = ws.empty(dev, (b_loc, 2), "free", dtype=BF16)
+            K.epilogue(dl, dl16)
+            dw[dev] = ws.empty(dev, (hb, 2), "param_grad", dtype=F32)
+            K.gemm(ctx["x0"][dev].t(), dl16, dw[dev])
+            dx0 = self._cls_x0(dx_final, dev)
+            K.gemm(dl16, self.cls_w16[dev % c].t(), dx0, c=dx0)
+        mesh.allreduce_col(dw, tag="classifier")
+        shards = [None] * c
+        for dev in mesh.local_devs:
+            if shards[dev % c] is None:
+                shards[dev % c] = dw[dev]
+        return shards
 
     def apply_sgd(self, grads: ModelGrads, lr: float) -> None:
         sgd_matrix(self.table, grads.table, lr)
         for layer, g in zip(self.layers, grads.layers):
             if g is not None:
                 layer.apply_sgd(g, lr)
+        self._cls_sgd(grads, lr)
 
-    def train_step(self, tokens, labels, ws: Workspace, lr: float, checkpointing: bool = False) -> torch.Tensor:
+    def _cls_sgd(self, grads: ModelGrads, lr: float) -> None:
+        if self.cls_w is not None and grads.cls_w is not None:
+            K.sgd_multi([(w, w16, g) for w, w16, g in zip(self.cls_w, self.cls_w16, grads.cls_w) if w is not None], lr)
+
+    def train_step(self, tokens, labels, ws: Workspace, lr: float, checkpointing: bool = False,
+                   cls_labels=None) -> torch.Tensor:
         """One fwd + bwd + SGD step with no host synchronisation; returns the loss tensor."""
         store = CheckpointStore(self.mesh.p) if checkpointing else None
-        loss, saved = self.forward(tokens, labels, ws, store=store, return_tensor=True)
+        loss, saved = self.forward(tokens, labels, ws, store=store, return_tensor=True, cls_labels=cls_labels)
         grads = self.backward(saved, ws, eager_update=True, lr=lr)
         sgd_matrix(self.table, grads.table, lr)
+        self._cls_sgd(grads, lr)
         return loss
 
     def infer(self, tokens, labels, ws: Workspace) -> torch.Tensor:
@@ -307,15 +402,13 @@ class MeshModel:
     # ------------------------------------------------------------------ checkpoint file
     def save(self, path) -> None:
         """Gather the parameters and write them in the reference checkpoint format."""
-        save_checkpoint(path, self.cfg, self.gather_params())
+        save_checkpoint(path, self.cfg, self.gather_params(), classifier=self.classifier)
 
     @classmethod
     def load(cls, path, mesh: Mesh, **kw) -> "MeshModel":
         """A model on ``mesh`` (any shape the dimensions divide) from a checkpoint file."""
         cfg, params, classifier = load_checkpoint(path)
-        if classifier:
-            raise ConfigError("the sequence-classifier branch is outside this build's hot path")
-        return cls(mesh, cfg, params, **kw)
+        return cls(mesh, cfg, params, classifier=classifier, **kw)
 
     # ------------------------------------------------------------------ gather for parity
     def gather_params(self) -> dict[str, np.ndarray]:
@@ -323,6 +416,9 @@ class MeshModel:
         out = {"table": gather(self.table)[:cfg.v]}
         for i, layer in enumerate(self.layers):
             out.update(_gather_layer(f"layers.{i}.", layer.params, c))
+        if self.cls_w is not None:
+            out["cls_w"] = RowHostedVector([None if w is None else w.reshape(-1) for w in self.cls_w]) \
+                .gathered().reshape(cfg.h, 2)
         return out
 
     def gather_grads(self, grads: ModelGrads) -> dict[str, np.ndarray]:
@@ -331,6 +427,9 @@ class MeshModel:
         for i, g in enumerate(grads.layers):
             if g is not None:
                 out.update(_gather_layer(f"layers.{i}.", g, c))
+        if grads.cls_w is not None:
+            out["cls_w"] = RowHostedVector([None if w is None else w.reshape(-1) for w in grads.cls_w]) \
+                .gathered().reshape(cfg.h, 2)
         return out
 
 

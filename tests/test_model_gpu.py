@@ -186,3 +186,23 @@ def test_checkpoint_file_across_meshes(tmp_path):
     la = float(a.infer(torch.as_tensor(tokens), torch.as_tensor(labels), a.make_workspace()).item())
     lb = float(b.infer(torch.as_tensor(tokens), torch.as_tensor(labels), b.make_workspace()).item())
     assert abs(la - lb) / abs(la) < 1e-3
+
+
+@pytest.mark.parametrize("rc", [(1, 1), (1, 2), (2, 2), (2, 4)])
+@pytest.mark.parametrize("checkpointing", [False, True])
+def test_classifier_branch_vs_reference(rc, checkpointing):
+    """Position-0 binary classifier head (model.py:238-292): loss and every gradient,
+    cls_w included, against the reference's own q = 2 run (tests/golden/model_cls.npz)."""
+    sg = _sg()
+    g = np.load(GOLD / "model_cls.npz")
+    cfg = sg.ModelConfig(b=4, s=8, h=32, n=4, v=24, num_layers=1)
+    params = {k[len("param."):]: g[k] for k in g.files if k.startswith("param.")}
+    model = sg.MeshModel(mesh(*rc), cfg, params, classifier=True)
+    loss, grads, _, _ = sg.run_loss_and_grads(model, g["tokens"], g["labels"], checkpointing=checkpointing,
+                                              cls_labels=g["cls_labels"])
+    assert abs(loss - float(g["loss"])) / abs(float(g["loss"])) < 1e-2
+    got = model.gather_grads(grads)
+    assert set(got) == {k[len("grad."):] for k in g.files if k.startswith("grad.")}
+    _compare_grads(sg, got, {k[len("grad."):]: g[k] for k in g.files if k.startswith("grad.")})
+    with pytest.raises(sg.ConfigError):
+        model.forward(g["tokens"], g["labels"], model.make_workspace())  # cls_labels missing
