@@ -299,6 +299,11 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t y, uint64_t z) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(y), "l"(z));
   return r;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t x, uint64_t y) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return r;
+}
 __device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
   uint64_t r;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
@@ -1126,17 +1131,25 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(t_s + lane_base + c * 32, sv);
         tmem_ld32(t_dp + lane_base + c * 32, dv);
         tmem_wait_ld();
+        // pairs of keys on the paired fp32 pipe: y = s * scale - lse, P = 2^y,
+        // dS = (P * scale) * (dP - D)
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nl2 = f2_pack(-lse2, -lse2);
+        const uint64_t nd2 = f2_pack(-dd, -dd), ss2 = f2_pack(scale, scale);
 #pragma unroll
         for (int e2 = 0; e2 < 16; ++e2) {
-          float p0 = ex2f_fast(fmaf(__uint_as_float(sv[2 * e2]), scale_log2, -lse2));
-          float p1 = ex2f_fast(fmaf(__uint_as_float(sv[2 * e2 + 1]), scale_log2, -lse2));
+          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * e2]), __uint_as_float(sv[2 * e2 + 1])), sc2, nl2);
+          float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
+          float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
           if (!full_keys || !qok) {
             if (!qok || c * 32 + 2 * e2 >= kvalid) p0 = 0.f;
             if (!qok || c * 32 + 2 * e2 + 1 >= kvalid) p1 = 0.f;
           }
-          const float d0 = p0 * (__uint_as_float(dv[2 * e2]) - dd) * scale;
-          const float d1 = p1 * (__uint_as_float(dv[2 * e2 + 1]) - dd) * scale;
-          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d0, d1);
+          const uint64_t pp = f2_pack(p0, p1);
+          const uint64_t dmd = fadd2(f2_pack(__uint_as_float(dv[2 * e2]), __uint_as_float(dv[2 * e2 + 1])), nd2);
+          const uint64_t ds = fmul2(fmul2(pp, ss2), dmd);
+          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
+          __nv_bfloat162 hd = __floats2bfloat162_rn(__uint_as_float(static_cast<uint32_t>(ds)),
+                                                   __uint_as_float(static_cast<uint32_t>(ds >> 32)));
           pk[cc][e2] = *reinterpret_cast<uint32_t*>(&hp);
           dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
         }
