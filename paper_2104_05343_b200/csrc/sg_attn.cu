@@ -291,25 +291,6 @@ struct Flash2Cfg {
   static constexpr size_t SMEM = Q_SLOTS * kQT * T64 + KV_SLOTS * 2 * T64 + kQT * P_BYTES + 256;
 };
 
-__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
-  return static_cast<uint64_t>(__float_as_uint(a)) | (static_cast<uint64_t>(__float_as_uint(b)) << 32);
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t x, uint64_t y, uint64_t z) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(y), "l"(z));
-  return r;
-}
-__device__ __forceinline__ uint64_t fmul2(uint64_t x, uint64_t y) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
-  return r;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t x, uint64_t y) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
-  return r;
-}
-
 // Persistent: CTA c processes work items t = c, c + grid, ... with t = (query-tile
 // pair, head, batch), pair index fastest (neighbouring CTAs share K / V in L2).
 // All per-block barriers run on a CTA-wide block counter G across items, so the

@@ -102,7 +102,7 @@ struct GemmCfg {
   static constexpr int STAGES =
       PAIR ? (EW == 8 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 6 : 8))
            : (EW == 8 ? (BN == 256 ? 3 : 4) : (BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8))));
-  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + EW * kStgBytes + 512;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + EW * (kStgBytes + 128) + 512;
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(!PAIR || BN == 128 || BN == 256, "pair tiles are 256 x 128 or 256 x 256");
 };
@@ -163,6 +163,23 @@ __device__ __forceinline__ void unit_k_range(const GemmParams& p, int t, int& kb
   const int split = t / (p.num_tiles / p.k_splits);
   kb0 = split * p.kb_per_split;
   kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+}
+
+// tanh-GELU of 32 values on the paired fp32 pipe: 0.5 x (1 + tanh(c x (1 + a x^2)))
+__device__ __forceinline__ void gelu_row(float (&v)[32]) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const uint64_t ca2 = f2_pack(c * a, c * a), c2 = f2_pack(c, c), h2 = f2_pack(0.5f, 0.5f);
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const uint64_t x = f2_pack(v[j], v[j + 1]);
+    const uint64_t t = ffma2(fmul2(x, x), ca2, c2);  // c + c a x^2
+    const uint64_t u = fmul2(x, t);                  // c (x + a x^3)
+    const uint64_t hx = fmul2(x, h2);
+    const uint64_t th = f2_pack(tanh_fast(f2_lo(u)), tanh_fast(f2_hi(u)));
+    const uint64_t y = ffma2(hx, th, hx);
+    v[j] = f2_lo(y);
+    v[j + 1] = f2_hi(y);
+  }
 }
 
 __device__ __forceinline__ float gelu_fast(float x) {
@@ -264,7 +281,8 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint8_t* stg_all = sB + STAGES * B_BYTES;  // 1024-aligned
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + EW * kStgBytes);
+  float* bias_all = reinterpret_cast<float*>(stg_all + EW * kStgBytes);  // [EW][32] bias chunk per warp
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + EW * (kStgBytes + 128));
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
@@ -598,8 +616,18 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
                              p.vec_d, min(32, p.N - col0), v);
           } else {
             if (p.bias) {
+              // lane j's coalesced bias value -> the warp's 128-byte slot -> every row thread
+              float* bw = bias_all + e * 32;
+              bw[lane] = bias_cur;
+              __syncwarp();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bias_cur, j);
+              for (int k = 0; k < 8; ++k) {
+                const float4 b4 = reinterpret_cast<const float4*>(bw)[k];
+                const uint64_t lo = fadd2(f2_pack(v[4 * k], v[4 * k + 1]), f2_pack(b4.x, b4.y));
+                const uint64_t hi = fadd2(f2_pack(v[4 * k + 2], v[4 * k + 3]), f2_pack(b4.z, b4.w));
+                v[4 * k] = f2_lo(lo); v[4 * k + 1] = f2_hi(lo); v[4 * k + 2] = f2_lo(hi); v[4 * k + 3] = f2_hi(hi);
+              }
+              __syncwarp();
             }
             if (in_kind == 1) {
               float cv[32];
@@ -612,8 +640,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
             }
             if (p.act == SG_ACT_GELU) {
               if (p.aux_out) st_row_bf16(s1, lane, v);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+              gelu_row(v);
             } else if (p.act == SG_ACT_DGELU) {
               float xv[32];
               ld_row_bf16(s1, lane, xv);
