@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--checkpointing", action="store_true", help="activation checkpointing (recompute)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--summa-n", type=int, default=8192)
+    ap.add_argument("--summa-sweep", action="store_true",
+                    help="also time the SUMMA forms at N = 4096, 8192, 16384, 32768 (configs[1])")
     ap.add_argument("--mode", choices=("train", "infer"), default="train",
                     help="train: fwd+bwd+SGD step; infer: forward (with the CE loss, as the reference) only")
     ap.add_argument("--max-batch", action="store_true",
@@ -341,6 +343,8 @@ def main():
 
     # ------------------------------------------------------------- SUMMA sweep point (configs[1])
     summa = summa_point(sg, K, mesh, args.summa_n, pk, barrier, world)
+    if args.summa_sweep:
+        summa["sweep"] = [summa_point(sg, K, mesh, n, pk, barrier, world) for n in (4096, 8192, 16384, 32768)]
 
     # ------------------------------------------------------------- CPU baseline (rank 0, N = 1)
     cpu = None
