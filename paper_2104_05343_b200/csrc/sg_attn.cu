@@ -656,6 +656,7 @@ struct FlashBwdParams {
 };
 
 constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
+constexpr int kMaxItems = 256;           // per-CTA work items of the persistent backward (item table in smem)
 
 __global__ void __launch_bounds__(256, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -904,6 +905,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sDS = sP + 2 * kT64;       // 32 KB
   uint8_t* sStg = sDS + 2 * kT64;     // 8 warps x 4 KB dQ staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 4096);
+  int* items_tab = reinterpret_cast<int*>(bars + 32);  // this CTA's items as packed (kb, h, b)
   uint64_t* kv_full = bars;        // [2]
   uint64_t* kv_empty = bars + 2;   // [2]
   uint64_t* qd_full = bars + 4;    // [2]
@@ -952,6 +954,12 @@ __global__ void __launch_bounds__(384, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
+  // item coordinates, decoded once: kb | h << 10 | b << 20 (kb < 1024, h < 1024 checked by the host)
+  for (int it = threadIdx.x; it < my_items && it < kMaxItems; it += blockDim.x) {
+    int kb, h, b;
+    decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
+    items_tab[it] = kb | (h << 10) | (b << 20);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1047,25 +1055,30 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     uint8_t* stg = sStg + e * 4096;
     const float scale = p.scale, scale_log2 = p.scale_log2;
+    auto item = [&](int it, int& kb, int& h, int& b) {
+      const int v = items_tab[it];
+      kb = v & 1023;
+      h = (v >> 10) & 1023;
+      b = v >> 20;
+    };
     // raw loads only: converting here would make the prefetch wait for the load
-    auto row_stats = [&](int G, float& lse, float& dd) {
+    auto row_stats = [&](int it, int i, float& lse, float& dd) {
       lse = dd = 0.f;
-      if (G >= total) return;
+      if (it >= my_items) return;
       int kb, h, b;
-      decode((int)blockIdx.x + (G / nqb) * (int)gridDim.x, kb, h, b);
-      const int qrow = (G % nqb) * 128 + r;
+      item(it, kb, h, b);
+      const int qrow = i * 128 + r;
       if (qrow >= p.s) return;
       const size_t off = ((size_t)b * p.nh + h) * p.s + qrow;
       lse = __ldg(p.lse + off);
       dd = __ldg(p.drow + off);
     };
-    // dQ columns [32 half, 32 half + 32) of global query block G: TMEM -> fp32
-    // staging -> TMA reduce-add, then release the buffer
-    auto drain_dq = [&](int G) {
+    // dQ columns [32 half, 32 half + 32) of query block i of local item it (global block
+    // G): TMEM -> fp32 staging -> TMA reduce-add, then release the buffer
+    auto drain_dq = [&](int G, int it, int i) {
       const int slot = G & 1;
       int kb, h, b;
-      decode((int)blockIdx.x + (G / nqb) * (int)gridDim.x, kb, h, b);
-      const int i = G % nqb;
+      item(it, kb, h, b);
       mbar_wait(&dq_full[slot], (G >> 1) & 1);
       tc_fence_after();
       if (lane == 0) bulk_wait_read<0>();
@@ -1091,15 +1104,19 @@ __global__ void __launch_bounds__(384, 1)
       }
     };
     float lse_n, dd_n;
-    row_stats(0, lse_n, dd_n);
+    row_stats(0, 0, lse_n, dd_n);
+    int it = 0, i = 0;            // (item, query block) of G, advanced incrementally
+    int pit = 0, pi = 0;          // of G - 1 (its dQ drains this iteration)
+    int kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
     for (int G = 0; G < total; ++G) {
-      const int it = G / nqb, i = G % nqb;
-      int kb, h, b;
-      decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
       const int kvalid = min(128, p.s - kb * 128);
       const bool full_keys = kvalid == 128;
       const float lse_c = lse_n, dd = dd_n;
-      row_stats(G + 1, lse_n, dd_n);  // prefetch
+      {
+        const int ni = i + 1 == nqb ? 0 : i + 1, nit = i + 1 == nqb ? it + 1 : it;
+        row_stats(nit, ni, lse_n, dd_n);  // prefetch
+      }
       const bool qok = i * 128 + r < p.s;
       mbar_wait(s_full, G & 1);
       tc_fence_after();
@@ -1154,7 +1171,9 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      if (G > 0) drain_dq(G - 1);
+      if (G > 0) drain_dq(G - 1, pit, pi);
+      pit = it;
+      pi = i;
       if (i == nqb - 1) {
         // this item's dK, dV: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
         mbar_wait(acc_full, it & 1);
@@ -1173,19 +1192,24 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t* v = which == 0 ? vk : vv;
             __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64 + half * 32;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k2 = 0; k2 < 4; ++k2) {
               uint4 x;
               __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
               for (int e2 = 0; e2 < 4; ++e2)
-                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e2]), __uint_as_float(v[8 * k + 2 * e2 + 1]));
-              *reinterpret_cast<uint4*>(dst + 8 * k) = x;
+                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
+              *reinterpret_cast<uint4*>(dst + 8 * k2) = x;
             }
           }
         }
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
       }
     }
-    if (total > 0) drain_dq(total - 1);
+    if (total > 0) drain_dq(total - 1, pit, pi);
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
@@ -1224,7 +1248,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_f32_tile_4d(&tdq, dq_acc, d, s, nh, b, lddq, d, s * lddq, &p.dq_b2_first);
   if (rc) return rc;
   constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
-  constexpr size_t SMEM2 = 12 * kT64 + 8 * 4096 + 256;  // v2: K, V double-buffered per item
+  constexpr size_t SMEM2 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;  // v2: K, V double-buffered per item
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
@@ -1243,6 +1267,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   {
     const int items = (int)grid.x * (int)grid.y * (int)grid.z;
     const int sms = sg_device_sm_count();
+    if (grid.x > 1024 || nh > 1024 || b > 2047 || (items + (sms > 0 ? sms : 148) - 1) / (sms > 0 ? sms : 148) > kMaxItems)
+      return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
     launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), SMEM2,
              static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, p, (int)b);
   }
