@@ -14,15 +14,17 @@ extern "C" int sg_device_sm_count(void);
 #include <utility>
 
 namespace sg {
-// Programmatic dependent launch: every libsg kernel is launched with programmatic
-// stream serialisation, triggers its dependents at entry and waits for its
-// predecessor (griddepcontrol) before touching memory, so a kernel's launch and
-// prologue overlap the tail of the previous one (also inside CUDA graphs).
-// SG_PDL=0 launches plainly (A/B measurements).
+// Programmatic dependent launch (opt-in, SG_PDL=1): every libsg kernel triggers its
+// dependents at entry and waits for its predecessor (griddepcontrol) before
+// touching memory, so with the launch attribute set a kernel's launch and prologue
+// overlap the tail of the previous one (also inside CUDA graphs). Measured on the
+// BERT step it costs ~1.3% (679 vs 688 samples/s: early-resident CTAs of the next
+// kernel only spin), so plain launches are the default; the device-side
+// griddepcontrol instructions are no-ops then.
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("SG_PDL");
-    return !(e && atoi(e) == 0);
+    return e && atoi(e) != 0;
   }();
   return on;
 }
