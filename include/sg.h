@@ -81,6 +81,11 @@ typedef struct sg_gemm_args {
   int32_t mode; /* SG_EPI_* */
   /* SOFTMAX_BWD: D_i = rowsum(dO * O) per output row, rowvec[z1*srv1 + z2*srv2 + m] */
   const float* rowvec; int64_t srv1, srv2;
+  /* optional LayerNorm-backward row statistics of the fp32 output dy = D (layers.py:319-326):
+   * ln_stats[2m] += sum_n xhat(m,n) * g(m,n), ln_stats[2m+1] += sum_n g(m,n) with
+   * g = dy * ln_gamma[n], xhat = (C(m,n) - ln_mean[m]) * ln_rstd[m]; C is then the
+   * LayerNorm input x (fp32, read by TMA, not added). Unbatched, fp32 D, no bias / act. */
+  const float* ln_gamma; const float* ln_mean; const float* ln_rstd; float* ln_stats;
 } sg_gemm_args;
 
 int sg_gemm(const sg_gemm_args* args, void* stream);

@@ -43,6 +43,7 @@ class GemmArgs(ctypes.Structure):
         ("colsum", vp), ("scs1", i64), ("scs2", i64),
         ("mode", i32),
         ("rowvec", vp), ("srv1", i64), ("srv2", i64),
+        ("ln_gamma", vp), ("ln_mean", vp), ("ln_rstd", vp), ("ln_stats", vp),
     ]
 
 

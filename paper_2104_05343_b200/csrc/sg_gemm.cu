@@ -66,6 +66,13 @@ struct GemmParams {
   long long scs1, scs2;
   const float* rowvec;          // SOFTMAX_BWD: D_i = rowsum(dO * O) per row
   long long srv1, srv2;
+  // LayerNorm-backward row statistics of the fp32 output (C = LayerNorm input x,
+  // loaded but not added): ln_stats[2 r] += sum xhat g, ln_stats[2 r + 1] += sum g,
+  // g = D * gamma, xhat = (x - mean) rstd
+  const float* ln_gamma;
+  const float* ln_mean;
+  const float* ln_rstd;
+  float* ln_stats;
   int act;
   float alpha;
 };
@@ -469,6 +476,11 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       const int nrows = min(32, p.M - row0);
       float rv = 0.f;
       if (p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
+      float ln_mu = 0.f, ln_rs = 0.f, ln_sxg = 0.f, ln_sg = 0.f;
+      if (p.ln_stats && lane < nrows) {
+        ln_mu = p.ln_mean[row0 + lane];
+        ln_rs = p.ln_rstd[row0 + lane];
+      }
       mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const uint32_t tacc = tmem_base + lane_base + as * BN;
@@ -547,11 +559,12 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         }
       };
       bool pref = false;  // the current chunk's input is already in flight
-      // bias: lane j holds column j of the chunk (one coalesced load, prefetched a
-      // chunk ahead) and the row-threads pick it up by shuffle
+      // bias (or the LayerNorm gamma): lane j holds column j of the chunk (one
+      // coalesced load, prefetched a chunk ahead), broadcast to the row threads via smem
+      const float* vecp = p.bias ? p.bias : p.ln_gamma;
       auto load_bias = [&](int c) -> float {
         const int col = nb * BN + c * 32 + lane;
-        return (p.bias && c < NCH && col < p.N) ? __ldg(p.bias + col) : 0.f;
+        return (vecp && c < NCH && col < p.N) ? __ldg(vecp + col) : 0.f;
       };
       float bias_cur = load_bias(c_first), bias_nxt = 0.f;
 #pragma unroll 1
@@ -560,7 +573,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         const bool active = col0 < p.N && nrows > 0;  // warp-uniform
         const int col = col0 + lane;
         const bool col_ok = col < p.N;
-        if (p.bias) bias_nxt = load_bias(c + CSTEP);
+        if (vecp) bias_nxt = load_bias(c + CSTEP);
         // accumulator chunk, thread = row
         uint32_t r[32];
         tmem_ld32(tacc + c * 32, r);
@@ -629,7 +642,27 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               }
               __syncwarp();
             }
-            if (in_kind == 1) {
+            if (p.ln_stats) {
+              // C holds the LayerNorm input x (fp32, main tile); g = dy gamma
+              float xv[32];
+              ld_row_f32(s0, lane, xv);
+              float* bw = bias_all + e * 32;
+              bw[lane] = bias_cur;
+              __syncwarp();
+              uint64_t a_sxg = 0, a_sg = 0;  // two f32x2 partial sums each
+              const uint64_t nmu = f2_pack(-ln_mu, -ln_mu);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float2 g2 = reinterpret_cast<const float2*>(bw)[k];
+                const uint64_t g = fmul2(f2_pack(v[2 * k], v[2 * k + 1]), f2_pack(g2.x, g2.y));
+                const uint64_t xc = fadd2(f2_pack(xv[2 * k], xv[2 * k + 1]), nmu);
+                a_sxg = ffma2(xc, g, a_sxg);
+                a_sg = fadd2(a_sg, g);
+              }
+              __syncwarp();
+              ln_sxg += (f2_lo(a_sxg) + f2_hi(a_sxg)) * ln_rs;
+              ln_sg += f2_lo(a_sg) + f2_hi(a_sg);
+            } else if (in_kind == 1) {
               float cv[32];
               if (c_f32)
                 ld_row_f32(s0, lane, cv);
@@ -684,6 +717,10 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         }
         bias_cur = bias_nxt;
       }
+      if (p.ln_stats && lane < nrows) {
+        atomicAdd(p.ln_stats + 2 * (size_t)(row0 + lane), ln_sxg);
+        atomicAdd(p.ln_stats + 2 * (size_t)(row0 + lane) + 1, ln_sg);
+      }
     }
     if (lane == 0) bulk_wait_all();  // global writes complete before the CTA retires
   }
@@ -725,7 +762,12 @@ __global__ void gemm_simt_kernel(const __grid_constant__ sg_gemm_args a) {
     }
     float v = acc * a.alpha;
     if (a.bias) v += a.bias[n];
-    if (a.C) {
+    if (a.ln_stats) {
+      const float g = v * a.ln_gamma[n];
+      const float xh = (static_cast<const float*>(a.C)[m * a.ldc + n] - a.ln_mean[m]) * a.ln_rstd[m];
+      atomicAdd(a.ln_stats + 2 * m, xh * g);
+      atomicAdd(a.ln_stats + 2 * m + 1, g);
+    } else if (a.C) {
       const long long ci = z1 * a.sc1 + z2 * a.sc2 + m * a.ldc + n;
       v += a.c_dtype == SG_DTYPE_F32 ? static_cast<const float*>(a.C)[ci]
                                      : __bfloat162float(static_cast<const __nv_bfloat16*>(a.C)[ci]);
@@ -955,6 +997,10 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (a->C && a->act == SG_ACT_DGELU) return set_error(SG_ERR_CONFIG, "gemm: C input together with GELU' input");
   if (a->C && a->C != a->D && a->c_dtype != SG_DTYPE_F32 && (a->D2 || (a->act == SG_ACT_GELU && a->aux)))
     return set_error(SG_ERR_CONFIG, "gemm: a bf16 C input shares the side tile with D2 / the GELU input copy");
+  if (a->ln_stats && (!a->ln_gamma || !a->ln_mean || !a->ln_rstd || !a->C || a->C == a->D ||
+                      a->c_dtype != SG_DTYPE_F32 || a->d_dtype != SG_DTYPE_F32 || a->bias || a->act ||
+                      a->D2 || a->colsum || a->mode != SG_EPI_NORMAL || a->nb1 * a->nb2 != 1))
+    return set_error(SG_ERR_CONFIG, "gemm: LayerNorm statistics need an unbatched fp32 product with x as C only");
   if (a->mode != SG_EPI_NORMAL) {
     if (a->mode != SG_EPI_SOFTMAX && a->mode != SG_EPI_SOFTMAX_BWD) return set_error(SG_ERR_CONFIG, "gemm: mode");
     if (a->N > 512) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need N <= 512");
@@ -1038,6 +1084,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.has_d2 = a->D2 ? 1 : 0;
   p.colsum = a->colsum; p.scs1 = a->scs1; p.scs2 = a->scs2;
   p.rowvec = a->rowvec; p.srv1 = a->srv1; p.srv2 = a->srv2;
+  p.ln_gamma = a->ln_gamma; p.ln_mean = a->ln_mean; p.ln_rstd = a->ln_rstd; p.ln_stats = a->ln_stats;
   p.act = a->act;
   p.alpha = a->alpha;
 

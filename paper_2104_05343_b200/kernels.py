@@ -48,7 +48,7 @@ def _batch(t: torch.Tensor, nbatch: int) -> tuple[int, int, int, int]:
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
          bias: torch.Tensor | None = None, c: torch.Tensor | None = None, act: int = ACT_NONE,
          aux: torch.Tensor | None = None, out2: torch.Tensor | None = None, colsum: torch.Tensor | None = None,
-         mode: int = EPI_NORMAL, rowvec: torch.Tensor | None = None) -> torch.Tensor:
+         mode: int = EPI_NORMAL, rowvec: torch.Tensor | None = None, ln_stats=None) -> torch.Tensor:
     """out = act(alpha * a @ b + bias + c) on the tcgen05 tensor cores.
 
     ``a`` [..., M, K] and ``b`` [..., K, N] are bf16 logical views; either may
@@ -60,6 +60,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     sums. ``mode`` selects the row-softmax epilogues (EPI_SOFTMAX: out =
     softmax(alpha * a @ b); EPI_SOFTMAX_BWD: out = aux * (acc - rowvec) *
     alpha with rowvec [..., M] = rowsum(acc * aux), e.g. rowsum(dO * O)).
+    ``ln_stats = (x, gamma, mean, rstd, stats)`` accumulates the LayerNorm-
+    backward row statistics of the fp32 output dy into ``stats`` [M, 2]
+    (sum xhat * dy * gamma, sum dy * gamma); ``x`` is the LayerNorm input.
     """
     _require_cuda(a, b, out, bias, c, aux)
     if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
@@ -135,6 +138,17 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
             raise ShapeError("gemm: rowvec must be fp32 [*batch, M] with unit stride")
         _, _, sr1, sr2 = _batch(rowvec, nbd)
         args.rowvec, args.srv1, args.srv2 = rowvec.data_ptr(), sr1, sr2
+    if ln_stats is not None:
+        x, gamma, mean, rstd, stats = ln_stats
+        if c is not None or bias is not None or act != ACT_NONE or nbd != 0 or out.dtype != torch.float32:
+            raise ConfigError("gemm: LayerNorm statistics need an unbatched fp32 output without C / bias / act")
+        if tuple(x.shape) != tuple(out.shape) or x.dtype != torch.float32 or x.stride(-1) != 1:
+            raise ShapeError("gemm: the LayerNorm input must be fp32 with the output shape")
+        if stats.dtype != torch.float32 or not stats.is_contiguous() or stats.numel() != 2 * M:
+            raise ShapeError("gemm: LayerNorm statistics must be a contiguous fp32 [M, 2]")
+        args.C, args.ldc, args.c_dtype = x.data_ptr(), x.stride(-2), DTYPE_F32
+        args.ln_gamma, args.ln_mean, args.ln_rstd, args.ln_stats = (gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                                                    stats.data_ptr())
     args.mode = mode
     args.act = act
     args.alpha = alpha

@@ -393,11 +393,13 @@ def layernorm_backward(out_grad: ShardedMatrix, ctx: LayerNormContext, cfg: Mode
     """
     mesh = out_grad.mesh
     rows, cols = out_grad.block_rows, out_grad.block_cols
-    stats = [None] * mesh.p
-    for dev in mesh.local_devs:
-        stats[dev] = ws.empty(dev, (rows, 2), "free", dtype=F32, pad=False)
-        K.ln_bwd_stats(out_grad.blocks[dev], ctx.x.blocks[dev], ctx.mean[dev], ctx.rstd[dev],
-                       ctx.gamma.for_position(mesh, dev), stats[dev])
+    stats = getattr(out_grad, "ln_stats", None)  # accumulated by the producing GEMM (summa_abt ln_ctx)
+    if stats is None:
+        stats = [None] * mesh.p
+        for dev in mesh.local_devs:
+            stats[dev] = ws.empty(dev, (rows, 2), "free", dtype=F32, pad=False)
+            K.ln_bwd_stats(out_grad.blocks[dev], ctx.x.blocks[dev], ctx.mean[dev], ctx.rstd[dev],
+                           ctx.gamma.for_position(mesh, dev), stats[dev])
     if mesh.c > 1:
         mesh.allreduce_row(stats, tag=tag)
     dx, dx16, gb = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
@@ -638,8 +640,9 @@ def _bf16_of(x: ShardedMatrix, ws: Workspace) -> ShardedMatrix:
 
 
 def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: ShardedMatrix,
-                       w_dense: ShardedMatrix, cfg: ModelConfig, ws: Workspace):
-    """(dx, dW_qkv, db_qkv, dW_dense, db_dense) (layers.py:424-465)."""
+                       w_dense: ShardedMatrix, cfg: ModelConfig, ws: Workspace, ln_ctx=None):
+    """(dx, dW_qkv, db_qkv, dW_dense, db_dense) (layers.py:424-465); ``ln_ctx`` is
+    the LayerNorm whose backward consumes dx (its statistics fused into dx's GEMM)."""
     mesh = out_grad.mesh
     b_loc, n_loc = cfg.b // mesh.r, cfg.n // mesh.c
     hb = cfg.h // mesh.c
@@ -658,7 +661,7 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     dqkv = ShardedMatrix(mesh, cfg.b * cfg.s, 3 * cfg.h, dqkv_blocks)
     dqkv.colsum_parts = bq_parts
     _, b_qkv_grad = bias_add_backward(dqkv, ws)
-    x_grad = summa_abt(dqkv, w_qkv, ws, out_category="backward", out_dtype=F32)
+    x_grad = summa_abt(dqkv, w_qkv, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
     w_qkv_grad = summa_atb(ctx.x_in, dqkv, ws, out_category="param_grad")
     return x_grad, w_qkv_grad, b_qkv_grad, w_dense_grad, b_dense_grad
 
@@ -692,8 +695,9 @@ def mlp_forward(x: ShardedMatrix, w1: ShardedMatrix, b1: RowHostedVector, w2: Sh
 
 
 def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2: ShardedMatrix,
-                 cfg: ModelConfig, ws: Workspace):
-    """(dx, dW1, db1, dW2, db2) with GELU' fused into the dAct product (layers.py:494-508)."""
+                 cfg: ModelConfig, ws: Workspace, ln_ctx=None):
+    """(dx, dW1, db1, dW2, db2) with GELU' fused into the dAct product (layers.py:494-508);
+    ``ln_ctx`` as in attention_backward."""
     mesh = out_grad.mesh
     dy16 = _bf16_of(out_grad, ws)
     _, b2_grad = bias_add_backward(out_grad, ws)
@@ -705,7 +709,7 @@ def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2
     dmid.colsum_parts = b1_parts
     w2_grad = summa_atb(ctx.act, dy16, ws, out_category="param_grad")
     _, b1_grad = bias_add_backward(dmid, ws)
-    x_grad = summa_abt(dmid, w1, ws, out_category="backward", out_dtype=F32)
+    x_grad = summa_abt(dmid, w1, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
     w1_grad = summa_atb(ctx.x_in, dmid, ws, out_category="param_grad")
     return x_grad, w1_grad, b1_grad, w2_grad, b2_grad
 
@@ -919,10 +923,11 @@ class TransformerLayer:
         bsh_p = (cfg.b * cfg.s // mesh.r) * (cfg.h // mesh.c)
         for dev in mesh.local_devs:
             ws.release_forward(dev, (4 if self._last_was_skip else 5) * bsh_p)
-        da2, w1_g, b1_g, w2_g, b2_g = mlp_backward(out_grad, saved.mlp, p.w1, p.w2, cfg, ws)
+        da2, w1_g, b1_g, w2_g, b2_g = mlp_backward(out_grad, saved.mlp, p.w1, p.w2, cfg, ws, ln_ctx=saved.ln2)
         dy1, ln2_g, ln2_b = layernorm_backward(da2, saved.ln2, cfg, ws, resid=out_grad, want_bf16=True,
                                                want_colsum=True)
-        da1, wqkv_g, bqkv_g, wd_g, bd_g = attention_backward(dy1, saved.attn, p.w_qkv, p.w_dense, cfg, ws)
+        da1, wqkv_g, bqkv_g, wd_g, bd_g = attention_backward(dy1, saved.attn, p.w_qkv, p.w_dense, cfg, ws,
+                                                             ln_ctx=saved.ln1)
         dx, ln1_g, ln1_b = layernorm_backward(da1, saved.ln1, cfg, ws, resid=dy1, want_bf16=True,
                                               want_colsum=True)
         return dx, LayerGrads(w_qkv=wqkv_g, b_qkv=bqkv_g, w_dense=wd_g, b_dense=bd_g, w1=w1_g, b1=b1_g, w2=w2_g,

@@ -265,8 +265,13 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
 
 def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
               out_dtype: torch.dtype = F32, act: int = K.ACT_NONE, aux=None, resid=None,
-              colsum=None) -> ShardedMatrix:
-    """C = A B^T: B(l,j) down column j, A_ij B_lj^T, row-reduce to (i, l) (summa.py:119-140)."""
+              colsum=None, ln_ctx=None) -> ShardedMatrix:
+    """C = A B^T: B(l,j) down column j, A_ij B_lj^T, row-reduce to (i, l) (summa.py:119-140).
+
+    ``ln_ctx`` (a LayerNormContext whose backward consumes C) lets a one-column
+    local mesh accumulate that backward's row statistics in the GEMM epilogue;
+    they are attached to the result as ``ln_stats`` (per-device [rows, 2]).
+    """
     mesh = check_same_mesh(a, b)
     if a.global_cols != b.global_cols:
         raise ShapeError(f"summa_abt contraction dims differ: {a.global_cols} vs {b.global_cols}")
@@ -276,6 +281,13 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
     out = _new_blocks(mesh, ws, (m_b, n_b), out_category, out_dtype)
     aux_b = None if aux is None else aux.blocks
     res_b = None if resid is None else resid.blocks
+    fuse_ln = (ln_ctx is not None and mesh.is_local and mesh.c == 1 and out_dtype == F32 and act == K.ACT_NONE
+               and resid is None and colsum is None)
+    ln_stats = [None] * mesh.p
+    if fuse_ln:
+        for dev in mesh.local_devs:
+            if ln_ctx.x.blocks[dev].dtype != F32:
+                fuse_ln = False
     if mesh.is_local:
         # reduce fused into the accumulating GEMM chain, group-position order j = 0..c-1;
         # with c > 1 and GELU' the chain ends in fp32 and the epilogue runs as a pass
@@ -294,7 +306,14 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                 for j in range(mesh.c):
                     bt = b16.block(l, j).t()
                     prev = chain if (j > 0 or res_b is not None) else None
-                    if j == mesh.c - 1 and not split_epi:
+                    if j == mesh.c - 1 and fuse_ln:
+                        ln_stats[d] = ws.empty(d, (m_b, 2), "free", dtype=F32, pad=False) if ws is not None \
+                            else torch.empty((m_b, 2), dtype=F32, device=mesh.device(d))
+                        K.zero(ln_stats[d])
+                        K.gemm(a16.block(i, j), bt, out[d], ln_stats=(
+                            ln_ctx.x.blocks[d], ln_ctx.gamma.for_position(mesh, d), ln_ctx.mean[d], ln_ctx.rstd[d],
+                            ln_stats[d]))
+                    elif j == mesh.c - 1 and not split_epi:
                         K.gemm(a16.block(i, j), bt, out[d], c=prev, act=act, aux=None if aux_b is None else aux_b[d],
                                colsum=None if colsum is None else colsum[d])
                     else:
@@ -303,7 +322,10 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                     K.epilogue(chain, out[d], act=act, aux=None if aux_b is None else aux_b[d])
                     if colsum is not None:
                         K.colsum(out[d], colsum[d], accumulate=True)
-        return ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
+        res = ShardedMatrix(mesh, a.global_rows, b.global_rows, out)
+        if fuse_ln:
+            res.ln_stats = ln_stats
+        return res
     # dist pipeline: B(l+1, j) arrives while step l's partial product runs, and step
     # l's row reduce overlaps step l+1's product (two partial-sum slots)
     acc = _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)

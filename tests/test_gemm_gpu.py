@@ -172,3 +172,28 @@ def test_gemm_softmax_epilogues(s):
     dr = torch.empty(bl, nl, s, device="cuda")
     k.attn_rowdot(flat(do), flat(o), nl, d, s, dr)
     assert _rel(dr, (do.float() * o.float()).sum(-1)) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 1024, 4096), (300, 200, 100), (4096, 2048, 8192), (130, 72, 64)])
+def test_gemm_layernorm_stats(M, N, K):
+    """LayerNorm-backward row statistics accumulated in the dx GEMM's epilogue equal
+    the separate stats pass (layers.py:310-351: sum xhat g, sum g with g = dy gamma)."""
+    k = _k()
+    torch.manual_seed(7)
+    a, b = _rand(M, K, scale=0.05), _rand(K, N)
+    x = torch.randn(M, N, device="cuda") * 3 + 1
+    gamma = torch.randn(N, device="cuda")
+    mean = x.mean(1)
+    rstd = torch.rsqrt(x.var(1, unbiased=False) + 1e-5)
+    dy = torch.empty(M, N, device="cuda")
+    stats = torch.zeros(M, 2, device="cuda")
+    k.gemm(a, b, dy, ln_stats=(x, gamma, mean, rstd, stats))
+    ref = a.float() @ b.float()
+    assert _rel(dy, ref) < 4e-5  # fp32 accumulation order over K = 8192
+    g = ref * gamma
+    xhat = (x - mean[:, None]) * rstd[:, None]
+    assert _rel(stats[:, 0], (xhat * g).sum(1)) < 1e-4
+    assert _rel(stats[:, 1], g.sum(1)) < 1e-4
+    sep = torch.empty(M, 2, device="cuda")
+    k.ln_bwd_stats(dy, x, mean, rstd, gamma, sep)
+    assert _rel(stats, sep) < 1e-4
