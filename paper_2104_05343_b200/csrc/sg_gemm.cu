@@ -79,6 +79,19 @@ struct GemmParams {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
+// Epilogue kinds: GENERIC decides every feature from GemmParams at run time; the
+// others fix the feature set at compile time for the step's hot products, so the
+// epilogue loop is short and branch-free (measured: the generic loop's size and
+// flag branches cost instruction-fetch and branch stalls at ~2 epilogue warps / SMSP)
+enum EpiKind : int {
+  EK_GENERIC = 0,
+  EK_STORE = 1,     // D = alpha acc (bf16 / fp32), optional TMA reduce-add
+  EK_BIAS = 2,      // D = alpha acc + bias, optional TMA reduce-add
+  EK_CIN_BIAS = 3,  // fp32 D = acc + bias + fp32 C (residual)
+  EK_GELU_BIAS = 4, // D = gelu(acc + bias), pre-activation stored through tmX
+  EK_DGELU = 5,     // D = acc * gelu'(aux) [+ column sums]
+  EK_LN = 6,        // fp32 D = acc, LayerNorm-backward row statistics (C = x)
+};
 // Epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
 // taking every other 32-column chunk) for epilogues without global inputs,
 // where the epilogue otherwise paces the tensor pipe at small K.
@@ -189,6 +202,26 @@ __device__ __forceinline__ void gelu_row(float (&v)[32]) {
   }
 }
 
+// v *= gelu'(x), paired: with t = tanh(c (x + a x^3)) and w = x (0.5 c + 1.5 a c x^2),
+// gelu'(x) = 0.5 (1 + t) + w (1 - t^2) = (0.5 + w) + t (0.5 - w t)
+__device__ __forceinline__ void dgelu_row(float (&v)[32], const float (&x)[32]) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const uint64_t ca2 = f2_pack(c * a, c * a), c2 = f2_pack(c, c), h2 = f2_pack(0.5f, 0.5f),
+                 m1 = f2_pack(-1.f, -1.f), k1 = f2_pack(-1.5f * a * c, -1.5f * a * c), k0 = f2_pack(-0.5f * c, -0.5f * c);
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const uint64_t xx = f2_pack(x[j], x[j + 1]);
+    const uint64_t x2 = fmul2(xx, xx);
+    const uint64_t u = fmul2(xx, ffma2(x2, ca2, c2));  // c (x + a x^3)
+    const uint64_t wn = fmul2(xx, ffma2(x2, k1, k0));  // -w
+    const uint64_t t = f2_pack(tanh_fast(f2_lo(u)), tanh_fast(f2_hi(u)));
+    const uint64_t g = ffma2(t, ffma2(wn, t, h2), ffma2(wn, m1, h2));
+    const uint64_t y = fmul2(f2_pack(v[j], v[j + 1]), g);
+    v[j] = f2_lo(y);
+    v[j + 1] = f2_hi(y);
+  }
+}
+
 __device__ __forceinline__ float gelu_fast(float x) {
   const float c = 0.7978845608028654f, a = 0.044715f;
   return 0.5f * x * (1.f + tanh_fast(c * (x + a * x * x * x)));
@@ -267,7 +300,7 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* d, bool vec, int n
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR, int KIND>
 __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
@@ -457,7 +490,18 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     const int c_first = e >> 2;
     uint8_t* stg_w = stg_all + e * kStgBytes;
     uint32_t it = 0, slot = 0, inph = 0;
-    const bool d_f32 = p.d_f32 != 0, c_f32 = p.c_f32 != 0;
+    // feature flags: compile-time constants unless KIND == EK_GENERIC
+    constexpr bool G = KIND == EK_GENERIC;
+    const bool f_bias = G ? p.bias != nullptr : (KIND == EK_BIAS || KIND == EK_CIN_BIAS || KIND == EK_GELU_BIAS);
+    const bool f_ln = G ? p.ln_stats != nullptr : KIND == EK_LN;
+    const int f_act = G ? p.act : (KIND == EK_GELU_BIAS ? SG_ACT_GELU : (KIND == EK_DGELU ? SG_ACT_DGELU : SG_ACT_NONE));
+    const int f_mode = G ? p.mode : SG_EPI_NORMAL;
+    const bool f_colsum = G ? p.colsum != nullptr : (KIND == EK_DGELU && p.colsum != nullptr);
+    const bool f_d2 = G ? p.has_d2 != 0 : false;
+    const bool f_aux_out = G ? p.aux_out != 0 : KIND == EK_GELU_BIAS;
+    const bool f_reduce = G ? p.reduce_add != 0 : ((KIND == EK_STORE || KIND == EK_BIAS) && p.reduce_add != 0);
+    const bool d_f32 = (KIND == EK_CIN_BIAS || KIND == EK_LN) ? true : p.d_f32 != 0;
+    const bool c_f32 = G ? p.c_f32 != 0 : true;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     constexpr int NCH = BN / 32;
     const uint32_t tempty_leader = PAIR ? mapa_smem(&tempty[0], 0) : 0;
@@ -468,6 +512,35 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       else
         mbar_arrive(&tempty[as]);
     };
+    // one global input per chunk at most (C, or the GELU' / softmax-backward aux),
+    // brought into the chunk's staging slot by TMA in the same swizzled layout the
+    // stores use (fp32 C -> main tile, bf16 aux / C -> side tile); with two slots
+    // the next chunk's tile is requested before this chunk is processed, and the
+    // next tile's first chunk before that tile's accumulator is waited for
+    const int in_kind =
+        G ? ((p.C && !p.reduce_add) ? 1 : ((p.act == SG_ACT_DGELU || p.mode == SG_EPI_SOFTMAX_BWD) ? 2 : 0))
+          : ((KIND == EK_CIN_BIAS || KIND == EK_LN) ? 1 : (KIND == EK_DGELU ? 2 : 0));
+    const bool c_side = in_kind == 1 && !c_f32;  // bf16 C: side tile
+    // slot = main tile (fp32: 4 KB, bf16: 2 KB) [+ 2 KB bf16 side tile]; two 4 KB slots when it fits
+    const bool side = f_aux_out || f_d2 || in_kind == 2 || c_side;
+    const int main_bytes = (d_f32 || (in_kind == 1 && c_f32)) ? 4096 : 2048;
+    const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
+    auto issue_in = [&](int tnb, int trow0, int tz1, int tz2, int c, uint32_t si) {  // lane 0 only
+      uint8_t* base = stg_w + (dual ? si * 4096 : 0);
+      uint64_t* bar = &inbar[e * 2 + si];
+      const int col0 = tnb * BN + c * 32;
+      if (in_kind == 1 && c_f32) {
+        mbar_arrive_expect_tx(bar, 4096);
+        load_box(&tmC, base, bar, col0, trow0, tz2, tz1, p.c_b2_first);
+      } else if (in_kind == 1) {
+        mbar_arrive_expect_tx(bar, 2048);
+        load_box(&tmC, base + main_bytes, bar, col0, trow0, tz2, tz1, p.c_b2_first);
+      } else {
+        mbar_arrive_expect_tx(bar, 2048);
+        load_box(&tmX, base + main_bytes, bar, col0, trow0, tz2, tz1, p.x_b2_first);
+      }
+    };
+    bool pref_next = false;  // the next tile's first chunk input is in flight
     for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
       int mb, nb, z1, z2;
       decode_tile(p, t, mb, nb, z1, z2);
@@ -475,9 +548,9 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       const int row0 = mb * TM + (int)rank * kBM + q * 32;
       const int nrows = min(32, p.M - row0);
       float rv = 0.f;
-      if (p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
+      if (G && p.rowvec && lane < nrows) rv = p.rowvec[(size_t)z1 * p.srv1 + (size_t)z2 * p.srv2 + row0 + lane];
       float ln_mu = 0.f, ln_rs = 0.f, ln_sxg = 0.f, ln_sg = 0.f;
-      if (p.ln_stats && lane < nrows) {
+      if (f_ln && lane < nrows) {
         ln_mu = p.ln_mean[row0 + lane];
         ln_rs = p.ln_rstd[row0 + lane];
       }
@@ -485,7 +558,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       tc_fence_after();
       const uint32_t tacc = tmem_base + lane_base + as * BN;
 
-      if (EW == 4 && p.mode == SG_EPI_SOFTMAX) {
+      if (EW == 4 && f_mode == SG_EPI_SOFTMAX) {
         // whole row in TMEM: max, sum of exponentials, then P chunks through smem + TMA
         const float sl2 = p.alpha * 1.4426950408889634f;
         float m = -INFINITY;
@@ -532,36 +605,11 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         continue;
       }
 
-      // one global input per chunk at most (C, or the GELU' / softmax-backward aux),
-      // brought into the chunk's staging slot by TMA in the same swizzled layout the
-      // stores use (fp32 C -> main tile, bf16 aux / C -> side tile); with two slots
-      // the next chunk's tile is requested before this chunk is processed
-      const int in_kind =
-          (p.C && !p.reduce_add) ? 1 : ((p.act == SG_ACT_DGELU || p.mode == SG_EPI_SOFTMAX_BWD) ? 2 : 0);
-      const bool c_side = in_kind == 1 && !c_f32;  // bf16 C: side tile
-      // slot = main tile (fp32: 4 KB, bf16: 2 KB) [+ 2 KB bf16 side tile]; two 4 KB slots when it fits
-      const bool side = p.aux_out || p.has_d2 || in_kind == 2 || c_side;
-      const int main_bytes = (d_f32 || (in_kind == 1 && c_f32)) ? 4096 : 2048;
-      const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
-      auto issue_in = [&](int c, uint32_t si) {  // lane 0 only
-        uint8_t* base = stg_w + (dual ? si * 4096 : 0);
-        uint64_t* bar = &inbar[e * 2 + si];
-        const int col0 = nb * BN + c * 32;
-        if (in_kind == 1 && c_f32) {
-          mbar_arrive_expect_tx(bar, 4096);
-          load_box(&tmC, base, bar, col0, row0, z2, z1, p.c_b2_first);
-        } else if (in_kind == 1) {
-          mbar_arrive_expect_tx(bar, 2048);
-          load_box(&tmC, base + main_bytes, bar, col0, row0, z2, z1, p.c_b2_first);
-        } else {
-          mbar_arrive_expect_tx(bar, 2048);
-          load_box(&tmX, base + main_bytes, bar, col0, row0, z2, z1, p.x_b2_first);
-        }
-      };
-      bool pref = false;  // the current chunk's input is already in flight
+      bool pref = pref_next;  // the current chunk's input is already in flight
+      pref_next = false;
       // bias (or the LayerNorm gamma): lane j holds column j of the chunk (one
       // coalesced load, prefetched a chunk ahead), broadcast to the row threads via smem
-      const float* vecp = p.bias ? p.bias : p.ln_gamma;
+      const float* vecp = f_bias ? p.bias : (f_ln ? p.ln_gamma : nullptr);
       auto load_bias = [&](int c) -> float {
         const int col = nb * BN + c * 32 + lane;
         return (vecp && c < NCH && col < p.N) ? __ldg(vecp + col) : 0.f;
@@ -591,12 +639,12 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
           if (lane == 0) {
             if (in_kind && !pref) {  // not prefetched (first chunk of the tile / one slot)
               bulk_wait_read<0>();
-              issue_in(c, si);
+              issue_in(nb, row0, z1, z2, c, si);
             }
             const int cn = c + CSTEP;
             if (in_kind && dual && cn < NCH && nb * BN + cn * 32 < p.N) {
               bulk_wait_read<0>();  // the other slot's last store has read it
-              issue_in(cn, si ^ 1);
+              issue_in(nb, row0, z1, z2, cn, si ^ 1);
             } else if (dual) {
               bulk_wait_read<1>();  // this slot's previous TMA stores have read it
             } else {
@@ -617,7 +665,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           }
-          if (EW == 4 && p.mode == SG_EPI_SOFTMAX_BWD) {
+          if (EW == 4 && f_mode == SG_EPI_SOFTMAX_BWD) {
             float pv[32];
             ld_row_bf16(s1, lane, pv);
 #pragma unroll
@@ -628,7 +676,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
                                  (size_t)row * p.ldd + col0,
                              p.vec_d, min(32, p.N - col0), v);
           } else {
-            if (p.bias) {
+            if (f_bias) {
               // lane j's coalesced bias value -> the warp's 128-byte slot -> every row thread
               float* bw = bias_all + e * 32;
               bw[lane] = bias_cur;
@@ -642,7 +690,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               }
               __syncwarp();
             }
-            if (p.ln_stats) {
+            if (f_ln) {
               // C holds the LayerNorm input x (fp32, main tile); g = dy gamma
               float xv[32];
               ld_row_f32(s0, lane, xv);
@@ -671,23 +719,22 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] += cv[j];
             }
-            if (p.act == SG_ACT_GELU) {
-              if (p.aux_out) st_row_bf16(s1, lane, v);
+            if (f_act == SG_ACT_GELU) {
+              if (f_aux_out) st_row_bf16(s1, lane, v);
               gelu_row(v);
-            } else if (p.act == SG_ACT_DGELU) {
+            } else if (f_act == SG_ACT_DGELU) {
               float xv[32];
               ld_row_bf16(s1, lane, xv);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_fast(xv[j]);
+              dgelu_row(v, xv);
             }
             __syncwarp();  // every lane has consumed the staged inputs before D overwrites them
             if (d_f32)
               st_row_f32(s0, lane, v);
             else
               st_row_bf16(s0, lane, v);
-            if (p.has_d2) st_row_bf16(s1, lane, v);
+            if (f_d2) st_row_bf16(s1, lane, v);
             __syncwarp();
-            if (p.colsum) {
+            if (f_colsum) {
               // column sums over this warp's valid rows, lane = column
               float cs = 0.f;
               if (d_f32) {
@@ -705,19 +752,31 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if (p.reduce_add)
+              if (f_reduce)
                 reduce_box(&tmD, s0, col0, row0, z2, z1, p.o_b2_first);
               else
                 store_box(&tmD, s0, col0, row0, z2, z1, p.o_b2_first);
-              if (p.aux_out) store_box(&tmX, s1, col0, row0, z2, z1, p.o_b2_first);
-              if (p.has_d2) store_box(&tmD2, s1, col0, row0, z2, z1, p.o_b2_first);
+              if (f_aux_out) store_box(&tmX, s1, col0, row0, z2, z1, p.o_b2_first);
+              if (f_d2) store_box(&tmD2, s1, col0, row0, z2, z1, p.o_b2_first);
               bulk_commit();
             }
           }
         }
         bias_cur = bias_nxt;
       }
-      if (p.ln_stats && lane < nrows) {
+      if (in_kind && dual && t + nunits < p.num_tiles) {
+        int mb2, nb2, y1, y2;
+        decode_tile(p, t + nunits, mb2, nb2, y1, y2);
+        const int row0n = mb2 * TM + (int)rank * kBM + q * 32;
+        if (nb2 * BN + c_first * 32 < p.N && row0n < p.M) {
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            issue_in(nb2, row0n, y1, y2, c_first, slot);
+          }
+          pref_next = true;
+        }
+      }
+      if (f_ln && lane < nrows) {
         atomicAdd(p.ln_stats + 2 * (size_t)(row0 + lane), ln_sxg);
         atomicAdd(p.ln_stats + 2 * (size_t)(row0 + lane) + 1, ln_sg);
       }
@@ -876,10 +935,10 @@ struct Maps {
   CUtensorMap a, b, d, x, d2, c;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR, int KIND = EK_GENERIC>
 static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, int grid) {
   using Cfg = GemmCfg<BN, EW, PAIR>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, EW, PAIR>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EW, PAIR, KIND>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
@@ -915,7 +974,31 @@ static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, 
 }
 
 template <int BN, int EW, bool PAIR = false>
-static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p, cudaStream_t s, int grid) {
+static int dispatch_major(bool amn, bool bmn, const Maps& m, const GemmParams& p, cudaStream_t s, int grid,
+                          int kind = EK_GENERIC) {
+  // specialised epilogues for the operand layouts the step uses them with:
+  // forward products (K-major A, MN-major B), dX products (both K-major),
+  // weight gradients (both MN-major)
+  if (PAIR && kind != EK_GENERIC) {
+    if (!amn && bmn) {
+      switch (kind) {
+        case EK_STORE: return launch_gemm<BN, false, true, EW, PAIR, EK_STORE>(m, p, s, grid);
+        case EK_BIAS: return launch_gemm<BN, false, true, EW, PAIR, EK_BIAS>(m, p, s, grid);
+        case EK_CIN_BIAS: return launch_gemm<BN, false, true, EW, PAIR, EK_CIN_BIAS>(m, p, s, grid);
+        case EK_GELU_BIAS: return launch_gemm<BN, false, true, EW, PAIR, EK_GELU_BIAS>(m, p, s, grid);
+        default: break;
+      }
+    } else if (!amn && !bmn) {
+      switch (kind) {
+        case EK_STORE: return launch_gemm<BN, false, false, EW, PAIR, EK_STORE>(m, p, s, grid);
+        case EK_DGELU: return launch_gemm<BN, false, false, EW, PAIR, EK_DGELU>(m, p, s, grid);
+        case EK_LN: return launch_gemm<BN, false, false, EW, PAIR, EK_LN>(m, p, s, grid);
+        default: break;
+      }
+    } else if (amn && bmn && kind == EK_STORE) {
+      return launch_gemm<BN, true, true, EW, PAIR, EK_STORE>(m, p, s, grid);
+    }
+  }
   if (!amn && !bmn) return launch_gemm<BN, false, false, EW, PAIR>(m, p, s, grid);
   if (!amn && bmn) return launch_gemm<BN, false, true, EW, PAIR>(m, p, s, grid);
   if (amn && !bmn) return launch_gemm<BN, true, false, EW, PAIR>(m, p, s, grid);
@@ -1136,12 +1219,31 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   // variant's shallower smem ring (3 stages at BN = 256) costs ~10%)
   const bool ew8 = force_ew != 4 && a->mode == SG_EPI_NORMAL && (bn == 128 || bn == 256) &&
                    (force_ew == 8 || p.kb_per_split <= 24);
+  // compile-time epilogue kind for the step's feature combinations (else generic)
+  static const bool generic_only = [] {
+    const char* e = getenv("SG_GEMM_GENERIC_EPI");
+    return e && atoi(e) != 0;
+  }();
+  int kind = EK_GENERIC;
+  const bool c_in = a->C && !p.reduce_add;
+  if (!generic_only && a->mode == SG_EPI_NORMAL && !a->D2) {
+    if (a->ln_stats)
+      kind = EK_LN;
+    else if (a->act == SG_ACT_DGELU && !a->bias && !c_in)
+      kind = EK_DGELU;
+    else if (a->act == SG_ACT_GELU && a->aux && a->bias && !c_in && !a->colsum)
+      kind = EK_GELU_BIAS;
+    else if (a->act == SG_ACT_NONE && c_in && p.c_f32 && p.d_f32 && a->bias && !a->colsum && a->alpha == 1.f)
+      kind = EK_CIN_BIAS;
+    else if (a->act == SG_ACT_NONE && !c_in && !a->colsum)
+      kind = a->bias ? EK_BIAS : EK_STORE;
+  }
   if (pair) {
     if (bn == 128)
-      return ew8 ? dispatch_major<128, 8, true>(amn, bmn, m, p, s, grid)
-                 : dispatch_major<128, 4, true>(amn, bmn, m, p, s, grid);
-    return ew8 ? dispatch_major<256, 8, true>(amn, bmn, m, p, s, grid)
-               : dispatch_major<256, 4, true>(amn, bmn, m, p, s, grid);
+      return ew8 ? dispatch_major<128, 8, true>(amn, bmn, m, p, s, grid, kind)
+                 : dispatch_major<128, 4, true>(amn, bmn, m, p, s, grid, kind);
+    return ew8 ? dispatch_major<256, 8, true>(amn, bmn, m, p, s, grid, kind)
+               : dispatch_major<256, 4, true>(amn, bmn, m, p, s, grid, kind);
   }
   switch (bn) {
     case 64: return dispatch_major<64, 4>(amn, bmn, m, p, s, grid);

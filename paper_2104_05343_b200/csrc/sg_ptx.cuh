@@ -194,7 +194,9 @@ __device__ __forceinline__ uint32_t mapa_smem(const void* p, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  // release at CTA scope (no GPU-scope MEMBAR): the arrivals order tcgen05 reads
+  // already completed by tcgen05.wait::ld, or smem reads, before the peer's reuse
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(

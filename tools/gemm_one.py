@@ -1,4 +1,4 @@
-"""One step GEMM shape in isolation (ncu target): python tools/gemm_one.py {dmid|fc1|qkv|dense} [reps]."""
+"""One step GEMM shape in isolation (ncu target): python tools/gemm_one.py {dmid|dmidg|fc1|qkv|dense} [reps]."""
 import sys
 
 import torch
@@ -15,6 +15,10 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 if which == "dmid":
     a, b, o = r(M, h), r(4 * h, h).t(), torch.empty(M, 4 * h, device=dev, dtype=bf)
     fn = lambda: K.gemm(a, b, o)  # noqa: E731
+elif which == "dmidg":
+    a, b, o = r(M, h), r(4 * h, h).t(), torch.empty(M, 4 * h, device=dev, dtype=bf)
+    aux = r(M, 4 * h)
+    fn = lambda: K.gemm(a, b, o, act=K.ACT_DGELU, aux=aux)  # noqa: E731
 elif which == "fc1":
     a, b, o = r(M, h), r(h, 4 * h), torch.empty(M, 4 * h, device=dev, dtype=bf)
     mid, bias = torch.empty_like(o), torch.randn(4 * h, device=dev)
