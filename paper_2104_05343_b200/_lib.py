@@ -13,7 +13,8 @@ from pathlib import Path
 
 from .errors import ConfigError, ShapeError, SummaGridError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
+# SG_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+_LIB_PATH = Path(os.environ.get("SG_LIB_PATH") or Path(__file__).resolve().parent / "libsg.so")
 
 SG_OK, SG_ERR_SHAPE, SG_ERR_CONFIG, SG_ERR_CUDA = 0, 1, 2, 3
 DTYPE_BF16, DTYPE_F32 = 0, 1

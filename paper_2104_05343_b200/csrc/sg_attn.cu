@@ -37,6 +37,7 @@ struct FlashFwdParams {
   __nv_bfloat16* O;
   long long ldo;    // row pitch of the context block
   float* lse;       // [b, nh, s] natural-log log-sum-exp of the scaled scores
+  int o_b2_first;   // O tile map (32 x 32 bf16 boxes): heads before rows
 };
 
 constexpr int kQB = 128;   // query rows per CTA
@@ -298,7 +299,8 @@ struct Flash2Cfg {
 // the current item finishes.
 __global__ void __launch_bounds__(384, 1)
     flash_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p, int bsz) {
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                      const __grid_constant__ FlashFwdParams p, int bsz) {
   using Cfg = Flash2Cfg;
   constexpr uint32_t T64 = Cfg::T64;
   constexpr int NS = Cfg::KV_SLOTS;
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmO);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -534,36 +537,53 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&o_full[i], it & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * 64;
+      // normalised bf16 rows -> this warp's (now idle) P_i rows as two 32 x 32 SW64 tiles
+      // -> TMA stores into the context block (rows past s clipped)
+      uint8_t* ostg = sP + i * Cfg::P_BYTES + qd * 32 * 128;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t ov[32];
         tmem_ld32(t_o + c * 32, ov);
         tmem_wait_ld();
-        if (qrow < p.s) {
+        uint8_t* orow = ostg + c * 2048 + lane * 64;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint4 x;
-            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+        for (int k = 0; k < 4; ++k) {
+          uint4 x;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv,
-                                            __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
-            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
-          }
+          for (int e = 0; e < 4; ++e)
+            hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv,
+                                          __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
+          *reinterpret_cast<uint4*>(orow + ((k ^ ((lane >> 1) & 3)) << 4)) = x;
         }
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int row0 = (qb * kQT + i) * kQB + qd * 32;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (p.o_b2_first)
+            tma_store_4d(&tmO, ostg + c * 2048, c * 32, h, row0, b);
+          else
+            tma_store_4d(&tmO, ostg + c * 2048, c * 32, row0, h, b);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();  // staging = this warp's P rows, rewritten by the next item
+      }
+      __syncwarp();
       tc_fence_before();
       if (qrow < p.s && p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p, int b,
-                       cudaStream_t stream) {
+static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                       const FlashFwdParams& p, int b, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(flash_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Flash2Cfg::SMEM) !=
@@ -573,7 +593,8 @@ static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
   }
   const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
   const int sms = sg_device_sm_count();
-  launch_k(flash_fwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), Flash2Cfg::SMEM, stream, q, k, v, p, b);
+  launch_k(flash_fwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), Flash2Cfg::SMEM, stream, q, k, v, o,
+           p, b);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -627,7 +648,12 @@ extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_
     const char* e = getenv("SG_FLASH_FWD_V1");
     return e ? atoi(e) : 0;
   }();
-  if (d == 64 && !fwd_v1) return launch_fwd2(tq, tk, tv, p, (int)b, st);
+  if (d == 64 && !fwd_v1) {
+    CUtensorMap to;
+    rc = tmap_bf16_tile_4d(&to, out, d, s, nh, b, ldo, d, s * ldo, &p.o_b2_first);
+    if (rc) return rc;
+    return launch_fwd2(tq, tk, tv, to, p, (int)b, st);
+  }
   return d == 64 ? launch_fwd<64>(tq, tk, tv, p, (int)b, st) : launch_fwd<128>(tq, tk, tv, p, (int)b, st);
 }
 
@@ -653,6 +679,7 @@ struct FlashBwdParams {
   __nv_bfloat16* dK;  // [b*s, ldg] head columns h*64
   __nv_bfloat16* dV;
   long long ldg;
+  int dkv_b2_first;   // dK / dV tile maps: heads before rows
 };
 
 constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
@@ -893,7 +920,8 @@ __global__ void __launch_bounds__(256, 1)
 __global__ void __launch_bounds__(384, 1)
     flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p, int bsz) {
+                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
+                      const __grid_constant__ CUtensorMap tmDV, const __grid_constant__ FlashBwdParams p, int bsz) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
@@ -918,6 +946,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* acc_full = bars + 15;
   uint64_t* acc_empty = bars + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* s_free = bars + 18;    // S_G / dP_G read out of TMEM (8 softmax warps)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (p.s + 127) / 128;
@@ -938,6 +967,8 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
     tma_prefetch_desc(&tmDQ);
+    tma_prefetch_desc(&tmDK);
+    tma_prefetch_desc(&tmDV);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -951,6 +982,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(bufs_free, 1);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 8);
+    mbar_init(s_free, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -1012,9 +1044,13 @@ __global__ void __launch_bounds__(384, 1)
       if (total > 0) issue_sdp(0);
       for (int G = 0; G < total; ++G) {
         const int slot = G & 1, it = G / nqb, i = G % nqb;
-        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem; S_G / dP_G read
+        // S_G+1 / dP_G+1 overwrite S_G / dP_G as soon as the softmax warps have read
+        // them, overlapping the second half of block G's exponentials
+        mbar_wait(s_free, G & 1);
         tc_fence_after();
         if (G + 1 < total) issue_sdp(G + 1);
+        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem
+        tc_fence_after();
         // the previous item's dK / dV have been read out before this item's first products
         if (i == 0 && it > 0) {
           mbar_wait(acc_empty, (it - 1) & 1);
@@ -1129,6 +1165,11 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(t_s + lane_base + c * 32, sv);
         tmem_ld32(t_dp + lane_base + c * 32, dv);
         tmem_wait_ld();
+        if (cc == 1) {  // both chunks of S / dP are in registers: the next block's products may start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_free);
+        }
         // pairs of keys on the paired fp32 pipe: y = s * scale - lse, P = 2^y,
         // dS = (P * scale) * (dP - D)
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nl2 = f2_pack(-lse2, -lse2);
@@ -1178,7 +1219,6 @@ __global__ void __launch_bounds__(384, 1)
         // this item's dK, dV: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
         mbar_wait(acc_full, it & 1);
         tc_fence_after();
-        const int key = kb * 128 + r;
         uint32_t vk[32], vv[32];
         tmem_ld32(t_dk + lane_base + half * 32, vk);
         tmem_ld32(t_dv + lane_base + half * 32, vv);
@@ -1186,21 +1226,36 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
-        if (key < p.s) {
+        // bf16 rows -> the warp's staging slot (32 x 32 SW64 tiles: dK, then dV) -> two TMA
+        // stores (rows past s clipped); the previous dQ reduce-add has read the slot
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
 #pragma unroll
-          for (int which = 0; which < 2; ++which) {
-            const uint32_t* v = which == 0 ? vk : vv;
-            __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64 + half * 32;
+        for (int which = 0; which < 2; ++which) {
+          const uint32_t* v = which == 0 ? vk : vv;
+          uint8_t* row = stg + which * 2048 + lane * 64;
 #pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2) {
-              uint4 x;
-              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+          for (int k2 = 0; k2 < 4; ++k2) {
+            uint4 x;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
-              for (int e2 = 0; e2 < 4; ++e2)
-                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
-              *reinterpret_cast<uint4*>(dst + 8 * k2) = x;
-            }
+            for (int e2 = 0; e2 < 4; ++e2)
+              hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
+            *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
           }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int key0 = kb * 128 + q * 32;
+          if (p.dkv_b2_first) {
+            tma_store_4d(&tmDK, stg, half * 32, h, key0, b);
+            tma_store_4d(&tmDV, stg + 2048, half * 32, h, key0, b);
+          } else {
+            tma_store_4d(&tmDK, stg, half * 32, key0, h, b);
+            tma_store_4d(&tmDV, stg + 2048, half * 32, key0, h, b);
+          }
+          bulk_commit();
         }
         i = 0;
         ++it;
@@ -1230,7 +1285,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if ((reinterpret_cast<uintptr_t>(dqkv) & 15) || (ldg * 2) % 16) return set_error(SG_ERR_SHAPE, "flash bwd: unaligned");
   const __nv_bfloat16* base = static_cast<const __nv_bfloat16*>(qkv);
   const long long hb = nh * d;
-  CUtensorMap tq, tk, tv, tdo, tdq;
+  CUtensorMap tq, tk, tv, tdo, tdq, tdk, tdv;
   FlashBwdParams p{};
   p.s = (int)s;
   p.nh = (int)nh;
@@ -1246,6 +1301,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.v_b2_first);
   if (!rc) rc = tmap_bf16_4d(&tdo, dout, d, s, nh, b, lddo, d, s * lddo, 64, 128, &p.do_b2_first);
   if (!rc) rc = tmap_f32_tile_4d(&tdq, dq_acc, d, s, nh, b, lddq, d, s * lddq, &p.dq_b2_first);
+  if (!rc) rc = tmap_bf16_tile_4d(&tdk, p.dK, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
+  if (!rc) rc = tmap_bf16_tile_4d(&tdv, p.dV, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (rc) return rc;
   constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
   constexpr size_t SMEM2 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;  // v2: K, V double-buffered per item
@@ -1270,7 +1327,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
     if (grid.x > 1024 || nh > 1024 || b > 2047 || (items + (sms > 0 ? sms : 148) - 1) / (sms > 0 ? sms : 148) > kMaxItems)
       return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
     launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), SMEM2,
-             static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, p, (int)b);
+             static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, tdk, tdv, p, (int)b);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

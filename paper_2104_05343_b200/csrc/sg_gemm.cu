@@ -734,21 +734,6 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               st_row_bf16(s0, lane, v);
             if (f_d2) st_row_bf16(s1, lane, v);
             __syncwarp();
-            if (f_colsum) {
-              // column sums over this warp's valid rows, lane = column
-              float cs = 0.f;
-              if (d_f32) {
-#pragma unroll 8
-                for (int i = 0; i < 32; ++i)
-                  if (i < nrows) cs += *reinterpret_cast<const float*>(s0 + swz_f32(i, lane));
-              } else {
-#pragma unroll 8
-                for (int i = 0; i < 32; ++i)
-                  if (i < nrows)
-                    cs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
-              }
-              if (col_ok) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col, cs);
-            }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -760,6 +745,25 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               if (f_d2) store_box(&tmD2, s1, col0, row0, z2, z1, p.o_b2_first);
               bulk_commit();
             }
+            if (f_colsum) {
+              // column sums over this warp's valid rows, lane = column, read back from
+              // the staged tile while the TMA store drains it (both only read)
+              float cs[4] = {0.f, 0.f, 0.f, 0.f};
+              if (nrows == 32) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  cs[i & 3] += d_f32 ? *reinterpret_cast<const float*>(s0 + swz_f32(i, lane))
+                                     : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
+              } else {
+#pragma unroll 4
+                for (int i = 0; i < nrows; ++i)
+                  cs[i & 3] += d_f32 ? *reinterpret_cast<const float*>(s0 + swz_f32(i, lane))
+                                     : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
+              }
+              if (col_ok)
+                atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col, (cs[0] + cs[1]) + (cs[2] + cs[3]));
+            }
+
           }
         }
         bias_cur = bias_nxt;
@@ -915,6 +919,12 @@ int tmap_f32_tile_4d(CUtensorMap* map, const void* ptr, long long inner, long lo
                      long long nb1, long long ld, long long s2, long long s1, int* b2_first) {
   return make_map(map, ptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, inner, outer, nb2, nb1, ld, s2, s1, 32, 32,
                   CU_TENSOR_MAP_SWIZZLE_128B, b2_first);
+}
+
+int tmap_bf16_tile_4d(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
+                      long long nb1, long long ld, long long s2, long long s1, int* b2_first) {
+  return make_map(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, inner, outer, nb2, nb1, ld, s2, s1, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_64B, b2_first);
 }
 
 static int operand_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,

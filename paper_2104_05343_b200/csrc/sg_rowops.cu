@@ -586,10 +586,17 @@ __global__ void xent_local_kernel(const TL* __restrict__ logits, long long rows,
         s *= __expf(m - cm);
         m = cm;
       }
+      const float l2e = 1.4426950408889634f, ml = -m * l2e;
+      float sp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s += __expf(v[k][i] - m);
+        for (int i = 0; i < 8; ++i) {
+          float e;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(v[k][i], l2e, ml)));
+          sp[k] += e;
+        }
+      s += (sp[0] + sp[1]) + (sp[2] + sp[3]);
     }
     for (; c < n_real; c += 256) {
       float v[8];
@@ -671,21 +678,28 @@ __global__ void xent_bwd_kernel(const TL* logits, long long rows, long long ldl,
     const float m = gmax[r];
     const float inv = 1.0f / packed[2 * r];
     const long long lab = labels[r] - col_lo;
+    // g = 2^(x log2e - m log2e) (scale / sum), the label column then - scale
+    const float l2e = 1.4426950408889634f, ml = -m * l2e, sc = inv * scale;
     int c = lane * 8;
-    for (; c + 256 + 8 <= ncols; c += 512) {  // interior, two chunks in flight
-      Vec8<TL> raw[2];
-      raw[0].load(logits + r * ldl + c);
-      raw[1].load(logits + r * ldl + c + 256);
+    for (; c + 3 * 256 + 8 <= n_real; c += 1024) {  // interior (all columns real), four chunks in flight
+      Vec8<TL> raw[4];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < 4; ++k) raw[k].load(logits + r * ldl + c + k * 256);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
         float v[8];
         raw[k].to(v);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int cc = c + k * 256 + i;
-          float g = cc < n_real ? __expf(v[i] - m) * inv : 0.f;
-          if (cc == lab) g -= 1.f;
-          v[i] = g * scale;
+          float e;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(v[i], l2e, ml)));
+          v[i] = e * sc;
+        }
+        const long long off = lab - (c + k * 256);
+        if (off >= 0 && off < 8) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i == off) v[i] -= scale;
         }
         st8(dl + r * lddl + c + k * 256, 8, v);
       }
@@ -930,42 +944,53 @@ __global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long 
 // read of x; the (sum, sumsq) row statistics come from the mesh all-reduce
 // (stats != nullptr) or, on a 1-column mesh, from the registers themselves.
 template <typename TX, typename TY, int NV>
-__global__ void __launch_bounds__(256) ln_fwd_rows_kernel(
+__global__ void __launch_bounds__(256, NV <= 4 ? 4 : 1) ln_fwd_rows_kernel(
     const TX* __restrict__ x, long long rows, long long ldx, const float* __restrict__ stats, float inv_h, float eps,
     const float* __restrict__ gamma, const float* __restrict__ beta, TY* __restrict__ y, long long ldy,
     float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   pdl_begin();
+  // RU rows per warp iteration (their loads in flight together, each gamma / beta
+  // load serving RU rows); measured: RU = 2 at h = 1024 loses to the occupancy it costs
+  constexpr int RU = 1;
   const int lane = threadIdx.x & 31;
   const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
-  for (long long r = wid; r < rows; r += nw) {
-    Vec8<TX> raw[NV];
+  for (long long r0 = wid * RU; r0 < rows; r0 += nw * RU) {
+    Vec8<TX> raw[RU][NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) raw[k].load(x + r * ldx + k * 256 + lane * 8);
-    float s1, s2;
-    if (stats) {
-      s1 = stats[2 * r];
-      s2 = stats[2 * r + 1];
+    for (int u = 0; u < RU; ++u) {
+      const long long r = min(r0 + u, rows - 1);  // clamped: a duplicate row is computed, not stored
+#pragma unroll
+      for (int k = 0; k < NV; ++k) raw[u][k].load(x + r * ldx + k * 256 + lane * 8);
     }
-    float v[NV][8];
+    float mu[RU], rs[RU];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) raw[k].to(v[k]);
-    if (!stats) {
-      s1 = 0.f;
-      s2 = 0.f;
+    for (int u = 0; u < RU; ++u) {
+      const long long r = min(r0 + u, rows - 1);
+      float s1, s2;
+      if (stats) {
+        s1 = stats[2 * r];
+        s2 = stats[2 * r + 1];
+      } else {
+        s1 = 0.f;
+        s2 = 0.f;
 #pragma unroll
-      for (int k = 0; k < NV; ++k)
+        for (int k = 0; k < NV; ++k) {
+          float v[8];
+          raw[u][k].to(v);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          s1 += v[k][i];
-          s2 += v[k][i] * v[k][i];
+          for (int i = 0; i < 8; ++i) {
+            s1 += v[i];
+            s2 = fmaf(v[i], v[i], s2);
+          }
         }
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+      }
+      mu[u] = s1 * inv_h;
+      const float var = s2 * inv_h - mu[u] * mu[u];  // one-pass variance, layers.py:296-297
+      rs[u] = 1.0f / sqrtf(var + eps);
     }
-    const float mu = s1 * inv_h;
-    const float var = s2 * inv_h - mu * mu;  // one-pass variance, layers.py:296-297
-    const float rs = 1.0f / sqrtf(var + eps);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int c = k * 256 + lane * 8;
@@ -976,12 +1001,22 @@ __global__ void __launch_bounds__(256) ln_fwd_rows_kernel(
       gv.to(g);
       bv.to(bb);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[k][i] = (v[k][i] - mu) * rs * g[i] + bb[i];
-      st8(y + r * ldy + c, 8, v[k]);
+      for (int u = 0; u < RU; ++u) {
+        if (r0 + u >= rows) break;
+        float v[8];
+        raw[u][k].to(v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fmaf((v[i] - mu[u]) * rs[u], g[i], bb[i]);
+        st8(y + (r0 + u) * ldy + c, 8, v);
+      }
     }
-    if (lane == 0) {
-      if (mean_out) mean_out[r] = mu;
-      if (rstd_out) rstd_out[r] = rs;
+    if (lane < RU && r0 + lane < rows) {
+      float m = mu[0], q = rs[0];
+#pragma unroll
+      for (int u = 1; u < RU; ++u)
+        if (lane == u) m = mu[u], q = rs[u];
+      if (mean_out) mean_out[r0 + lane] = m;
+      if (rstd_out) rstd_out[r0 + lane] = q;
     }
   }
 }

@@ -15,3 +15,9 @@ namespace sg {
 int tmap_f32_tile_4d(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
                      long long nb1, long long ld, long long s2, long long s1, int* b2_first);
 }  // namespace sg
+
+namespace sg {
+// 4-D bf16 map with a 32 x 32 box, SWIZZLE_64B (64-byte rows): bf16 epilogue tiles.
+int tmap_bf16_tile_4d(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long nb2,
+                      long long nb1, long long ld, long long s2, long long s1, int* b2_first);
+}  // namespace sg

@@ -38,7 +38,16 @@ def main():
     cs4 = torch.zeros(4 * h, device=dev)
     qkv = torch.randn(M, 3 * h, device=dev).to(bf)
     cs3 = torch.zeros(3 * h, device=dev)
+    V, Vp = 30522, 30528
+    logits = (torch.randn(M, Vp, device=dev) * 3).to(bf)
+    labels = torch.randint(0, V, (M,), device=dev)
+    lmax, gmax = torch.empty(M, device=dev), torch.empty(M, device=dev)
+    packed = torch.empty(M, 2, device=dev)
+    K.xent_local(logits, V, labels, 0, lmax, gmax, packed)
+    dlog = torch.empty_like(logits)
     cases = {
+        "xent_local [M,V] bf16": (lambda: K.xent_local(logits, V, labels, 0, lmax, gmax, packed), M * Vp * 2),
+        "xent_bwd [M,V] bf16": (lambda: K.xent_bwd(logits, V, labels, 0, gmax, packed, 1.0 / M, dlog), M * Vp * 4),
         "ln_bwd(+resid,dx2,dg,db,ds)": (lambda: K.ln_bwd(dy, x, mean, rstd, gamma, stats, h, res, dx, dx2, dg, db, ds),
                                         M * h * (4 * 4 + 2)),
         "ln_bwd_stats": (lambda: K.ln_bwd_stats(dy, x, mean, rstd, gamma, stats), M * h * 8),
