@@ -138,12 +138,14 @@ int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_t s, int64_
  * drow = rowsum(dO * O) from sg_attn_rowdot. */
 int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
                       const float* drow, int64_t b, int64_t s, int64_t nh, int64_t d, float* dq_acc, int64_t lddq,
-                      void* dqkv, int64_t ldg, void* stream);
-/* After sg_flash_attn_bwd: dqkv[:, 0:hb] = bf16(dq_acc) and colsum[0:3hb] += column sums
- * of the whole dQKV gradient block (the b_qkv gradient, layers.py:238), one pass;
- * hb % 256 == 0. */
+                      void* dqkv, int64_t ldg, float* kv_colsum, void* stream);
+/* (kv_colsum, optional: [2*nh*d] += column sums of the bf16 dK, dV written, i.e. the
+ * K / V parts of the b_qkv gradient.)
+ * After sg_flash_attn_bwd: dqkv[:, 0:hb] = bf16(dq_acc) and colsum[0:cols] += column
+ * sums of dQKV columns [0, cols) (cols = 3hb: the whole b_qkv gradient, layers.py:238;
+ * cols = hb when the flash backward already summed dK / dV), one pass; hb % 256 == 0. */
 int sg_qkv_grad_finish(const float* dq_acc, int64_t lddq, void* dqkv, int64_t ldg, int64_t rows, int64_t hb,
-                       float* colsum, void* stream);
+                       float* colsum, int64_t cols, void* stream);
 /* D[b, h, t] = rowsum(dO * O) per head and token (= rowsum(dP * P)), the
  * SG_EPI_SOFTMAX_BWD row term; dO / O are [b*s, nh*d] head-interleaved blocks. */
 int sg_attn_rowdot(const void* dO, int dt, int64_t ldo, const void* O, int64_t ldO, int64_t rows, int64_t nh,

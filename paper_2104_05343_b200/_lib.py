@@ -68,8 +68,8 @@ SIGNATURES: dict[str, tuple] = {
     "sg_softmax_rows": (i32, [vp, i32, i64, i64, i64, vp, i32, i64, vp]),
     "sg_softmax_bwd": (i32, [vp, i32, i64, vp, i32, i64, i64, i64, ctypes.c_float, vp, i32, i64, vp]),
     "sg_flash_attn_fwd": (i32, [vp, i64, i64, i64, i64, i64, vp, i64, vp, vp]),
-    "sg_flash_attn_bwd": (i32, [vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, vp, i64, vp, i64, vp]),
-    "sg_qkv_grad_finish": (i32, [vp, i64, vp, i64, i64, i64, vp, vp]),
+    "sg_flash_attn_bwd": (i32, [vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, vp, i64, vp, i64, vp, vp]),
+    "sg_qkv_grad_finish": (i32, [vp, i64, vp, i64, i64, i64, vp, i64, vp]),
     "sg_attn_rowdot": (i32, [vp, i32, i64, vp, i64, i64, i64, i64, i64, vp, vp]),
     "sg_xent_local": (i32, [vp, i32, i64, i64, i64, vp, i64, vp, vp, vp, vp]),
     "sg_xent_rescale": (i32, [i64, vp, vp, vp, vp]),

@@ -680,6 +680,7 @@ struct FlashBwdParams {
   __nv_bfloat16* dV;
   long long ldg;
   int dkv_b2_first;   // dK / dV tile maps: heads before rows
+  float* kv_colsum;   // optional [2 nh 64]: += column sums of dK (then dV)
 };
 
 constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
@@ -1257,6 +1258,20 @@ __global__ void __launch_bounds__(384, 1)
           }
           bulk_commit();
         }
+        if (p.kv_colsum) {
+          // bias-gradient column sums of the staged bf16 tiles (rows past s hold zeros),
+          // lane = column, read while the TMA stores drain the same tiles
+          float sk[2] = {0.f, 0.f}, sv[2] = {0.f, 0.f};
+#pragma unroll
+          for (int i2 = 0; i2 < 32; ++i2) {
+            const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
+            sk[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(stg + off));
+            sv[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(stg + 2048 + off));
+          }
+          const int col = h * 64 + half * 32 + lane;
+          atomicAdd(p.kv_colsum + col, sk[0] + sk[1]);
+          atomicAdd(p.kv_colsum + p.nh * 64 + col, sv[0] + sv[1]);
+        }
         i = 0;
         ++it;
         if (it < my_items) item(it, kb, h, b);
@@ -1276,7 +1291,7 @@ __global__ void __launch_bounds__(384, 1)
 
 extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
                                  const float* drow, int64_t b, int64_t s, int64_t nh, int64_t d, float* dq_acc,
-                                 int64_t lddq, void* dqkv, int64_t ldg, void* stream) {
+                                 int64_t lddq, void* dqkv, int64_t ldg, float* kv_colsum, void* stream) {
   using namespace sg;
   clear_error();
   if (b < 1 || s < 1 || nh < 1 || d != 64) return set_error(SG_ERR_SHAPE, "flash bwd: d must be 64");
@@ -1296,6 +1311,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   p.dK = static_cast<__nv_bfloat16*>(dqkv) + hb;
   p.dV = static_cast<__nv_bfloat16*>(dqkv) + 2 * hb;
   p.ldg = ldg;
+  p.kv_colsum = kv_colsum;
   int rc = tmap_bf16_4d(&tq, base, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.q_b2_first);
   if (!rc) rc = tmap_bf16_4d(&tk, base + hb, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.k_b2_first);
   if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, 128, &p.v_b2_first);

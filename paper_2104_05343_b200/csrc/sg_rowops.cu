@@ -1479,12 +1479,14 @@ extern "C" int sg_dgelu(const void* dact, int64_t lda, const void* mid, int64_t 
 }
 
 extern "C" int sg_qkv_grad_finish(const float* dq, int64_t lddq, void* dqkv, int64_t ldg, int64_t rows, int64_t hb,
-                                  float* colsum, void* stream) {
+                                  float* colsum, int64_t cols, void* stream) {
   clear_error();
   if (rows < 0 || hb < 1 || hb % 256 != 0) return set_error(SG_ERR_SHAPE, "qkv_grad_finish: hb must be a multiple of 256");
+  if (cols != hb && cols != 3 * hb) return set_error(SG_ERR_SHAPE, "qkv_grad_finish: cols must be hb or 3 hb");
   if (!aligned16(dq, lddq, 4) || !aligned16(dqkv, ldg, 2)) return set_error(SG_ERR_SHAPE, "qkv_grad_finish: unaligned");
   if (rows == 0) return SG_OK;
-  launch_k(qkv_grad_finish_kernel<2>, seg_grid(rows, 3 * hb, 2, 3), dim3(256), 0, S(stream), dq, lddq,
-           static_cast<bf16*>(dqkv), ldg, rows, (int)hb, colsum);
+  // cols = hb: only the dQ segments (their bf16 conversion and column sums)
+  launch_k(qkv_grad_finish_kernel<2>, seg_grid(rows, cols, 2, 3), dim3(256), 0, S(stream), dq,
+           lddq, static_cast<bf16*>(dqkv), ldg, rows, (int)hb, colsum);
   return launch_check();
 }

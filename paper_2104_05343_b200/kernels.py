@@ -417,11 +417,13 @@ def dgelu(dact, mid, out, colsum=None):
     _call("sg_dgelu", _p(dact), lda, _p(mid), ldm, rows, cols, _p(out), _dt(out), ldo, _p(colsum), _stream(dact))
 
 
-def qkv_grad_finish(dq_acc, dqkv, hb, colsum):
-    """dqkv[:, :hb] = bf16(dq_acc); colsum += column sums of dqkv (fused; hb % 256 == 0)."""
+def qkv_grad_finish(dq_acc, dqkv, hb, colsum, q_only=False):
+    """dqkv[:, :hb] = bf16(dq_acc); colsum += column sums of dqkv (fused; hb % 256 == 0),
+    of its dQ columns only with ``q_only`` (dK / dV summed by the flash backward)."""
     rows, _, lddq = _rows2d(dq_acc)
     _, _, ldg = _rows2d(dqkv)
-    _call("sg_qkv_grad_finish", _p(dq_acc), lddq, _p(dqkv), ldg, rows, hb, _p(colsum), _stream(dqkv))
+    _call("sg_qkv_grad_finish", _p(dq_acc), lddq, _p(dqkv), ldg, rows, hb, _p(colsum), hb if q_only else 3 * hb,
+          _stream(dqkv))
 
 
 def flash_attn_fwd(qkv, b, s, n_heads, d, out, lse=None):
@@ -431,11 +433,15 @@ def flash_attn_fwd(qkv, b, s, n_heads, d, out, lse=None):
     _call("sg_flash_attn_fwd", _p(qkv), ldq, b, s, n_heads, d, _p(out), ldo, _p(lse), _stream(out))
 
 
-def flash_attn_bwd(qkv, dout, lse, drow, b, s, n_heads, d, dq_acc, dqkv):
-    """dK, dV -> dqkv[:, nh*d:], dQ added into dq_acc (fp32, zeroed by the caller)."""
+def flash_attn_bwd(qkv, dout, lse, drow, b, s, n_heads, d, dq_acc, dqkv, kv_colsum=None):
+    """dK, dV -> dqkv[:, nh*d:], dQ added into dq_acc (fp32, zeroed by the caller);
+    ``kv_colsum`` ([2*nh*d] fp32) accumulates the column sums of dK, dV."""
     _, _, ldq = _rows2d(qkv)
     _, _, lddo = _rows2d(dout)
     _, _, lddq = _rows2d(dq_acc)
     _, _, ldg = _rows2d(dqkv)
+    if kv_colsum is not None and (kv_colsum.dtype != torch.float32 or not kv_colsum.is_contiguous()
+                                  or kv_colsum.numel() != 2 * n_heads * d):
+        raise ShapeError("flash_attn_bwd: kv_colsum must be a contiguous fp32 [2 * nh * d]")
     _call("sg_flash_attn_bwd", _p(qkv), ldq, _p(dout), lddo, _p(lse), _p(drow), b, s, n_heads, d, _p(dq_acc), lddq,
-          _p(dqkv), ldg, _stream(dqkv))
+          _p(dqkv), ldg, _p(kv_colsum), _stream(dqkv))

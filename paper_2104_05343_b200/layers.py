@@ -601,9 +601,12 @@ def attention_core_backward(cfg: ModelConfig, b_loc: int, n_loc: int, qkv_blk, c
         drow = ws.empty(dev, (b_loc, n_loc, s), "free", dtype=F32, pad=False)
         K.attn_rowdot(dctx_blk, ctx_blk, n_loc, d, s, drow)
         dq_acc = ws.alloc(dev, (bs_loc, hb), "free", dtype=F32)
-        K.flash_attn_bwd(qkv_blk, dctx_blk, lse, drow, b_loc, s, n_loc, d, dq_acc, dq_blk)
-        if hb % 256 == 0:  # dQ to bf16 and the b_qkv gradient in one pass
-            K.qkv_grad_finish(dq_acc, dq_blk, hb, bq_part)
+        fused = hb % 256 == 0
+        # the K / V parts of the b_qkv gradient summed from the staged dK / dV tiles
+        K.flash_attn_bwd(qkv_blk, dctx_blk, lse, drow, b_loc, s, n_loc, d, dq_acc, dq_blk,
+                         kv_colsum=bq_part[hb:] if fused else None)
+        if fused:  # dQ to bf16 and its b_qkv gradient part in one pass
+            K.qkv_grad_finish(dq_acc, dq_blk, hb, bq_part, q_only=True)
         else:
             K.epilogue(dq_acc, dq_blk[:, :hb])
             K.colsum(dq_blk, bq_part, accumulate=True)

@@ -50,8 +50,22 @@ def test_flash_backward(b, s, nh, d):
     K.attn_rowdot(dout, out, nh, d, s, drow)
     dq = torch.zeros(b * s, hb, device="cuda")
     dqkv = torch.full((b * s, 3 * hb), float("nan"), device="cuda", dtype=torch.bfloat16)
-    K.flash_attn_bwd(qkv, dout, lse, drow, b, s, nh, d, dq, dqkv)
+    kv_cs = torch.zeros(2 * hb, device="cuda")
+    K.flash_attn_bwd(qkv, dout, lse, drow, b, s, nh, d, dq, dqkv, kv_colsum=kv_cs)
     torch.cuda.synchronize()
+    # fused K / V bias-gradient column sums equal the sums of the bf16 dK, dV written
+    want_cs = dqkv[:, hb:].float().sum(0)
+    assert (kv_cs - want_cs).abs().max().item() <= 1e-3 * want_cs.abs().max().item() + 1e-4
+    # the dQ finishing pass: bf16 dQ and its column sums only
+    q_cs = torch.zeros(3 * hb, device="cuda")
+    dqkv2 = dqkv.clone()
+    if hb % 256 == 0:
+        K.qkv_grad_finish(dq, dqkv2, hb, q_cs, q_only=True)
+        assert torch.equal(dqkv2[:, :hb], dq.to(torch.bfloat16))
+        assert torch.equal(dqkv2[:, hb:], dqkv[:, hb:])
+        # (the dQ part is summed from the fp32 accumulator, before the bf16 rounding)
+        assert (q_cs[:hb] - dq.sum(0)).abs().max().item() <= 1e-4 * q_cs.abs().max().item() + 1e-5
+        assert q_cs[hb:].abs().max().item() == 0.0
 
     x = qkv.float().requires_grad_(True)
     o, _, _ = _ref(x, b, s, nh, d)

@@ -38,6 +38,7 @@ def main():
     cs4 = torch.zeros(4 * h, device=dev)
     qkv = torch.randn(M, 3 * h, device=dev).to(bf)
     cs3 = torch.zeros(3 * h, device=dev)
+    dqa = torch.randn(M, h, device=dev)
     V, Vp = 30522, 30528
     logits = (torch.randn(M, Vp, device=dev) * 3).to(bf)
     labels = torch.randint(0, V, (M,), device=dev)
@@ -46,6 +47,8 @@ def main():
     K.xent_local(logits, V, labels, 0, lmax, gmax, packed)
     dlog = torch.empty_like(logits)
     cases = {
+        "qkv_grad_finish (all 3hb)": (lambda: K.qkv_grad_finish(dqa, qkv, h, cs3), M * h * (4 + 2 + 4)),
+        "qkv_grad_finish (q only)": (lambda: K.qkv_grad_finish(dqa, qkv, h, cs3, q_only=True), M * h * 6),
         "xent_local [M,V] bf16": (lambda: K.xent_local(logits, V, labels, 0, lmax, gmax, packed), M * Vp * 2),
         "xent_bwd [M,V] bf16": (lambda: K.xent_bwd(logits, V, labels, 0, gmax, packed, 1.0 / M, dlog), M * Vp * 4),
         "ln_bwd(+resid,dx2,dg,db,ds)": (lambda: K.ln_bwd(dy, x, mean, rstd, gamma, stats, h, res, dx, dx2, dg, db, ds),
