@@ -18,7 +18,7 @@ _ALL_VARIANTS = [
     {"SG_GEMM_EPI_WARPS": "8"},
     {"SG_GEMM_PAIR": "0"},
 ]
-CASES = ["qkv", "dense", "fc1", "fc2", "dctx", "dWd", "dWqkv", "dmid", "dxln"]
+CASES = ["qkv", "dense", "fc1", "fc2", "dctx", "dWd", "dWqkv", "dW1", "dW2", "dmid", "dxln"]
 
 
 def child(case):
@@ -54,6 +54,10 @@ def child(case):
         a, b, o, kw = r(M, h), r(h, h).t(), torch.empty(M, h, device="cuda", dtype=bf), {}
     elif case == "dWd":
         a, b, o, kw = r(M, h).t(), r(M, h), torch.empty(h, h, device="cuda"), {}
+    elif case == "dW1":
+        a, b, o, kw = r(M, h).t(), r(M, 4 * h), torch.empty(h, 4 * h, device="cuda"), {}
+    elif case == "dW2":
+        a, b, o, kw = r(M, 4 * h).t(), r(M, h), torch.empty(4 * h, h, device="cuda"), {}
     elif case == "dWqkv":
         a, b, o, kw = r(M, h).t(), r(M, 3 * h), torch.empty(h, 3 * h, device="cuda"), {}
     else:
