@@ -42,7 +42,25 @@
 
 namespace sg {
 
+// n / d for 0 <= n < 2^31 as (n * m) >> (32 + s), m = ceil(2^(32+s) / d), s = ceil(log2 d)
+// (exact: the rounding error n e / (d 2^(32+s)) stays below 1/d), precomputed on the
+// host: every role decodes a tile index per tile, cheaply only without divisions
+struct FastDiv {
+  unsigned long long m;
+  uint32_t d, s;
+  __host__ void set(uint32_t div) {
+    d = div;
+    s = 0;
+    while ((1ull << s) < div) ++s;
+    m = (((unsigned long long)1 << (32 + s)) + div - 1) / div;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((unsigned long long)n * m) >> (32 + s));
+  }
+};
+
 struct GemmParams {
+  FastDiv fd_tiles, fd_per, fd_span, fd_nb2;  // tiles per split, m x n tiles, group span, nb2
   int M, N, K;
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
@@ -164,17 +182,21 @@ __device__ __forceinline__ void reduce_box(const CUtensorMap* tm, const void* sr
 // each operand is then streamed from HBM about once even when A exceeds L2.
 constexpr int kGroupM = 16;
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb, int& nb, int& z1, int& z2) {
-  t %= p.num_tiles / p.k_splits;  // split-K units share the output tile
-  const int per = p.m_tiles * p.n_tiles;
-  const int z = t / per;
-  const int r = t - z * per;
-  const int group = r / (kGroupM * p.n_tiles);
+  t -= (int)p.fd_tiles.div((uint32_t)t) * (int)p.fd_tiles.d;  // split-K units share the output tile
+  const int z = (int)p.fd_per.div((uint32_t)t);
+  const int r = t - z * (int)p.fd_per.d;
+  const int group = (int)p.fd_span.div((uint32_t)r);
   const int first_m = group * kGroupM;
   const int gm = min(kGroupM, p.m_tiles - first_m);
-  const int rr = r - group * kGroupM * p.n_tiles;
-  mb = first_m + rr % gm;
-  nb = rr / gm;
-  z1 = z / p.nb2;
+  const int rr = r - group * (int)p.fd_span.d;
+  if (gm == kGroupM) {
+    mb = first_m + (rr & (kGroupM - 1));
+    nb = rr / kGroupM;
+  } else {
+    mb = first_m + rr % gm;
+    nb = rr / gm;
+  }
+  z1 = (int)p.fd_nb2.div((uint32_t)z);
   z2 = z - z1 * p.nb2;
 }
 
@@ -746,24 +768,45 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               bulk_commit();
             }
             if (f_colsum) {
-              // column sums over this warp's valid rows, lane = column, read back from
-              // the staged tile while the TMA store drains it (both only read)
-              float cs[4] = {0.f, 0.f, 0.f, 0.f};
-              if (nrows == 32) {
+              // column sums of the staged tile (read while the TMA store drains it): lane
+              // = (row group g of 8 rows, column quad cq), the four groups folded by
+              // shuffles, then one 16-byte vector reduction per column quad
+              const int g = lane >> 3, cq = lane & 7;
+              float cs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  cs[i & 3] += d_f32 ? *reinterpret_cast<const float*>(s0 + swz_f32(i, lane))
-                                     : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
-              } else {
-#pragma unroll 4
-                for (int i = 0; i < nrows; ++i)
-                  cs[i & 3] += d_f32 ? *reinterpret_cast<const float*>(s0 + swz_f32(i, lane))
-                                     : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(s0 + swz_bf16(i, lane)));
+              for (int i = 0; i < 8; ++i) {
+                const int row = g * 8 + i;
+                if (row < nrows) {
+                  if (d_f32) {
+                    const float4 x = *reinterpret_cast<const float4*>(s0 + swz_f32(row, 4 * cq));
+                    cs4[0] += x.x; cs4[1] += x.y; cs4[2] += x.z; cs4[3] += x.w;
+                  } else {
+                    const uint2 x = *reinterpret_cast<const uint2*>(s0 + swz_bf16(row, 4 * cq));
+                    const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.x));
+                    const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.y));
+                    cs4[0] += lo.x; cs4[1] += lo.y; cs4[2] += hi.x; cs4[3] += hi.y;
+                  }
+                }
               }
-              if (col_ok)
-                atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col, (cs[0] + cs[1]) + (cs[2] + cs[3]));
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                cs4[j] += __shfl_xor_sync(0xffffffffu, cs4[j], 8);
+                cs4[j] += __shfl_xor_sync(0xffffffffu, cs4[j], 16);
+              }
+              const int cb = col0 + 4 * cq;
+              float* dst = p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + cb;
+              if (g == 0) {
+                if (cb + 3 < p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(cs4[0]), "f"(cs4[1]),
+                               "f"(cs4[2]), "f"(cs4[3])
+                               : "memory");
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (cb + j < p.N) atomicAdd(dst + j, cs4[j]);
+                }
+              }
             }
-
           }
         }
         bias_cur = bias_nxt;
@@ -1150,6 +1193,10 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   tiles *= p.k_splits;
   p.num_tiles = (int)tiles;
+  p.fd_tiles.set((uint32_t)(tiles / p.k_splits));
+  p.fd_per.set((uint32_t)(p.m_tiles * p.n_tiles));
+  p.fd_span.set((uint32_t)(kGroupM * p.n_tiles));
+  p.fd_nb2.set((uint32_t)p.nb2);
   p.d_f32 = a->d_dtype == SG_DTYPE_F32;
   p.D = a->D; p.ldd = a->ldd; p.sd1 = a->sd1; p.sd2 = a->sd2;
   p.vec_d = (reinterpret_cast<uintptr_t>(a->D) % 16) == 0 && (a->ldd * 2) % 16 == 0 && (a->sd1 * 2) % 16 == 0 &&

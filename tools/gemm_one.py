@@ -17,8 +17,8 @@ if which == "dmid":
     fn = lambda: K.gemm(a, b, o)  # noqa: E731
 elif which == "dmidg":
     a, b, o = r(M, h), r(4 * h, h).t(), torch.empty(M, 4 * h, device=dev, dtype=bf)
-    aux = r(M, 4 * h)
-    fn = lambda: K.gemm(a, b, o, act=K.ACT_DGELU, aux=aux)  # noqa: E731
+    aux, cs = r(M, 4 * h), torch.zeros(4 * h, device=dev)
+    fn = lambda: K.gemm(a, b, o, act=K.ACT_DGELU, aux=aux, colsum=cs)  # noqa: E731
 elif which == "fc1":
     a, b, o = r(M, h), r(h, 4 * h), torch.empty(M, 4 * h, device=dev, dtype=bf)
     mid, bias = torch.empty_like(o), torch.randn(4 * h, device=dev)
