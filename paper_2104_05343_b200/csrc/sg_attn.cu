@@ -63,6 +63,13 @@ __device__ __forceinline__ void tma4(const CUtensorMap* tm, void* dst, uint64_t*
     tma_load_4d(dst, tm, bar, inner, outer, z2, z1);
 }
 
+__device__ __forceinline__ void tma4_l2(const CUtensorMap* tm, int inner, int outer, int z2, int z1, int b2f) {
+  if (b2f)
+    tma_prefetch_l2_4d(tm, inner, z2, outer, z1);
+  else
+    tma_prefetch_l2_4d(tm, inner, outer, z2, z1);
+}
+
 __device__ __forceinline__ float ex2f_fast(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -1013,6 +1020,20 @@ __global__ void __launch_bounds__(384, 1)
         tma4(&tmV, sV + ks * kT64, &kv_full[ks], 0, kb * 128, h, b, p.v_b2_first);
         for (int i = 0; i < nqb; ++i, ++G) {
           const int slot = G & 1;
+          {
+            // Q / dO of block G + 2 into L2 now: with two smem slots its TMA load can only
+            // start when block G's products finish, shortly before it is needed
+            int i2 = i + 2, t2 = t, kb2 = kb, h2 = h, b2 = b;
+            while (i2 >= nqb) {
+              i2 -= nqb;
+              t2 += gridDim.x;
+            }
+            if (t2 != t && t2 < n_items) decode(t2, kb2, h2, b2);
+            if (t2 < n_items) {
+              tma4_l2(&tmQ, 0, i2 * 128, h2, b2, p.q_b2_first);
+              tma4_l2(&tmDO, 0, i2 * 128, h2, b2, p.do_b2_first);
+            }
+          }
           mbar_wait(&qd_empty[slot], ((G >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
           tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
