@@ -641,8 +641,6 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       for (int c = c_first; c < NCH; c += CSTEP) {
         const int col0 = nb * BN + c * 32;
         const bool active = col0 < p.N && nrows > 0;  // warp-uniform
-        const int col = col0 + lane;
-        const bool col_ok = col < p.N;
         if (vecp) bias_nxt = load_bias(c + CSTEP);
         // accumulator chunk, thread = row
         uint32_t r[32];
