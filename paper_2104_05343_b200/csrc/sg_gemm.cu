@@ -766,44 +766,40 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
               bulk_commit();
             }
             if (f_colsum) {
-              // column sums of the staged tile (read while the TMA store drains it): lane
-              // = (row group g of 8 rows, column quad cq), the four groups folded by
-              // shuffles, then one 16-byte vector reduction per column quad
-              const int g = lane >> 3, cq = lane & 7;
-              float cs4[4] = {0.f, 0.f, 0.f, 0.f};
+              // column sums by a register butterfly (reduce-scatter over the 32 row lanes:
+              // five xor-shuffle rounds halve the columns each lane carries, lane j ends
+              // with column j), of the fp32 values, rows past M masked; one coalesced
+              // 128-byte reduction per chunk
+              const bool full_rows = nrows == 32;
+              float w16[16];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int row = g * 8 + i;
-                if (row < nrows) {
-                  if (d_f32) {
-                    const float4 x = *reinterpret_cast<const float4*>(s0 + swz_f32(row, 4 * cq));
-                    cs4[0] += x.x; cs4[1] += x.y; cs4[2] += x.z; cs4[3] += x.w;
-                  } else {
-                    const uint2 x = *reinterpret_cast<const uint2*>(s0 + swz_bf16(row, 4 * cq));
-                    const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.x));
-                    const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.y));
-                    cs4[0] += lo.x; cs4[1] += lo.y; cs4[2] += hi.x; cs4[3] += hi.y;
-                  }
-                }
+              for (int j = 0; j < 16; ++j) {
+                const float a = full_rows || lane < nrows ? v[j] : 0.f;
+                const float b = full_rows || lane < nrows ? v[j + 16] : 0.f;
+                const bool hi = lane & 16;
+                w16[j] = (hi ? b : a) + __shfl_xor_sync(0xffffffffu, hi ? a : b, 16);
               }
+              float w8[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const bool hi = lane & 8;
+                w8[j] = (hi ? w16[j + 8] : w16[j]) + __shfl_xor_sync(0xffffffffu, hi ? w16[j] : w16[j + 8], 8);
+              }
+              float w4[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                cs4[j] += __shfl_xor_sync(0xffffffffu, cs4[j], 8);
-                cs4[j] += __shfl_xor_sync(0xffffffffu, cs4[j], 16);
+                const bool hi = lane & 4;
+                w4[j] = (hi ? w8[j + 4] : w8[j]) + __shfl_xor_sync(0xffffffffu, hi ? w8[j] : w8[j + 4], 4);
               }
-              const int cb = col0 + 4 * cq;
-              float* dst = p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + cb;
-              if (g == 0) {
-                if (cb + 3 < p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(cs4[0]), "f"(cs4[1]),
-                               "f"(cs4[2]), "f"(cs4[3])
-                               : "memory");
-                } else {
+              float w2[2];
 #pragma unroll
-                  for (int j = 0; j < 4; ++j)
-                    if (cb + j < p.N) atomicAdd(dst + j, cs4[j]);
-                }
+              for (int j = 0; j < 2; ++j) {
+                const bool hi = lane & 2;
+                w2[j] = (hi ? w4[j + 2] : w4[j]) + __shfl_xor_sync(0xffffffffu, hi ? w4[j] : w4[j + 2], 2);
               }
+              const bool hi = lane & 1;
+              const float cs = (hi ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, hi ? w2[0] : w2[1], 1);
+              if (col0 + lane < p.N) atomicAdd(p.colsum + (size_t)z1 * p.scs1 + (size_t)z2 * p.scs2 + col0 + lane, cs);
             }
           }
         }
