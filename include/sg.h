@@ -172,7 +172,9 @@ int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const vo
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);
 /* Multi-tensor form: every (w, bf16 twin, g) of a layer / model in one launch per
- * 96 tensors (the reference's per-parameter loop, layers.py:761-772). */
+ * 96 tensors (the reference's per-parameter loop, layers.py:761-772). g == NULL:
+ * w was already updated (its weight-gradient product reduce-added -lr dW into it),
+ * only the bf16 twin is refreshed. */
 typedef struct sg_sgd_item {
   float* w; void* w_bf16; const float* g;
   int64_t ldw, ldl, ldg, rows, cols;

@@ -1135,9 +1135,11 @@ __global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ 
       for (long long e = e0 + threadIdx.x * 4; e < e1; e += 1024) {
         const long long r = e / cols, cc = e - r * cols;
         float4 wv = *reinterpret_cast<float4*>(w + r * b.ldw[t] + cc);
-        const float4 gv = *reinterpret_cast<const float4*>(g + r * b.ldg[t] + cc);
-        wv.x -= b.lr * gv.x; wv.y -= b.lr * gv.y; wv.z -= b.lr * gv.z; wv.w -= b.lr * gv.w;
-        *reinterpret_cast<float4*>(w + r * b.ldw[t] + cc) = wv;
+        if (g) {  // (g == nullptr: w already updated, refresh its bf16 copy only)
+          const float4 gv = *reinterpret_cast<const float4*>(g + r * b.ldg[t] + cc);
+          wv.x -= b.lr * gv.x; wv.y -= b.lr * gv.y; wv.z -= b.lr * gv.z; wv.w -= b.lr * gv.w;
+          *reinterpret_cast<float4*>(w + r * b.ldw[t] + cc) = wv;
+        }
         if (wl) {
           __nv_bfloat162 lo = __floats2bfloat162_rn(wv.x, wv.y), hi = __floats2bfloat162_rn(wv.z, wv.w);
           uint2 pk;
@@ -1149,8 +1151,8 @@ __global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ 
     } else {
       for (long long e = e0 + threadIdx.x; e < e1; e += 256) {
         const long long r = e / cols, cc = e - r * cols;
-        const float v = w[r * b.ldw[t] + cc] - b.lr * g[r * b.ldg[t] + cc];
-        w[r * b.ldw[t] + cc] = v;
+        const float v = g ? w[r * b.ldw[t] + cc] - b.lr * g[r * b.ldg[t] + cc] : w[r * b.ldw[t] + cc];
+        if (g) w[r * b.ldw[t] + cc] = v;
         if (wl) wl[r * b.ldl[t] + cc] = __float2bfloat16_rn(v);
       }
     }
@@ -1372,7 +1374,7 @@ extern "C" int sg_sgd_multi(const sg_sgd_item* items, int n, float lr, void* str
     long long chunks = 0;
     for (int i = base; i < n && bt.n < kSgdMax; ++i) {
       const sg_sgd_item& it = items[i];
-      if (it.rows < 0 || it.cols < 0 || !it.w || !it.g) return set_error(SG_ERR_SHAPE, "sgd: bad item");
+      if (it.rows < 0 || it.cols < 0 || !it.w || (!it.g && !it.w_bf16)) return set_error(SG_ERR_SHAPE, "sgd: bad item");
       if (it.rows == 0 || it.cols == 0) continue;
       const int k = bt.n++;
       bt.w[k] = it.w;
@@ -1380,7 +1382,7 @@ extern "C" int sg_sgd_multi(const sg_sgd_item* items, int n, float lr, void* str
       bt.g[k] = it.g;
       bt.ldw[k] = it.ldw; bt.ldl[k] = it.ldl; bt.ldg[k] = it.ldg; bt.cols[k] = it.cols;
       bt.total[k] = it.rows * it.cols;
-      bt.vec4[k] = it.cols % 4 == 0 && it.ldw % 4 == 0 && it.ldg % 4 == 0 && (!it.w_bf16 || it.ldl % 4 == 0) &&
+      bt.vec4[k] = it.cols % 4 == 0 && it.ldw % 4 == 0 && (!it.g || it.ldg % 4 == 0) && (!it.w_bf16 || it.ldl % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(it.w) & 15) == 0 && (reinterpret_cast<uintptr_t>(it.g) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(it.w_bf16) & 7) == 0;
       bt.first_chunk[k] = chunks;

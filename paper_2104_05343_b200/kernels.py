@@ -339,20 +339,26 @@ def sgd(w, w_bf16, g, lr):
 
 
 def sgd_multi(triples, lr):
-    """w -= lr * g for every (w, w_bf16 | None, g) in one launch (multi-tensor SGD)."""
+    """w -= lr * g for every (w, w_bf16 | None, g) in one launch (multi-tensor SGD); g None:
+    w was already updated (by its weight-gradient product), only its bf16 copy is refreshed."""
     items = []
     stream = None
     for w, wl, g in triples:
         if w.dim() == 1:
-            w2, g2, l2 = w.view(1, -1), g.view(1, -1), None if wl is None else wl.view(1, -1)
+            w2, l2 = w.view(1, -1), None if wl is None else wl.view(1, -1)
+            g2 = None if g is None else g.view(1, -1)
         else:
             w2, g2, l2 = w, g, wl
-        if tuple(g2.shape) != tuple(w2.shape) or (l2 is not None and tuple(l2.shape) != tuple(w2.shape)):
+        if (g2 is not None and tuple(g2.shape) != tuple(w2.shape)) or \
+                (l2 is not None and tuple(l2.shape) != tuple(w2.shape)):
             raise ShapeError("sgd: parameter / gradient shapes differ")
+        if g2 is None and l2 is None:
+            continue
         rows, cols, ldw = _rows2d(w2)
         it = _lib.SgdItem()
         it.w, it.w_bf16, it.g = _p(w2), _p(l2), _p(g2)
-        it.ldw, it.ldl, it.ldg = ldw, (_rows2d(l2)[2] if l2 is not None else 0), _rows2d(g2)[2]
+        it.ldw, it.ldl, it.ldg = ldw, (_rows2d(l2)[2] if l2 is not None else 0), \
+            (_rows2d(g2)[2] if g2 is not None else 0)
         it.rows, it.cols = rows, cols
         items.append(it)
         stream = _stream(w) if stream is None else stream

@@ -642,17 +642,27 @@ def _bf16_of(x: ShardedMatrix, ws: Workspace) -> ShardedMatrix:
     return twin if twin is not None else as_bf16(x)
 
 
+def _weight_grad(a: ShardedMatrix, b: ShardedMatrix, w: ShardedMatrix, ws: Workspace, lr):
+    """dW = a^T b, or with ``lr`` (eager SGD on a local mesh) w -= lr a^T b in place by
+    the product's reduce-add epilogue (returns None: no gradient is materialised)."""
+    if lr is not None and a.mesh.is_local:
+        summa_atb(a, b, ws, accumulate_into=w, alpha=-lr)
+        return None
+    return summa_atb(a, b, ws, out_category="param_grad")
+
+
 def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: ShardedMatrix,
-                       w_dense: ShardedMatrix, cfg: ModelConfig, ws: Workspace, ln_ctx=None):
+                       w_dense: ShardedMatrix, cfg: ModelConfig, ws: Workspace, ln_ctx=None, lr=None):
     """(dx, dW_qkv, db_qkv, dW_dense, db_dense) (layers.py:424-465); ``ln_ctx`` is
-    the LayerNorm whose backward consumes dx (its statistics fused into dx's GEMM)."""
+    the LayerNorm whose backward consumes dx (its statistics fused into dx's GEMM);
+    ``lr``: weights updated in place by their gradient products (dW entries None)."""
     mesh = out_grad.mesh
     b_loc, n_loc = cfg.b // mesh.r, cfg.n // mesh.c
     hb = cfg.h // mesh.c
     dy16 = _bf16_of(out_grad, ws)
     _, b_dense_grad = bias_add_backward(out_grad, ws)
     dctx = summa_abt(dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
-    w_dense_grad = summa_atb(ctx.ctx_mat, dy16, ws, out_category="param_grad")
+    w_dense_grad = _weight_grad(ctx.ctx_mat, dy16, w_dense, ws, lr)
     bq_parts = new_colsum_parts(mesh, ws, 3 * hb)  # b_qkv gradient fused into dQ / dK / dV epilogues
     mesh.add_macs_all(4 * b_loc * n_loc * cfg.s * cfg.s * cfg.head_dim)  # dP, dV, dQ, dK (layers.py:457)
     dqkv_blocks = [None] * mesh.p
@@ -665,7 +675,7 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     dqkv.colsum_parts = bq_parts
     _, b_qkv_grad = bias_add_backward(dqkv, ws)
     x_grad = summa_abt(dqkv, w_qkv, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
-    w_qkv_grad = summa_atb(ctx.x_in, dqkv, ws, out_category="param_grad")
+    w_qkv_grad = _weight_grad(ctx.x_in, dqkv, w_qkv, ws, lr)
     return x_grad, w_qkv_grad, b_qkv_grad, w_dense_grad, b_dense_grad
 
 
@@ -698,9 +708,9 @@ def mlp_forward(x: ShardedMatrix, w1: ShardedMatrix, b1: RowHostedVector, w2: Sh
 
 
 def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2: ShardedMatrix,
-                 cfg: ModelConfig, ws: Workspace, ln_ctx=None):
+                 cfg: ModelConfig, ws: Workspace, ln_ctx=None, lr=None):
     """(dx, dW1, db1, dW2, db2) with GELU' fused into the dAct product (layers.py:494-508);
-    ``ln_ctx`` as in attention_backward."""
+    ``ln_ctx``, ``lr`` as in attention_backward."""
     mesh = out_grad.mesh
     dy16 = _bf16_of(out_grad, ws)
     _, b2_grad = bias_add_backward(out_grad, ws)
@@ -710,10 +720,10 @@ def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2
     dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
                      colsum=b1_parts)
     dmid.colsum_parts = b1_parts
-    w2_grad = summa_atb(ctx.act, dy16, ws, out_category="param_grad")
+    w2_grad = _weight_grad(ctx.act, dy16, w2, ws, lr)
     _, b1_grad = bias_add_backward(dmid, ws)
     x_grad = summa_abt(dmid, w1, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
-    w1_grad = summa_atb(ctx.x_in, dmid, ws, out_category="param_grad")
+    w1_grad = _weight_grad(ctx.x_in, dmid, w1, ws, lr)
     return x_grad, w1_grad, b1_grad, w2_grad, b2_grad
 
 
@@ -885,6 +895,8 @@ class TransformerLayer:
     fuses the residual-gradient adds into the two LayerNorm backward passes.
     """
 
+    fused_sgd = True  # backward(lr=...) updates the weight matrices inside their dW products
+
     def __init__(self, mesh: Mesh, cfg: ModelConfig, params: LayerParams, skip_dead_recompute: bool = False) -> None:
         self.mesh = mesh
         self.cfg = cfg
@@ -921,16 +933,19 @@ class TransformerLayer:
             out, mlp = mlp_forward(a2, p.w1, p.b1, p.w2, p.b2, cfg, ws, resid=y1)
         return out, LayerSaved(x_in=x, ln1=ln1, attn=attn, y1=y1, ln2=ln2, mlp=mlp, out=out)
 
-    def backward(self, out_grad: ShardedMatrix, saved: LayerSaved, ws: Workspace):
+    def backward(self, out_grad: ShardedMatrix, saved: LayerSaved, ws: Workspace, lr=None):
+        """Layer gradients; with ``lr`` (eager SGD) the four weight matrices are updated in
+        place by their gradient products and their LayerGrads entries are None."""
         cfg, mesh, p = self.cfg, self.mesh, self.params
         bsh_p = (cfg.b * cfg.s // mesh.r) * (cfg.h // mesh.c)
         for dev in mesh.local_devs:
             ws.release_forward(dev, (4 if self._last_was_skip else 5) * bsh_p)
-        da2, w1_g, b1_g, w2_g, b2_g = mlp_backward(out_grad, saved.mlp, p.w1, p.w2, cfg, ws, ln_ctx=saved.ln2)
+        da2, w1_g, b1_g, w2_g, b2_g = mlp_backward(out_grad, saved.mlp, p.w1, p.w2, cfg, ws, ln_ctx=saved.ln2,
+                                                   lr=lr)
         dy1, ln2_g, ln2_b = layernorm_backward(da2, saved.ln2, cfg, ws, resid=out_grad, want_bf16=True,
                                                want_colsum=True)
         da1, wqkv_g, bqkv_g, wd_g, bd_g = attention_backward(dy1, saved.attn, p.w_qkv, p.w_dense, cfg, ws,
-                                                             ln_ctx=saved.ln1)
+                                                             ln_ctx=saved.ln1, lr=lr)
         dx, ln1_g, ln1_b = layernorm_backward(da1, saved.ln1, cfg, ws, resid=dy1, want_bf16=True,
                                               want_colsum=True)
         return dx, LayerGrads(w_qkv=wqkv_g, b_qkv=bqkv_g, w_dense=wd_g, b_dense=bd_g, w1=w1_g, b1=b1_g, w2=w2_g,
@@ -947,10 +962,11 @@ class TransformerLayer:
         K.sgd_multi(triples, lr)
 
 
-def _sgd_triples_matrix(w: ShardedMatrix, g: ShardedMatrix) -> list:
+def _sgd_triples_matrix(w: ShardedMatrix, g: ShardedMatrix | None) -> list:
+    """(w, bf16 twin, g) per block; g None: w already updated, refresh the twin only."""
     twin = getattr(w, "bf16_twin", None)
-    return [(blk, None if twin is None else twin.blocks[k], g.blocks[k]) for k, blk in enumerate(w.blocks)
-            if blk is not None]
+    return [(blk, None if twin is None else twin.blocks[k], None if g is None else g.blocks[k])
+            for k, blk in enumerate(w.blocks) if blk is not None]
 
 
 def _sgd_triples_vector(v: RowHostedVector, g: RowHostedVector) -> list:

@@ -258,7 +258,10 @@ def checkpointed_backward(layers: Sequence, loss_grad, store: CheckpointStore, w
         fwd = getattr(layers[li], "recompute_forward", layers[li].forward)
         _, saved = fwd(x_in, ws)
         ws.reset_all("backward")
-        dx, g = layers[li].backward(dy, saved, ws)
+        if eager_update and getattr(layers[li], "fused_sgd", False):
+            dx, g = layers[li].backward(dy, saved, ws, lr=lr)  # weights updated by their dW products
+        else:
+            dx, g = layers[li].backward(dy, saved, ws)
         dy = clone_to_conjunction(dx, ws)
         store.discard(li)
         if eager_update:

@@ -291,7 +291,10 @@ class MeshModel:
             dy = dx
             for li in reversed(range(len(self.layers))):
                 ws.reset_all("backward")
-                dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws)
+                if eager_update and getattr(self.layers[li], "fused_sgd", False):
+                    dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws, lr=lr)
+                else:
+                    dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws)
                 if eager_update:
                     self.layers[li].apply_sgd(g, lr)
                 else:

@@ -358,11 +358,14 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
 
 
 def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free", tag: str = "summa", *,
-              out_dtype: torch.dtype = F32, accumulate_into: ShardedMatrix | None = None) -> ShardedMatrix:
+              out_dtype: torch.dtype = F32, accumulate_into: ShardedMatrix | None = None,
+              alpha: float = 1.0) -> ShardedMatrix:
     """C = A^T B: A(i,l) along row i, A_il^T B_ij, column-reduce to the owner of (l, j) (summa.py:143-164).
 
     ``accumulate_into`` adds the product to an existing weight-layout fp32
-    matrix (gradient accumulation) instead of allocating the output.
+    matrix (gradient accumulation) instead of allocating the output; with
+    ``alpha = -lr`` into the weight itself, that is the SGD step fused into the
+    weight-gradient product (in-place TMA reduce-add, local meshes).
     """
     mesh = check_same_mesh(a, b)
     if a.global_rows != b.global_rows:
@@ -388,8 +391,10 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                 for i in range(mesh.r):
                     prev = chain if (i > 0 or acc_in) else None
                     dst = out[k] if i == mesh.r - 1 else chain
-                    K.gemm(a16.block(i, l).t(), b16.block(i, j), dst, c=prev)
+                    K.gemm(a16.block(i, l).t(), b16.block(i, j), dst, c=prev, alpha=alpha)
         return out_mat
+    if alpha != 1.0:
+        raise ConfigError("summa_atb: alpha is supported on local meshes only")
     # dist pipeline: A(i, l+1) arrives while step l's partial product runs, and step
     # l's column reduce overlaps step l+1's product
     a_rx = _rx_slots(mesh, ws, (t_b, m_b))
