@@ -1080,21 +1080,23 @@ static int pick_bn(long long M, long long N, long long batch, int sms, int mode,
 }
 
 // Split-K factor for tile-starved products (e.g. the weight gradients, M x N =
-// h x h with K = b*s tokens, under 3/4 of a wave): the smallest split count whose (split, tile) work
-// units fill the SMs to >= 90%, each split keeping >= 8 k-blocks.
+// h x h with K = b*s tokens, under 3/4 of a wave): the split count minimising
+// waves x (k-blocks per unit x t_kb + t_epi), each split keeping >= 8 k-blocks. The
+// per-unit epilogue (a 256 x 256 fp32 reduce-add, ~4 us) is what makes many short
+// units lose to fewer long ones (measured h x h, K = 16k: 4 splits 33 us vs 9 splits 36 us).
 static int pick_splits(long long tiles, int k_blocks, int sms) {
   if (4 * tiles >= 3LL * sms) return 1;  // (measured: splitting a ~0.9-wave product loses to the reduce traffic)
+  constexpr double t_kb = 1.0, t_epi = 14.0;  // in units of one 256 x 256 x 64 pair MMA step (512 clocks)
   int best = 1;
-  double best_eff = wave_eff(tiles, sms);
+  double best_cost = (double)((tiles + sms - 1) / sms) * (k_blocks * t_kb + t_epi);
   for (int s = 2; s <= 16 && k_blocks / s >= 8; ++s) {
     const int per = (k_blocks + s - 1) / s;
     const int real = (k_blocks + per - 1) / per;
-    const double e = wave_eff(tiles * real, sms);
-    if (e > best_eff + 0.02) {
+    const double cost = (double)((tiles * real + sms - 1) / sms) * (per * t_kb + t_epi);
+    if (cost < best_cost * 0.98) {
       best = real;
-      best_eff = e;
+      best_cost = cost;
     }
-    if (best_eff >= 0.9) break;
   }
   return best;
 }
