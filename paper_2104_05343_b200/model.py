@@ -254,6 +254,8 @@ class MeshModel:
             for layer in self.layers:
                 x, saved = layer.forward(x, ws)
                 layer_saves.append(saved)
+        if getattr(x, "bf16_twin", None) is None and x.dtype != BF16:
+            x.bf16_twin = as_bf16(x)  # one cast, shared by the logits and the table-gradient products
         logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor)
         cls_ctx = None
