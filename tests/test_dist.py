@@ -187,6 +187,19 @@ def _gpu_worker(rank, world, port, rows, cols, out_dir):
         err["loss"] = abs(loss - ref_loss) / abs(ref_loss)
         g = model.gather_grads(grads)
         err["grads"] = max(rel(g[k], ref[k]) for k in g)
+        # eager SGD (train_step) on the process mesh equals gradients + apply_sgd there, and
+        # the same step on a local 1 x 1 mesh to bf16 accuracy
+        tok_t, lab_t = torch.as_tensor(tokens), torch.as_tensor(labels)
+        dm = sg.MeshModel(m, cfg, params)
+        dm.train_step(tok_t, lab_t, dm.make_workspace(), lr=0.25)
+        rm = sg.MeshModel(m, cfg, params)
+        _, rg, _, _ = sg.run_loss_and_grads(rm, tokens, labels)
+        rm.apply_sgd(rg, 0.25)
+        lm = sg.MeshModel(sg.create_mesh(sg.MeshConfig(rows=1, cols=1)), cfg, params)
+        lm.train_step(tok_t, lab_t, lm.make_workspace(), lr=0.25)
+        pd, pr, pl = dm.gather_params(), rm.gather_params(), lm.gather_params()
+        err["train_step"] = max(rel(pd[k], pr[k]) for k in pr)
+        err["train_step_vs_1x1"] = max(rel(pd[k], pl[k]) for k in pl)
         (out_dir / f"r{rank}.json").write_text(json.dumps(err))
     finally:
         dist.destroy_process_group()
@@ -201,3 +214,4 @@ def test_dist_backend_on_one_gpu(tmp_path, rows, cols):
         err = json.loads((tmp_path / f"r{rank}.json").read_text())
         assert err["ab"] < 1e-4 and err["abt"] < 1e-4 and err["atb"] < 1e-4, err
         assert err["loss"] < 1e-3 and err["grads"] < 2e-2, err
+        assert err["train_step"] < 1e-5 and err["train_step_vs_1x1"] < 2e-2, err
