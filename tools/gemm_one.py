@@ -1,4 +1,4 @@
-"""One step GEMM shape in isolation (ncu target): python tools/gemm_one.py {dmid|dmidg|fc1|qkv|dense} [reps]."""
+"""One step GEMM shape in isolation (ncu target): python tools/gemm_one.py {dmid|dmidg|dW1|fc1|qkv|dense} [reps]."""
 import sys
 
 import torch
@@ -19,6 +19,9 @@ elif which == "dmidg":
     a, b, o = r(M, h), r(4 * h, h).t(), torch.empty(M, 4 * h, device=dev, dtype=bf)
     aux, cs = r(M, 4 * h), torch.zeros(4 * h, device=dev)
     fn = lambda: K.gemm(a, b, o, act=K.ACT_DGELU, aux=aux, colsum=cs)  # noqa: E731
+elif which == "dW1":  # weight gradient x^T dmid (both operands MN-major), the step's top GEMM
+    a, b, o = r(M, h).t(), r(M, 4 * h), torch.empty(h, 4 * h, device=dev)
+    fn = lambda: K.gemm(a, b, o)  # noqa: E731
 elif which == "fc1":
     a, b, o = r(M, h), r(h, 4 * h), torch.empty(M, 4 * h, device=dev, dtype=bf)
     mid, bias = torch.empty_like(o), torch.randn(4 * h, device=dev)
