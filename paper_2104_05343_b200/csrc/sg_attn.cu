@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(256, 1)
 //   lse / D row statistics are prefetched a block ahead.
 // G counts query blocks over all of the CTA's items (barrier phases).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                       const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
   uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
   uint8_t* sDS = sP + 2 * kT64;       // 32 KB
-  uint8_t* sStg = sDS + 2 * kT64;     // 8 warps x 4 KB dQ staging
+  uint8_t* sStg = sDS + 2 * kT64;     // 4 drain warps x 8 KB (dQ fp32 / dK, dV bf16 staging)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 4096);
   int* items_tab = reinterpret_cast<int*>(bars + 32);  // this CTA's items as packed (kb, h, b)
   uint64_t* kv_full = bars;        // [2]
@@ -983,13 +983,13 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
       mbar_init(&dq_full[i], 1);
-      mbar_init(&dq_empty[i], 8);
+      mbar_init(&dq_empty[i], 4);
     }
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
     mbar_init(bufs_free, 1);
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 8);
+    mbar_init(acc_empty, 4);
     mbar_init(s_free, 8);
     fence_mbar_init();
   }
@@ -1006,8 +1006,17 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_begin();
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+  // registers per warpgroup (set at the top of each role): producer / MMA / idle 56,
+  // softmax 176, drain 96
+  auto item = [&](int it, int& kb, int& h, int& b) {
+    const int v = items_tab[it];
+    kb = v & 1023;
+    h = (v >> 10) & 1023;
+    b = v >> 20;
+  };
 
   if (warp == 0) {
+    reg_dealloc<56>();
     if (lane == 0) {
       int G = 0;
       for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
@@ -1042,6 +1051,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
+    reg_dealloc<56>();
     if (lane == 0) {
       constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
       constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
@@ -1104,21 +1114,17 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 4) {
-    // 8 warps: warp e owns TMEM lane quadrant e % 4 (32 query rows) and key half
+  } else if (warp < 4) {
+    reg_dealloc<56>();
+  } else if (warp < 12) {
+    reg_alloc<176>();
+    // 8 softmax warps: warp e owns TMEM lane quadrant e % 4 (32 query rows) and key half
     // e / 4 (64 of the 128 key columns = one 64-key atom of P / dS)
     const int e = warp - 4;
     const int q = e & 3, half = e >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sStg + e * 4096;
     const float scale = p.scale, scale_log2 = p.scale_log2;
-    auto item = [&](int it, int& kb, int& h, int& b) {
-      const int v = items_tab[it];
-      kb = v & 1023;
-      h = (v >> 10) & 1023;
-      b = v >> 20;
-    };
     // raw loads only: converting here would make the prefetch wait for the load
     auto row_stats = [&](int it, int i, float& lse, float& dd) {
       lse = dd = 0.f;
@@ -1131,40 +1137,9 @@ __global__ void __launch_bounds__(384, 1)
       lse = __ldg(p.lse + off);
       dd = __ldg(p.drow + off);
     };
-    // dQ columns [32 half, 32 half + 32) of query block i of local item it (global block
-    // G): TMEM -> fp32 staging -> TMA reduce-add, then release the buffer
-    auto drain_dq = [&](int G, int it, int i) {
-      const int slot = G & 1;
-      int kb, h, b;
-      item(it, kb, h, b);
-      mbar_wait(&dq_full[slot], (G >> 1) & 1);
-      tc_fence_after();
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-      uint32_t v[32];
-      tmem_ld32(t_dq + slot * 64 + lane_base + half * 32, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-            make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
-                        __uint_as_float(v[4 * k + 3]));
-      tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&dq_empty[slot]);
-        if (p.dq_b2_first)
-          tma_reduce_add_4d(&tmDQ, stg, half * 32, h, i * 128 + q * 32, b);
-        else
-          tma_reduce_add_4d(&tmDQ, stg, half * 32, i * 128 + q * 32, h, b);
-        bulk_commit();
-      }
-    };
     float lse_n, dd_n;
     row_stats(0, 0, lse_n, dd_n);
     int it = 0, i = 0;            // (item, query block) of G, advanced incrementally
-    int pit = 0, pi = 0;          // of G - 1 (its dQ drains this iteration)
     int kb = 0, h = 0, b = 0;
     if (my_items > 0) item(0, kb, h, b);
     for (int G = 0; G < total; ++G) {
@@ -1234,64 +1209,115 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      if (G > 0) drain_dq(G - 1, pit, pi);
-      pit = it;
-      pi = i;
       if (i == nqb - 1) {
-        // this item's dK, dV: TMEM (row = key) -> bf16 rows of the dQKV block, 32 columns per warp
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
+      }
+    }
+  } else {
+    // 4 drain warps (lane quadrant q = warp % 4, 32 rows): dQ of every block (TMEM ->
+    // fp32 staging -> TMA reduce-add) and, at each item's end, its dK / dV (TMEM ->
+    // bf16 staging -> TMA stores, bias-gradient column sums), off the softmax warps'
+    // critical path
+    reg_dealloc<96>();
+    const int q = warp & 3;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sStg + (warp - 12) * 8192;
+    int it = 0, i = 0, kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
+    for (int G = 0; G < total; ++G) {
+      const int slot = G & 1;
+      mbar_wait(&dq_full[slot], (G >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) bulk_wait_read<0>();  // the previous TMA operations have read the staging
+      __syncwarp();
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v[32];
+        tmem_ld32(t_dq + slot * 64 + lane_base + hf * 32, v);
+        tmem_wait_ld();
+        uint8_t* box = stg + hf * 4096;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
+                          __uint_as_float(v[4 * k + 3]));
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&dq_empty[slot]);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          if (p.dq_b2_first)
+            tma_reduce_add_4d(&tmDQ, stg + hf * 4096, hf * 32, h, i * 128 + q * 32, b);
+          else
+            tma_reduce_add_4d(&tmDQ, stg + hf * 4096, hf * 32, i * 128 + q * 32, h, b);
+        }
+        bulk_commit();
+      }
+      if (i == nqb - 1) {
+        // this item's dK, dV: bf16 rows -> 4 SW64 32 x 32 tiles (dK cols 0-31, 32-63, dV ...)
         mbar_wait(acc_full, it & 1);
         tc_fence_after();
-        uint32_t vk[32], vv[32];
-        tmem_ld32(t_dk + lane_base + half * 32, vk);
-        tmem_ld32(t_dv + lane_base + half * 32, vv);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
-        // bf16 rows -> the warp's staging slot (32 x 32 SW64 tiles: dK, then dV) -> two TMA
-        // stores (rows past s clipped); the previous dQ reduce-add has read the slot
-        if (lane == 0) bulk_wait_read<0>();
+        if (lane == 0) bulk_wait_read<0>();  // the dQ reduce-adds above have read the staging
         __syncwarp();
 #pragma unroll
         for (int which = 0; which < 2; ++which) {
-          const uint32_t* v = which == 0 ? vk : vv;
-          uint8_t* row = stg + which * 2048 + lane * 64;
 #pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) {
-            uint4 x;
-            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v[32];
+            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + hf * 32, v);
+            tmem_wait_ld();
+            uint8_t* row = stg + (which * 2 + hf) * 2048 + lane * 64;
 #pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2)
-              hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
-            *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
+            for (int k2 = 0; k2 < 4; ++k2) {
+              uint4 x;
+              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2)
+                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
+              *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
+            }
           }
         }
+        tc_fence_before();
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+          mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
           const int key0 = kb * 128 + q * 32;
-          if (p.dkv_b2_first) {
-            tma_store_4d(&tmDK, stg, half * 32, h, key0, b);
-            tma_store_4d(&tmDV, stg + 2048, half * 32, h, key0, b);
-          } else {
-            tma_store_4d(&tmDK, stg, half * 32, key0, h, b);
-            tma_store_4d(&tmDV, stg + 2048, half * 32, key0, h, b);
-          }
+#pragma unroll
+          for (int which = 0; which < 2; ++which)
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const CUtensorMap* tm = which == 0 ? &tmDK : &tmDV;
+              if (p.dkv_b2_first)
+                tma_store_4d(tm, stg + (which * 2 + hf) * 2048, hf * 32, h, key0, b);
+              else
+                tma_store_4d(tm, stg + (which * 2 + hf) * 2048, hf * 32, key0, h, b);
+            }
           bulk_commit();
         }
         if (p.kv_colsum) {
           // bias-gradient column sums of the staged bf16 tiles (rows past s hold zeros),
-          // lane = column, read while the TMA stores drain the same tiles
-          float sk[2] = {0.f, 0.f}, sv[2] = {0.f, 0.f};
+          // lane = column within each 32-column tile, read while the TMA stores drain them
 #pragma unroll
-          for (int i2 = 0; i2 < 32; ++i2) {
-            const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
-            sk[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(stg + off));
-            sv[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(stg + 2048 + off));
+          for (int t4 = 0; t4 < 4; ++t4) {
+            const uint8_t* tile = stg + t4 * 2048;
+            float acc2[2] = {0.f, 0.f};
+#pragma unroll
+            for (int i2 = 0; i2 < 32; ++i2) {
+              const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
+              acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
+            }
+            const int which = t4 >> 1, hf = t4 & 1;
+            atomicAdd(p.kv_colsum + which * p.nh * 64 + h * 64 + hf * 32 + lane, acc2[0] + acc2[1]);
           }
-          const int col = h * 64 + half * 32 + lane;
-          atomicAdd(p.kv_colsum + col, sk[0] + sk[1]);
-          atomicAdd(p.kv_colsum + p.nh * 64 + col, sv[0] + sv[1]);
         }
         i = 0;
         ++it;
@@ -1300,7 +1326,6 @@ __global__ void __launch_bounds__(384, 1)
         ++i;
       }
     }
-    if (total > 0) drain_dq(total - 1, pit, pi);
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
@@ -1363,7 +1388,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
     const int sms = sg_device_sm_count();
     if (grid.x > 1024 || nh > 1024 || b > 2047 || (items + (sms > 0 ? sms : 148) - 1) / (sms > 0 ? sms : 148) > kMaxItems)
       return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
-    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), SMEM2,
+    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(512), SMEM2,
              static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, tdk, tdv, p, (int)b);
   }
   count_launch();
