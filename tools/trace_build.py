@@ -46,19 +46,16 @@ ATTN = [
      "        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem\n        tc_fence_after();\n        if (trm) ftr(1, tri, 23);\n"),
     ("        umma_commit(&qd_empty[slot]);\n        if (G >= 2)",
      "        umma_commit(&qd_empty[slot]);\n        if (trm) ftr(1, tri, 24);\n        if (G >= 2)"),
-    ("    if (my_items > 0) item(0, kb, h, b);\n    for (int G = 0; G < total; ++G) {\n",
-     "    if (my_items > 0) item(0, kb, h, b);\n    const bool trs = blockIdx.x == 0 && e == 0 && lane == 0;\n"
+    ("    int kb = 0, h = 0, b = 0;\n    if (my_items > 0) item(0, kb, h, b);\n    for (int G = 0; G < total; ++G) {\n",
+     "    int kb = 0, h = 0, b = 0;\n    if (my_items > 0) item(0, kb, h, b);\n"
+     "    const bool trs = blockIdx.x == 0 && e == 0 && lane == 0;\n"
      "    int tri = 0;\n    for (int G = 0; G < total; ++G) {\n      if (trs) ftr(0, tri, 0);\n"),
     ("      mbar_wait(s_full, G & 1);\n      tc_fence_after();\n",
      "      mbar_wait(s_full, G & 1);\n      tc_fence_after();\n      if (trs) ftr(0, tri, 1);\n"),
     ("      // the previous block's dV / dK / dQ products have finished reading P / dS\n",
      "      if (trs) ftr(0, tri, 4);\n      // the previous block's dV / dK / dQ products have finished reading P / dS\n"),
-    ("      if (lane == 0) mbar_arrive(ds_full);\n      if (G > 0) drain_dq(G - 1, pit, pi);\n",
-     "      if (lane == 0) mbar_arrive(ds_full);\n      if (trs) ftr(0, tri, 6);\n"
-     "      if (G > 0) drain_dq(G - 1, pit, pi);\n      if (trs) ftr(0, tri, 7);\n"),
-    ("        mbar_wait(acc_full, it & 1);\n        tc_fence_after();\n        uint32_t vk[32], vv[32];\n",
-     "        mbar_wait(acc_full, it & 1);\n        tc_fence_after();\n        if (trs) ftr(0, tri, 8);\n"
-     "        uint32_t vk[32], vv[32];\n"),
+    ("      if (lane == 0) mbar_arrive(ds_full);\n      if (i == nqb - 1) {",
+     "      if (lane == 0) mbar_arrive(ds_full);\n      if (trs) ftr(0, tri, 6);\n      if (i == nqb - 1) {"),
 ]
 
 GEMM = [
