@@ -117,6 +117,9 @@ template <int EW>
 struct EpiCfg {
   static constexpr int kThreads = 128 + 32 * EW;
   static constexpr int CSTEP = EW / 4;
+  // 12 epilogue warps (512 threads, 128 registers at launch): the producer / MMA
+  // warpgroup gives registers up and the epilogue warpgroups take them (setmaxnreg)
+  static constexpr bool kRealloc = EW == 12;
 };
 // Per epilogue warp 8 KB of staging: two 4 KB slots (main tile up to 4 KB, or a
 // 2 KB bf16 main tile + 2 KB bf16 side tile) so chunk c+1 never waits for chunk
@@ -138,7 +141,7 @@ struct GemmCfg {
   static constexpr uint32_t A_BYTES = kBM * kBK * 2;
   static constexpr uint32_t B_BYTES = BNL * kBK * 2;
   static constexpr int STAGES =
-      PAIR ? (EW == 8 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 6 : 8))
+      PAIR ? (EW == 12 ? (BN == 256 ? 4 : 5) : EW == 8 ? (BN == 256 ? 5 : 6) : (BN == 256 ? 6 : 8))
            : (EW == 8 ? (BN == 256 ? 3 : 4) : (BN == 512 ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8))));
   static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + EW * (kStgBytes + 128) + 512;
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
   pdl_begin();  // prologue above overlaps the previous kernel; inputs are read below
 
   if (warp == 0) {
+    if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
     if (lane == 0) {
       // ------------------------------------------------------------ producer
       uint32_t stage = 0, phase = 0;
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       }
     }
   } else if (warp == 1) {
+    if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
     if (lane == 0 && rank == 0) {
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t IDESC = umma_idesc_bf16(TM, Cfg::MMA_N, A_MN, B_MN);
@@ -501,7 +506,10 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
           umma_commit(&tfull[as]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
+  } else {
+    if constexpr (EpiCfg<EW>::kRealloc) reg_alloc<152>();
     // -------------------------------------------------------------- epilogue
     // epilogue warp e owns TMEM lane quadrant q = e % 4 (tile rows 32q .. 32q+31,
     // a hardware restriction: warp w reads lanes 32 (w % 4) ..) and the chunks
@@ -1290,6 +1298,14 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     else if (a->act == SG_ACT_NONE && !c_in && !a->colsum)
       kind = a->bias ? EK_BIAS : EK_STORE;
   }
+  // GELU' + column sums is the one epilogue-bound product at the step's shapes: 12
+  // epilogue warps (3 per TMEM lane quadrant) for it; SG_GEMM_EW12=0 disables
+  static const int env_ew12 = [] {
+    const char* e = getenv("SG_GEMM_EW12");
+    return e ? atoi(e) : 1;
+  }();
+  if (pair && bn == 256 && kind == EK_DGELU && !amn && !bmn && env_ew12 && force_ew != 4 && force_ew != 8)
+    return launch_gemm<256, false, false, 12, true, EK_DGELU>(m, p, s, grid);
   if (pair) {
     if (bn == 128)
       return ew8 ? dispatch_major<128, 8, true>(amn, bmn, m, p, s, grid, kind)
