@@ -197,3 +197,35 @@ def test_gemm_layernorm_stats(M, N, K):
     sep = torch.empty(M, 2, device="cuda")
     k.ln_bwd_stats(dy, x, mean, rstd, gamma, sep)
     assert _rel(stats, sep) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", [(700, 520, 256), (4096, 4096, 1024), (1000, 4100, 320)])
+def test_gemm_dgelu_colsum_abt(M, N, K):
+    """GELU' + column sums on the dX layout (both operands K-major): the 12-warp
+    epilogue at pair tiles, ragged edges included, against a PyTorch fp32 reference."""
+    k = _k()
+    torch.manual_seed(9)
+    a, w = _rand(M, K), _rand(N, K)
+    mid = _rand(M, N, scale=2.0)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.zeros(N, device="cuda")
+    k.gemm(a, w.t(), out, act=k.ACT_DGELU, aux=mid, colsum=cs)
+    xm = mid.float()
+    t = torch.tanh(math.sqrt(2 / math.pi) * (xm + 0.044715 * xm ** 3))
+    dg = 0.5 * (1 + t) + 0.5 * xm * (1 - t * t) * math.sqrt(2 / math.pi) * (1 + 3 * 0.044715 * xm ** 2)
+    ref = (a.float() @ w.float().t()) * dg
+    assert _rel(out, ref) < 1e-2
+    assert _rel(cs, ref.sum(0)) < 1e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 16384), (1024, 4096, 16384), (300, 260, 4096)])
+def test_gemm_in_place_update_with_alpha(M, N, K):
+    """w += alpha a^T b in place (the fused SGD step, split-K partials reduce-added with
+    alpha applied per split) against w + alpha (a^T b) in fp32."""
+    k = _k()
+    torch.manual_seed(10)
+    a, b = _rand(K, M), _rand(K, N)
+    w = torch.randn(M, N, device="cuda")
+    want = w + (-0.125) * (a.float().t() @ b.float())
+    k.gemm(a.t(), b, w, c=w, alpha=-0.125)
+    assert _rel(w, want) < 5e-5  # fp32 accumulation order over K = 16384
