@@ -4,23 +4,24 @@
 // `a @ b` via mesh.py:349-361) and of the per-head attention products of
 // layers.py:404-459.
 //
-// CTA layout (384 threads, 1 CTA per SM, grid = min(#tiles, #SMs)):
+// CTA layout (256 / 384 / 512 threads, 1 CTA per SM, grid = min(#tiles, #SMs), or
+// CTA pairs (cluster of 2, cta_group::2) for 256 x {128, 256} tiles):
 //   warp 0      TMA producer (one lane): A/B tiles -> SWIZZLE_128B smem ring
-//   warp 1      MMA issuer (one lane): tcgen05.mma 128 x min(BN,256) x 16 into TMEM
+//   warp 1      MMA issuer (one lane, the pair's leader): tcgen05.mma into TMEM
 //   warp 2      TMEM allocator
-//   warps 4..11 epilogue; warp w owns TMEM lane quadrant (w % 4) = 32 tile rows and
-//               every other 32-column chunk, so two warps share a quadrant
+//   warps 4..   4, 8 or 12 epilogue warps; warp w owns TMEM lane quadrant (w % 4)
+//               = 32 tile rows and every (EW / 4)-th 32-column chunk
 // Two TMEM accumulator buffers (one when BN = 512) let the epilogue of tile i
 // overlap the MMAs of tile i+1; the smem ring has STAGES slots guarded by
 // full/empty mbarriers.
 //
 // Epilogue modes:
 //   NORMAL       tcgen05.ld (thread = row, 32 columns) -> alpha, bias, +C, GELU
-//                (saves the pre-activation) or GELU', bf16/fp32 D, optional
-//                bf16 copy D2 — 16-byte vector row accesses, every load of a
-//                chunk issued before its stores (C may alias D); optional
-//                column sums (bias gradients) via a swizzled smem transpose and
-//                one atomic per column per warp.
+//                (saves the pre-activation) or GELU', LayerNorm-backward row
+//                statistics, bf16/fp32 D, optional bf16 copy D2, optional column
+//                sums (bias gradients, register butterfly); inputs (C / aux) and
+//                outputs move through swizzled smem staging by TMA, C == D
+//                accumulates in place by TMA reduce-add (split-K, fused SGD).
 //   SOFTMAX      D = softmax_row(alpha * acc) over the whole row (N <= 512 fits
 //                TMEM): attention probabilities without an fp32 score matrix.
 //   SOFTMAX_BWD  D = aux * (acc - rowsum(acc * aux)) * alpha with aux = P:
@@ -110,9 +111,9 @@ enum EpiKind : int {
   EK_DGELU = 5,     // D = acc * gelu'(aux) [+ column sums]
   EK_LN = 6,        // fp32 D = acc, LayerNorm-backward row statistics (C = x)
 };
-// Epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
-// taking every other 32-column chunk) for epilogues without global inputs,
-// where the epilogue otherwise paces the tensor pipe at small K.
+// Epilogue warps: 4 (one per TMEM lane quadrant), 8 (two per quadrant, each taking
+// every other 32-column chunk) where the epilogue otherwise paces the tensor pipe
+// at small K, or 12 for the epilogue-bound GELU' + column-sum product.
 template <int EW>
 struct EpiCfg {
   static constexpr int kThreads = 128 + 32 * EW;
