@@ -919,10 +919,12 @@ __global__ void __launch_bounds__(256, 1)
 //         products — across item boundaries too (K / V double-buffered per item);
 //         dQ alternates between two TMEM buffers
 //   warps 4-11 (lane quadrant x key half) compute P / dS for their 64 keys in
-//         registers, wait only for the previous products to release the smem
-//         tiles, drain dQ (TMEM -> smem -> TMA reduce-add) one block behind, and
-//         at an item's end write its dK / dV and release the TMEM accumulators
-//   lse / D row statistics are prefetched a block ahead.
+//         registers and wait only for the previous products to release the smem
+//         tiles; lse / D row statistics are prefetched a block ahead
+//   warps 12-15 (one per lane quadrant) drain dQ (TMEM -> smem -> TMA reduce-add)
+//         and at an item's end write its dK / dV (TMA stores, bias-gradient column
+//         sums) and release the TMEM accumulators
+//   setmaxnreg: producer / MMA warpgroup 56 registers, softmax 176, drain 96.
 // G counts query blocks over all of the CTA's items (barrier phases).
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(512, 1)
