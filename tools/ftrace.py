@@ -1,4 +1,4 @@
-"""Phase timeline of the flash backward (trace build only: libsg_trace.so with
+"""Phase timeline of the flash backward (instrumented build from tools/trace_build.py: libsg_trace.so with
 sg_debug_ftrace): CTA 0, softmax warp 4 lane 0 (buffer 0) and the MMA thread (buffer 1)."""
 import ctypes
 import os

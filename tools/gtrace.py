@@ -1,4 +1,4 @@
-"""Epilogue phase timeline of sg_gemm (trace build only: libsg_trace.so with
+"""Epilogue phase timeline of sg_gemm (instrumented build from tools/trace_build.py: libsg_trace.so with
 sg_debug_gtrace): CTA 0 epilogue warp 4 lane 0 (buffer 0), MMA thread (buffer 1).
     python tools/gtrace.py CASE   (CASE as in tools/gemm_one.py)"""
 import ctypes
