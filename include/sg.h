@@ -168,6 +168,10 @@ int sg_embed_fwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const vo
                  int64_t hc, void* out, int odt, int64_t ldo, void* stream);
 int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const void* dout, int ddt, int64_t ldd,
                  int64_t hc, float* grad, int64_t ldg, void* stream);
+/* Device-side id range check (layers.py:164-165 tokens, layers.py:552-553 labels):
+ * *flag |= 1 when any of the n ids lies outside [0, v). The host reads the flag at
+ * its next synchronisation (the loss read-back) and raises ConfigError. */
+int sg_check_ids(const int64_t* ids, int64_t n, int64_t v, int* flag, void* stream);
 /* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);

@@ -77,6 +77,7 @@ SIGNATURES: dict[str, tuple] = {
     "sg_xent_bwd": (i32, [vp, i32, i64, i64, i64, i64, vp, i64, vp, vp, ctypes.c_float, vp, i32, i64, vp]),
     "sg_embed_fwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i32, i64, vp]),
     "sg_embed_bwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i64, vp]),
+    "sg_check_ids": (i32, [vp, i64, i64, vp, vp]),
     "sg_dgelu": (i32, [vp, i64, vp, i64, i64, i64, vp, i32, i64, vp, vp]),
     "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
     "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),

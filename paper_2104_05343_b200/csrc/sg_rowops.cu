@@ -215,7 +215,7 @@ __global__ void ln_fwd_kernel(const TX* __restrict__ x, long long rows, int cols
       s2 = warp_sum(s2);
     }
     const float mu = s1 * inv_h;
-    const float var = s2 * inv_h - mu * mu;  // one-pass variance, layers.py:296-297
+    const float var = fmaxf(s2 * inv_h - mu * mu, 0.f);  // one-pass variance (layers.py:296-297), clamped: fp32 cancellation on near-constant rows
     const float rs = 1.0f / sqrtf(var + eps);
     for (int c = lane * 8; c < cols; c += 256) {
       const int n = min(8, cols - c);
@@ -742,6 +742,19 @@ __global__ void embed_fwd_kernel(const int64_t* __restrict__ ids, long long n, l
   }
 }
 
+// *flag |= 1 when any id lies outside [0, v): the device-side form of the reference's
+// range checks (layers.py:164-165 token ids, layers.py:552-553 labels), read back by
+// the host at the next synchronisation point instead of stalling the step.
+__global__ void check_ids_kernel(const int64_t* __restrict__ ids, long long n, long long v, int* flag) {
+  pdl_begin();
+  bool bad = false;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long id = ids[t];
+    bad |= (id < 0) | (id >= v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // grad[ids[t] - lo, :] += dout[t, :] for ids in the block; repeated ids accumulate (layers.py:202-205)
 template <typename TD>
 __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, long long lo, long long vb,
@@ -988,7 +1001,7 @@ __global__ void __launch_bounds__(256, NV <= 4 ? 4 : 1) ln_fwd_rows_kernel(
         s2 = warp_sum(s2);
       }
       mu[u] = s1 * inv_h;
-      const float var = s2 * inv_h - mu[u] * mu[u];  // one-pass variance, layers.py:296-297
+      const float var = fmaxf(s2 * inv_h - mu[u] * mu[u], 0.f);  // one-pass variance (layers.py:296-297), clamped
       rs[u] = 1.0f / sqrtf(var + eps);
     }
 #pragma unroll
@@ -1352,6 +1365,15 @@ extern "C" int sg_embed_fwd(const int64_t* ids, int64_t n, int64_t lo, int64_t v
     return set_error(SG_ERR_SHAPE, "embed_fwd: unaligned");
   if (n == 0) return SG_OK;
   SG_DISPATCH_T(tdt, TT, SG_DISPATCH_T(odt, TO, (launch_k(embed_fwd_kernel<TT, TO>, dim3(grid_for(n, 8)), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TT*>(table), ldt, (int)hc, static_cast<TO*>(out), ldo))));
+  return launch_check();
+}
+
+extern "C" int sg_check_ids(const int64_t* ids, int64_t n, int64_t v, int* flag, void* stream) {
+  clear_error();
+  if (n < 0 || v < 1 || !flag) return set_error(SG_ERR_CONFIG, "check_ids: bad arguments");
+  if (n == 0) return SG_OK;
+  launch_k(check_ids_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, 1184)), dim3(256), 0, S(stream), ids,
+           (long long)n, (long long)v, flag);
   return launch_check();
 }
 

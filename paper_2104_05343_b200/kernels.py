@@ -401,8 +401,16 @@ def fold(dst, srcs, accumulate=False, op_max=False):
         if f.numel() != d.numel() or s.dtype != dst.dtype or tuple(s.shape) != tuple(dst.shape):
             raise ShapeError("fold sources must match the destination")
         ss.append(f)
-    arr = (ctypes.c_void_p * max(1, len(ss)))(*[s.data_ptr() for s in ss])
-    _call("sg_fold", _p(d), _dt(d), arr, len(ss), d.numel(), int(accumulate), int(op_max), _stream(d))
+    # the kernel takes at most 8 sources per launch; longer groups (p > 8 meshes) fold
+    # in list-order chunks, each chunk after the first accumulating into dst
+    for k in range(0, max(1, len(ss)), _FOLD_MAX):
+        chunk = ss[k:k + _FOLD_MAX]
+        arr = (ctypes.c_void_p * max(1, len(chunk)))(*[s.data_ptr() for s in chunk])
+        _call("sg_fold", _p(d), _dt(d), arr, len(chunk), d.numel(), int(accumulate or k > 0), int(op_max),
+              _stream(d))
+
+
+_FOLD_MAX = 8
 
 
 def epilogue(x, out, *, bias=None, c=None, act=ACT_NONE, aux=None, alpha=1.0):
@@ -451,3 +459,8 @@ def flash_attn_bwd(qkv, dout, lse, drow, b, s, n_heads, d, dq_acc, dqkv, kv_cols
         raise ShapeError("flash_attn_bwd: kv_colsum must be a contiguous fp32 [2 * nh * d]")
     _call("sg_flash_attn_bwd", _p(qkv), ldq, _p(dout), lddo, _p(lse), _p(drow), b, s, n_heads, d, _p(dq_acc), lddq,
           _p(dqkv), ldg, _p(kv_colsum), _stream(dqkv))
+
+
+def check_ids(ids, v: int, flag):
+    """flag (int32 [1]) |= 1 when any of ``ids`` lies outside [0, v) (sg_check_ids)."""
+    _call("sg_check_ids", _p(ids), ids.numel(), v, _p(flag), _stream(flag))

@@ -194,9 +194,24 @@ def _token_block(tokens, row: int, r: int):
     return tokens[row * bb:(row + 1) * bb].reshape(-1)
 
 
-def _check_ids(ids, v: int, what: str) -> None:
+def _check_ids(ids, v: int, what: str, flag: torch.Tensor | None = None) -> None:
+    """ConfigError unless every id lies in [0, v) (layers.py:164-165, 552-553).
+
+    Host ids are checked on the host. Device ids are checked by a device kernel
+    (sg_check_ids): with ``flag`` (int32 [1] on the device) the result is only
+    OR-ed into it and read at the caller's next synchronisation (the step's loss
+    read-back, MeshModel.check_inputs), otherwise it is read back here."""
     if isinstance(ids, torch.Tensor) and ids.is_cuda:
-        return  # device ids are validated by the caller (avoids a host sync in the step)
+        flat = ids.reshape(-1)
+        if flat.dtype != torch.int64 or not flat.is_contiguous():
+            flat = flat.to(torch.int64).contiguous()
+        own = flag is None
+        if own:
+            flag = torch.zeros(1, dtype=torch.int32, device=ids.device)
+        K.check_ids(flat, v, flag)
+        if own and int(flag.item()):
+            raise ConfigError(f"{what} must lie in [0, {v})")
+        return
     arr = np.asarray(ids.cpu() if isinstance(ids, torch.Tensor) else ids)
     if arr.size and (arr.min() < 0 or arr.max() >= v):
         raise ConfigError(f"{what} must lie in [0, {v})")
@@ -228,7 +243,8 @@ def embedding_forward(tokens, table: ShardedMatrix, cfg: ModelConfig, ws: Worksp
     mesh = table.mesh
     r, c = mesh.r, mesh.c
     v_pad = cfg.v_padded(mesh)
-    _check_ids(tokens, cfg.v, "token ids")
+    if ids is None:  # callers passing ``ids`` validated them (MeshModel.forward)
+        _check_ids(tokens, cfg.v, "token ids")
     vb, hb = v_pad // c, cfg.h // c
     bs_loc = (cfg.b // r) * cfg.s
     ids = _device_ids(mesh, tokens) if ids is None else ids
@@ -789,7 +805,8 @@ def cross_entropy_forward(logits: ShardedMatrix, labels, cfg: ModelConfig, ws: W
     r, c = mesh.r, mesh.c
     v_pad = cfg.v_padded(mesh)
     vb = v_pad // c
-    _check_ids(labels, cfg.v, "labels")
+    if label_ids is None:  # callers passing ``label_ids`` validated them (MeshModel.forward)
+        _check_ids(labels, cfg.v, "labels")
     labs = _device_ids(mesh, labels) if label_ids is None else label_ids
     rows = logits.block_rows
     lmax, gmax, packed, loss_rows, part, n_real = ([None] * mesh.p for _ in range(6))

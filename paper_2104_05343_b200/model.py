@@ -178,6 +178,7 @@ class MeshModel:
         self.cfg = cfg
         self.classifier = classifier
         self.logits_dtype = logits_dtype
+        self._bad_ids: torch.Tensor | None = None  # device-side id range-check flag
         c = mesh.c
         v_pad = cfg.v_padded(mesh)
         if global_params is None:
@@ -244,7 +245,7 @@ class MeshModel:
             raise ConfigError("classifier enabled but cls_labels missing")
         ws.reset_all("forward")
         ws.reset_all("free")
-        ids = _device_ids(self.mesh, tokens)
+        ids, label_ids = self._validated_ids(tokens, labels)
         x = embedding_forward(tokens, self.table, cfg, ws, out_category="forward", ids=ids)
         layer_saves = None
         if store is not None:
@@ -257,7 +258,10 @@ class MeshModel:
         if getattr(x, "bf16_twin", None) is None and x.dtype != BF16:
             x.bf16_twin = as_bf16(x)  # one cast, shared by the logits and the table-gradient products
         logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
-        loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor)
+        loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor,
+                                             label_ids=label_ids)
+        if not return_tensor:
+            self.check_inputs()  # the loss read-back already synchronised
         cls_ctx = None
         if self.classifier:
             cls_loss, cls_ctx = self._cls_forward(x, cls_labels, ws)
@@ -265,8 +269,30 @@ class MeshModel:
         return loss, ModelSaved(tokens=tokens, labels=labels, x_final=x, ce_ctx=ce_ctx, layer_saves=layer_saves,
                                 store=store, ids=ids, cls_ctx=cls_ctx)
 
+    # ------------------------------------------------------------------ input validation
+    def _validated_ids(self, tokens, labels):
+        """Per-position device ids of tokens and labels, range-checked against v
+        (layers.py:164-165, 552-553): host arrays on the host (ConfigError now),
+        device tensors by a device kernel into ``self._bad_ids`` (no host sync in
+        the step; ConfigError at the next check_inputs / float loss read-back)."""
+        from .layers import _check_ids
+
+        if self._bad_ids is None:
+            self._bad_ids = torch.zeros(1, dtype=torch.int32, device=self.mesh.device())
+        for arr, what in ((tokens, "token ids"), (labels, "labels")):
+            _check_ids(arr, self.cfg.v, what, flag=self._bad_ids if isinstance(arr, torch.Tensor) and arr.is_cuda
+                       else None)
+        return _device_ids(self.mesh, tokens), _device_ids(self.mesh, labels)
+
+    def check_inputs(self) -> None:
+        """Raise ConfigError if a device-side id check of an earlier step failed (one
+        host synchronisation); clears the flag."""
+        if self._bad_ids is not None and int(self._bad_ids.item()):
+            self._bad_ids.zero_()
+            raise ConfigError(f"token ids / labels must lie in [0, {self.cfg.v})")
+
     def backward(self, saved: ModelSaved, ws: Workspace, upstream: float = 1.0, eager_update: bool = False,
-                 lr: float = 0.0) -> ModelGrads:
+                 lr: float = 0.0, *, _fused_sgd_lr: float | None = None) -> ModelGrads:
         """Gradients of every parameter (model.py:326-354); the tied table gets
         lm-head dW plus the embedding scatter-add, accumulated in place."""
         cfg, mesh = self.cfg, self.mesh
@@ -289,16 +315,19 @@ class MeshModel:
             dx0, layer_grads = checkpointed_backward(self.layers, dx, saved.store, ws, eager_update=eager_update,
                                                      lr=lr)
         else:
+            # the reference's non-checkpointed backward ignores eager_update: it returns every
+            # layer gradient and leaves the parameters alone (model.py:343-351); the fused
+            # update is train_step's (``_fused_sgd_lr``)
             layer_grads = [None] * len(self.layers)
             dy = dx
             for li in reversed(range(len(self.layers))):
                 ws.reset_all("backward")
-                if eager_update and getattr(self.layers[li], "fused_sgd", False):
-                    dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws, lr=lr)
+                if _fused_sgd_lr is not None and getattr(self.layers[li], "fused_sgd", False):
+                    dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws, lr=_fused_sgd_lr)
                 else:
                     dy, g = self.layers[li].backward(dy, saved.layer_saves[li], ws)
-                if eager_update:
-                    self.layers[li].apply_sgd(g, lr)
+                if _fused_sgd_lr is not None:
+                    self.layers[li].apply_sgd(g, _fused_sgd_lr)
                 else:
                     layer_grads[li] = g
             dx0 = dy
@@ -381,10 +410,12 @@ class MeshModel:
 
     def train_step(self, tokens, labels, ws: Workspace, lr: float, checkpointing: bool = False,
                    cls_labels=None) -> torch.Tensor:
-        """One fwd + bwd + SGD step with no host synchronisation; returns the loss tensor."""
+        """One fwd + bwd + SGD step with no host synchronisation; returns the loss tensor.
+        Device token / label ids are range-checked on the device: ``check_inputs()``
+        raises ConfigError for a step that saw an out-of-range id."""
         store = CheckpointStore(self.mesh.p) if checkpointing else None
         loss, saved = self.forward(tokens, labels, ws, store=store, return_tensor=True, cls_labels=cls_labels)
-        grads = self.backward(saved, ws, eager_update=True, lr=lr)
+        grads = self.backward(saved, ws, eager_update=True, lr=lr, _fused_sgd_lr=None if checkpointing else lr)
         sgd_matrix(self.table, grads.table, lr)
         self._cls_sgd(grads, lr)
         return loss
@@ -396,18 +427,33 @@ class MeshModel:
         cfg = self.cfg
         if tuple(tokens.shape) != (cfg.b, cfg.s):
             raise ShapeError(f"tokens must be [{cfg.b}, {cfg.s}], got {tuple(tokens.shape)}")
-        ids = _device_ids(self.mesh, tokens)
+        ids, label_ids = self._validated_ids(tokens, labels)
         x = embedding_forward(tokens, self.table, cfg, ws, out_category="forward", ids=ids)
         for layer in self.layers:
             x, _ = layer.forward(x, ws)
         logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
-        loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True)
+        loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True, label_ids=label_ids)
         return loss
 
     # ------------------------------------------------------------------ checkpoint file
     def save(self, path) -> None:
-        """Gather the parameters and write them in the reference checkpoint format."""
-        save_checkpoint(path, self.cfg, self.gather_params(), classifier=self.classifier)
+        """Gather the parameters and write them in the reference checkpoint format.
+
+        The gather is collective (every process takes part); on the dist backend only
+        rank 0 writes, to a temporary file renamed into place, and every rank waits at
+        a barrier so no process can read a partially written file."""
+        import os
+
+        params = self.gather_params()
+        rank0 = self.mesh.is_local or _dist_rank() == 0
+        if rank0:
+            tmp = f"{os.fspath(path)}.tmp{os.getpid()}"
+            save_checkpoint(tmp, self.cfg, params, classifier=self.classifier)
+            os.replace(tmp, path)
+        if not self.mesh.is_local:
+            import torch.distributed as dist
+
+            dist.barrier()
 
     @classmethod
     def load(cls, path, mesh: Mesh, **kw) -> "MeshModel":
@@ -436,6 +482,12 @@ class MeshModel:
             out["cls_w"] = RowHostedVector([None if w is None else w.reshape(-1) for w in grads.cls_w]) \
                 .gathered().reshape(cfg.h, 2)
         return out
+
+
+def _dist_rank() -> int:
+    import torch.distributed as dist
+
+    return dist.get_rank() if dist.is_initialized() else 0
 
 
 def _gather_layer(pre: str, p, c: int) -> dict:

@@ -206,3 +206,36 @@ def test_classifier_branch_vs_reference(rc, checkpointing):
     _compare_grads(sg, got, {k[len("grad."):]: g[k] for k in g.files if k.startswith("grad.")})
     with pytest.raises(sg.ConfigError):
         model.forward(g["tokens"], g["labels"], model.make_workspace())  # cls_labels missing
+
+
+def test_out_of_range_device_ids_raise():
+    """Token ids / labels outside [0, v) raise ConfigError (layers.py:164-165, 552-553)
+    also for device tensors: the operator API checks on the device and reads the flag
+    back; the model defers the read to the loss read-back / check_inputs()."""
+    import torch
+
+    sg = _sg()
+    from paper_2104_05343_b200 import layers
+
+    cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=40, num_layers=1)
+    params = sg.init_global_params(cfg, 3)
+    model = sg.MeshModel(mesh(1, 2), cfg, params)
+    rng = np.random.default_rng(2)
+    tok = torch.as_tensor(rng.integers(0, 40, (4, 16))).cuda()
+    lab = torch.as_tensor(rng.integers(0, 40, (4, 16))).cuda()
+    ws = model.make_workspace()
+    model.forward(tok, lab, ws)  # in range: no error
+    model.check_inputs()
+    bad_tok, bad_lab = tok.clone(), lab.clone()
+    bad_tok[1, 3] = 40
+    bad_lab[2, 5] = -1
+    with pytest.raises(sg.ConfigError):
+        model.forward(bad_tok, lab, model.make_workspace())
+    with pytest.raises(sg.ConfigError):
+        model.forward(tok, bad_lab, model.make_workspace())
+    model.train_step(bad_tok, lab, model.make_workspace(), lr=0.1)
+    with pytest.raises(sg.ConfigError):
+        model.check_inputs()
+    model.check_inputs()  # the flag was cleared
+    with pytest.raises(sg.ConfigError):
+        layers.embedding_forward(bad_tok, model.table, cfg, ws)
