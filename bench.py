@@ -37,6 +37,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# the CPU legs (cpu_baseline, --impl reference) use every host core; OpenBLAS reads this
+# when numpy is first imported, so it is set before anything imports numpy
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
 
 METRIC = "2D transformer train samples/sec & SUMMA TFLOP/s at 1/2/4/8 B200 vs CPU ref"
 WORKLOADS = {
@@ -87,11 +90,15 @@ def model_flops(w: dict, mode: str = "train") -> float:
 
 
 def cpu_sample(w: dict, mode: str) -> dict:
+    """One bounded CPU sample of the workload: one layer (+ embedding / lm-head / CE) at the
+    bench's own batch for the BERT shape (~6 fp64 TFLOP, 10-20 s on the box's host cores),
+    at b = 1 for the h = 4096 stack (one such layer at b = 8 is ~20 fp64 TFLOP)."""
     from oracle import cpu_bench
 
+    b_sample = w["b"] if w["h"] <= 1024 else 1
     if mode == "infer":
-        return cpu_bench.inference_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=1)
-    return cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=2)
+        return cpu_bench.inference_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=b_sample)
+    return cpu_bench.training_samples_per_sec(w["h"], w["n"], w["s"], w["v"], w["layers"], b_sample=b_sample)
 
 
 def peaks() -> dict:
@@ -171,7 +178,6 @@ def run_reference(args):
 
     w = workload(args)
     cores = cpu_bench.host_cores()
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
     vals = []
     for i in range(args.warmup + args.steps):
         r = cpu_sample(w, args.mode)
@@ -299,7 +305,6 @@ def main():
     d2h = 4 * world
     barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()

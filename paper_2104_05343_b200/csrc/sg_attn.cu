@@ -591,13 +591,8 @@ __global__ void __launch_bounds__(384, 1)
 
 static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const FlashFwdParams& p, int b, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(flash_fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Flash2Cfg::SMEM) !=
-        cudaSuccess)
-      return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
-    attr = true;
-  }
+  if (!ensure_smem(reinterpret_cast<const void*>(flash_fwd2_kernel), (int)Flash2Cfg::SMEM))
+    return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
   const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
   const int sms = sg_device_sm_count();
   launch_k(flash_fwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), Flash2Cfg::SMEM, stream, q, k, v, o,
@@ -611,13 +606,8 @@ template <int HD>
 static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p,
                       int b, cudaStream_t stream) {
   using Cfg = FlashCfg<HD>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(flash_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) !=
-        cudaSuccess)
-      return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
-    attr = true;
-  }
+  if (!ensure_smem(reinterpret_cast<const void*>(flash_fwd_kernel<HD>), (int)Cfg::SMEM))
+    return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
   dim3 grid((p.s + kQB - 1) / kQB, p.nh, b);
   launch_k(flash_fwd_kernel<HD>, grid, dim3(256), Cfg::SMEM, stream, q, k, v, p);
   count_launch();
@@ -651,17 +641,13 @@ extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_
   if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, kKB, &p.v_b2_first);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static const int fwd_v1 = [] {
-    const char* e = getenv("SG_FLASH_FWD_V1");
-    return e ? atoi(e) : 0;
-  }();
-  if (d == 64 && !fwd_v1) {
+  if (d == 64) {
     CUtensorMap to;
     rc = tmap_bf16_tile_4d(&to, out, d, s, nh, b, ldo, d, s * ldo, &p.o_b2_first);
     if (rc) return rc;
     return launch_fwd2(tq, tk, tv, to, p, (int)b, st);
   }
-  return d == 64 ? launch_fwd<64>(tq, tk, tv, p, (int)b, st) : launch_fwd<128>(tq, tk, tv, p, (int)b, st);
+  return launch_fwd<128>(tq, tk, tv, p, (int)b, st);
 }
 
 // ============================================================================
@@ -692,224 +678,6 @@ struct FlashBwdParams {
 
 constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
 constexpr int kMaxItems = 256;           // per-CTA work items of the persistent backward (item table in smem)
-
-__global__ void __launch_bounds__(256, 1)
-    flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                     const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ FlashBwdParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
-  uint8_t* sK = smem;                 // 16 KB
-  uint8_t* sV = sK + kT64;            // 16 KB
-  uint8_t* sQ = sV + kT64;            // 2 slots
-  uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
-  uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
-  uint8_t* sDS = sP + 2 * kT64;       // 32 KB
-  uint8_t* sStg = sDS + 2 * kT64;     // 4 warps x 8 KB dQ staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
-  uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* dq_full = bars + 7;
-  uint64_t* acc_full = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int nqb = (p.s + 127) / 128;
-  const int kvalid = min(128, p.s - kb * 128);
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    tma_prefetch_desc(&tmDO);
-    tma_prefetch_desc(&tmDQ);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&qd_full[i], 1);
-      mbar_init(&qd_empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(ds_full, 4);
-    mbar_init(dq_full, 1);
-    mbar_init(acc_full, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_begin();
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * kT64);
-      tma4(&tmK, sK, kv_full, 0, kb * 128, h, b, p.k_b2_first);
-      tma4(&tmV, sV, kv_full, 0, kb * 128, h, b, p.v_b2_first);
-      for (int i = 0; i < nqb; ++i) {
-        const int slot = i & 1;
-        mbar_wait(&qd_empty[slot], ((i >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
-        tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
-        tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
-      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
-      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, false, true);    // dQ: A = dS, B = K
-      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), p_base = smem_u32(sP), ds_base = smem_u32(sDS);
-      mbar_wait(kv_full, 0);
-      for (int i = 0; i < nqb; ++i) {
-        const int slot = i & 1;
-        mbar_wait(&qd_full[slot], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
-          umma_bf16(t_s, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
-                    ID_SQ, kk > 0 ? 1u : 0u);
-          umma_bf16(t_dp, umma_desc_sw128(do_base + kk * 32, 0, 1024), umma_desc_sw128(v_base + kk * 32, 0, 1024),
-                    ID_SQ, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(s_full);
-        mbar_wait(ds_full, i & 1);  // P, dS in smem; S / dP read
-        tc_fence_after();
-#pragma unroll
-        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
-          const uint32_t acc = (i | kq) != 0 ? 1u : 0u;
-          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
-          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
-        }
-        umma_commit(&qd_empty[slot]);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
-          umma_bf16(t_dq, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
-                    umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(dq_full);
-      }
-      umma_commit(acc_full);
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sStg + q * 8192;
-    const size_t head_off = ((size_t)b * p.nh + h) * p.s;
-    for (int i = 0; i < nqb; ++i) {
-      const int qrow = i * 128 + r;
-      const bool qok = qrow < p.s;
-      const float lse2 = qok ? p.lse[head_off + qrow] * 1.4426950408889634f : 0.f;
-      const float dd = qok ? p.drow[head_off + qrow] : 0.f;
-      mbar_wait(s_full, i & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sv[32], dv[32];
-        tmem_ld32(t_s + lane_base + c * 32, sv);
-        tmem_ld32(t_dp + lane_base + c * 32, dv);
-        tmem_wait_ld();
-        float pr[32], ds[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = qok && (c * 32 + j) < kvalid;
-          pr[j] = ok ? ex2f_fast(fmaf(__uint_as_float(sv[j]), p.scale_log2, -lse2)) : 0.f;
-          ds[j] = pr[j] * (__uint_as_float(dv[j]) - dd) * p.scale;
-        }
-        uint8_t* prow = sP + (c >> 1) * kT64 + r * 128;
-        uint8_t* drow_ = sDS + (c >> 1) * kT64 + r * 128;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 x, y;
-          __nv_bfloat162* hx = reinterpret_cast<__nv_bfloat162*>(&x);
-          __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&y);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            hx[e] = __floats2bfloat162_rn(pr[8 * k + 2 * e], pr[8 * k + 2 * e + 1]);
-            hy[e] = __floats2bfloat162_rn(ds[8 * k + 2 * e], ds[8 * k + 2 * e + 1]);
-          }
-          const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
-          *reinterpret_cast<uint4*>(prow + (chunk << 4)) = x;
-          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) = y;
-        }
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
-      // dQ tile of this query block: TMEM -> fp32 staging -> TMA reduce-add
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      if (lane == 0) bulk_wait_read<0>();
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_dq + lane_base + c * 32, v);
-        tmem_wait_ld();
-        uint8_t* box = stg + c * 4096;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
-                          __uint_as_float(v[4 * k + 3]));
-      }
-      tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (p.dq_b2_first)
-            tma_reduce_add_4d(&tmDQ, stg + c * 4096, c * 32, h, i * 128 + q * 32, b);
-          else
-            tma_reduce_add_4d(&tmDQ, stg + c * 4096, c * 32, i * 128 + q * 32, h, b);
-        }
-        bulk_commit();
-      }
-    }
-    // dK, dV of this key block: TMEM (row = key) -> bf16 rows of the dQKV block
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const int key = kb * 128 + r;
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tsrc = (which == 0 ? t_dk : t_dv) + lane_base;
-      __nv_bfloat16* dst = (which == 0 ? p.dK : p.dV) + ((size_t)b * p.s + key) * p.ldg + (size_t)h * 64;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tsrc + c * 32, v);
-        tmem_wait_ld();
-        if (key < p.s) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint4 x;
-            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              hh[e] = __floats2bfloat162_rn(__uint_as_float(v[8 * k + 2 * e]), __uint_as_float(v[8 * k + 2 * e + 1]));
-            *reinterpret_cast<uint4*>(dst + c * 32 + 8 * k) = x;
-          }
-        }
-      }
-    }
-    if (lane == 0) bulk_wait_all();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<512>(tmem);
-}
 
 // ----------------------------------------------------------------------------
 // Backward v2 (d = 64), persistent: CTA c walks work items t = c, c + grid, ...
@@ -1335,6 +1103,409 @@ __global__ void __launch_bounds__(512, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// ----------------------------------------------------------------------------
+// Backward, d = 128 (the GPT configs), persistent over work items t = (key block,
+// head, batch) like bwd2. TMEM holds S | dP | dV | dK (4 x 128 columns), so the
+// 128-column dQ product of a query block is written into the S columns once the
+// softmax warps have read S (ds_full), drained by the drain warps while dV / dK
+// run, and the next block's S waits for that drain. Shared memory (224 KB): K, V,
+// Q, dO, P, dS as 128 x 128 bf16 tiles (two SWIZZLE_128B atoms along the 128-wide
+// dimension) and 4 x 8 KB drain staging; Q / dO are single-buffered, with the next
+// block's tiles prefetched into L2 a block ahead. Per query block:
+//   MMA    dP_G = dO_G V^T, S_G = Q_G K^T                 (M = queries, N = keys)
+//   warps 4-11 (lane quadrant x key half): P, dS -> smem    (as bwd2)
+//   MMA    dQ_G = dS K -> S columns; dV += P^T dO; dK += dS^T Q
+//   warps 12-15 dQ_G: TMEM -> fp32 staging -> TMA reduce-add; dK / dV at item end
+// ----------------------------------------------------------------------------
+constexpr uint32_t kT128 = 128 * 128 * 2;  // one 128 x 128 bf16 tile (2 atoms, 32 KB)
+
+__global__ void __launch_bounds__(512, 1)
+    flash_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                        const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
+                        const __grid_constant__ CUtensorMap tmDV, const __grid_constant__ FlashBwdParams p, int bsz) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + kT128;
+  uint8_t* sQ = sV + kT128;
+  uint8_t* sDO = sQ + kT128;
+  uint8_t* sP = sDO + kT128;
+  uint8_t* sDS = sP + kT128;
+  uint8_t* sStg = sDS + kT128;  // 4 drain warps x 8 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
+  int* items_tab = reinterpret_cast<int*>(bars + 32);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* q_full = bars + 2;
+  uint64_t* q_empty = bars + 3;
+  uint64_t* do_full = bars + 4;
+  uint64_t* do_empty = bars + 5;
+  uint64_t* s_full = bars + 6;
+  uint64_t* ds_full = bars + 7;
+  uint64_t* bufs_free = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint64_t* acc_full = bars + 11;
+  uint64_t* acc_empty = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (p.s + 127) / 128;
+  const int nkb = nqb;
+  const int n_items = nkb * p.nh * bsz;
+  auto decode = [&](int t, int& kb, int& h, int& b) {
+    kb = t % nkb;
+    const int r = t / nkb;
+    h = r % p.nh;
+    b = r / p.nh;
+  };
+  const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_items * nqb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmDQ);
+    tma_prefetch_desc(&tmDK);
+    tma_prefetch_desc(&tmDV);
+    for (uint64_t* bar : {kv_full, kv_empty, q_full, q_empty, do_full, do_empty, s_full, bufs_free, dq_full, acc_full})
+      mbar_init(bar, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_empty, 4);
+    mbar_init(acc_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  for (int it = threadIdx.x; it < my_items && it < kMaxItems; it += blockDim.x) {
+    int kb, h, b;
+    decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
+    items_tab[it] = kb | (h << 10) | (b << 20);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_begin();
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384, t_dq = t_s;
+  auto item = [&](int it, int& kb, int& h, int& b) {
+    const int v = items_tab[it];
+    kb = v & 1023;
+    h = (v >> 10) & 1023;
+    b = v >> 20;
+  };
+
+  if (warp == 0) {
+    reg_dealloc<56>();
+    if (lane == 0) {
+      int G = 0;
+      for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
+        int kb, h, b;
+        decode(t, kb, h, b);
+        mbar_wait(kv_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full, 2 * kT128);
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          tma4(&tmK, sK + a * kT64, kv_full, a * 64, kb * 128, h, b, p.k_b2_first);
+          tma4(&tmV, sV + a * kT64, kv_full, a * 64, kb * 128, h, b, p.v_b2_first);
+        }
+        for (int i = 0; i < nqb; ++i, ++G) {
+          {
+            // the next block's Q / dO into L2 while this block's products run
+            int i2 = i + 1, t2 = t, kb2 = kb, h2 = h, b2 = b;
+            if (i2 >= nqb) {
+              i2 = 0;
+              t2 += gridDim.x;
+            }
+            if (t2 != t && t2 < n_items) decode(t2, kb2, h2, b2);
+            if (t2 < n_items) {
+#pragma unroll
+              for (int a = 0; a < 2; ++a) {
+                tma4_l2(&tmQ, a * 64, i2 * 128, h2, b2, p.q_b2_first);
+                tma4_l2(&tmDO, a * 64, i2 * 128, h2, b2, p.do_b2_first);
+              }
+            }
+          }
+          mbar_wait(do_empty, (G & 1) ^ 1);
+          mbar_arrive_expect_tx(do_full, kT128);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tma4(&tmDO, sDO + a * kT64, do_full, a * 64, i * 128, h, b, p.do_b2_first);
+          mbar_wait(q_empty, (G & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, kT128);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tma4(&tmQ, sQ + a * kT64, q_full, a * 64, i * 128, h, b, p.q_b2_first);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    reg_dealloc<56>();
+    if (lane == 0) {
+      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: A, B K-major (over d)
+      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 128, true, true);    // dV, dK: A = P^T / dS^T, B = dO / Q
+      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 128, false, true);   // dQ: A = dS (K-major), B = K (MN-major)
+      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), q_base = smem_u32(sQ), do_base = smem_u32(sDO);
+      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+      for (int G = 0; G < total; ++G) {
+        const int it = G / nqb, i = G % nqb;
+        if (i == 0) mbar_wait(kv_full, it & 1);
+        if (G > 0) mbar_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained from the S columns
+        mbar_wait(do_full, G & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K-dim = d = 128: two atoms of 4 x 16
+          const uint32_t off = (kk >> 2) * kT64 + (kk & 3) * 32;
+          umma_bf16(t_dp, umma_desc_sw128(do_base + off, 0, 1024), umma_desc_sw128(v_base + off, 0, 1024), ID_SQ,
+                    kk > 0 ? 1u : 0u);
+        }
+        mbar_wait(q_full, G & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kT64 + (kk & 3) * 32;
+          umma_bf16(t_s, umma_desc_sw128(q_base + off, 0, 1024), umma_desc_sw128(k_base + off, 0, 1024), ID_SQ,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+        mbar_wait(ds_full, G & 1);  // S / dP read, P / dS in smem
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
+          umma_bf16(t_dq, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
+                    umma_desc_sw128(k_base + kk * 2048, kT64, 1024), ID_DQ, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(dq_full);
+        if (i == 0 && it > 0) {
+          mbar_wait(acc_empty, (it - 1) & 1);  // the previous item's dK / dV were read out
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
+          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, kT64, 1024),
+                    umma_desc_sw128(do_base + kq * 2048, kT64, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
+        }
+        umma_commit(do_empty);
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) {
+          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, kT64, 1024),
+                    umma_desc_sw128(q_base + kq * 2048, kT64, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
+        }
+        umma_commit(q_empty);
+        umma_commit(bufs_free);
+        if (i == nqb - 1) {
+          umma_commit(acc_full);
+          umma_commit(kv_empty);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    reg_dealloc<56>();
+  } else if (warp < 12) {
+    reg_alloc<176>();
+    const int e = warp - 4;
+    const int q = e & 3, half = e >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const float scale = p.scale, scale_log2 = p.scale_log2;
+    auto row_stats = [&](int it, int i, float& lse, float& dd) {
+      lse = dd = 0.f;
+      if (it >= my_items) return;
+      int kb, h, b;
+      item(it, kb, h, b);
+      const int qrow = i * 128 + r;
+      if (qrow >= p.s) return;
+      const size_t off = ((size_t)b * p.nh + h) * p.s + qrow;
+      lse = __ldg(p.lse + off);
+      dd = __ldg(p.drow + off);
+    };
+    float lse_n, dd_n;
+    row_stats(0, 0, lse_n, dd_n);
+    int it = 0, i = 0;
+    int kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
+    for (int G = 0; G < total; ++G) {
+      const int kvalid = min(128, p.s - kb * 128);
+      const bool full_keys = kvalid == 128;
+      const float lse_c = lse_n, dd = dd_n;
+      {
+        const int ni = i + 1 == nqb ? 0 : i + 1, nit = i + 1 == nqb ? it + 1 : it;
+        row_stats(nit, ni, lse_n, dd_n);
+      }
+      const bool qok = i * 128 + r < p.s;
+      mbar_wait(s_full, G & 1);
+      tc_fence_after();
+      const float lse2 = lse_c * 1.4426950408889634f;
+      uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;
+        uint32_t sv[32], dv[32];
+        tmem_ld32(t_s + lane_base + c * 32, sv);
+        tmem_ld32(t_dp + lane_base + c * 32, dv);
+        tmem_wait_ld();
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nl2 = f2_pack(-lse2, -lse2);
+        const uint64_t nd2 = f2_pack(-dd, -dd), ss2 = f2_pack(scale, scale);
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2) {
+          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * e2]), __uint_as_float(sv[2 * e2 + 1])), sc2, nl2);
+          float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
+          float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
+          if (!full_keys || !qok) {
+            if (!qok || c * 32 + 2 * e2 >= kvalid) p0 = 0.f;
+            if (!qok || c * 32 + 2 * e2 + 1 >= kvalid) p1 = 0.f;
+          }
+          const uint64_t pp = f2_pack(p0, p1);
+          const uint64_t dmd = fadd2(f2_pack(__uint_as_float(dv[2 * e2]), __uint_as_float(dv[2 * e2 + 1])), nd2);
+          const uint64_t ds = fmul2(fmul2(pp, ss2), dmd);
+          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
+          __nv_bfloat162 hd = __floats2bfloat162_rn(__uint_as_float(static_cast<uint32_t>(ds)),
+                                                   __uint_as_float(static_cast<uint32_t>(ds >> 32)));
+          pk[cc][e2] = *reinterpret_cast<uint32_t*>(&hp);
+          dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
+        }
+      }
+      if (G > 0) mbar_wait(bufs_free, (G - 1) & 1);  // block G-1's products have read P / dS
+      uint8_t* prow = sP + half * kT64 + r * 128;
+      uint8_t* drow_ = sDS + half * kT64 + r * 128;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int chunk = (cc * 4 + k) ^ (r & 7);
+          *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
+              make_uint4(pk[cc][4 * k], pk[cc][4 * k + 1], pk[cc][4 * k + 2], pk[cc][4 * k + 3]);
+          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
+              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (i == nqb - 1) {
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
+      }
+    }
+  } else {
+    // 4 drain warps (lane quadrant q, 32 rows): dQ of every block in four 32-column
+    // fp32 chunks through two 4 KB staging buffers; dK / dV at each item's end as
+    // 32 x 32 bf16 tiles (4 per tensor)
+    reg_dealloc<96>();
+    const int q = warp & 3;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sStg + (warp - 12) * 8192;
+    int it = 0, i = 0, kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
+    for (int G = 0; G < total; ++G) {
+      mbar_wait(dq_full, G & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_dq + lane_base + c * 32, v);
+        tmem_wait_ld();
+        if (c == 3) {  // all of dQ_G in registers / staging: the S columns may take the next scores
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);
+        }
+        if (lane == 0) bulk_wait_read<1>();  // the reduce-add two chunks back has read this buffer
+        __syncwarp();
+        uint8_t* box = stg + (c & 1) * 4096;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
+                          __uint_as_float(v[4 * k + 3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (p.dq_b2_first)
+            tma_reduce_add_4d(&tmDQ, box, c * 32, h, i * 128 + q * 32, b);
+          else
+            tma_reduce_add_4d(&tmDQ, box, c * 32, i * 128 + q * 32, h, b);
+          bulk_commit();
+        }
+      }
+      if (i == nqb - 1) {
+        mbar_wait(acc_full, it & 1);
+        tc_fence_after();
+        const int key0 = kb * 128 + q * 32;
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {
+          if (lane == 0) bulk_wait_read<0>();  // earlier TMA operations have read the staging
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t w[32];
+            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + c * 32, w);
+            tmem_wait_ld();
+            if (which == 1 && c == 3) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
+            }
+            uint8_t* row = stg + c * 2048 + lane * 64;
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) {
+              uint4 x;
+              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2)
+                hh[e2] = __floats2bfloat162_rn(__uint_as_float(w[8 * k2 + 2 * e2]),
+                                               __uint_as_float(w[8 * k2 + 2 * e2 + 1]));
+              *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const CUtensorMap* tm = which == 0 ? &tmDK : &tmDV;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (p.dkv_b2_first)
+                tma_store_4d(tm, stg + c * 2048, c * 32, h, key0, b);
+              else
+                tma_store_4d(tm, stg + c * 2048, c * 32, key0, h, b);
+            }
+            bulk_commit();
+          }
+          if (p.kv_colsum) {
+            // bias-gradient column sums from the staged bf16 tiles (rows past s are zero)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint8_t* tile = stg + c * 2048;
+              float acc2[2] = {0.f, 0.f};
+#pragma unroll
+              for (int i2 = 0; i2 < 32; ++i2) {
+                const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
+                acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
+              }
+              atomicAdd(p.kv_colsum + which * p.nh * 128 + h * 128 + c * 32 + lane, acc2[0] + acc2[1]);
+            }
+          }
+        }
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace sg
 
 extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout, int64_t lddo, const float* lse,
@@ -1342,7 +1513,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
                                  int64_t lddq, void* dqkv, int64_t ldg, float* kv_colsum, void* stream) {
   using namespace sg;
   clear_error();
-  if (b < 1 || s < 1 || nh < 1 || d != 64) return set_error(SG_ERR_SHAPE, "flash bwd: d must be 64");
+  if (b < 1 || s < 1 || nh < 1 || (d != 64 && d != 128)) return set_error(SG_ERR_SHAPE, "flash bwd: d must be 64 or 128");
   if (ldq < 3 * nh * d || lddo < nh * d || lddq < nh * d || ldg < 3 * nh * d)
     return set_error(SG_ERR_SHAPE, "flash bwd: leading dimensions");
   if ((reinterpret_cast<uintptr_t>(dqkv) & 15) || (ldg * 2) % 16) return set_error(SG_ERR_SHAPE, "flash bwd: unaligned");
@@ -1368,30 +1539,26 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_bf16_tile_4d(&tdk, p.dK, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (!rc) rc = tmap_bf16_tile_4d(&tdv, p.dV, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (rc) return rc;
-  constexpr size_t SMEM = 10 * kT64 + 4 * 8192 + 128;  // K, V, 2 Q, 2 dO, P, dS (2 atoms each), dQ staging
-  constexpr size_t SMEM2 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;  // v2: K, V double-buffered per item
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(flash_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2) != cudaSuccess)
+  // d = 64: K, V double-buffered per item, 2 Q, 2 dO, P, dS (2 atoms each), 8 x 4 KB staging;
+  // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
+  constexpr size_t SMEM64 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;
+  constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
+  const int nkb = (int)((s + 127) / 128);
+  const int items = nkb * (int)nh * (int)b;
+  const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
+  if (nkb > 1024 || nh > 1024 || b > 2047 || (items + sms - 1) / sms > kMaxItems)
+    return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (d == 64) {
+    if (!ensure_smem(reinterpret_cast<const void*>(flash_bwd2_kernel), (int)SMEM64))
       return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
-    attr = true;
-  }
-  static const int bwd_v1 = [] {
-    const char* e = getenv("SG_FLASH_BWD_V1");
-    return e ? atoi(e) : 0;
-  }();
-  dim3 grid((unsigned)((s + 127) / 128), (unsigned)nh, (unsigned)b);
-  if (bwd_v1)
-    launch_k(flash_bwd_kernel, grid, dim3(256), SMEM, static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, p);
-  else
-  {
-    const int items = (int)grid.x * (int)grid.y * (int)grid.z;
-    const int sms = sg_device_sm_count();
-    if (grid.x > 1024 || nh > 1024 || b > 2047 || (items + (sms > 0 ? sms : 148) - 1) / (sms > 0 ? sms : 148) > kMaxItems)
-      return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
-    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(512), SMEM2,
-             static_cast<cudaStream_t>(stream), tq, tk, tv, tdo, tdq, tdk, tdv, p, (int)b);
+    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq, tdk, tdv, p,
+             (int)b);
+  } else {
+    if (!ensure_smem(reinterpret_cast<const void*>(flash_bwd128_kernel), (int)SMEM128))
+      return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
+    launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk, tdv,
+             p, (int)b);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

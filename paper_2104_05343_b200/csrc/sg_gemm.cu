@@ -995,12 +995,8 @@ template <int BN, bool A_MN, bool B_MN, int EW, bool PAIR, int KIND = EK_GENERIC
 static int launch_gemm(const Maps& m, const GemmParams& p, cudaStream_t stream, int grid) {
   using Cfg = GemmCfg<BN, EW, PAIR>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EW, PAIR, KIND>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
-      return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
-    attr_set = true;
-  }
+  if (!ensure_smem(reinterpret_cast<const void*>(kern), (int)Cfg::SMEM))
+    return set_error(SG_ERR_CUDA, "cudaFuncSetAttribute(max smem) failed");
   if (PAIR) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -2,7 +2,27 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace sg {
+// cudaFuncSetAttribute(max dynamic smem) once per (kernel, device): a process may drive
+// several devices, and the attribute is per device.
+inline bool ensure_smem(const void* kern, int bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(kern, dev);
+  if (done.count(key)) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  done.insert(key);
+  return true;
+}
+
 int set_error(int code, const char* msg);
 void clear_error();
 void count_launch();  // every kernel this library launches (bench gpu_launches)
@@ -10,8 +30,6 @@ void count_launch();  // every kernel this library launches (bench gpu_launches)
 
 extern "C" int sg_device_sm_count(void);
 
-#include <cstdlib>
-#include <utility>
 
 namespace sg {
 // Programmatic dependent launch (opt-in, SG_PDL=1): every libsg kernel triggers its

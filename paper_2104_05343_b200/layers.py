@@ -517,8 +517,8 @@ def flash_ok(cfg: ModelConfig) -> bool:
 
 
 def flash_bwd_ok(cfg: ModelConfig) -> bool:
-    """The flash backward covers head_dim 64; otherwise P is rebuilt from Q, K (AttentionContext.probs)."""
-    return FLASH_ATTENTION and cfg.head_dim == 64
+    """The flash backward covers head_dim 64 and 128; otherwise P is rebuilt from Q, K (AttentionContext.probs)."""
+    return FLASH_ATTENTION and cfg.head_dim in (64, 128)
 
 
 FLASH_ATTENTION = True

@@ -35,7 +35,9 @@ def test_flash_forward(b, s, nh, d):
 
 
 @pytest.mark.parametrize("b,s,nh,d", [(2, 512, 4, 64), (3, 200, 2, 64), (2, 1024, 2, 64), (2, 64, 3, 64),
-                                      (1, 130, 1, 64), (1, 2048, 2, 64), (40, 128, 8, 64)])
+                                      (1, 130, 1, 64), (1, 2048, 2, 64), (40, 128, 8, 64),
+                                      (1, 2048, 2, 128), (2, 512, 2, 128), (3, 200, 2, 128), (1, 130, 1, 128),
+                                      (40, 128, 4, 128), (1, 384, 4, 128)])
 def test_flash_backward(b, s, nh, d):
     from paper_2104_05343_b200 import kernels as K
 
