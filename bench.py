@@ -200,7 +200,7 @@ def _config(w, n_gpus, args, extra=None) -> dict:
     cfg = {"workload": w["name"], "model": f"2D transformer L={w['layers']} h={w['h']} n={w['n']} v={w['v']}",
            "global_batch": w["b"], "seq_len": w["s"], "hidden": w["h"], "heads": w["n"], "layers": w["layers"],
            "vocab": w["v"], "mesh": f"{mc.rows}x{mc.cols}", "parallelism": f"2d-summa r{mc.rows}xc{mc.cols}",
-           "checkpointing": bool(args.checkpointing), "cuda_graph": (not args.no_graph) and n_gpus == 1,
+           "checkpointing": bool(args.checkpointing), "cuda_graph": not args.no_graph,
            "mode": args.mode, "optimizer": "sgd" if args.mode == "train" else None, "l2": "working set (weights fp32+bf16, >10 GB activations) larger than the 126 MB L2"}
     if extra:
         cfg.update(extra)
@@ -229,6 +229,9 @@ def main():
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's panel broadcasts run beside the persistent GEMMs, which leave SG_SM_RESERVE
+        # SMs free (mesh.py); cap NCCL's channels (one CTA each) to that budget
+        os.environ.setdefault("NCCL_MAX_NCHANNELS", os.environ.get("SG_SM_RESERVE", "8"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args)
     mesh = sg.create_mesh(sg.mesh_for_world(world), backend="dist" if world > 1 else "local")
@@ -253,20 +256,33 @@ def main():
     for _ in range(args.warmup):
         loss = step()
     torch.cuda.synchronize()
-    use_graph = (not args.no_graph) and world == 1
+    if getattr(mesh, "peer", None) is not None:
+        mesh.peer.check()
+    use_graph = not args.no_graph
     graph = None
+    graph_error = None
     if use_graph:
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            step()
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            loss = step()
-        graph.replay()
-        torch.cuda.synchronize()
+        # one graph replay per step on every rank: the dist step's NCCL panel broadcasts /
+        # statistics all-reduces are captured with it, the peer-memory reduces are plain
+        # kernels (device-side barrier epochs, peer.py)
+        try:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                step()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            barrier()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                loss = step()
+            graph.replay()
+            torch.cuda.synchronize()
+            barrier()
+        except Exception as e:  # capture unsupported here: time the eager step instead
+            graph, use_graph, graph_error = None, False, f"{type(e).__name__}: {e}"[:300]
+            torch.cuda.synchronize()
+    if use_graph:
         run = graph.replay
     else:
         def run():
@@ -374,7 +390,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, uniform token ids)",
-                "config": _config(w, world, args),
+                "config": _config(w, world, args, extra={"cuda_graph": use_graph, "graph_error": graph_error,
+                                                         "peer_memory": getattr(mesh, "peer", None) is not None,
+                                                         "gemm_sm_budget": K.gemm_sm_budget()}),
                 "model_tflops": flops / (ms_step * 1e-3) / 1e12,
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches), "roofline": roof, "summa": summa, "cpu_baseline": cpu,

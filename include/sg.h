@@ -172,6 +172,25 @@ int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t vb, const vo
  * *flag |= 1 when any of the n ids lies outside [0, v). The host reads the flag at
  * its next synchronisation (the loss read-back) and raises ConfigError. */
 int sg_check_ids(const int64_t* ids, int64_t n, int64_t v, int* flag, void* stream);
+
+/* ---- Peer memory of the SPMD mesh (replaces the reference's row / column reduce
+ * collectives mesh.py:458-482 on the AB^T / A^T B paths, summa.py:128-139, 152-163).
+ * sg_sym_alloc: zeroed device arena + its CUDA IPC handle (sg_ipc_handle_size bytes);
+ * sg_ipc_open maps a peer's arena into the calling device (peer access enabled
+ * lazily); sg_peer_barrier: stream-ordered group barrier over signal pads in such
+ * arenas. args = n pad pointers then n member flat ranks (int64, device memory);
+ * the epoch counter lives on the device (graph-capturable); on timeout *err |= 1. */
+int sg_sym_alloc(int64_t bytes, void** ptr, void* handle);
+int sg_sym_free(void* ptr);
+int sg_ipc_open(const void* handle, void** ptr);
+int sg_ipc_close(void* ptr);
+int sg_ipc_handle_size(void);
+/* SMs the persistent GEMM grid leaves free (dist meshes: the NCCL kernels moving the
+ * next SUMMA step's panels co-reside with the current product); default 0. */
+int sg_set_sm_reserve(int n);
+int sg_gemm_sm_budget(void);
+int sg_peer_barrier(const int64_t* args, int n, int me_idx, int* epoch, int* err, int64_t timeout_cycles,
+                    void* stream);
 /* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);

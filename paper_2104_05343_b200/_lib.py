@@ -78,6 +78,14 @@ SIGNATURES: dict[str, tuple] = {
     "sg_embed_fwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i32, i64, vp]),
     "sg_embed_bwd": (i32, [vp, i64, i64, i64, vp, i32, i64, i64, vp, i64, vp]),
     "sg_check_ids": (i32, [vp, i64, i64, vp, vp]),
+    "sg_sym_alloc": (i32, [i64, ctypes.POINTER(vp), vp]),
+    "sg_sym_free": (i32, [vp]),
+    "sg_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
+    "sg_ipc_close": (i32, [vp]),
+    "sg_ipc_handle_size": (i32, []),
+    "sg_set_sm_reserve": (i32, [i32]),
+    "sg_gemm_sm_budget": (i32, []),
+    "sg_peer_barrier": (i32, [vp, i32, i32, vp, vp, i64, vp]),
     "sg_dgelu": (i32, [vp, i64, vp, i64, i64, i64, vp, i32, i64, vp, vp]),
     "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
     "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),

@@ -39,6 +39,25 @@ extern "C" int sg_device_sm_count(void) {
   return n;
 }
 
+namespace sg {
+static std::atomic<int> g_sm_reserve{0};
+}  // namespace sg
+
+// SMs left free by the persistent GEMM grid (dist meshes: room for the NCCL kernels
+// that move step l+1's panels while step l's product runs, summa.py).
+extern "C" int sg_set_sm_reserve(int n) {
+  if (n < 0 || n > 64) return sg::set_error(SG_ERR_CONFIG, "sm reserve must lie in [0, 64]");
+  sg::g_sm_reserve.store(n, std::memory_order_relaxed);
+  return SG_OK;
+}
+
+extern "C" int sg_gemm_sm_budget(void) {
+  const int sms = sg_device_sm_count();
+  if (sms <= 0) return sms;
+  const int left = sms - sg::g_sm_reserve.load(std::memory_order_relaxed);
+  return left < 2 ? 2 : (left & ~1);  // CTA pairs need an even grid
+}
+
 extern "C" const char* sg_build_info(void) {
   return "libsg sm_100a (tcgen05/TMA) built with nvcc " __DATE__;
 }

@@ -1147,7 +1147,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
       return set_error(SG_ERR_CONFIG, "gemm: softmax bwd needs P (aux) and D_i (rowvec)");
     if (a->mode == SG_EPI_SOFTMAX && a->alpha <= 0.f) return set_error(SG_ERR_CONFIG, "gemm: softmax alpha > 0");
   }
-  const int sms = sg_device_sm_count();
+  const int sms = sg_gemm_sm_budget();  // every SM unless a dist mesh reserves some for NCCL
   if (sms <= 0) return set_error(SG_ERR_CUDA, "no CUDA device");
 
   GemmParams p{};

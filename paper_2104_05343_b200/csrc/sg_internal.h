@@ -29,6 +29,7 @@ void count_launch();  // every kernel this library launches (bench gpu_launches)
 }  // namespace sg
 
 extern "C" int sg_device_sm_count(void);
+extern "C" int sg_gemm_sm_budget(void);
 
 
 namespace sg {

@@ -19,7 +19,8 @@ __all__ = ["gemm", "ACT_NONE", "ACT_GELU", "ACT_DGELU", "EPI_NORMAL", "EPI_SOFTM
 
 
 def _stream(t: torch.Tensor) -> int:
-    return torch.cuda.current_stream(t.device).cuda_stream
+    # the current device's stream: peer-mapped tensors report their owner GPU as device
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _require_cuda(*ts: torch.Tensor) -> None:
@@ -464,3 +465,12 @@ def flash_attn_bwd(qkv, dout, lse, drow, b, s, n_heads, d, dq_acc, dqkv, kv_cols
 def check_ids(ids, v: int, flag):
     """flag (int32 [1]) |= 1 when any of ``ids`` lies outside [0, v) (sg_check_ids)."""
     _call("sg_check_ids", _p(ids), ids.numel(), v, _p(flag), _stream(flag))
+
+
+def set_sm_reserve(n: int) -> None:
+    """Leave ``n`` SMs free of the persistent GEMM grid (sg_set_sm_reserve)."""
+    _call("sg_set_sm_reserve", int(n))
+
+
+def gemm_sm_budget() -> int:
+    return int(_lib.lib().sg_gemm_sm_budget())

@@ -31,7 +31,7 @@ import torch
 
 from . import kernels as K
 from .errors import ConfigError, ShapeError
-from .membuf import Workspace, padded_empty
+from .membuf import Workspace, full_storage, padded_empty
 from .mesh import Mesh, MeshConfig
 from .summa import (
     BF16,
@@ -282,6 +282,11 @@ def embedding_backward(out_grad: ShardedMatrix, tokens, table: ShardedMatrix, cf
             if mesh.owns(o):
                 blocks[k] = ws.alloc(o, (vb, hb), out_category, dtype=F32)
         res = ShardedMatrix(mesh, v_pad, cfg.h, blocks, "weight")
+    parts = [None] * mesh.p
+    if not mesh.is_local:  # one staging block per position, reused by every vocabulary step
+        ws.reset_all("workspace")
+        for dev in mesh.local_devs:
+            parts[dev] = ws.empty(dev, (vb, hb), "workspace", dtype=F32)
     for l in range(c):
         if mesh.is_local:
             # the column reduce collapses into atomics on the owner's block
@@ -291,9 +296,8 @@ def embedding_backward(out_grad: ShardedMatrix, tokens, table: ShardedMatrix, cf
                 for i in range(r):
                     K.embed_bwd(ids[mesh.flat(i, j)], l * vb, vb, out_grad.blocks[mesh.flat(i, j)], dst)
             continue
-        parts = [None] * mesh.p
         for dev in mesh.local_devs:
-            parts[dev] = ws.alloc(dev, (vb, hb), "workspace", dtype=F32)
+            K.zero(full_storage(parts[dev]))
             K.embed_bwd(ids[dev], l * vb, vb, out_grad.blocks[dev], parts[dev])
         dest = [None] * mesh.p
         for j in range(c):
@@ -659,9 +663,10 @@ def _bf16_of(x: ShardedMatrix, ws: Workspace) -> ShardedMatrix:
 
 
 def _weight_grad(a: ShardedMatrix, b: ShardedMatrix, w: ShardedMatrix, ws: Workspace, lr):
-    """dW = a^T b, or with ``lr`` (eager SGD on a local mesh) w -= lr a^T b in place by
-    the product's reduce-add epilogue (returns None: no gradient is materialised)."""
-    if lr is not None and a.mesh.is_local:
+    """dW = a^T b, or with ``lr`` (eager SGD; local mesh, or dist mesh with peer memory)
+    w -= lr a^T b in place by the product's (remote) reduce-add epilogue (returns None:
+    no gradient is materialised)."""
+    if lr is not None and (a.mesh.is_local or a.mesh.peer is not None):
         summa_atb(a, b, ws, accumulate_into=w, alpha=-lr)
         return None
     return summa_atb(a, b, ws, out_category="param_grad")

@@ -128,7 +128,8 @@ class Mesh:
     """The r x c grid. Drive it from one controller context per process."""
 
     def __init__(self, cfg: MeshConfig, cost: CostParams | None = None, mode: str = "lockstep", *,
-                 backend: str = "local", device: torch.device | str | int | None = None) -> None:
+                 backend: str = "local", device: torch.device | str | int | None = None,
+                 peer: bool | None = None) -> None:
         if mode not in _MODES:
             raise ConfigError(f"unknown mesh mode {mode!r}")
         if backend not in ("local", "dist"):
@@ -156,7 +157,9 @@ class Mesh:
             self._slot.append(n * cfg.node_size + seen[n])
             seen[n] += 1
         self.stats: Counter = Counter()
+        self.calls: Counter = Counter()  # torch.distributed calls actually issued (dist backend)
         self.ledger = CommLedger(self.p)
+        self.peer = None
         self._closed = False
         if backend == "local":
             if device is None:
@@ -183,6 +186,22 @@ class Mesh:
             rows = [dist.new_group([self._slot[f] for f in g]) if len(g) > 1 else None for g in self._row_groups]
             cols = [dist.new_group([self._slot[f] for f in g]) if len(g) > 1 else None for g in self._col_groups]
             self._groups = (rows, cols)
+            # peer memory (CUDA IPC arenas + device barriers): the AB^T / A^T B reduces
+            # become remote reduce-adds of the GEMM epilogues (peer.py); default on CUDA
+            if peer is None:
+                peer = self._device.type == "cuda" and self.p > 1
+            if peer:
+                if self._device.type != "cuda":
+                    raise ConfigError("peer memory needs a CUDA device")
+                from .peer import PeerNet
+
+                self.peer = PeerNet(self)
+            if self._device.type == "cuda" and self.p > 1 and dist.get_backend() == "nccl":
+                # the persistent GEMMs leave SMs to the NCCL kernels that move step l+1's
+                # panels during step l's product (NCCL_MAX_NCHANNELS is set to match by bench.py)
+                import os
+
+                K.set_sm_reserve(int(os.environ.get("SG_SM_RESERVE", "8")))
 
     # ------------------------------------------------------------- topology
     def flat(self, row: int, col: int) -> int:
@@ -212,6 +231,16 @@ class Mesh:
 
     def device(self, flat: int | None = None) -> torch.device:
         return self._device
+
+    def persistent_empty(self, shape, dtype) -> torch.Tensor:
+        """A long-lived block (weight masters): in the symmetric peer arena when the mesh
+        has peer memory (so remote GEMM epilogues can reduce-add into it), else a
+        padded device block."""
+        if self.peer is not None:
+            return self.peer.heap.empty(shape, dtype)
+        from .membuf import padded_empty
+
+        return padded_empty(shape, dtype, self._device)
 
     @property
     def is_local(self) -> bool:
@@ -301,6 +330,7 @@ class Mesh:
 
         buf = src[f] if f == s else padded_empty(shape, dtype, self._device)
         dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group)
+        self.calls["broadcast"] += 1
         out[f] = buf
         return out
 
@@ -327,6 +357,7 @@ class Mesh:
             return Pending(out, [])
         buf = src[f] if f == s else recv
         work = dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group, async_op=True)
+        self.calls["broadcast"] += 1
         out[f] = buf
         return Pending(out, [work])
 
@@ -359,10 +390,12 @@ class Mesh:
         works = []
         if group is not None:
             flat = K._flat_storage(parts[f])
-            if dist.get_backend(group) == "nccl":
+            if _reduce_ok(group, flat):
                 works.append(dist.reduce(flat, dst=self._slot[d], group=group, async_op=True))
+                self.calls["reduce"] += 1
             else:  # gloo reduce is CPU-only; all_reduce covers CUDA tensors
                 works.append(dist.all_reduce(flat, group=group, async_op=True))
+                self.calls["allreduce"] += 1
         return Pending(list(parts), works, fold=[(d, [parts[f]])] if f == d else [])
 
     def reduce_row_async(self, dest_col: int, parts: Sequence, tag: str = "misc") -> "Pending":
@@ -405,10 +438,12 @@ class Mesh:
         part = parts[f]
         if group is not None:
             flat = K._flat_storage(part)
-            if dist.get_backend(group) == "nccl":
+            if _reduce_ok(group, flat):
                 dist.reduce(flat, dst=self._slot[d], group=group)
+                self.calls["reduce"] += 1
             else:  # gloo reduce is CPU-only; all_reduce covers CUDA tensors
                 dist.all_reduce(flat, group=group)
+                self.calls["allreduce"] += 1
         if f == d:
             K.fold(out[d], [part], accumulate=accumulate)
 
@@ -449,6 +484,7 @@ class Mesh:
             return
         dist.all_reduce(K._flat_storage(bufs[f]), op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM,
                         group=group)
+        self.calls["allreduce"] += 1
 
     def allreduce_row(self, bufs: Sequence, op: str = "sum", tag: str = "misc") -> None:
         """In place: every position of row i holds the fold of the row (R5-R7, mesh.py:501-504)."""
@@ -557,6 +593,13 @@ class Mesh:
         return out
 
 
+def _reduce_ok(group, t: torch.Tensor) -> bool:
+    """dist.reduce is usable: NCCL, or gloo on CPU tensors (gloo's reduce is CPU-only)."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "nccl" or not t.is_cuda
+
+
 class Pending:
     """An issued (possibly asynchronous) collective: ``blocks`` is the per-position
     result list, valid on the current stream after ``wait()``; for reduces,
@@ -591,9 +634,9 @@ def _staged_copy(block: torch.Tensor, ws, dev: int, category: str) -> torch.Tens
 
 
 def create_mesh(cfg: MeshConfig, cost: CostParams | None = None, mode: str = "lockstep", *,
-                backend: str = "local", device=None) -> Mesh:
+                backend: str = "local", device=None, peer: bool | None = None) -> Mesh:
     """Build a mesh; raises ConfigError on an invalid config (mesh.py:516-518)."""
-    return Mesh(cfg, cost=cost, mode=mode, backend=backend, device=device)
+    return Mesh(cfg, cost=cost, mode=mode, backend=backend, device=device, peer=peer)
 
 
 def check_same_mesh(*objs) -> Mesh:

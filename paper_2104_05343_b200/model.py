@@ -201,10 +201,10 @@ class MeshModel:
             else:
                 g = global_params
                 kw = {"w_qkv": _with_twin(scatter(interleave_qkv(np.asarray(g[pre + "w_qkv"]), c), mesh,
-                                                  layout="weight")),
-                      "w_dense": _with_twin(scatter(g[pre + "w_dense"], mesh, layout="weight")),
-                      "w1": _with_twin(scatter(g[pre + "w1"], mesh, layout="weight")),
-                      "w2": _with_twin(scatter(g[pre + "w2"], mesh, layout="weight"))}
+                                                  layout="weight", persistent=True)),
+                      "w_dense": _with_twin(scatter(g[pre + "w_dense"], mesh, layout="weight", persistent=True)),
+                      "w1": _with_twin(scatter(g[pre + "w1"], mesh, layout="weight", persistent=True)),
+                      "w2": _with_twin(scatter(g[pre + "w2"], mesh, layout="weight", persistent=True))}
                 vec = {name: RowHostedVector.split(
                     interleave_qkv(np.asarray(g[pre + name]), c) if name == "b_qkv" else g[pre + name], c, mesh=mesh)
                     for name in _LAYER_KEYS if name not in _MATS}
@@ -228,11 +228,69 @@ class MeshModel:
                 self.cls_w16[j].copy_(self.cls_w[j])
 
     # ------------------------------------------------------------------ workspace
+    def workspace_capacities(self, checkpointing: bool = True, eager_update: bool = False) -> dict:
+        """Planned per-position scalars per arena category (the reference's plan,
+        model.py:197-222, restated for this build's allocations). Same as the reference:
+        forward 9 bsh/p per layer (QKV 3, attention out 1, MLP pre-activation 4, MLP out 1;
+        + the embedding output without checkpointing), backward 7 bsh/p, conjunction
+        bsh/p. Different, because of the fused kernels: the flash path keeps the row
+        log-sum-exp (b n s / p) instead of P; vector gradients 13 h/c per layer plus the
+        last layer's b2 gradient formed by the lm-head product (h/c); with eager SGD on a
+        local / peer-memory mesh the weight gradients never exist (updated inside their
+        products); the tied table gradient is one set of blocks (the embedding backward
+        accumulates into it); the per-product workspace is _workspace_plan's."""
+        from .layers import flash_ok
+
+        cfg, mesh = self.cfg, self.mesh
+        r, c, p = mesh.r, mesh.c, mesh.p
+        rows, hb, vb = cfg.b * cfg.s // r, cfg.h // c, cfg.v_padded(mesh) // c
+        bsh_p = rows * hb
+        lse = (cfg.b // r) * (cfg.n // c) * cfg.s if flash_ok(cfg) else 0
+        fwd_layer = 9 * bsh_p + lse
+        mats, vecs = 12 * cfg.h * cfg.h // p, 13 * hb
+        fused = mesh.is_local or mesh.peer is not None
+        cls = 2 * hb if self.classifier else 0
+        if eager_update and checkpointing:
+            param_grad = vecs + hb + cls + (0 if fused else mats)
+        else:
+            param_grad = max(cfg.num_layers, 1) * (mats + vecs) + hb + cls
+        return {"workspace": self._workspace_plan(),
+                "forward": fwd_layer if checkpointing else cfg.num_layers * fwd_layer + bsh_p,
+                "backward": 7 * bsh_p, "param_grad": param_grad, "param_grad_tied": (c // r) * vb * hb,
+                "conjunction": bsh_p, "free": None, "replicated": None}
+
+    def _workspace_plan(self) -> int:
+        """Largest per-product "workspace" use (reset at every SUMMA product, summa.py).
+
+        local mesh: one step needs none; c > 1 stages the fp32 sum of a product whose
+        epilogue needs the complete sum (bf16 QKV / fc1 / dctx / dAct outputs, the bf16
+        logits): max(4 bsh/p, bs v/(r c)). dist: two receive slots per broadcast operand,
+        plus (collective reduce) two partial-sum slots and the fold accumulator; with
+        peer memory the partial sums go to the destination's symmetric accumulator."""
+        cfg, mesh = self.cfg, self.mesh
+        r, c = mesh.r, mesh.c
+        R, hb, vb = cfg.b * cfg.s // r, cfg.h // c, cfg.v_padded(mesh) // c
+        bf16_logits = self.logits_dtype == BF16
+        if mesh.is_local:
+            return 0 if c == 1 else max(4 * R * hb, R * vb if bf16_logits else 0)
+        peer = mesh.peer is not None
+        # (m_b, k_b, n_b, epilogue needs the full sum) per product of the step
+        ab = [(R, hb, 3 * hb, True), (R, hb, hb, False), (R, hb, 4 * hb, True), (R, 4 * hb, hb, False),
+              (R, vb, hb, True)]
+        abt = [(R, hb, hb), (R, hb, 4 * hb), (R, 3 * hb, hb), (R, 4 * hb, hb), (R, hb, vb)]
+        atb = [(hb, R, hb), (4 * hb, R, hb), (hb, R, 4 * hb), (hb, R, 3 * hb), (vb, R, hb)]
+        need = [2 * m * k + 2 * k * n + (m * n if full else 0) for m, k, n, full in ab]
+        need += [2 * n * k + (0 if peer else 3 * m * n) for m, k, n in abt]
+        need += [2 * t * m + (0 if peer else 2 * m * n) for m, t, n in atb]
+        need.append(vb * hb)  # embedding backward staging (column reduce)
+        return max(need)
+
     def make_workspace(self, checkpointing: bool = True, eager_update: bool = False, merge_fwd_bwd: bool = False,
                        planned: bool = False) -> Workspace:
-        """Per-position arenas. Accounting only: the fused kernels allocate
-        differently from the reference's plan, so capacities are not enforced."""
-        return Workspace(self.mesh.p, capacities=None, merge_fwd_bwd=merge_fwd_bwd, device=self.mesh.device())
+        """Per-position arenas (membuf.py:74-127); ``planned`` enforces
+        workspace_capacities (BufferOverflowError on overflow, model.py:219-222)."""
+        caps = self.workspace_capacities(checkpointing, eager_update) if planned else None
+        return Workspace(self.mesh.p, capacities=caps, merge_fwd_bwd=merge_fwd_bwd, device=self.mesh.device())
 
     # ------------------------------------------------------------------ forward / backward
     def forward(self, tokens, labels, ws: Workspace, store: CheckpointStore | None = None, cls_labels=None, *,
@@ -512,7 +570,7 @@ def _device_random(mesh: Mesh, rows: int, cols: int, cfg: ModelConfig, seed: int
         if not mesh.owns(o):
             continue
         gen.manual_seed(seed * 7919 + k)
-        blk = padded_empty((rb, cb), F32, mesh.device())
+        blk = mesh.persistent_empty((rb, cb), F32)
         blk.uniform_(-lim, lim, generator=gen)
         if rows_real is not None and (l + 1) * rb > rows_real:
             first_pad = max(rows_real - l * rb, 0)
@@ -522,7 +580,7 @@ def _device_random(mesh: Mesh, rows: int, cols: int, cfg: ModelConfig, seed: int
 
 
 def run_loss_and_grads(model: MeshModel, tokens, labels, checkpointing: bool = True, cls_labels=None,
-                       merge_fwd_bwd: bool = False, planned: bool = False, eager_update: bool = False,
+                       merge_fwd_bwd: bool = False, planned: bool = True, eager_update: bool = False,
                        lr: float = 0.0):
     """One forward + backward; returns (loss, grads, workspace, store) (model.py:414-424)."""
     ws = model.make_workspace(checkpointing=checkpointing, eager_update=eager_update, merge_fwd_bwd=merge_fwd_bwd,

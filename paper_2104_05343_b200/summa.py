@@ -93,8 +93,9 @@ def _layout_grid(mesh: Mesh, layout: str) -> tuple[int, int]:
 
 
 def scatter(global_mat, mesh: Mesh, ws=None, category: str = "free", *, dtype: torch.dtype = F32,
-            layout: str = "act") -> ShardedMatrix:
-    """Split a global matrix (numpy or torch) into device blocks (summa.py:59-77)."""
+            layout: str = "act", persistent: bool = False) -> ShardedMatrix:
+    """Split a global matrix (numpy or torch) into device blocks (summa.py:59-77);
+    ``persistent`` blocks come from ``mesh.persistent_empty`` (weight masters)."""
     g = torch.as_tensor(np.asarray(global_mat) if not isinstance(global_mat, torch.Tensor) else global_mat)
     if g.dim() != 2:
         raise ShapeError(f"scatter expects a 2-d matrix, got {g.dim()}-d")
@@ -110,8 +111,11 @@ def scatter(global_mat, mesh: Mesh, ws=None, category: str = "free", *, dtype: t
         if not mesh.owns(owner):
             continue
         src = g[i * rb:(i + 1) * rb, j * cb:(j + 1) * cb]
-        blk = ws.empty(owner, (rb, cb), category, dtype=dtype) if ws is not None else \
-            padded_empty((rb, cb), dtype, mesh.device(owner))
+        if persistent:
+            blk = mesh.persistent_empty((rb, cb), dtype)
+        else:
+            blk = ws.empty(owner, (rb, cb), category, dtype=dtype) if ws is not None else \
+                padded_empty((rb, cb), dtype, mesh.device(owner))
         blk.copy_(src.to(device=blk.device, dtype=dtype))
         s.blocks[k] = blk
     return s
@@ -184,6 +188,13 @@ def _finish(mesh, acc_blocks, out_blocks, bias, c_blocks, act, aux_blocks, alpha
                    aux=None if aux_blocks is None else aux_blocks[k], alpha=alpha)
 
 
+def _reset_workspace(ws) -> None:
+    """Every SUMMA product starts with an empty "workspace" arena (its staging and partial
+    sums live for one product), as the reference resets it per step (summa.py:105, 129, 153)."""
+    if ws is not None and hasattr(ws, "reset_all"):
+        ws.reset_all("workspace")
+
+
 def _check_pair(mesh, a, b, need_a, need_b, what):
     if a.grid != _layout_grid(mesh, need_a) or b.grid != _layout_grid(mesh, need_b):
         raise ConfigError(f"{what}: operands need layouts ({need_a}, {need_b}) on a {mesh.r}x{mesh.c} mesh")
@@ -201,6 +212,7 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
     last step.
     """
     mesh = check_same_mesh(a, b)
+    _reset_workspace(ws)
     if a.global_cols != b.global_rows:
         raise ShapeError(f"summa_ab inner dims differ: {a.global_cols} vs {b.global_rows}")
     _check_pair(mesh, a, b, "act", "weight", "summa_ab")
@@ -273,6 +285,7 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
     they are attached to the result as ``ln_stats`` (per-device [rows, 2]).
     """
     mesh = check_same_mesh(a, b)
+    _reset_workspace(ws)
     if a.global_cols != b.global_cols:
         raise ShapeError(f"summa_abt contraction dims differ: {a.global_cols} vs {b.global_cols}")
     _check_pair(mesh, a, b, "act", "weight", "summa_abt")
@@ -326,6 +339,9 @@ def summa_abt(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
         if fuse_ln:
             res.ln_stats = ln_stats
         return res
+    if mesh.peer is not None:
+        return _abt_peer(mesh, ws, a16, b16, out, m_b, k_b, n_b, res_b, act, aux_b, colsum, tag, a.global_rows,
+                         b.global_rows)
     # dist pipeline: B(l+1, j) arrives while step l's partial product runs, and step
     # l's row reduce overlaps step l+1's product (two partial-sum slots)
     acc = _new_blocks(mesh, ws, (m_b, n_b), "workspace", F32)
@@ -368,6 +384,7 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
     weight-gradient product (in-place TMA reduce-add, local meshes).
     """
     mesh = check_same_mesh(a, b)
+    _reset_workspace(ws)
     if a.global_rows != b.global_rows:
         raise ShapeError(f"summa_atb contraction dims differ: {a.global_rows} vs {b.global_rows}")
     _check_pair(mesh, a, b, "act", "act", "summa_atb")
@@ -393,8 +410,10 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
                     dst = out[k] if i == mesh.r - 1 else chain
                     K.gemm(a16.block(i, l).t(), b16.block(i, j), dst, c=prev, alpha=alpha)
         return out_mat
+    if mesh.peer is not None:
+        return _atb_peer(mesh, ws, a16, b16, out_mat, m_b, t_b, n_b, acc_in, alpha, tag)
     if alpha != 1.0:
-        raise ConfigError("summa_atb: alpha is supported on local meshes only")
+        raise ConfigError("summa_atb: alpha needs a local mesh or peer memory")
     # dist pipeline: A(i, l+1) arrives while step l's partial product runs, and step
     # l's column reduce overlaps step l+1's product
     a_rx = _rx_slots(mesh, ws, (t_b, m_b))
@@ -426,6 +445,96 @@ def summa_atb(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free"
             red_prev[0].finish(red_prev[1], accumulate=acc_in)
         red_prev = red
     red_prev[0].finish(red_prev[1], accumulate=acc_in)
+    return out_mat
+
+
+def _abt_peer(mesh, ws, a16, b16, out, m_b, k_b, n_b, res_b, act, aux_b, colsum, tag, rows,
+              cols) -> ShardedMatrix:
+    """Dist AB^T with the row reduce fused into the GEMMs (peer memory, peer.py).
+
+    Step l: B(l, j) arrives down column j (R2, double-buffered, step l+1 in flight);
+    position (i, j)'s partial A(i,j) B(l,j)^T leaves its GEMM epilogue as a TMA
+    reduce-add straight into the fp32 accumulator of the destination (i, l)
+    (summa.py:128-139 reduce_row, mesh.py:458-475). No partial-sum buffers, reduce
+    collectives or fold passes; two row barriers: accumulators zeroed before the
+    first remote add, all adds landed before the epilogue reads them. The epilogue
+    (residual, GELU', column sums) then runs on the destination's complete sum.
+    """
+    f = mesh.my_flat
+    i = f // mesh.c
+    acc, peers = mesh.peer.scratch("abt_acc", (m_b, n_b))
+    K.zero(full_storage(acc))
+    mesh.peer.barrier("row")
+    b_rx = _rx_slots(mesh, ws, (n_b, k_b))
+
+    def issue(l):
+        return mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag)
+
+    pend = issue(0)
+    for l in range(mesh.c):
+        nxt = issue(l + 1) if l + 1 < mesh.c else None
+        b_pan = pend.wait()
+        pend = nxt
+        mesh.charge("reduce", "row", l, m_b * n_b, tag)  # the reference's reduce_row, for the ledger
+        mesh.add_macs_all(m_b * k_b * n_b)
+        dst = peers[mesh.flat(i, l)]
+        K.gemm(a16.blocks[f], b_pan[f].t(), dst, c=dst)
+    mesh.peer.barrier("row")
+    accs = [None] * mesh.p
+    accs[f] = acc
+    _finish(mesh, accs, out, None, res_b, act, aux_b)
+    if colsum is not None:
+        K.colsum(out[f], colsum[f], accumulate=True)
+    return ShardedMatrix(mesh, rows, cols, out)
+
+
+def _atb_peer(mesh, ws, a16, b16, out_mat, m_b, t_b, n_b, acc_in, alpha, tag) -> ShardedMatrix:
+    """Dist A^T B with the column reduce fused into the GEMMs (peer memory).
+
+    Step l: A(i, l) arrives along row i (R1); position (i, j)'s partial
+    alpha A(i,l)^T B(i,j) is reduce-added by its GEMM epilogue into the owner of weight
+    block (l, j), position (l mod r, j) (summa.py:152-163 reduce_col). When the
+    destination blocks are themselves symmetric (weight masters: ``accumulate_into``
+    with alpha = -lr is the SGD step fused into the weight-gradient product) the adds
+    land in them directly; otherwise in a zeroed symmetric accumulator that the owner
+    copies (or adds) into its output blocks after the closing column barrier.
+    """
+    f = mesh.my_flat
+    i, j = divmod(f, mesh.c)
+    r, c = mesh.r, mesh.c
+    out = out_mat.blocks
+    heap = mesh.peer.heap
+    mine = [l for l in range(c) if l % r == i]
+    direct = acc_in and all(heap.is_sym(out[l * c + j]) for l in mine)
+    if not direct:
+        acc, peers = mesh.peer.scratch("atb_acc", (c // r, m_b, n_b))
+        K.zero(acc)
+    mesh.peer.barrier("col")
+    a_rx = _rx_slots(mesh, ws, (t_b, m_b))
+
+    def issue(l):
+        return mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag)
+
+    pend = issue(0)
+    for l in range(c):
+        nxt = issue(l + 1) if l + 1 < c else None
+        a_pan = pend.wait()
+        pend = nxt
+        mesh.charge("reduce", "col", l % r, m_b * n_b, tag)
+        mesh.add_macs_all(m_b * t_b * n_b)
+        owner = mesh.flat(l % r, j)
+        if direct:
+            dst = heap.peer(out[l * c + j], owner) if owner != f else out[l * c + j]
+        else:
+            dst = peers[owner][l // r]
+        K.gemm(a_pan[f].t(), b16.blocks[f], dst, c=dst, alpha=alpha)
+    mesh.peer.barrier("col")
+    if not direct:
+        for l in mine:
+            if acc_in:
+                K.fold(out[l * c + j], [acc[l // r]], accumulate=True)
+            else:
+                copy_block(out[l * c + j], acc[l // r])
     return out_mat
 
 

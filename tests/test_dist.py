@@ -130,7 +130,7 @@ def _summa_cpu_worker(rank, world, port, rows, cols, out_dir):
                "abt": sg.gather(sg.summa_abt(A, BT, ws)).tolist(),
                "atb": sg.gather(sg.summa_atb(A, A2, ws)).tolist(),
                "ref": [(a @ b).tolist(), (a @ bt.T).tolist(), (a.T @ a2).tolist()],
-               "collectives": m.collective_count()}
+               "collectives": m.collective_count(), "calls": dict(m.calls)}
         (out_dir / f"r{rank}.json").write_text(json.dumps(res))
     finally:
         dist.destroy_process_group()
@@ -150,16 +150,19 @@ def test_dist_summa_pipeline_cpu(tmp_path, rows, cols):
         # c steps of (row bcast + column bcast) for AB, (column bcast + row reduce) for
         # AB^T and (row bcast + column reduce) for A^T B
         assert res["collectives"] == 6 * cols
+        # the reduces run as dist.reduce to the destination (the NCCL branch; gloo on CPU)
+        assert res["calls"].get("reduce", 0) == cols * (cols > 1) + cols * (rows > 1), res["calls"]
+        assert res["calls"].get("allreduce", 0) == 0, res["calls"]
 
 
-def _gpu_worker(rank, world, port, rows, cols, out_dir):
+def _gpu_worker(rank, world, port, rows, cols, peer, out_dir):
     import paper_2104_05343_b200 as sg
     from oracle import model_ref as M
 
     _init(rank, world, port)
     try:
         torch.cuda.set_device(0)
-        m = sg.create_mesh(sg.MeshConfig(rows=rows, cols=cols), backend="dist")
+        m = sg.create_mesh(sg.MeshConfig(rows=rows, cols=cols), backend="dist", peer=peer)
         rng = np.random.default_rng(0)
         bf = lambda a: torch.as_tensor(a, dtype=torch.float32).bfloat16().double().numpy()  # noqa: E731
         a = bf(rng.standard_normal((16 * rows, 16 * cols)))
@@ -176,6 +179,10 @@ def _gpu_worker(rank, world, port, rows, cols, out_dir):
         err["abt"] = rel(sg.gather(sg.summa_abt(A, BT, ws)), a @ bt.T)
         a2 = bf(rng.standard_normal((16 * rows, 24 * cols)))
         err["atb"] = rel(sg.gather(sg.summa_atb(A, sg.scatter(a2, m), ws)), a.T @ a2)
+        # with peer memory the AB^T / A^T B reduces are remote reduce-adds of the GEMM
+        # epilogues: no reduce / all-reduce collective, two barriers per product
+        err["summa_calls"] = dict(m.calls)
+        err["barriers"] = 0 if m.peer is None else m.peer.barriers
         cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=61, num_layers=2)
         rcfg = M.RefConfig(4, 16, 64, 8, 61, 2)
         params = {k: bf(v) for k, v in M.init_params(rcfg, 23).items()}
@@ -206,12 +213,22 @@ def _gpu_worker(rank, world, port, rows, cols, out_dir):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("peer", [True, False])
 @pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2)])
-def test_dist_backend_on_one_gpu(tmp_path, rows, cols):
+def test_dist_backend_on_one_gpu(tmp_path, rows, cols, peer):
+    """Processes sharing one B200: peer=True maps each other's arenas by CUDA IPC (the
+    fused-reduce product path); peer=False is the collective-reduce path."""
     world = rows * cols
-    mp.spawn(_gpu_worker, args=(world, _free_port(), rows, cols, tmp_path), nprocs=world, join=True)
+    mp.spawn(_gpu_worker, args=(world, _free_port(), rows, cols, peer, tmp_path), nprocs=world, join=True)
     for rank in range(world):
         err = json.loads((tmp_path / f"r{rank}.json").read_text())
         assert err["ab"] < 1e-4 and err["abt"] < 1e-4 and err["atb"] < 1e-4, err
         assert err["loss"] < 1e-3 and err["grads"] < 2e-2, err
         assert err["train_step"] < 1e-5 and err["train_step_vs_1x1"] < 2e-2, err
+        calls = err["summa_calls"]
+        if peer:
+            assert calls.get("reduce", 0) == 0 and calls.get("allreduce", 0) == 0, calls
+            # abt: one row group, atb: one column group, 2 barriers each (groups of 1 skip)
+            assert err["barriers"] == 2 * (cols > 1) + 2 * (rows > 1), err
+        else:
+            assert calls.get("reduce", 0) + calls.get("allreduce", 0) == cols * (cols > 1) + cols * (rows > 1), calls
