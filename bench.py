@@ -67,6 +67,12 @@ def parse():
                     help="train: fwd+bwd+SGD step; infer: forward (with the CE loss, as the reference) only")
     ap.add_argument("--max-batch", action="store_true",
                     help="after the timed run, find the largest global batch that fits (doubling, then bisection)")
+    ap.add_argument("--placement", choices=("natural", "bunched"), default="natural",
+                    help="rank placement of the mesh positions (mesh.py:230-275)")
+    ap.add_argument("--node-size", type=int, default=0,
+                    help="GPUs per placement node (default: all GPUs of the run = one NVSwitch node)")
+    ap.add_argument("--compare-1d", choices=("auto", "on", "off"), default="auto",
+                    help="also time one 2D layer against the Megatron 1D layer on the same GPUs (auto: N > 1)")
     return ap.parse_args()
 
 
@@ -108,6 +114,54 @@ def peaks() -> dict:
         return {"bf16_burst": d.get("bf16_tflops", 1590.0), "bf16_sustained": d.get("bf16_tflops_sustained", 1409.0),
                 "hbm": d.get("hbm_gbs", 6650.0), "src": "measured (MEASURED_PEAKS.json)"}
     return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+_FORM = {"qkv": "ab", "dense": "ab", "fc1": "ab", "fc2": "ab", "dx_lmhead": "ab", "dctx": "abt", "dact": "abt",
+         "dx_qkv": "abt", "dx_fc1": "abt", "logits": "abt", "dw_dense": "atb", "dw_qkv": "atb", "dw1": "atb",
+         "dw2": "atb", "dw_table": "atb"}
+
+
+def nvlink_peak() -> dict:
+    """Per-direction NVLink bandwidth: tools/nvlink_probe.py's measurement when committed,
+    else the B200 NVLink 5 figure (900 GB/s per direction)."""
+    p = ROOT / "profiles" / "nvlink_probe.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        if d.get("gbs"):
+            return {"gbs": d["gbs"], "src": "measured (profiles/nvlink_probe.json)"}
+    return {"gbs": 900.0, "src": "spec (NVLink 5, per direction; unmeasured: one-GPU pool)"}
+
+
+def gemm_rooflines(by_tag: dict, mesh, pk: dict) -> list:
+    """Each SUMMA product of the step against its roofline: the slower of the tensor-core
+    time (2 M N K / sustained bf16 peak) and its panel bytes per device at NVLink bandwidth
+    (SURVEY.md §8d). Per local launch (M, N, K): AB receives the A panel M K (all but the
+    root column's steps) and the B panel K N (all but the root row's); AB^T receives the
+    B^T panel N K and sends its fp32 partial M N to the row destination; A^T B receives the
+    A panel K M and sends its fp32 partial M N to the column destination."""
+    r, c = mesh.r, mesh.c
+    fa, fb = (c - 1) / c, (r - 1) / r
+    nv = nvlink_peak()
+    rows = []
+    for tag, d in sorted(by_tag.items(), key=lambda kv: -kv[1]["ms"]):
+        form = _FORM.get(tag)
+        panel = 0.0
+        for (M, N, K, batch), count in d["shapes"].items():
+            per = {"ab": 2 * M * K * fa + 2 * K * N * fb, "abt": 2 * N * K * fb + 4 * M * N * fa,
+                   "atb": 2 * K * M * fa + 4 * M * N * fb}.get(form, 0.0) * batch
+            panel += per * count
+        t_tensor = d["flops"] / (pk["bf16_sustained"] * 1e12) * 1e3
+        t_link = panel / (nv["gbs"] * 1e9) * 1e3
+        roof = max(t_tensor, t_link)
+        rows.append({"product": tag, "form": form, "launches": d["launches"], "ms": d["ms"],
+                     "tflops": d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else None,
+                     "roofline_ms": roof, "bound": "nvlink" if t_link > t_tensor else "tensor",
+                     "frac": roof / d["ms"] if d["ms"] > 0 else None, "panel_bytes": panel,
+                     "local_shapes": {"x".join(map(str, k)): v for k, v in d["shapes"].items()}})
+    if rows:
+        rows[0]["peaks"] = {"tensor": f"{pk['bf16_sustained']} TF/s ({pk['src']} sustained)",
+                            "nvlink": f"{nv['gbs']} GB/s ({nv['src']})"}
+    return rows
 
 
 def gemm_traffic():
@@ -197,7 +251,7 @@ def _config(w, n_gpus, args, extra=None) -> dict:
     from paper_2104_05343_b200.mesh import mesh_for_world
 
     mc = mesh_for_world(n_gpus)
-    cfg = {"workload": w["name"], "model": f"2D transformer L={w['layers']} h={w['h']} n={w['n']} v={w['v']}",
+    cfg = {"workload": w["name"], "placement": args.placement, "model": f"2D transformer L={w['layers']} h={w['h']} n={w['n']} v={w['v']}",
            "global_batch": w["b"], "seq_len": w["s"], "hidden": w["h"], "heads": w["n"], "layers": w["layers"],
            "vocab": w["v"], "mesh": f"{mc.rows}x{mc.cols}", "parallelism": f"2d-summa r{mc.rows}xc{mc.cols}",
            "checkpointing": bool(args.checkpointing), "cuda_graph": not args.no_graph,
@@ -234,7 +288,10 @@ def main():
         os.environ.setdefault("NCCL_MAX_NCHANNELS", os.environ.get("SG_SM_RESERVE", "8"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args)
-    mesh = sg.create_mesh(sg.mesh_for_world(world), backend="dist" if world > 1 else "local")
+    mc = sg.mesh_for_world(world)
+    mc = sg.MeshConfig(rows=mc.rows, cols=mc.cols, node_size=args.node_size or world,
+                       placement=sg.Placement(args.placement))
+    mesh = sg.create_mesh(mc, backend="dist" if world > 1 else "local")
     cfg = sg.ModelConfig(b=w["b"], s=w["s"], h=w["h"], n=w["n"], v=w["v"], num_layers=w["layers"])
     model = sg.MeshModel(mesh, cfg, None, seed=1234)
     ws = model.make_workspace(checkpointing=args.checkpointing)
@@ -349,6 +406,7 @@ def main():
     gsum = prof.summary()
     inst_step_ms = s_ev0.elapsed_time(s_ev1)
     pk = peaks()
+    per_gemm = gemm_rooflines(prof.by_tag(), mesh, pk)
     traffic = gemm_traffic()
     roof = {"kernel": "sg_gemm (tcgen05 persistent GEMM)", "bound": "tensor", "achieved": gsum["tflops"],
             "peak": pk["bf16_sustained"], "unit": "TFLOP/s", "frac": gsum["tflops"] / pk["bf16_sustained"],
@@ -360,7 +418,7 @@ def main():
             # and is host-launch bound, so it is not the denominator
             "gemm_share_of_step": gsum["ms"] / ms_step if ms_step > 0 else None,
             "instrumented_step_ms": inst_step_ms,
-            "algorithmic_flops_per_step": gsum["flops"]}
+            "algorithmic_flops_per_step": gsum["flops"], "per_gemm": per_gemm}
 
     # ------------------------------------------------------------- SUMMA sweep point (configs[1])
     summa = summa_point(sg, K, mesh, args.summa_n, pk, barrier, world)
@@ -375,6 +433,10 @@ def main():
         r = cpu_sample(w, args.mode)
         cpu = {"value": r["samples_per_s"], "unit": "samples/s", "cores": cpu_bench.host_cores(), "kind": "port",
                "sample": r["sample"]}
+
+    cmp1d = None
+    if args.compare_1d == "on" or (args.compare_1d == "auto" and world > 1):
+        cmp1d = compare_1d(sg, K, mesh, w, barrier, world)
 
     maxb = None
     if args.max_batch:
@@ -399,9 +461,72 @@ def main():
                 "clocks": clocks.summary(), "final_loss": final_loss}
         if maxb is not None:
             line["max_batch"] = maxb
+        if cmp1d is not None:
+            line["optimus_vs_megatron"] = cmp1d
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def compare_1d(sg, K, mesh, w, barrier, world, iters: int = 5) -> dict:
+    """One transformer layer fwd + bwd in the 2D (SUMMA) partition against the paper's
+    Megatron 1D baseline (baseline.py:40-224) on the same GPUs, same
+    shape and parameters: per-layer ms (CUDA events, max over ranks) and the speed-up."""
+    import numpy as np
+    import torch
+
+    from paper_2104_05343_b200.baseline1d import Baseline1DLayer
+    from paper_2104_05343_b200.layers import LayerParams, RowHostedVector, TransformerLayer, interleave_qkv
+    from paper_2104_05343_b200.summa import as_bf16
+
+    cfg = sg.ModelConfig(b=w["b"], s=w["s"], h=w["h"], n=w["n"], v=w["v"], num_layers=1)
+    g = {k[len("layers.0."):]: v for k, v in sg.init_global_params(cfg, 5).items() if k.startswith("layers.0.")}
+    c = mesh.c
+    mats = {k: sg.scatter(interleave_qkv(g[k], c) if k == "w_qkv" else g[k], mesh, layout="weight")
+            for k in ("w_qkv", "w_dense", "w1", "w2")}
+    for m in mats.values():
+        m.bf16_twin = as_bf16(m)
+    vecs = {k: RowHostedVector.split(interleave_qkv(g[k], c) if k == "b_qkv" else g[k], c, mesh=mesh)
+            for k in ("b_qkv", "b_dense", "b1", "b2", "ln1_gamma", "ln1_beta", "ln2_gamma", "ln2_beta")}
+    layer2d = TransformerLayer(mesh, cfg, LayerParams(**mats, **vecs))
+    layer1d = Baseline1DLayer(mesh, cfg, g)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((cfg.b * cfg.s, cfg.h)).astype(np.float32)
+    xs, dys = sg.scatter(x, mesh), sg.scatter(x, mesh)
+    xd = torch.as_tensor(x).cuda()
+
+    def run2d():
+        ws = sg.Workspace(mesh.p)
+        out, saved = layer2d.forward(xs, ws)
+        layer2d.backward(dys, saved, ws)
+
+    def run1d():
+        ws = sg.Workspace(mesh.p)
+        out, saved = layer1d.forward(xd, ws)
+        layer1d.backward(xd, saved, ws, host_grads=False)
+
+    res = {"mesh_2d": f"{mesh.r}x{mesh.c}", "partition_1d": f"1x{mesh.p} (Megatron)", "layer": "1 layer fwd+bwd",
+           "shape": {k: w[k] for k in ("b", "s", "h", "n")}}
+    for name, fn in (("ms_2d", run2d), ("ms_1d", run1d)):
+        fn()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        res[name] = ms
+    res["speedup_2d_over_1d"] = res["ms_1d"] / res["ms_2d"]
+    return res
 
 
 def max_batch_sweep(sg, mesh, w, args, world) -> dict:

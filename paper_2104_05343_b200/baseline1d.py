@@ -137,8 +137,9 @@ class Baseline1DLayer:
         return out, saved
 
     # ---------------------------------------------------------------- backward
-    def backward(self, dy, saved: dict, ws: Workspace):
-        """(dx, standard-layout parameter gradients as host arrays) (baseline.py:166-220)."""
+    def backward(self, dy, saved: dict, ws: Workspace, host_grads: bool = True):
+        """(dx, standard-layout parameter gradients as host arrays) (baseline.py:166-220);
+        ``host_grads=False`` keeps them as this process's device shards (timing)."""
         mesh, cfg = self.mesh, self.cfg
         p, bs = mesh.p, cfg.b * cfg.s
         n_loc, hp = cfg.n // p, cfg.h // p
@@ -187,6 +188,10 @@ class Baseline1DLayer:
             K.gemm(dqkv, sh["w_qkv"].t(), parts[d])
         da1 = self._all_reduce(parts, "baseline")
         dx, _, gb1 = self._ln_bwd(da1, saved["ln1"], dy1, ws, dev0)
+        if not host_grads:
+            return dx, {"w_qkv": dwqkv, "b_qkv": dbqkv, "w_dense": dwd, "w1": dw1, "b1": db1, "w2": dw2,
+                        "b2": b2_grad, "ln": (gb1, gb2)}
+
         def host(ts, axis):
             return np.concatenate(_gather_parts(mesh, ts), axis=axis)
 

@@ -673,6 +673,7 @@ struct FlashBwdParams {
   __nv_bfloat16* dV;
   long long ldg;
   int dkv_b2_first;   // dK / dV tile maps: heads before rows
+  int b0;             // first sequence of this launch (batch chunks keep the item table bounded)
   float* kv_colsum;   // optional [2 nh 64]: += column sums of dK (then dV)
 };
 
@@ -734,7 +735,7 @@ __global__ void __launch_bounds__(512, 1)
     kb = t % nkb;
     const int r = t / nkb;
     h = r % p.nh;
-    b = r / p.nh;
+    b = r / p.nh + p.b0;
   };
   const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int total = my_items * nqb;
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(512, 1)
   for (int it = threadIdx.x; it < my_items && it < kMaxItems; it += blockDim.x) {
     int kb, h, b;
     decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
-    items_tab[it] = kb | (h << 10) | (b << 20);
+    items_tab[it] = kb | (h << 10) | ((b - p.b0) << 20);
   }
   tc_fence_before();
   __syncthreads();
@@ -782,7 +783,7 @@ __global__ void __launch_bounds__(512, 1)
     const int v = items_tab[it];
     kb = v & 1023;
     h = (v >> 10) & 1023;
-    b = v >> 20;
+    b = (v >> 20) + p.b0;
   };
 
   if (warp == 0) {
@@ -1160,7 +1161,7 @@ __global__ void __launch_bounds__(512, 1)
     kb = t % nkb;
     const int r = t / nkb;
     h = r % p.nh;
-    b = r / p.nh;
+    b = r / p.nh + p.b0;
   };
   const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int total = my_items * nqb;
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(512, 1)
   for (int it = threadIdx.x; it < my_items && it < kMaxItems; it += blockDim.x) {
     int kb, h, b;
     decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
-    items_tab[it] = kb | (h << 10) | (b << 20);
+    items_tab[it] = kb | (h << 10) | ((b - p.b0) << 20);
   }
   tc_fence_before();
   __syncthreads();
@@ -1196,7 +1197,7 @@ __global__ void __launch_bounds__(512, 1)
     const int v = items_tab[it];
     kb = v & 1023;
     h = (v >> 10) & 1023;
-    b = v >> 20;
+    b = (v >> 20) + p.b0;
   };
 
   if (warp == 0) {
@@ -1544,23 +1545,31 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   constexpr size_t SMEM64 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
   const int nkb = (int)((s + 127) / 128);
-  const int items = nkb * (int)nh * (int)b;
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
-  if (nkb > 1024 || nh > 1024 || b > 2047 || (items + sms - 1) / sms > kMaxItems)
-    return set_error(SG_ERR_SHAPE, "flash bwd: too many key blocks / heads / sequences for the item table");
+  if (nkb > 1024 || nh > 1024) return set_error(SG_ERR_SHAPE, "flash bwd: more than 1024 key blocks / heads");
+  // sequences per launch: every CTA's items must fit its item table (large batches run
+  // as several back-to-back launches over batch chunks)
+  const long long per_seq = (long long)nkb * nh;
+  long long max_items = (long long)kMaxItems * sms;
+  if (const char* e = getenv("SG_FLASH_ITEMS_MAX")) max_items = std::max(1LL, std::min(max_items, atoll(e)));  // tests
+  const int chunk = (int)std::max<long long>(1, std::min<long long>(2047, max_items / per_seq));
+  if (per_seq > (long long)kMaxItems * sms) return set_error(SG_ERR_SHAPE, "flash bwd: one sequence exceeds the item table");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (d == 64) {
-    if (!ensure_smem(reinterpret_cast<const void*>(flash_bwd2_kernel), (int)SMEM64))
-      return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
-    launch_k(flash_bwd2_kernel, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq, tdk, tdv, p,
-             (int)b);
-  } else {
-    if (!ensure_smem(reinterpret_cast<const void*>(flash_bwd128_kernel), (int)SMEM128))
-      return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
-    launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk, tdv,
-             p, (int)b);
+  const void* kern = d == 64 ? reinterpret_cast<const void*>(flash_bwd2_kernel)
+                             : reinterpret_cast<const void*>(flash_bwd128_kernel);
+  if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : SMEM128))) return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
+  for (long long b0 = 0; b0 < b; b0 += chunk) {
+    const int bc = (int)std::min<long long>(chunk, b - b0);
+    const int items = (int)(per_seq * bc);
+    p.b0 = (int)b0;
+    if (d == 64)
+      launch_k(flash_bwd2_kernel, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq, tdk, tdv, p,
+               bc);
+    else
+      launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk,
+               tdv, p, bc);
+    count_launch();
   }
-  count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
 }

@@ -216,7 +216,7 @@ __global__ void ln_fwd_kernel(const TX* __restrict__ x, long long rows, int cols
     }
     const float mu = s1 * inv_h;
     const float var = fmaxf(s2 * inv_h - mu * mu, 0.f);  // one-pass variance (layers.py:296-297), clamped: fp32 cancellation on near-constant rows
-    const float rs = 1.0f / sqrtf(var + eps);
+    const float rs = rsqrtf(var + eps)  /* MUFU.RSQ: no IEEE-division slow-path call */;
     for (int c = lane * 8; c < cols; c += 256) {
       const int n = min(8, cols - c);
       float v[8], g[8], b[8];
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(256) dgelu_kernel(const bf16* dact, long long 
 // read of x; the (sum, sumsq) row statistics come from the mesh all-reduce
 // (stats != nullptr) or, on a 1-column mesh, from the registers themselves.
 template <typename TX, typename TY, int NV>
-__global__ void __launch_bounds__(256, NV <= 4 ? 4 : 1) ln_fwd_rows_kernel(
+__global__ void __launch_bounds__(256, NV <= 2 ? 4 : (NV == 4 ? 2 : 1)) ln_fwd_rows_kernel(
     const TX* __restrict__ x, long long rows, long long ldx, const float* __restrict__ stats, float inv_h, float eps,
     const float* __restrict__ gamma, const float* __restrict__ beta, TY* __restrict__ y, long long ldy,
     float* __restrict__ mean_out, float* __restrict__ rstd_out) {
@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(256, NV <= 4 ? 4 : 1) ln_fwd_rows_kernel(
       }
       mu[u] = s1 * inv_h;
       const float var = fmaxf(s2 * inv_h - mu[u] * mu[u], 0.f);  // one-pass variance (layers.py:296-297), clamped
-      rs[u] = 1.0f / sqrtf(var + eps);
+      rs[u] = rsqrtf(var + eps);
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {

@@ -155,18 +155,33 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     args.alpha = alpha
     prof = _GEMM_PROFILE
     if prof is not None:
-        s = torch.cuda.current_stream(out.device)
+        s = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-    with torch.cuda.device(out.device):
-        check(_lib.lib().sg_gemm(ctypes.byref(args), _stream(out)), "sg_gemm")
+    # launched on the current device (``out`` may be a peer-mapped block of another GPU)
+    check(_lib.lib().sg_gemm(ctypes.byref(args), _stream(out)), "sg_gemm")
     if prof is not None:
         e1.record(s)
-        prof.append((2.0 * M * N * K * args.nb1 * args.nb2, e0, e1, (M, N, K, args.nb1 * args.nb2)))
+        prof.append((2.0 * M * N * K * args.nb1 * args.nb2, e0, e1, (M, N, K, args.nb1 * args.nb2), _TAG[-1]))
     return out
 
 
 _GEMM_PROFILE = None
+_TAG = ["other"]
+
+
+class tagged:
+    """Label the GEMM launches inside the block (per-product roofline lists)."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        _TAG.append(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        _TAG.pop()
 
 
 class profile_gemms:
@@ -192,6 +207,17 @@ class profile_gemms:
         ms = sum(r[1].elapsed_time(r[2]) for r in self.records)
         return {"launches": len(self.records), "flops": flops, "ms": ms,
                 "tflops": flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0}
+
+    def by_tag(self) -> dict:
+        """Per product label: launches, flops, ms and the distinct local shapes."""
+        out: dict = {}
+        for fl, e0, e1, shape, tag in self.records:
+            d = out.setdefault(tag, {"launches": 0, "flops": 0.0, "ms": 0.0, "shapes": {}})
+            d["launches"] += 1
+            d["flops"] += fl
+            d["ms"] += e0.elapsed_time(e1)
+            d["shapes"][shape] = d["shapes"].get(shape, 0) + 1
+        return out
 
 
 def launch_count() -> int:

@@ -587,7 +587,7 @@ def attention_forward(x: ShardedMatrix, w_qkv: ShardedMatrix, b_qkv: RowHostedVe
     cfg.validate_mesh(mesh)
     hb = cfg.h // mesh.c
     bs_loc = (cfg.b // mesh.r) * cfg.s
-    qkv = summa_ab(x, w_qkv, ws, out_category="forward", tag="summa", out_dtype=BF16,
+    qkv = _tagged("qkv", summa_ab, x, w_qkv, ws, out_category="forward", tag="summa", out_dtype=BF16,
                    bias=[None if d is None else b_qkv.for_position(mesh, d) for d in _all(mesh)])
     ctx_blocks, probs, lse = [None] * mesh.p, [None] * mesh.p, [None] * mesh.p
     mac_per_dev = (cfg.b // mesh.r) * (cfg.n // mesh.c) * cfg.s * cfg.s * cfg.head_dim
@@ -596,7 +596,7 @@ def attention_forward(x: ShardedMatrix, w_qkv: ShardedMatrix, b_qkv: RowHostedVe
         ctx_blocks[dev] = ws.empty(dev, (bs_loc, hb), "free", dtype=BF16)
         probs[dev], lse[dev] = _local_attention(cfg, mesh, qkv.blocks[dev], ctx_blocks[dev], ws, dev)
     ctx_mat = ShardedMatrix(mesh, cfg.b * cfg.s, cfg.h, ctx_blocks)
-    out = summa_ab(ctx_mat, w_dense, ws, out_category="forward", tag="summa", out_dtype=F32,
+    out = _tagged("dense", summa_ab, ctx_mat, w_dense, ws, out_category="forward", tag="summa", out_dtype=F32,
                    bias=[None if d is None else b_dense.for_position(mesh, d) for d in _all(mesh)], resid=resid)
     return out, AttentionContext(x_in=x, qkv=qkv, saved_probs=probs, ctx_mat=ctx_mat, cfg=cfg,
                                  lse=lse if flash_ok(cfg) else None)
@@ -653,6 +653,12 @@ def attention_core_backward(cfg: ModelConfig, b_loc: int, n_loc: int, qkv_blk, c
     return dq_blk
 
 
+def _tagged(name: str, fn, *args, **kw):
+    """Run a SUMMA product with its GEMM launches labelled ``name`` (bench roofline list)."""
+    with K.tagged(name):
+        return fn(*args, **kw)
+
+
 def _all(mesh: Mesh) -> list:
     return [d if mesh.owns(d) else None for d in range(mesh.p)]
 
@@ -682,8 +688,8 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     hb = cfg.h // mesh.c
     dy16 = _bf16_of(out_grad, ws)
     _, b_dense_grad = bias_add_backward(out_grad, ws)
-    dctx = summa_abt(dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
-    w_dense_grad = _weight_grad(ctx.ctx_mat, dy16, w_dense, ws, lr)
+    dctx = _tagged("dctx", summa_abt, dy16, w_dense, ws, out_category="backward", out_dtype=BF16)
+    w_dense_grad = _tagged("dw_dense", _weight_grad, ctx.ctx_mat, dy16, w_dense, ws, lr)
     bq_parts = new_colsum_parts(mesh, ws, 3 * hb)  # b_qkv gradient fused into dQ / dK / dV epilogues
     mesh.add_macs_all(4 * b_loc * n_loc * cfg.s * cfg.s * cfg.head_dim)  # dP, dV, dQ, dK (layers.py:457)
     dqkv_blocks = [None] * mesh.p
@@ -695,8 +701,8 @@ def attention_backward(out_grad: ShardedMatrix, ctx: AttentionContext, w_qkv: Sh
     dqkv = ShardedMatrix(mesh, cfg.b * cfg.s, 3 * cfg.h, dqkv_blocks)
     dqkv.colsum_parts = bq_parts
     _, b_qkv_grad = bias_add_backward(dqkv, ws)
-    x_grad = summa_abt(dqkv, w_qkv, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
-    w_qkv_grad = _weight_grad(ctx.x_in, dqkv, w_qkv, ws, lr)
+    x_grad = _tagged("dx_qkv", summa_abt, dqkv, w_qkv, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
+    w_qkv_grad = _tagged("dw_qkv", _weight_grad, ctx.x_in, dqkv, w_qkv, ws, lr)
     return x_grad, w_qkv_grad, b_qkv_grad, w_dense_grad, b_dense_grad
 
 
@@ -720,10 +726,10 @@ def mlp_forward(x: ShardedMatrix, w1: ShardedMatrix, b1: RowHostedVector, w2: Sh
     for dev in mesh.local_devs:
         mid_blocks[dev] = ws.empty(dev, (rows, cols4), "forward", dtype=BF16)
     mid = ShardedMatrix(mesh, x.global_rows, 4 * cfg.h, mid_blocks)
-    act = summa_ab(x, w1, ws, out_category="free", tag="summa", out_dtype=BF16,
+    act = _tagged("fc1", summa_ab, x, w1, ws, out_category="free", tag="summa", out_dtype=BF16,
                    bias=[None if d is None else b1.for_position(mesh, d) for d in _all(mesh)], act=K.ACT_GELU,
                    aux=mid)
-    out = summa_ab(act, w2, ws, out_category="forward", tag="summa", out_dtype=F32,
+    out = _tagged("fc2", summa_ab, act, w2, ws, out_category="forward", tag="summa", out_dtype=F32,
                    bias=[None if d is None else b2.for_position(mesh, d) for d in _all(mesh)], resid=resid)
     return out, MlpContext(x_in=x, mid=mid, act=act)
 
@@ -738,13 +744,13 @@ def mlp_backward(out_grad: ShardedMatrix, ctx: MlpContext, w1: ShardedMatrix, w2
     b1_parts = new_colsum_parts(mesh, ws, ctx.mid.block_cols)
     # GELU' (from the saved pre-activation, TMA-loaded per output tile) and the b1
     # gradient column sums fused into the dAct product's epilogue (layers.py:502-504)
-    dmid = summa_abt(dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
+    dmid = _tagged("dact", summa_abt, dy16, w2, ws, out_category="backward", out_dtype=BF16, act=K.ACT_DGELU, aux=ctx.mid,
                      colsum=b1_parts)
     dmid.colsum_parts = b1_parts
-    w2_grad = _weight_grad(ctx.act, dy16, w2, ws, lr)
+    w2_grad = _tagged("dw2", _weight_grad, ctx.act, dy16, w2, ws, lr)
     _, b1_grad = bias_add_backward(dmid, ws)
-    x_grad = summa_abt(dmid, w1, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
-    w1_grad = _weight_grad(ctx.x_in, dmid, w1, ws, lr)
+    x_grad = _tagged("dx_fc1", summa_abt, dmid, w1, ws, out_category="backward", out_dtype=F32, ln_ctx=ln_ctx)
+    w1_grad = _tagged("dw1", _weight_grad, ctx.x_in, dmid, w1, ws, lr)
     return x_grad, w1_grad, b1_grad, w2_grad, b2_grad
 
 
@@ -946,7 +952,7 @@ class TransformerLayer:
             for dev in mesh.local_devs:
                 mid_blocks[dev] = ws.empty(dev, (a2.block_rows, 4 * cfg.h // mesh.c), "forward", dtype=BF16)
             mid = ShardedMatrix(mesh, a2.global_rows, 4 * cfg.h, mid_blocks)
-            act = summa_ab(a2, p.w1, ws, out_category="free", out_dtype=BF16,
+            act = _tagged("fc1", summa_ab, a2, p.w1, ws, out_category="free", out_dtype=BF16,
                            bias=[None if d is None else p.b1.for_position(mesh, d) for d in _all(mesh)],
                            act=K.ACT_GELU, aux=mid)
             mlp = MlpContext(x_in=a2, mid=mid, act=act)

@@ -315,7 +315,8 @@ class MeshModel:
                 layer_saves.append(saved)
         if getattr(x, "bf16_twin", None) is None and x.dtype != BF16:
             x.bf16_twin = as_bf16(x)  # one cast, shared by the logits and the table-gradient products
-        logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
+        with K.tagged("logits"):
+            logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, ce_ctx = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=return_tensor,
                                              label_ids=label_ids)
         if not return_tensor:
@@ -361,13 +362,16 @@ class MeshModel:
         if self.classifier:
             # the head adds into dx after the product: its bf16 twin and column sums are
             # formed later, by the layer (_bf16_of / bias_add_backward)
-            dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32)
+            with K.tagged("dx_lmhead"):
+                dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32)
         else:
             parts = new_colsum_parts(mesh, ws, cfg.h // mesh.c)  # last layer's b2 gradient, fused
-            dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32,
-                          want_bf16=True, colsum=parts)
+            with K.tagged("dx_lmhead"):
+                dx = summa_ab(dlogits, self.table, ws, out_category="conjunction", tag="lmhead", out_dtype=F32,
+                              want_bf16=True, colsum=parts)
             dx.colsum_parts = parts
-        table_grad = summa_atb(dlogits, saved.x_final, ws, out_category="param_grad_tied", tag="lmhead")
+        with K.tagged("dw_table"):
+            table_grad = summa_atb(dlogits, saved.x_final, ws, out_category="param_grad_tied", tag="lmhead")
         cls_w_grad = self._cls_backward(saved.cls_ctx, dx, ws, upstream) if self.classifier else None
         if saved.store is not None:
             dx0, layer_grads = checkpointed_backward(self.layers, dx, saved.store, ws, eager_update=eager_update,
@@ -489,7 +493,8 @@ class MeshModel:
         x = embedding_forward(tokens, self.table, cfg, ws, out_category="forward", ids=ids)
         for layer in self.layers:
             x, _ = layer.forward(x, ws)
-        logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
+        with K.tagged("logits"):
+            logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True, label_ids=label_ids)
         return loss
 

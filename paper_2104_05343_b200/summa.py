@@ -524,7 +524,10 @@ def _atb_peer(mesh, ws, a16, b16, out_mat, m_b, t_b, n_b, acc_in, alpha, tag) ->
         mesh.add_macs_all(m_b * t_b * n_b)
         owner = mesh.flat(l % r, j)
         if direct:
-            dst = heap.peer(out[l * c + j], owner) if owner != f else out[l * c + j]
+            # the owner's block (l, j) is its (l // r)-th block of this matrix: SPMD allocation
+            # put it at the offset of this position's own (l // r)-th block
+            mine_same = out[(i + (l // r) * r) * c + j]
+            dst = heap.peer(mine_same, owner) if owner != f else out[l * c + j]
         else:
             dst = peers[owner][l // r]
         K.gemm(a_pan[f].t(), b16.blocks[f], dst, c=dst, alpha=alpha)

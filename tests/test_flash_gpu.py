@@ -77,3 +77,34 @@ def test_flash_backward(b, s, nh, d):
         want = g[:, i * hb:(i + 1) * hb]
         err = (got - want).abs().max().item() / want.abs().max().item()
         assert err < 2e-2, (i, err)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_flash_backward_batch_chunks(d, monkeypatch):
+    """Large batches run as several launches over batch chunks (bounded per-CTA item
+    tables); forcing tiny chunks gives the same gradients as one launch."""
+    from paper_2104_05343_b200 import kernels as K
+
+    torch.manual_seed(3)
+    b, s, nh = 9, 256, 2
+    hb = nh * d
+    qkv = torch.randn(b * s, 3 * hb, device="cuda").bfloat16()
+    dout = torch.randn(b * s, hb, device="cuda").bfloat16()
+    out = torch.empty(b * s, hb, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, nh, s, device="cuda")
+    K.flash_attn_fwd(qkv, b, s, nh, d, out, lse)
+    drow = torch.empty(b, nh, s, device="cuda")
+    K.attn_rowdot(dout, out, nh, d, s, drow)
+    res = []
+    for items_max in (None, str(2 * nh * 2)):  # two sequences per launch
+        if items_max:
+            monkeypatch.setenv("SG_FLASH_ITEMS_MAX", items_max)
+        dq = torch.zeros(b * s, hb, device="cuda")
+        dqkv = torch.zeros(b * s, 3 * hb, device="cuda", dtype=torch.bfloat16)
+        cs = torch.zeros(2 * hb, device="cuda")
+        K.flash_attn_bwd(qkv, dout, lse, drow, b, s, nh, d, dq, dqkv, kv_colsum=cs)
+        torch.cuda.synchronize()
+        res.append((dq, dqkv[:, hb:].float(), cs))
+    monkeypatch.delenv("SG_FLASH_ITEMS_MAX", raising=False)
+    for a, c in zip(res[0], res[1]):
+        assert (a - c).abs().max().item() <= 1e-5 * a.abs().max().item() + 1e-6
