@@ -683,13 +683,15 @@ constexpr int kMaxItems = 256;           // per-CTA work items of the persistent
 // ----------------------------------------------------------------------------
 // Backward v2 (d = 64), persistent: CTA c walks work items t = c, c + grid, ...
 // with t = (key block, head, batch), key block fastest. Per query block:
-//   MMA   S_G+1, dP_G+1 are issued right after P_G / dS_G land in smem, ahead of
-//         dV_G, dK_G, dQ_G, so the next block's exponentials overlap this block's
-//         products — across item boundaries too (K / V double-buffered per item);
-//         dQ alternates between two TMEM buffers
+//   MMA   S_G+1, dP_G+1 are issued right after the softmax warps have read S_G / dP_G,
+//         ahead of dV_G, dK_G, dQ_G, so the next block's exponentials overlap this
+//         block's products — across item boundaries too (K double-buffered per
+//         item, V reloaded as soon as the item's last dP has read it); dV_G runs
+//         first and releases P at once, dS is double-buffered, so block G+1's P / dS
+//         stores wait only for dV_G (P) and for block G-1's dK / dQ (dS) instead of
+//         for all three products of block G; dQ alternates between two TMEM buffers
 //   warps 4-11 (lane quadrant x key half) compute P / dS for their 64 keys in
-//         registers and wait only for the previous products to release the smem
-//         tiles; lse / D row statistics are prefetched a block ahead
+//         registers; lse / D row statistics are prefetched a block ahead
 //   warps 12-15 (one per lane quadrant) drain dQ (TMEM -> smem -> TMA reduce-add)
 //         and at an item's end write its dK / dV (TMA stores, bias-gradient column
 //         sums) and release the TMEM accumulators
@@ -705,27 +707,30 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   uint8_t* sK = smem;                 // 2 slots (items)
-  uint8_t* sV = sK + 2 * kT64;        // 2 slots
-  uint8_t* sQ = sV + 2 * kT64;        // 2 slots (query blocks)
+  uint8_t* sV = sK + 2 * kT64;        // 1 slot
+  uint8_t* sQ = sV + kT64;            // 2 slots (query blocks)
   uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
   uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
-  uint8_t* sDS = sP + 2 * kT64;       // 32 KB
-  uint8_t* sStg = sDS + 2 * kT64;     // 4 drain warps x 8 KB (dQ fp32 / dK, dV bf16 staging)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 8 * 4096);
+  uint8_t* sDS = sP + 2 * kT64;       // 2 buffers x 32 KB
+  uint8_t* sStg = sDS + 4 * kT64;     // 4 drain warps x 4 KB (dQ fp32 / dK, dV bf16 staging)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 4096);
   int* items_tab = reinterpret_cast<int*>(bars + 32);  // this CTA's items as packed (kb, h, b)
-  uint64_t* kv_full = bars;        // [2]
-  uint64_t* kv_empty = bars + 2;   // [2]
+  uint64_t* k_full = bars;         // [2]
+  uint64_t* k_empty = bars + 2;    // [2]
   uint64_t* qd_full = bars + 4;    // [2]
   uint64_t* qd_empty = bars + 6;   // [2]
   uint64_t* s_full = bars + 8;
   uint64_t* ds_full = bars + 9;
-  uint64_t* bufs_free = bars + 10;
+  uint64_t* p_free = bars + 10;    // dV_G has read P_G
   uint64_t* dq_full = bars + 11;   // [2]
   uint64_t* dq_empty = bars + 13;  // [2]
   uint64_t* acc_full = bars + 15;
   uint64_t* acc_empty = bars + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   uint64_t* s_free = bars + 18;    // S_G / dP_G read out of TMEM (8 softmax warps)
+  uint64_t* v_full = bars + 19;
+  uint64_t* v_empty = bars + 20;   // the item's last dP has read V
+  uint64_t* ds_free = bars + 21;   // [2] dK_G / dQ_G have read dS buffer G & 1
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (p.s + 127) / 128;
@@ -749,16 +754,19 @@ __global__ void __launch_bounds__(512, 1)
     tma_prefetch_desc(&tmDK);
     tma_prefetch_desc(&tmDV);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
       mbar_init(&dq_full[i], 1);
       mbar_init(&dq_empty[i], 4);
+      mbar_init(&ds_free[i], 1);
     }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(ds_full, 8);
-    mbar_init(bufs_free, 1);
+    mbar_init(p_free, 1);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4);
     mbar_init(s_free, 8);
@@ -794,10 +802,12 @@ __global__ void __launch_bounds__(512, 1)
         int kb, h, b;
         decode(t, kb, h, b);
         const int ks = it & 1;
-        mbar_wait(&kv_empty[ks], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[ks], 2 * kT64);
-        tma4(&tmK, sK + ks * kT64, &kv_full[ks], 0, kb * 128, h, b, p.k_b2_first);
-        tma4(&tmV, sV + ks * kT64, &kv_full[ks], 0, kb * 128, h, b, p.v_b2_first);
+        mbar_wait(&k_empty[ks], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[ks], kT64);
+        tma4(&tmK, sK + ks * kT64, &k_full[ks], 0, kb * 128, h, b, p.k_b2_first);
+        mbar_wait(v_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full, kT64);
+        tma4(&tmV, sV, v_full, 0, kb * 128, h, b, p.v_b2_first);
         for (int i = 0; i < nqb; ++i, ++G) {
           const int slot = G & 1;
           {
@@ -830,10 +840,13 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
       auto issue_sdp = [&](int G) {
         const int it = G / nqb, slot = G & 1;
-        if (G % nqb == 0) mbar_wait(&kv_full[it & 1], (it >> 1) & 1);
+        if (G % nqb == 0) {
+          mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+          mbar_wait(v_full, it & 1);
+        }
         mbar_wait(&qd_full[slot], (G >> 1) & 1);
         tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64), v_base = smem_u32(sV + (it & 1) * kT64);
+        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64), v_base = smem_u32(sV);
         const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
@@ -843,6 +856,7 @@ __global__ void __launch_bounds__(512, 1)
                     ID_SQ, kk > 0 ? 1u : 0u);
         }
         umma_commit(s_full);
+        if (G % nqb == nqb - 1) umma_commit(v_empty);  // the item's last dP: V may be reloaded
       };
       if (total > 0) issue_sdp(0);
       for (int G = 0; G < total; ++G) {
@@ -861,27 +875,29 @@ __global__ void __launch_bounds__(512, 1)
         }
         const uint32_t k_base = smem_u32(sK + (it & 1) * kT64);
         const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
+        const uint32_t dsb = ds_base + slot * 2 * kT64;
 #pragma unroll
-        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
-          const uint32_t acc = (i | kq) != 0 ? 1u : 0u;
+        for (int kq = 0; kq < 8; ++kq)  // dV += P^T dO, K-dim = 128 queries: 16 rows = 2048 B per step
           umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
-          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, acc);
-        }
+                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
+        umma_commit(p_free);  // P_G read: block G+1 may store its P
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq)  // dK += dS^T Q
+          umma_bf16(t_dk, umma_desc_sw128(dsb + kq * 2048, 2 * 8192, 1024),
+                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
         umma_commit(&qd_empty[slot]);
         if (G >= 2) mbar_wait(&dq_empty[slot], ((G - 2) >> 1) & 1);  // dQ_G-2 drained from this buffer
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
-          umma_bf16(t_dq + slot * 64, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
+          umma_bf16(t_dq + slot * 64, umma_desc_sw128(dsb + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
                     umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
         }
         umma_commit(&dq_full[slot]);
-        umma_commit(bufs_free);  // P_G / dS_G no longer read
+        umma_commit(&ds_free[slot]);  // dS buffer G & 1 no longer read
         if (i == nqb - 1) {
           umma_commit(acc_full);          // this item's dK / dV complete
-          umma_commit(&kv_empty[it & 1]);  // and its K / V no longer needed
+          umma_commit(&k_empty[it & 1]);  // and its K no longer needed
         }
       }
     }
@@ -961,10 +977,20 @@ __global__ void __launch_bounds__(512, 1)
           dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
         }
       }
-      // the previous block's dV / dK / dQ products have finished reading P / dS
-      if (G > 0) mbar_wait(bufs_free, (G - 1) & 1);
+      // dS into buffer G & 1 once block G-2's dK / dQ have read it; P once dV_G-1 has
       uint8_t* prow = sP + half * kT64 + r * 128;
-      uint8_t* drow_ = sDS + half * kT64 + r * 128;
+      uint8_t* drow_ = sDS + (G & 1) * 2 * kT64 + half * kT64 + r * 128;
+      if (G >= 2) mbar_wait(&ds_free[G & 1], ((G - 2) >> 1) & 1);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int chunk = (cc * 4 + k) ^ (r & 7);
+          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
+              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
+        }
+      }
+      if (G > 0) mbar_wait(p_free, (G - 1) & 1);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
 #pragma unroll
@@ -972,8 +998,6 @@ __global__ void __launch_bounds__(512, 1)
           const int chunk = (cc * 4 + k) ^ (r & 7);
           *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
               make_uint4(pk[cc][4 * k], pk[cc][4 * k + 1], pk[cc][4 * k + 2], pk[cc][4 * k + 3]);
-          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
-              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
         }
       }
       fence_proxy_async_smem();
@@ -996,98 +1020,99 @@ __global__ void __launch_bounds__(512, 1)
     reg_dealloc<96>();
     const int q = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sStg + (warp - 12) * 8192;
+    uint8_t* stg = sStg + (warp - 12) * 4096;
     int it = 0, i = 0, kb = 0, h = 0, b = 0;
     if (my_items > 0) item(0, kb, h, b);
     for (int G = 0; G < total; ++G) {
       const int slot = G & 1;
       mbar_wait(&dq_full[slot], (G >> 1) & 1);
       tc_fence_after();
-      if (lane == 0) bulk_wait_read<0>();  // the previous TMA operations have read the staging
+      uint32_t v[2][32];
+      tmem_ld32(t_dq + slot * 64 + lane_base, v[0]);
+      tmem_ld32(t_dq + slot * 64 + lane_base + 32, v[1]);
+      tmem_wait_ld();
+      tc_fence_before();
       __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[slot]);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        uint32_t v[32];
-        tmem_ld32(t_dq + slot * 64 + lane_base + hf * 32, v);
-        tmem_wait_ld();
-        uint8_t* box = stg + hf * 4096;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
-                          __uint_as_float(v[4 * k + 3]));
-      }
-      tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&dq_empty[slot]);
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          if (p.dq_b2_first)
-            tma_reduce_add_4d(&tmDQ, stg + hf * 4096, hf * 32, h, i * 128 + q * 32, b);
-          else
-            tma_reduce_add_4d(&tmDQ, stg + hf * 4096, hf * 32, i * 128 + q * 32, h, b);
-        }
-        bulk_commit();
-      }
-      if (i == nqb - 1) {
-        // this item's dK, dV: bf16 rows -> 4 SW64 32 x 32 tiles (dK cols 0-31, 32-63, dV ...)
-        mbar_wait(acc_full, it & 1);
-        tc_fence_after();
-        if (lane == 0) bulk_wait_read<0>();  // the dQ reduce-adds above have read the staging
+        if (lane == 0) bulk_wait_read<0>();  // the previous TMA operation has read the staging box
         __syncwarp();
 #pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[hf][4 * k]), __uint_as_float(v[hf][4 * k + 1]),
+                          __uint_as_float(v[hf][4 * k + 2]), __uint_as_float(v[hf][4 * k + 3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (p.dq_b2_first)
+            tma_reduce_add_4d(&tmDQ, stg, hf * 32, h, i * 128 + q * 32, b);
+          else
+            tma_reduce_add_4d(&tmDQ, stg, hf * 32, i * 128 + q * 32, h, b);
+          bulk_commit();
+        }
+      }
+      if (i == nqb - 1) {
+        // this item's dK, then dV: bf16 rows -> two SW64 32 x 32 tiles (columns 0-31, 32-63)
+        // in the 4 KB staging box, TMA-stored, column sums read from the staged tiles
+        mbar_wait(acc_full, it & 1);
+        tc_fence_after();
+        const int key0 = kb * 128 + q * 32;
+#pragma unroll 1
         for (int which = 0; which < 2; ++which) {
+          uint32_t v2[2][32];
+          tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base, v2[0]);
+          tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + 32, v2[1]);
+          tmem_wait_ld();
+          if (which == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
+          }
+          if (lane == 0) bulk_wait_read<0>();  // earlier TMA operations have read the staging box
+          __syncwarp();
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            uint32_t v[32];
-            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + hf * 32, v);
-            tmem_wait_ld();
-            uint8_t* row = stg + (which * 2 + hf) * 2048 + lane * 64;
+            uint8_t* row = stg + hf * 2048 + lane * 64;
 #pragma unroll
             for (int k2 = 0; k2 < 4; ++k2) {
               uint4 x;
               __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
               for (int e2 = 0; e2 < 4; ++e2)
-                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v[8 * k2 + 2 * e2]), __uint_as_float(v[8 * k2 + 2 * e2 + 1]));
+                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v2[hf][8 * k2 + 2 * e2]),
+                                               __uint_as_float(v2[hf][8 * k2 + 2 * e2 + 1]));
               *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
             }
           }
-        }
-        tc_fence_before();
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
-          const int key0 = kb * 128 + q * 32;
-#pragma unroll
-          for (int which = 0; which < 2; ++which)
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const CUtensorMap* tm = which == 0 ? &tmDK : &tmDV;
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-              const CUtensorMap* tm = which == 0 ? &tmDK : &tmDV;
               if (p.dkv_b2_first)
-                tma_store_4d(tm, stg + (which * 2 + hf) * 2048, hf * 32, h, key0, b);
+                tma_store_4d(tm, stg + hf * 2048, hf * 32, h, key0, b);
               else
-                tma_store_4d(tm, stg + (which * 2 + hf) * 2048, hf * 32, key0, h, b);
+                tma_store_4d(tm, stg + hf * 2048, hf * 32, key0, h, b);
             }
-          bulk_commit();
-        }
-        if (p.kv_colsum) {
-          // bias-gradient column sums of the staged bf16 tiles (rows past s hold zeros),
-          // lane = column within each 32-column tile, read while the TMA stores drain them
+            bulk_commit();
+          }
+          if (p.kv_colsum) {
+            // bias-gradient column sums of the staged bf16 tiles (rows past s hold zeros),
+            // lane = column within each 32-column tile, read while the TMA stores drain them
 #pragma unroll
-          for (int t4 = 0; t4 < 4; ++t4) {
-            const uint8_t* tile = stg + t4 * 2048;
-            float acc2[2] = {0.f, 0.f};
+            for (int hf = 0; hf < 2; ++hf) {
+              const uint8_t* tile = stg + hf * 2048;
+              float acc2[2] = {0.f, 0.f};
 #pragma unroll
-            for (int i2 = 0; i2 < 32; ++i2) {
-              const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
-              acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
+              for (int i2 = 0; i2 < 32; ++i2) {
+                const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
+                acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
+              }
+              atomicAdd(p.kv_colsum + which * p.nh * 64 + h * 64 + hf * 32 + lane, acc2[0] + acc2[1]);
             }
-            const int which = t4 >> 1, hf = t4 & 1;
-            atomicAdd(p.kv_colsum + which * p.nh * 64 + h * 64 + hf * 32 + lane, acc2[0] + acc2[1]);
           }
         }
         i = 0;
@@ -1540,9 +1565,9 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_bf16_tile_4d(&tdk, p.dK, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (!rc) rc = tmap_bf16_tile_4d(&tdv, p.dV, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (rc) return rc;
-  // d = 64: K, V double-buffered per item, 2 Q, 2 dO, P, dS (2 atoms each), 8 x 4 KB staging;
+  // d = 64: 2 K, V, 2 Q, 2 dO, P, 2 dS (P / dS 2 atoms each), 4 x 4 KB staging;
   // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
-  constexpr size_t SMEM64 = 12 * kT64 + 8 * 4096 + 256 + kMaxItems * 4;
+  constexpr size_t SMEM64 = 13 * kT64 + 4 * 4096 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
   const int nkb = (int)((s + 127) / 128);
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
