@@ -191,6 +191,13 @@ int sg_set_sm_reserve(int n);
 int sg_gemm_sm_budget(void);
 int sg_peer_barrier(const int64_t* args, int n, int me_idx, int* epoch, int* err, int64_t timeout_cycles,
                     void* stream);
+/* Panel broadcasts and small all-reduces over peer memory (replacing the reference's
+ * mesh.py:440-456 broadcasts and 484-513 all-reduces on the dist mesh): sg_copy_async is
+ * a stream-ordered copy between any two device addresses (copy engines over NVLink
+ * for a peer-mapped side); sg_peer_fold folds n fp32 buffers (device array of
+ * pointers, member order) into dst, sum or max, optionally accumulating. */
+int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int sg_peer_fold(float* dst, const int64_t* srcs, int n, int64_t count, int accumulate, int op_max, void* stream);
 /* SGD on the fp32 master, refreshing the bf16 GEMM copy (layers.py:761-772, model.py:356-364). */
 int sg_sgd(float* w, int64_t ldw, void* w_bf16, int64_t ldl, const float* g, int64_t ldg, float lr, int64_t rows,
            int64_t cols, void* stream);

@@ -86,6 +86,8 @@ SIGNATURES: dict[str, tuple] = {
     "sg_set_sm_reserve": (i32, [i32]),
     "sg_gemm_sm_budget": (i32, []),
     "sg_peer_barrier": (i32, [vp, i32, i32, vp, vp, i64, vp]),
+    "sg_copy_async": (i32, [vp, vp, i64, vp]),
+    "sg_peer_fold": (i32, [vp, vp, i32, i64, i32, i32, vp]),
     "sg_dgelu": (i32, [vp, i64, vp, i64, i64, i64, vp, i32, i64, vp, vp]),
     "sg_epilogue": (i32, [vp, i64, i64, i64, ctypes.c_float, vp, vp, i32, i64, i32, vp, i64, vp, i32, i64, vp]),
     "sg_sgd": (i32, [vp, i64, vp, i64, vp, i64, ctypes.c_float, i64, i64, vp]),

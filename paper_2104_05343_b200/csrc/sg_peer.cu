@@ -12,6 +12,7 @@
 // no host state baked into a captured launch).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 
@@ -121,6 +122,51 @@ extern "C" int sg_peer_barrier(const int64_t* args, int n, int me_idx, int* epoc
     return set_error(SG_ERR_CONFIG, "peer_barrier: 1..32 members");
   launch_k(peer_barrier_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream),
            reinterpret_cast<const long long*>(args), n, me_idx, epoch, err, (long long)timeout_cycles);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+// ---- data movement over peer memory --------------------------------------------------
+extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  using namespace sg;
+  clear_error();
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return set_error(SG_ERR_CONFIG, "copy_async: bad arguments");
+  if (bytes == 0) return SG_OK;
+  // unified addressing: a peer-mapped source or destination is copied by the copy
+  // engines over NVLink (the same HBM for processes sharing a GPU)
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+namespace sg {
+// dst[i] (op)= fold over members m = 0..n-1, in member order, of srcs[m][i] (fp32): the
+// group-ordered reduce of the reference (mesh.py:464-466), read straight from the
+// members' published buffers
+__global__ void peer_fold_kernel(float* __restrict__ dst, const long long* __restrict__ srcs, int n, long long count,
+                                 int accumulate, int op_max) {
+  pdl_begin();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    float acc = accumulate ? dst[i] : reinterpret_cast<const float*>(srcs[0])[i];
+    for (int m = accumulate ? 0 : 1; m < n; ++m) {
+      const float v = reinterpret_cast<const float*>(srcs[m])[i];
+      acc = op_max ? fmaxf(acc, v) : acc + v;
+    }
+    dst[i] = acc;
+  }
+}
+}  // namespace sg
+
+extern "C" int sg_peer_fold(float* dst, const int64_t* srcs, int n, int64_t count, int accumulate, int op_max,
+                            void* stream) {
+  using namespace sg;
+  clear_error();
+  if (n < 1 || n > 64 || count < 0 || !dst || !srcs) return set_error(SG_ERR_CONFIG, "peer_fold: bad arguments");
+  if (count == 0) return SG_OK;
+  const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
+  launch_k(peer_fold_kernel, dim3((unsigned)blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), dst,
+           reinterpret_cast<const long long*>(srcs), n, (long long)count, accumulate, op_max);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));

@@ -251,13 +251,21 @@ def embedding_forward(tokens, table: ShardedMatrix, cfg: ModelConfig, ws: Worksp
     out = [None] * mesh.p
     for dev in mesh.local_devs:
         out[dev] = ws.empty(dev, (bs_loc, hb), out_category, dtype=F32)
+    pubs = None
+    if not mesh.is_local and mesh.peer is not None:
+        # peer memory: this position's table blocks (i + k r, j) readable by its column;
+        # step l's root (l mod r, j) holds block (l, j) as its (l // r)-th block
+        i, j = divmod(mesh.my_flat, c)
+        pubs = [mesh.publish(f"emb{k}", table.block(i + k * r, j)) for k in range(c // r)]
+        mesh.peer.barrier("col")
     for l in range(c):
         src = [None] * mesh.p
         for j in range(c):
             o = table.owner(l, j)
             if mesh.owns(o):
                 src[o] = table.block(l, j)
-        tab = mesh.bcast_col(l % r, src, (vb, hb), table.dtype, tag=tag)
+        tab = mesh.bcast_col(l % r, src, (vb, hb), table.dtype, tag=tag,
+                             views=None if pubs is None else pubs[l // r])
         for dev in mesh.local_devs:
             K.embed_fwd(ids[dev], l * vb, vb, tab[dev], out[dev])
     return ShardedMatrix(mesh, cfg.b * cfg.s, cfg.h, out)

@@ -196,7 +196,7 @@ class Mesh:
                 from .peer import PeerNet
 
                 self.peer = PeerNet(self)
-            if self._device.type == "cuda" and self.p > 1 and dist.get_backend() == "nccl":
+            if self._device.type == "cuda" and self.p > 1 and self.peer is None and dist.get_backend() == "nccl":
                 # the persistent GEMMs leave SMs to the NCCL kernels that move step l+1's
                 # panels during step l's product (NCCL_MAX_NCHANNELS is set to match by bench.py)
                 import os
@@ -307,7 +307,7 @@ class Mesh:
         rows, cols = self._groups
         return rows[index] if axis == "row" else cols[index]
 
-    def _bcast(self, axis: str, root: int, src: Sequence, shape, dtype, tag: str) -> list:
+    def _bcast(self, axis: str, root: int, src: Sequence, shape, dtype, tag: str, views=None) -> list:
         """Each owned position receives the block of the group member at ``root``."""
         self.charge("broadcast", axis, root, int(math.prod(shape)) if shape else self._numel(src), tag)
         out: list = [None] * self.p
@@ -329,8 +329,16 @@ class Mesh:
         from .membuf import padded_empty
 
         buf = src[f] if f == s else padded_empty(shape, dtype, self._device)
-        dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group)
-        self.calls["broadcast"] += 1
+        if self.peer is not None and f != s:
+            if views is None:
+                raise ConfigError("peer broadcast needs the root's published view")
+            self.peer.transport.pull(buf, views[s]).wait()
+            self.calls["peer_pull"] += 1
+            out[f] = buf
+            return out
+        if self.peer is None or f != s:
+            dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group)
+            self.calls["broadcast"] += 1
         out[f] = buf
         return out
 
@@ -338,7 +346,7 @@ class Mesh:
     # communicator's own stream, ordered after everything already enqueued on the
     # current stream, and ``wait()`` makes the current stream wait for it; step
     # l+1's panels are issued before step l's product so the two overlap.
-    def _bcast_async(self, axis: str, root: int, src: Sequence, recv, tag: str) -> "Pending":
+    def _bcast_async(self, axis: str, root: int, src: Sequence, recv, tag: str, views=None) -> "Pending":
         self.charge("broadcast", axis, root, self._numel(src), tag)
         out: list = [None] * self.p
         if self.is_local:
@@ -352,26 +360,54 @@ class Mesh:
         i, j = divmod(f, self.c)
         s = self.flat(i, root) if axis == "row" else self.flat(root, j)
         group = self._dist_group(axis, i if axis == "row" else j)
-        if group is None:
+        if group is None or (f == s and self.peer is not None):
             out[f] = src[f]
             return Pending(out, [])
+        if self.peer is not None:
+            # pull the root's published / symmetric block with a copy-engine copy (peer.py)
+            if views is None:
+                raise ConfigError("peer broadcast needs the root's published view")
+            pend = self.peer.transport.pull(recv, views[s])
+            self.calls["peer_pull"] += 1
+            out[f] = recv
+            pend.blocks = out
+            return pend
         buf = src[f] if f == s else recv
         work = dist.broadcast(K._flat_storage(buf), src=self._slot[s], group=group, async_op=True)
         self.calls["broadcast"] += 1
         out[f] = buf
         return Pending(out, [work])
 
-    def bcast_row_async(self, root_col: int, src: Sequence, recv, tag: str = "misc") -> "Pending":
-        """Asynchronous bcast_row into the preallocated receive block ``recv`` (R1)."""
+    def bcast_row_async(self, root_col: int, src: Sequence, recv, tag: str = "misc", views=None) -> "Pending":
+        """Asynchronous bcast_row into the preallocated receive block ``recv`` (R1);
+        ``views`` (peer memory): every position's view of the root's block."""
         if not 0 <= root_col < self.c:
             raise ConfigError(f"broadcast root column {root_col} out of range for c={self.c}")
-        return self._bcast_async("row", root_col, src, recv, tag)
+        return self._bcast_async("row", root_col, src, recv, tag, views)
 
-    def bcast_col_async(self, root_row: int, src: Sequence, recv, tag: str = "misc") -> "Pending":
+    def bcast_col_async(self, root_row: int, src: Sequence, recv, tag: str = "misc", views=None) -> "Pending":
         """Asynchronous bcast_col into the preallocated receive block ``recv`` (R2)."""
         if not 0 <= root_row < self.r:
             raise ConfigError(f"broadcast root row {root_row} out of range for r={self.r}")
-        return self._bcast_async("col", root_row, src, recv, tag)
+        return self._bcast_async("col", root_row, src, recv, tag, views)
+
+    def publish(self, name: str, block) -> list | None:
+        """Peer memory: make this position's ``block`` readable by the mesh (a copy into a
+        symmetric slot unless it already is symmetric); returns the views by flat rank.
+        The caller orders the publish before the readers with a barrier."""
+        if self.peer is None or block is None:
+            return None
+        self.calls["peer_publish"] += 1
+        return self.peer.transport.publish(name, block)
+
+    def sym_views(self, block, index_owner: int) -> list | None:
+        """Peer memory: views, in every position, of the symmetric block that ``index_owner``
+        holds at the same arena offset as this position's ``block`` (SPMD allocation)."""
+        if self.peer is None or block is None:
+            return None
+        views = [None] * self.p
+        views[index_owner] = self.peer.heap.peer(block, index_owner)
+        return views
 
     def _reduce_async(self, axis: str, dest: int, parts: Sequence, tag: str) -> "Pending":
         """Start the group reduce of ``parts`` to group position ``dest``; ``finish``
@@ -408,17 +444,17 @@ class Mesh:
             raise ConfigError(f"reduce destination row {dest_row} out of range for r={self.r}")
         return self._reduce_async("col", dest_row, parts, tag)
 
-    def bcast_row(self, root_col: int, src: Sequence, shape=None, dtype=None, tag: str = "misc") -> list:
+    def bcast_row(self, root_col: int, src: Sequence, shape=None, dtype=None, tag: str = "misc", views=None) -> list:
         """Position (i, j) gets src[(i, root_col)] (R1 panels, mesh.py:440-449)."""
         if not 0 <= root_col < self.c:
             raise ConfigError(f"broadcast root column {root_col} out of range for c={self.c}")
-        return self._bcast("row", root_col, src, shape, dtype, tag)
+        return self._bcast("row", root_col, src, shape, dtype, tag, views)
 
-    def bcast_col(self, root_row: int, src: Sequence, shape=None, dtype=None, tag: str = "misc") -> list:
+    def bcast_col(self, root_row: int, src: Sequence, shape=None, dtype=None, tag: str = "misc", views=None) -> list:
         """Position (i, j) gets src[(root_row, j)] (R2 panels, mesh.py:451-456)."""
         if not 0 <= root_row < self.r:
             raise ConfigError(f"broadcast root row {root_row} out of range for r={self.r}")
-        return self._bcast("col", root_row, src, shape, dtype, tag)
+        return self._bcast("col", root_row, src, shape, dtype, tag, views)
 
     def _reduce_into(self, axis: str, dest: int, parts: Sequence, out: Sequence, accumulate: bool, tag: str) -> None:
         self.charge("reduce", axis, dest, self._numel(parts), tag)
@@ -436,6 +472,11 @@ class Mesh:
         d = g[dest]
         group = self._dist_group(axis, i if axis == "row" else j)
         part = parts[f]
+        if self.peer is not None and group is not None:
+            # the destination folds the group's published parts in group order (peer.py)
+            self.peer.transport.reduce_into(axis, d, part, out[d] if f == d else None, accumulate)
+            self.calls["peer_reduce"] += 1
+            return
         if group is not None:
             flat = K._flat_storage(part)
             if _reduce_ok(group, flat):
@@ -482,6 +523,10 @@ class Mesh:
         group = self._dist_group(axis, i if axis == "row" else j)
         if group is None:
             return
+        if self.peer is not None:
+            self.peer.transport.allreduce(axis, K._flat_storage(bufs[f]), op)
+            self.calls["peer_allreduce"] += 1
+            return
         dist.all_reduce(K._flat_storage(bufs[f]), op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM,
                         group=group)
         self.calls["allreduce"] += 1
@@ -508,9 +553,13 @@ class Mesh:
             return
         import torch.distributed as dist
 
-        if self.p > 1:
+        if self.p > 1 and self.peer is not None:
+            self.peer.transport.allreduce("all", K._flat_storage(bufs[self.my_flat]), op)
+            self.calls["peer_allreduce"] += 1
+        elif self.p > 1:
             dist.all_reduce(K._flat_storage(bufs[self.my_flat]),
                             op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+            self.calls["allreduce"] += 1
 
     # ------------------------------------------------ reference single-controller API
     # (local backend only: the caller holds every position's block, as in the reference)

@@ -162,9 +162,18 @@ class ModelSaved:
 
 
 def _with_twin(m: ShardedMatrix) -> ShardedMatrix:
-    m.bf16_twin = as_bf16(m) if m.dtype != BF16 else m
-    if m.bf16_twin is m:
+    """Attach the bf16 GEMM copy of an fp32 master; on a peer-memory mesh both live in
+    the symmetric arena (remote reduce-adds into the master, panel pulls of the twin)."""
+    if m.dtype == BF16:
         raise ConfigError("masters must be fp32")
+    if m.mesh.peer is not None:
+        from .membuf import copy_block
+
+        blocks = [None if b is None else copy_block(m.mesh.persistent_empty(tuple(b.shape), BF16), b)
+                  for b in m.blocks]
+        m.bf16_twin = ShardedMatrix(m.mesh, m.global_rows, m.global_cols, blocks, m.layout)
+    else:
+        m.bf16_twin = as_bf16(m)
     return m
 
 
@@ -187,7 +196,7 @@ class MeshModel:
             tab = np.asarray(global_params["table"], dtype=np.float64)
             if v_pad != cfg.v:
                 tab = np.vstack([tab, np.zeros((v_pad - cfg.v, cfg.h))])
-            self.table = _with_twin(scatter(tab, mesh, layout="weight"))
+            self.table = _with_twin(scatter(tab, mesh, layout="weight", persistent=True))
         self.layers: list[TransformerLayer] = []
         for i in range(cfg.num_layers):
             pre = f"layers.{i}."

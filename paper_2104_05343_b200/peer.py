@@ -156,6 +156,7 @@ class PeerNet:
         self._scratch: dict = {}
         self._views: dict = {}
         self.barriers = 0
+        self.transport = Transport(self)
 
     def _group(self, axis: str) -> list[int]:
         m = self.mesh
@@ -220,3 +221,119 @@ class PeerNet:
         """Raise if a barrier timed out (one host synchronisation)."""
         if int(self.err.item()):
             raise SummaGridError("peer barrier timed out: a mesh position did not arrive")
+
+
+# ---------------------------------------------------------------- transfers over peer memory
+class PeerPending:
+    """A pull issued on the mesh's copy stream; ``wait()`` makes the current stream wait."""
+
+    def __init__(self, blocks: list, event):
+        self.blocks = blocks
+        self.event = event
+
+    def wait(self) -> list:
+        if self.event is not None:
+            torch.cuda.current_stream().wait_event(self.event)
+            self.event = None
+        return self.blocks
+
+
+def _full(t: torch.Tensor) -> tuple[int, int]:
+    """(pointer, bytes) of a block's whole padded storage (rows x pitch)."""
+    if t.dim() >= 2:
+        rows = 1
+        for s in t.shape[:-1]:
+            rows *= s
+        return t.data_ptr(), rows * t.stride(-2) * t.element_size()
+    return t.data_ptr(), t.numel() * t.element_size()
+
+
+class Transport:
+    """Panel broadcasts and small all-reduces of a dist mesh over its peer memory.
+
+    * Broadcast (R1 / R2 panels, mesh.py:440-456): the root's block must be readable by
+      the group: persistent symmetric blocks (weight masters / twins) are read where they
+      are, other blocks are first published into a double-buffered symmetric slot
+      (one local copy). Members then pull the panel with a copy-engine copy on the
+      mesh's copy stream, ordered after everything already on the compute stream, so
+      step l+1's panel moves while step l's product runs; the compute stream waits only
+      for the panel it consumes.
+    * All-reduce (R5-R8, mesh.py:484-513): each member publishes its buffer, one group
+      barrier, then every member folds the group's buffers in group order
+      (sg_peer_fold): the reference's rank-ordered fold, bit-identical on every member.
+    A published slot is reused two publishes later on the same axis; the barrier of the
+    publish in between orders every member's earlier reads before the overwrite.
+    """
+
+    def __init__(self, net: PeerNet):
+        self.net = net
+        self.stream = torch.cuda.Stream()
+        self._parity: dict = {}
+        self._ptrs: dict = {}
+
+    def _slot(self, name: str, shape, dtype):
+        k = self._parity.get(name, 0)
+        self._parity[name] = k ^ 1
+        return self.net.scratch(f"{name}.{k}", shape, dtype)
+
+    def publish(self, name: str, block: torch.Tensor):
+        """Copy a local block into its symmetric slot; returns peer views by flat rank."""
+        if self.net.heap.is_sym(block):
+            return [self.net.heap.peer(block, f) for f in range(self.net.mesh.p)]
+        local, peers = self._slot(name, tuple(block.shape), block.dtype)
+        dst, n = _full(local)
+        src, n2 = _full(block)
+        if n != n2:
+            raise ConfigError("publish: blocks differ in pitch")
+        _lib.check(_lib.lib().sg_copy_async(dst, src, n, torch.cuda.current_stream().cuda_stream), "sg_copy_async")
+        return peers
+
+    def pull(self, dst: torch.Tensor, src: torch.Tensor) -> PeerPending:
+        """dst <- src (a peer's block) on the copy stream, after the compute stream's work so far."""
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        d, n = _full(dst)
+        s, n2 = _full(src)
+        if n != n2:
+            raise ConfigError("pull: blocks differ in pitch")
+        _lib.check(_lib.lib().sg_copy_async(d, s, n, self.stream.cuda_stream), "sg_copy_async")
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        return PeerPending([dst], ev)
+
+    def _ptr_array(self, ptrs: list) -> torch.Tensor:
+        """Device array of member pointers, cached by the pointers themselves (a slot region
+        that grew has moved: its old arrays are never reused)."""
+        key = tuple(ptrs)
+        if key not in self._ptrs:
+            self._ptrs[key] = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        return self._ptrs[key]
+
+    def allreduce(self, axis: str, buf: torch.Tensor, op: str = "sum") -> None:
+        """In place: buf = fold over this position's ``axis`` group, in group order."""
+        group = self.net._group(axis)
+        if len(group) == 1:
+            return
+        if buf.dtype != torch.float32 or not buf.is_contiguous():
+            raise ConfigError("peer all-reduce: contiguous fp32 buffers")
+        peers = self.publish(f"ar.{axis}", buf.view(-1))
+        self.net.barrier(axis)
+        srcs = self._ptr_array([peers[f].data_ptr() for f in group])
+        _lib.check(_lib.lib().sg_peer_fold(buf.data_ptr(), srcs.data_ptr(), len(group), buf.numel(), 0,
+                                           int(op == "max"), torch.cuda.current_stream().cuda_stream),
+                   "sg_peer_fold")
+
+    def reduce_into(self, axis: str, dest_flat: int, part: torch.Tensor, out, accumulate: bool) -> None:
+        """out (+)= fold of the group's ``part`` blocks in group order, at ``dest_flat`` only."""
+        group = self.net._group(axis)
+        peers = self.publish(f"rd.{axis}", part)
+        self.net.barrier(axis)
+        if self.net.mesh.my_flat != dest_flat:
+            return
+        srcs = self._ptr_array([peers[f].data_ptr() for f in group])
+        if out.stride(-2) != part.stride(-2):
+            raise ConfigError("peer reduce: pitches differ")
+        _, nbytes = _full(out)
+        _lib.check(_lib.lib().sg_peer_fold(out.data_ptr(), srcs.data_ptr(), len(group), nbytes // 4,
+                                           int(accumulate), 0, torch.cuda.current_stream().cuda_stream),
+                   "sg_peer_fold")

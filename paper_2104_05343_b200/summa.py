@@ -241,10 +241,12 @@ def summa_ab(a: ShardedMatrix, b: ShardedMatrix, ws, out_category: str = "free",
     # panels of step l+1 are in flight (double-buffered receive slots) while step l's
     # product runs; on the local backend the "broadcasts" alias the root's block
     a_rx, b_rx = _rx_slots(mesh, ws, (m_b, k_b)), _rx_slots(mesh, ws, (k_b, n_b))
+    a_views, w_views = _peer_panels(mesh, a16, b16)
 
     def issue(l):
-        return (mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag),
-                mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag))
+        return (mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag, views=a_views),
+                mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag,
+                                     views=None if w_views is None else w_views[l]))
 
     pend = issue(0)
     for l in range(steps):
@@ -464,11 +466,12 @@ def _abt_peer(mesh, ws, a16, b16, out, m_b, k_b, n_b, res_b, act, aux_b, colsum,
     i = f // mesh.c
     acc, peers = mesh.peer.scratch("abt_acc", (m_b, n_b))
     K.zero(full_storage(acc))
-    mesh.peer.barrier("row")
+    _, w_views = _peer_panels(mesh, None, b16)
+    mesh.peer.barrier("all")  # accumulators zeroed, weight panels published / current
     b_rx = _rx_slots(mesh, ws, (n_b, k_b))
 
     def issue(l):
-        return mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag)
+        return mesh.bcast_col_async(l % mesh.r, _weight_row(mesh, b16, l), b_rx[l % 2], tag=tag, views=w_views[l])
 
     pend = issue(0)
     for l in range(mesh.c):
@@ -509,11 +512,12 @@ def _atb_peer(mesh, ws, a16, b16, out_mat, m_b, t_b, n_b, acc_in, alpha, tag) ->
     if not direct:
         acc, peers = mesh.peer.scratch("atb_acc", (c // r, m_b, n_b))
         K.zero(acc)
-    mesh.peer.barrier("col")
+    a_views, _ = _peer_panels(mesh, a16, None)
+    mesh.peer.barrier("all")  # accumulators zeroed, A panels published
     a_rx = _rx_slots(mesh, ws, (t_b, m_b))
 
     def issue(l):
-        return mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag)
+        return mesh.bcast_row_async(l, a16.blocks, a_rx[l % 2], tag=tag, views=a_views)
 
     pend = issue(0)
     for l in range(c):
@@ -539,6 +543,29 @@ def _atb_peer(mesh, ws, a16, b16, out_mat, m_b, t_b, n_b, acc_in, alpha, tag) ->
             else:
                 copy_block(out[l * c + j], acc[l // r])
     return out_mat
+
+
+def _peer_panels(mesh: Mesh, a16: ShardedMatrix | None, w16: ShardedMatrix | None):
+    """Peer memory: publish this position's panel sources and return the views the
+    pulls read. ``a`` (act layout): this position's one block, read along its row.
+    ``w`` (weight layout): this position owns blocks (i + k r, j), k = 0..c/r-1; the
+    root of step l, (l mod r, j), holds block (l, j) as its (l // r)-th block, at the
+    offset of this position's own (l // r)-th block (SPMD) -> w_views[l]. Symmetric
+    blocks (weight twins) are read in place; others are copied into a symmetric slot.
+    (None, None) without peer memory; an AB / A^T B caller barriers after this."""
+    if mesh.is_local or mesh.peer is None:
+        return None, None
+    f = mesh.my_flat
+    i, j = divmod(f, mesh.c)
+    a_views = None if a16 is None else mesh.publish("pan_a", a16.blocks[f])
+    w_views = None
+    if w16 is not None:
+        r = mesh.r
+        mine = [mesh.publish(f"pan_w{k}", w16.block(i + k * r, j)) for k in range(mesh.c // r)]
+        w_views = [mine[l // r] for l in range(mesh.c)]
+    if a16 is not None and w16 is not None:
+        mesh.peer.barrier("all")
+    return a_views, w_views
 
 
 def _rx_slots(mesh: Mesh, ws, shape, dtype=BF16) -> list:

@@ -2,10 +2,13 @@
 
 * CPU: gloo process groups with world sizes 2 / 4 / 8 check the row / column
   communicators, broadcast roots and all-reduce folds of the runtime.
-* GPU: 4 processes (2x2 mesh) share one B200 through gloo with CUDA tensors
-  and run the SUMMA forms and a full training step; results must equal the
-  oracle like the single-controller path (NCCL needs one GPU per rank, which
-  the round's single-GPU box does not have).
+* GPU: 2, 4 and 8 processes (1x2, 2x2, 2x4 meshes) share one B200 and run the
+  SUMMA forms and a full training step; results must equal the oracle like the
+  single-controller path. With peer memory (the default on CUDA) every transfer of
+  the step goes through CUDA-IPC arenas (panel pulls, fused reduce-adds, group-order
+  all-reduces, device barriers) and the whole step is captured into one CUDA graph;
+  without it, gloo carries the collectives (NCCL needs one GPU per rank, which the
+  round's single-GPU box does not have).
 """
 
 import json
@@ -212,9 +215,74 @@ def _gpu_worker(rank, world, port, rows, cols, peer, out_dir):
         dist.destroy_process_group()
 
 
+def _graph_worker(rank, world, port, rows, cols, out_dir):
+    """The whole dist training step over peer memory (panel pulls, fused reduces, peer
+    all-reduces, device barriers: no torch.distributed call inside the step) captured
+    into one CUDA graph per process; replays equal eager steps."""
+    import paper_2104_05343_b200 as sg
+    from oracle import model_ref as M
+
+    _init(rank, world, port)
+    try:
+        torch.cuda.set_device(0)
+        m = sg.create_mesh(sg.MeshConfig(rows=rows, cols=cols), backend="dist", peer=True)
+        cfg = sg.ModelConfig(b=4, s=16, h=64, n=8, v=61, num_layers=2)
+        rcfg = M.RefConfig(4, 16, 64, 8, 61, 2)
+        bf = lambda a: torch.as_tensor(a, dtype=torch.float32).bfloat16().double().numpy()  # noqa: E731
+        params = {k: bf(v) for k, v in M.init_params(rcfg, 23).items()}
+        tokens, labels = M.sample_data(rcfg, 23)
+        tok, lab = torch.as_tensor(tokens).cuda(), torch.as_tensor(labels).cuda()
+        eager = sg.MeshModel(m, cfg, params)
+        ws_e = eager.make_workspace(checkpointing=False)
+        calls0 = dict(m.calls)
+        losses_e = [float(eager.train_step(tok, lab, ws_e, lr=0.25).item()) for _ in range(3)]
+        step_calls = {k: v - calls0.get(k, 0) for k, v in m.calls.items()}
+        graphed = sg.MeshModel(m, cfg, params)
+        ws_g = graphed.make_workspace(checkpointing=False)
+        graphed.train_step(tok, lab, ws_g, lr=0.25)  # warm-up: arenas, pointer tables
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            pass
+        torch.cuda.current_stream().wait_stream(st)
+        with torch.cuda.graph(g):
+            loss_t = graphed.train_step(tok, lab, ws_g, lr=0.25)
+        losses_g = []
+        for _ in range(2):
+            g.replay()
+            losses_g.append(float(loss_t.item()))
+        m.peer.check()
+        pe, pg = eager.gather_params(), graphed.gather_params()
+
+        def rel(x, r):
+            return float(np.max(np.abs(x - r)) / max(np.max(np.abs(r)), 1e-30))
+
+        res = {"loss_e": losses_e, "loss_g": losses_g, "params": max(rel(pg[k], pe[k]) for k in pe),
+               "step_calls": step_calls}
+        (out_dir / f"r{rank}.json").write_text(json.dumps(res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2), (2, 4)])
+def test_dist_step_cuda_graph_on_one_gpu(tmp_path, rows, cols):
+    world = rows * cols
+    mp.spawn(_graph_worker, args=(world, _free_port(), rows, cols, tmp_path), nprocs=world, join=True)
+    for rank in range(world):
+        res = json.loads((tmp_path / f"r{rank}.json").read_text())
+        # no torch.distributed collective inside the step: everything moved over peer memory
+        assert all(k.startswith("peer_") for k in res["step_calls"]), res["step_calls"]
+        assert res["loss_g"][0] == pytest.approx(res["loss_e"][1], rel=1e-5), res
+        assert res["loss_g"][1] == pytest.approx(res["loss_e"][2], rel=1e-5), res
+        assert res["params"] < 1e-5, res
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("peer", [True, False])
-@pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2)])
+@pytest.mark.parametrize("rows,cols", [(1, 2), (2, 2), (2, 4)])
 def test_dist_backend_on_one_gpu(tmp_path, rows, cols, peer):
     """Processes sharing one B200: peer=True maps each other's arenas by CUDA IPC (the
     fused-reduce product path); peer=False is the collective-reduce path."""
@@ -228,7 +296,9 @@ def test_dist_backend_on_one_gpu(tmp_path, rows, cols, peer):
         calls = err["summa_calls"]
         if peer:
             assert calls.get("reduce", 0) == 0 and calls.get("allreduce", 0) == 0, calls
-            # abt: one row group, atb: one column group, 2 barriers each (groups of 1 skip)
-            assert err["barriers"] == 2 * (cols > 1) + 2 * (rows > 1), err
+            assert calls.get("broadcast", 0) == 0, calls  # panels pulled over peer memory
+            # a whole-mesh barrier per product (panels published, accumulators zeroed) and a
+            # closing row (AB^T) / column (A^T B) barrier (groups of one position skip it)
+            assert err["barriers"] == 1 + (1 + (cols > 1)) + (1 + (rows > 1)), err
         else:
             assert calls.get("reduce", 0) + calls.get("allreduce", 0) == cols * (cols > 1) + cols * (rows > 1), calls
