@@ -275,36 +275,68 @@ __global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
 }
 
 // ============================================================================
-// Forward, d = 64, two query tiles per CTA ("ping-pong"): 384 threads
-//   warp 0      TMA: Q0, Q1 once; K_j / V_j blocks (three slots)
-//   warp 1      MMA issuer: S_i,j+1 = Q_i K_j+1^T is issued as soon as softmax i has
-//               pulled S_i,j into registers, PV_i,j = P_i,j V_j when P_i,j is in
-//               smem, so the tensor core works on one tile's products while the
-//               softmax warpgroups work on their exponentials
-//   warp 2      TMEM allocator: S0 | S1 | O0 | O1 (512 columns)
-//   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1 (thread = query row)
-// Each score block is read from TMEM once (the 128-key row in registers); O
-// accumulates in TMEM across key blocks; the row max used for the exponent only
-// advances (O and l rescaled through tcgen05.ld/st) when it grows by more than
-// 2^8, so most blocks need no correction. Scale/shift and the row sums use the
-// paired fp32 pipe (FFMA2 / FADD2).
+// Forward, d = 64, two query tiles per CTA ("ping-pong"): 640 threads
+//   warp 0      TMA: Q0, Q1 once per item; K_j / V_j blocks (three slots)
+//   warps 1, 3  MMA issuers of tile 0 / tile 1: S_i,G+1 = Q_i K_G+1^T as soon as the
+//               softmax warps hold S_i,G in registers, PV_i,G = P_i,G V_G once P_i,G
+//               is in TMEM
+//   warp 2      TMEM allocator: S0 | S1 | O0 | O1 | P0 | P1
+//   warps 4-11  softmax of tile 0, warps 12-19 softmax of tile 1
+// P never touches shared memory: the softmax warps write it as packed bf16 pairs
+// into TMEM (tcgen05.st) and PV reads A from TMEM ("TS" MMA), so per key block the
+// CTA's shared-memory traffic is only the K / V tiles and the score products'
+// operands. Each query tile has its own MMA-issuing thread (a shared issuer forces
+// the tiles into lockstep) and 8 softmax warps: warp (tile, key half, lane
+// quadrant) owns 64 keys of 32 rows, so two warps of a tile share an SMSP's MUFU
+// and fill each other's dependency gaps; the two halves of a row exchange the row
+// max per block and the row sum per item through shared memory + an mbarrier. The
+// tiles take turns on the exponentials (named barriers). A share of the exponentials
+// runs as a polynomial on the FMA pipe (ex2_poly2). O accumulates in TMEM; the row
+// max used for the exponent only advances (O and l rescaled through tcgen05.ld/st)
+// when it grows by more than 2^8. Measured (tools/ftrace.py): a key block costs
+// ~3500 clocks against 2048 of MUFU and ~1250 of tensor-core time; the M=128, N=64
+// PV products issue at ~46 clocks each (tools/micro/umma_rate.cu) and both tiles'
+// products queue on one tensor core.
 // ============================================================================
 constexpr int kQT = 2;  // query tiles per CTA
 
 struct Flash2Cfg {
   static constexpr uint32_t T64 = 128 * 64 * 2;   // one 128 x 64 bf16 tile
-  static constexpr uint32_t P_BYTES = 2 * T64;     // 128 rows x 128 keys (2 atoms)
   static constexpr int KV_SLOTS = 3;
   static constexpr int Q_SLOTS = 2;                // Q of the next item prefetched
-  static constexpr size_t SMEM = Q_SLOTS * kQT * T64 + KV_SLOTS * 2 * T64 + kQT * P_BYTES + 256;
+  static constexpr uint32_t O_STG = kQT * 8 * 2048;  // per softmax warp one 32 x 32 bf16 output tile
+  static constexpr uint32_t X_XCH = (kQT * 2 + kQT) * 256 * 4;  // row max (2 slots) / row sum exchange
+  static constexpr size_t SMEM = Q_SLOTS * kQT * T64 + KV_SLOTS * 2 * T64 + O_STG + X_XCH + 512;
 };
+
+// 2^y for a pair of exponents on the FMA pipe (no MUFU): y = j + f with j = rint(y)
+// by the 1.5 * 2^23 shifter, 2^f by a degree-3 minimax polynomial on [-1/2, 1/2]
+// (relative error 7.5e-5, far under the bf16 rounding of P), j added to the
+// exponent field. y is clamped at -126 (2^-126 vanishes in bf16 P and in the row sum;
+// below it the 2^f factor < 1 would underflow the exponent field).
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t y) {
+  const float lo = fmaxf(f2_lo(y), -126.f), hi = fmaxf(f2_hi(y), -126.f);
+  const uint64_t yc = f2_pack(lo, hi);
+  const uint64_t sh = f2_pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(yc, sh);                                   // j in the low mantissa bits
+  const uint64_t f = fadd2(yc, fadd2(f2_pack(-12582912.f, -12582912.f), t) ^ 0x8000000080000000ull);  // y - j
+  uint64_t q = ffma2(f, f2_pack(0.0551716687545781f, 0.0551716687545781f),
+                     f2_pack(0.24261114787053215f, 0.24261114787053215f));
+  q = ffma2(q, f, f2_pack(0.6932609877583421f, 0.6932609877583421f));
+  q = ffma2(q, f, f2_pack(0.9999280720307991f, 0.9999280720307991f));
+  const uint32_t rl = static_cast<uint32_t>(q) + (static_cast<uint32_t>(t) << 23);
+  const uint32_t rh = static_cast<uint32_t>(q >> 32) + (static_cast<uint32_t>(t >> 32) << 23);
+  return static_cast<uint64_t>(rl) | (static_cast<uint64_t>(rh) << 32);
+}
 
 // Persistent: CTA c processes work items t = c, c + grid, ... with t = (query-tile
 // pair, head, batch), pair index fastest (neighbouring CTAs share K / V in L2).
 // All per-block barriers run on a CTA-wide block counter G across items, so the
 // next item's Q, first K / V block and first score products are in flight while
-// the current item finishes.
-__global__ void __launch_bounds__(384, 1)
+// the current item finishes. NPOLY of every 16 exponent pairs go to the FMA-pipe
+// polynomial instead of MUFU.EX2 (the MUFU rate bounds the softmax warps).
+template <int NPOLY>
+__global__ void __launch_bounds__(640, 1)
     flash_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                       const __grid_constant__ FlashFwdParams p, int bsz) {
@@ -317,8 +349,9 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQ = smem;                             // [Q_SLOTS][kQT] tiles
   uint8_t* sK = sQ + Cfg::Q_SLOTS * kQT * T64;    // [NS]
   uint8_t* sV = sK + NS * T64;                    // [NS]
-  uint8_t* sP = sV + NS * T64;                    // [kQT] x 2 atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kQT * Cfg::P_BYTES);
+  uint8_t* sO = sV + NS * T64;                    // [kQT][4 warps] x 4 KB output staging
+  float* sX = reinterpret_cast<float*>(sO + Cfg::O_STG);  // half-row exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + Cfg::O_STG + Cfg::X_XCH);
   uint64_t* q_full = bars;                // [2]
   uint64_t* q_empty = bars + 2;           // [2]
   uint64_t* k_full = bars + 4;            // [NS]
@@ -329,12 +362,16 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = s_free + kQT;        // [kQT]
   uint64_t* pv_done = p_full + kQT;       // [kQT]
   uint64_t* o_full = pv_done + kQT;       // [kQT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + kQT);
+  uint64_t* xbar = o_full + kQT;          // [kQT][4] half-row meeting per block (row max)
+  uint64_t* lbar = xbar + kQT * 4;        // [kQT][4] half-row meeting per item (row sum)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lbar + kQT * 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = (p.s + kKB - 1) / kKB;
   const int npairs = (p.s + kQT * kQB - 1) / (kQT * kQB);
   const int n_items = npairs * p.nh * bsz;
+  const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_items * nkb;  // this CTA's key blocks over all its items
   auto decode = [&](int t, int& qb, int& h, int& b) {
     qb = t % npairs;
     const int r = t / npairs;
@@ -349,19 +386,23 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmO);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
+      mbar_init(&q_empty[i], kQT);
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&kv_empty[i], kQT);  // one commit per tile issuer
     }
     for (int i = 0; i < kQT; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_full[i], 1);
+    }
+    for (int i = 0; i < kQT * 4; ++i) {
+      mbar_init(&xbar[i], 2);
+      mbar_init(&lbar[i], 2);
     }
     fence_mbar_init();
   }
@@ -371,7 +412,7 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_begin();
-  // TMEM columns: S_i at 128 i, O_i at 256 + 64 i
+  // TMEM columns: S_i at 128 i, O_i at 256 + 64 i, P_i (packed bf16 pairs) at 384 + 64 i
   if (warp == 0) {
     if (lane == 0) {
       int g = 0;
@@ -394,14 +435,20 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 3) {
     if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer of tile i
+      // one issuing thread per query tile, so neither tile's products wait for the
+      // other tile's softmax progress (a shared issuer forces the tiles into lockstep
+      // and both softmax warpgroups then contend for MUFU at the same time)
+      const int i = warp >> 1;
       constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
-      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P K-major, V MN-major
-      const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-      const int total = my_items * nkb;  // this CTA's key blocks over all its items
+      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P (TMEM), V MN-major
+      const bool trm = blockIdx.x == 0 && i == 0;
+      int tri = 0;
+      (void)trm; (void)tri;
       // S_i for global block G (item G / nkb, key block G % nkb)
-      auto issue_s = [&](int i, int G) {
+      auto issue_s = [&](int G) {
         const int it = G / nkb;
         const uint32_t q_base = smem_u32(sQ + ((it & 1) * kQT + i) * T64), k_base = smem_u32(sK + (G % NS) * T64);
 #pragma unroll
@@ -417,45 +464,58 @@ __global__ void __launch_bounds__(384, 1)
       };
       if (total > 0) {
         ready_s(0);
-        for (int i = 0; i < kQT; ++i) issue_s(i, 0);
+        issue_s(0);
       }
       for (int G = 0; G < total; ++G) {
         const int slot = G % NS, j = G % nkb;
+        SG_TR(trm, 2, tri, 10);
         if (G + 1 < total) {
           ready_s(G + 1);
-          for (int i = 0; i < kQT; ++i) {
-            mbar_wait(&s_free[i], G & 1);  // softmax i holds S_i,G in registers
-            tc_fence_after();
-            issue_s(i, G + 1);
-          }
-        }
-        if (j == nkb - 1) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score products issued
-        mbar_wait(&v_full[slot], (G / NS) & 1);
-        for (int i = 0; i < kQT; ++i) {
-          mbar_wait(&p_full[i], G & 1);  // P_i,G in smem, O_i corrected (or read out, first block)
+          SG_TR(trm, 2, tri, 14);
+          mbar_wait(&s_free[i], G & 1);  // softmax i holds S_i,G in registers
           tc_fence_after();
-          const uint32_t p_base = smem_u32(sP + i * Cfg::P_BYTES), v_base = smem_u32(sV + slot * T64);
-#pragma unroll
-          for (int kk = 0; kk < kKB / 16; ++kk) {
-            const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * (kQB * 128) + (kk & 3) * 32, 0, 1024);
-            const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024);
-            umma_bf16(tmem + 256 + i * 64, ad, bd, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
-          }
-          umma_commit(&pv_done[i]);
-          if (j == nkb - 1) umma_commit(&o_full[i]);
+          SG_TR(trm, 2, tri, 15);
+          issue_s(G + 1);
         }
-        umma_commit(&kv_empty[slot]);  // K_G, V_G no longer needed
+        if (j == nkb - 1) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score product issued
+        SG_TR(trm, 2, tri, 11);
+        mbar_wait(&v_full[slot], (G / NS) & 1);
+        mbar_wait(&p_full[i], G & 1);  // P_i,G in TMEM, O_i corrected (or read out, first block)
+        tc_fence_after();
+        SG_TR(trm, 2, tri, 12);
+        const uint32_t v_base = smem_u32(sV + slot * T64);
+#pragma unroll
+        for (int kk = 0; kk < kKB / 16; ++kk)
+          umma_bf16_ts(tmem + 256 + i * 64, tmem + 384 + i * 64 + kk * 8,
+                       umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024), IDESC_PV, (j | kk) != 0 ? 1u : 0u);
+        SG_TR(trm, 2, tri, 13);
+        umma_commit(&pv_done[i]);
+        if (j == nkb - 1) umma_commit(&o_full[i]);
+        umma_commit(&kv_empty[slot]);  // this tile is done with K_G, V_G
       }
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax tile i
-    const int i = (warp - 4) >> 2;
-    const int qd = warp & 3;                      // TMEM lane quadrant
+    // ------------------------------------------------------------ softmax
+    // warp 4 + 8 i + 4 h + q: tile i, key half h (keys 64 h .. 64 h + 63 of a block,
+    // O / P columns 32 h ..), TMEM lane quadrant q (rows 32 q ..). The two halves of a
+    // row meet once per block (row max) and once per item (row sum) through a
+    // shared-memory exchange and an mbarrier. The two tiles' warps of an SMSP take
+    // turns on the exponentials (named barriers, 2 x 2 warps): tile 1's block G after
+    // tile 0's block G, tile 0's block G + 1 after tile 1's block G, so one tile's MUFU
+    // phase overlaps the other tile's TMEM loads, row max and tensor-core round trip.
+    const int w = warp - 4;
+    const int i = w >> 3, kh = (w >> 2) & 1, qd = warp & 3;
     const int r = qd * 32 + lane;                 // row inside the tile
     const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
-    const uint32_t t_s = tmem + i * 128 + lane_base, t_o = tmem + 256 + i * 64 + lane_base;
-    uint8_t* prow_base = sP + i * Cfg::P_BYTES + r * 128;
+    const uint32_t t_s = tmem + i * 128 + kh * 64 + lane_base, t_o = tmem + 256 + i * 64 + kh * 32 + lane_base,
+                   t_p = tmem + 384 + i * 64 + kh * 32 + lane_base;
+    uint64_t* my_xbar = &xbar[i * 4 + qd];
+    uint64_t* my_lbar = &lbar[i * 4 + qd];
+    float* xm = sX + (i * 2) * 2 * 128;           // [2 slots][2 halves][128] row maxima
     const uint64_t scale2 = f2_pack(p.scale_log2, p.scale_log2);
+    const bool trs = blockIdx.x == 0 && qd == 0 && kh == 0 && lane == 0;
+    int tri = 0;
+    (void)trs; (void)tri;
     int G = 0;
     for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
       int qb, h, b;
@@ -463,96 +523,117 @@ __global__ void __launch_bounds__(384, 1)
       const int qrow = (qb * kQT + i) * kQB + r;  // query position
       float m_use = -INFINITY, l = 0.f;
       for (int j = 0; j < nkb; ++j, ++G) {
-        const int kvalid = min(kKB, p.s - j * kKB);
+        const int kvalid = min(kKB, p.s - j * kKB) - kh * 64;  // valid keys of this half
+        SG_TR(trs, i, tri, 0);
         mbar_wait(&s_full[i], G & 1);
         tc_fence_after();
-        uint32_t sv[4][32];
+        SG_TR(trs, i, tri, 1);
+        uint32_t sv[2][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sv[c]);
+        for (int c = 0; c < 2; ++c) tmem_ld32(t_s + c * 32, sv[c]);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[i]);  // the MMA may overwrite S_i now
-        if (kvalid < kKB) {  // partial last block: keys past the end never contribute
+        if (kvalid < 64) {  // partial last block: keys past the end never contribute
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int e = 0; e < 32; ++e)
               if (c * 32 + e >= kvalid) sv[c][e] = __float_as_uint(-INFINITY);
         }
-        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mx[e & 3] = fmaxf(mx[e & 3], __uint_as_float(sv[c][e]));
-        const float m_cand = fmaxf(m_use, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2);
+          for (int e = 0; e < 32; e += 2)
+            mx[(e >> 1) & 1] = fmax3f(mx[(e >> 1) & 1], __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
+        const float m_loc = fmaxf(mx[0], mx[1]) * p.scale_log2;
+        float* slot = xm + (G & 1) * 256;  // double-buffered: a half rewrites a slot only after the next meeting
+        slot[kh * 128 + r] = m_loc;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(my_xbar);
+        SG_TR(trs, i, tri, 2);
+        // PV_i,G-1 has finished reading P_i (and writing O_i)
+        if (G > 0) mbar_wait(&pv_done[i], (G - 1) & 1);
+        // this tile's turn on MUFU
+        if (i == 1 || G > 0) named_bar_sync(1 + (1 - i) * 4 + qd, 128);
+        mbar_wait(my_xbar, G & 1);
+        // (a volatile shared load after the barrier: no exponential is scheduled ahead of the turn)
+        const float m_cand = fmax3f(m_use, m_loc, *static_cast<volatile float*>(&slot[(kh ^ 1) * 128 + r]));
         float alpha = 1.f;
         bool correct = false;
         if (j == 0) {
           m_use = m_cand;
-        } else if (__any_sync(0xffffffffu, m_cand > m_use + 8.f)) {
+        } else if (__any_sync(0xffffffffu, m_cand > m_use + 8.f)) {  // same rows, same vote in both halves
           alpha = ex2f_fast(m_use - m_cand);
           m_use = m_cand;
           correct = true;
         }
         const uint64_t neg2 = f2_pack(-m_use, -m_use);
-        // PV_i,G-1 has finished reading P_i (and writing O_i)
-        if (G > 0) mbar_wait(&pv_done[i], (G - 1) & 1);
+        SG_TR(trs, i, tri, 3);
         uint64_t ps2 = 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
+        for (int c = 0; c < 2; ++c) {
+          // packed pairs overwrite the consumed scores in place (contiguous STTM source)
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const uint64_t y =
                 ffma2(f2_pack(__uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1])), scale2, neg2);
-            const float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
-            const float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
+            float p0, p1;
+            if ((e * NPOLY) % 16 < NPOLY) {  // NPOLY of 16 pairs, spread over the chunk
+              const uint64_t pp = ex2_poly2(y);
+              p0 = f2_lo(pp);
+              p1 = f2_hi(pp);
+            } else {
+              p0 = ex2f_fast(f2_lo(y));
+              p1 = ex2f_fast(f2_hi(y));
+            }
             ps2 = fadd2(ps2, f2_pack(p0, p1));
             __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-            pk[e] = *reinterpret_cast<uint32_t*>(&hv);
+            sv[c][e] = *reinterpret_cast<uint32_t*>(&hv);
           }
-          uint8_t* prow = prow_base + (c >> 1) * (kQB * 128);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
-            *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
-                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-          }
+          tmem_st16(t_p + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&sv[c][0]));  // 32 keys, packed pairs
         }
-        l = l * alpha + (__uint_as_float(static_cast<uint32_t>(ps2)) + __uint_as_float(static_cast<uint32_t>(ps2 >> 32)));
+        SG_TR(trs, i, tri, 4);
+        if (i == 0 || G + 1 < total) named_bar_arrive(1 + i * 4 + qd, 128);
+        l = l * alpha + (f2_lo(ps2) + f2_hi(ps2));
         if (correct) {
-          // O_i row *= 2^(m_old - m_new) before PV_i,G accumulates into it
+          // this half's O_i columns *= 2^(m_old - m_new) before PV_i,G accumulates into them
+          uint32_t ov[32];
+          tmem_ld32(t_o, ov);
+          tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(t_o + c * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st32(t_o + c * 32, ov);
-          }
-          tmem_wait_st();
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st32(t_o, ov);
         }
-        fence_proxy_async_smem();
+        tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
       }
-      // O_i of this item complete: normalise, bf16 row into the context block, lse.
-      // The next item's first PV overwrites O_i only after this warpgroup's next p_full.
+      // O_i of this item complete: row sum of both halves, normalise, bf16 into the
+      // context block, lse. The next item's first PV overwrites O_i only after this
+      // warpgroup's next p_full.
+      float* xl = sX + 4 * 256 + i * 256;  // [2 halves][128] row sums
+      xl[kh * 128 + r] = l;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(my_lbar);
+      mbar_wait(my_lbar, it & 1);
+      l += xl[(kh ^ 1) * 128 + r];
       mbar_wait(&o_full[i], it & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      // normalised bf16 rows -> this warp's (now idle) P_i rows as two 32 x 32 SW64 tiles
-      // -> TMA stores into the context block (rows past s clipped)
-      uint8_t* ostg = sP + i * Cfg::P_BYTES + qd * 32 * 128;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      // normalised bf16 rows -> this warp's 32 x 32 SW64 staging tile -> TMA store
+      // into the context block (rows past s clipped)
+      uint8_t* ostg = sO + w * 2048;
+      if (lane == 0) bulk_wait_read<0>();  // the previous item's store has read the staging
+      __syncwarp();
+      {
         uint32_t ov[32];
-        tmem_ld32(t_o + c * 32, ov);
+        tmem_ld32(t_o, ov);
         tmem_wait_ld();
-        uint8_t* orow = ostg + c * 2048 + lane * 64;
+        uint8_t* orow = ostg + lane * 64;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           uint4 x;
@@ -568,19 +649,16 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) {
         const int row0 = (qb * kQT + i) * kQB + qd * 32;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (p.o_b2_first)
-            tma_store_4d(&tmO, ostg + c * 2048, c * 32, h, row0, b);
-          else
-            tma_store_4d(&tmO, ostg + c * 2048, c * 32, row0, h, b);
-        }
+        if (p.o_b2_first)
+          tma_store_4d(&tmO, ostg, kh * 32, h, row0, b);
+        else
+          tma_store_4d(&tmO, ostg, kh * 32, row0, h, b);
         bulk_commit();
-        bulk_wait_read<0>();  // staging = this warp's P rows, rewritten by the next item
       }
       __syncwarp();
       tc_fence_before();
-      if (qrow < p.s && p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
+      if (kh == 0 && qrow < p.s && p.lse)
+        p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -589,14 +667,37 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+template <int NPOLY>
+static void launch_fwd2_k(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
+                          const FlashFwdParams& p, int b, int grid, cudaStream_t stream) {
+  launch_k(flash_fwd2_kernel<NPOLY>, dim3(grid), dim3(640), Flash2Cfg::SMEM, stream, q, k, v, o, p, b);
+}
+
 static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const FlashFwdParams& p, int b, cudaStream_t stream) {
-  if (!ensure_smem(reinterpret_cast<const void*>(flash_fwd2_kernel), (int)Flash2Cfg::SMEM))
-    return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
+  // SG_FLASH_POLY = pairs of 16 on the FMA-pipe exp2 (experiments; default below)
+  static const int npoly = [] {  // measured at b=32 s=512 / b=4 s=2048: 0 -> 63.6 / 115.9 us, 2 -> 62.7 / 113.0,
+    const char* e = getenv("SG_FLASH_POLY");  // 4 -> 63.7 / 115.1, 6 -> 67.2 / 123.2
+    return e ? atoi(e) : 2;
+  }();
+  const void* kern = npoly >= 8 ? (const void*)flash_fwd2_kernel<8>
+                     : npoly >= 6 ? (const void*)flash_fwd2_kernel<6>
+                     : npoly >= 4 ? (const void*)flash_fwd2_kernel<4>
+                     : npoly >= 2 ? (const void*)flash_fwd2_kernel<2> : (const void*)flash_fwd2_kernel<0>;
+  if (!ensure_smem(kern, (int)Flash2Cfg::SMEM)) return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
   const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
   const int sms = sg_device_sm_count();
-  launch_k(flash_fwd2_kernel, dim3(std::min(items, sms > 0 ? sms : 148)), dim3(384), Flash2Cfg::SMEM, stream, q, k, v, o,
-           p, b);
+  const int grid = std::min(items, sms > 0 ? sms : 148);
+  if (npoly >= 8)
+    launch_fwd2_k<8>(q, k, v, o, p, b, grid, stream);
+  else if (npoly >= 6)
+    launch_fwd2_k<6>(q, k, v, o, p, b, grid, stream);
+  else if (npoly >= 4)
+    launch_fwd2_k<4>(q, k, v, o, p, b, grid, stream);
+  else if (npoly >= 2)
+    launch_fwd2_k<2>(q, k, v, o, p, b, grid, stream);
+  else
+    launch_fwd2_k<0>(q, k, v, o, p, b, grid, stream);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -618,6 +719,16 @@ static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensor
 }  // namespace sg
 
 using namespace sg;
+
+#ifdef SG_TRACE
+extern "C" int sg_debug_trace(void* host) {
+  return cudaMemcpyFromSymbol(host, sg::g_sgtrace, sizeof(sg::g_sgtrace)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int sg_debug_trace_clear(void) {
+  static unsigned long long zero[4][8192];
+  return cudaMemcpyToSymbol(sg::g_sgtrace, zero, sizeof zero) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_t s, int64_t nh, int64_t d,
                                  void* out, int64_t ldo, float* lse, void* stream) {

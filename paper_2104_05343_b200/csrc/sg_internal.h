@@ -64,3 +64,24 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 }  // namespace sg
+
+// Phase-timeline stamps for the instrumented build only (tools/trace_build.py
+// compiles with -DSG_TRACE into libsg_trace.so; the product library has none):
+// SG_TR(cond, buffer, index, event) appends (event << 56 | clock64) to a per-TU
+// device buffer read back by sg_debug_trace (tools/ftrace.py).
+#ifdef SG_TRACE
+namespace sg {
+static __device__ unsigned long long g_sgtrace[4][8192];
+__device__ __forceinline__ void sg_trace_stamp(int buf, int& i, int ev) {
+  if (i < 8192) g_sgtrace[buf][i++] = ((unsigned long long)ev << 56) | (clock64() & 0xffffffffffffffull);
+}
+}  // namespace sg
+#define SG_TR(cond, buf, idx, ev) \
+  do {                            \
+    if (cond) sg::sg_trace_stamp(buf, idx, ev); \
+  } while (0)
+#else
+#define SG_TR(cond, buf, idx, ev) \
+  do {                            \
+  } while (0)
+#endif

@@ -1,7 +1,8 @@
-"""Instrumented build for phase timelines: patches copies of csrc/sg_attn.cu (flash
-backward) and csrc/sg_gemm.cu (GEMM epilogue / MMA warps) with clock64() stamps and
-links paper_2104_05343_b200/libsg_trace.so (read by tools/ftrace.py, tools/gtrace.py
-through SG_LIB_PATH). The product library is untouched.
+"""Instrumented build for phase timelines: compiles csrc/ with -DSG_TRACE (the flash
+kernels' SG_TR clock64() stamps, read back by sg_debug_trace / tools/ftrace.py) and
+patches a copy of csrc/sg_gemm.cu (GEMM epilogue / MMA warps, tools/gtrace.py), linked
+into paper_2104_05343_b200/libsg_trace.so (selected through SG_LIB_PATH). The product
+library is untouched.
 
     python tools/trace_build.py
 """
@@ -14,6 +15,7 @@ CSRC = ROOT / "paper_2104_05343_b200" / "csrc"
 OUT = ROOT / "paper_2104_05343_b200" / "libsg_trace.so"
 TMP = Path("/tmp/sg_trace")
 NVCC = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        "-DSG_TRACE",
         "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 
 
@@ -24,39 +26,6 @@ def patch(src: str, edits) -> str:
         src = src.replace(old, new)
     return src
 
-
-ATTN = [
-    ("constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)",
-     "constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)\n"
-     "__device__ unsigned long long g_ftrace[2][8192];\n"
-     "__device__ __forceinline__ void ftr(int which, int& i, int ev) {\n"
-     "  if (i < 8192) g_ftrace[which][i++] = ((unsigned long long)ev << 56) | (clock64() & 0xffffffffffffffull);\n}"),
-    ('extern "C" int sg_flash_attn_bwd(',
-     'extern "C" int sg_debug_ftrace(void* host) {\n'
-     "  return cudaMemcpyFromSymbol(host, sg::g_ftrace, sizeof(sg::g_ftrace)) == cudaSuccess ? 0 : 1;\n}\n"
-     'extern "C" int sg_flash_attn_bwd('),
-    ("      if (total > 0) issue_sdp(0);\n      for (int G = 0; G < total; ++G) {\n"
-     "        const int slot = G & 1, it = G / nqb, i = G % nqb;\n",
-     "      const bool trm = blockIdx.x == 0;\n      int tri = 0;\n"
-     "      if (total > 0) issue_sdp(0);\n      for (int G = 0; G < total; ++G) {\n"
-     "        const int slot = G & 1, it = G / nqb, i = G % nqb;\n        if (trm) ftr(1, tri, 20);\n"),
-    ("        if (G + 1 < total) issue_sdp(G + 1);\n",
-     "        if (trm) ftr(1, tri, 21);\n        if (G + 1 < total) issue_sdp(G + 1);\n        if (trm) ftr(1, tri, 22);\n"),
-    ("        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem\n        tc_fence_after();\n",
-     "        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem\n        tc_fence_after();\n        if (trm) ftr(1, tri, 23);\n"),
-    ("        umma_commit(&qd_empty[slot]);\n        if (G >= 2)",
-     "        umma_commit(&qd_empty[slot]);\n        if (trm) ftr(1, tri, 24);\n        if (G >= 2)"),
-    ("    int kb = 0, h = 0, b = 0;\n    if (my_items > 0) item(0, kb, h, b);\n    for (int G = 0; G < total; ++G) {\n",
-     "    int kb = 0, h = 0, b = 0;\n    if (my_items > 0) item(0, kb, h, b);\n"
-     "    const bool trs = blockIdx.x == 0 && e == 0 && lane == 0;\n"
-     "    int tri = 0;\n    for (int G = 0; G < total; ++G) {\n      if (trs) ftr(0, tri, 0);\n"),
-    ("      mbar_wait(s_full, G & 1);\n      tc_fence_after();\n",
-     "      mbar_wait(s_full, G & 1);\n      tc_fence_after();\n      if (trs) ftr(0, tri, 1);\n"),
-    ("      // the previous block's dV / dK / dQ products have finished reading P / dS\n",
-     "      if (trs) ftr(0, tri, 4);\n      // the previous block's dV / dK / dQ products have finished reading P / dS\n"),
-    ("      if (lane == 0) mbar_arrive(ds_full);\n      if (i == nqb - 1) {",
-     "      if (lane == 0) mbar_arrive(ds_full);\n      if (trs) ftr(0, tri, 6);\n      if (i == nqb - 1) {"),
-]
 
 GEMM = [
     ("constexpr int kBM = 128;\nconstexpr int kBK = 64;",
@@ -95,9 +64,7 @@ def main():
     objs = []
     for src in sorted(CSRC.glob("*.cu")):
         text = src.read_text()
-        if src.name == "sg_attn.cu":
-            text = patch(text, ATTN)
-        elif src.name == "sg_gemm.cu":
+        if src.name == "sg_gemm.cu":
             text = patch(text, GEMM)
         dst = TMP / src.name
         dst.write_text(text)
