@@ -66,6 +66,7 @@ struct GemmParams {
   int nb2;
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int k_splits, kb_per_split;   // split-K: work unit = (split, tile), partial sums reduce-added into D
+  int full_units;               // units >= full_units are half-width (BN / 2) tiles of the last round
   int a_b2_first, b_b2_first, o_b2_first, x_b2_first, c_b2_first;
   int mode;
   int d_f32;
@@ -202,6 +203,22 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb,
   }
   z1 = (int)p.fd_nb2.div((uint32_t)z);
   z2 = z - z1 * p.nb2;
+}
+
+// Work unit t -> tile. The last partial round of a pair-tile product can be issued
+// as twice as many half-width units (tile columns [0, BN/2) and [BN/2, BN)): the
+// round then costs one narrow tile instead of one full tile on fewer pairs
+// (N = 1024 products: 3.46 -> 3.73 tile times... measured in DESIGN.md).
+// half = -1 for a full tile.
+__device__ __forceinline__ void decode_unit(const GemmParams& p, int t, int& mb, int& nb, int& z1, int& z2, int& half) {
+  if (t >= p.full_units) {
+    const int h = t - p.full_units;
+    half = h & 1;
+    t = p.full_units + (h >> 1);
+  } else {
+    half = -1;
+  }
+  decode_tile(p, t, mb, nb, z1, z2);
 }
 
 // k-block range of work unit t (the whole K unless split-K)
@@ -396,12 +413,14 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       // ------------------------------------------------------------ producer
       uint32_t stage = 0, phase = 0;
       for (int t = unit0; t < p.num_tiles; t += nunits) {
-        int mb, nb, z1, z2;
-        decode_tile(p, t, mb, nb, z1, z2);
+        int mb, nb, z1, z2, half;
+        decode_unit(p, t, mb, nb, z1, z2, half);
         int kb0, kb1;
         unit_k_range(p, t, kb0, kb1);
         const int m0 = mb * TM + (int)rank * kBM;  // this CTA's A rows
-        const int n0 = nb * BN + (int)rank * BNL;  // this CTA's B rows (N)
+        // this CTA's B rows (N); a half-width pair unit uses the first BNL / 2 rows of each
+        // CTA's B tile (the box still loads BNL rows: same transaction bytes)
+        const int n0 = half < 0 ? nb * BN + (int)rank * BNL : nb * BN + half * (BN / 2) + (int)rank * (BNL / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * A_BYTES;
@@ -455,10 +474,12 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
     if (lane == 0 && rank == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t IDESC = umma_idesc_bf16(TM, Cfg::MMA_N, A_MN, B_MN);
+      constexpr uint32_t IDESC_FULL = umma_idesc_bf16(TM, Cfg::MMA_N, A_MN, B_MN);
+      constexpr uint32_t IDESC_HALF = umma_idesc_bf16(TM, Cfg::MMA_N / 2, A_MN, B_MN);
       constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;  // second MMA_N-wide half of B
       uint32_t stage = 0, phase = 0, it = 0;
       for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
+        const uint32_t IDESC = (PAIR && t >= p.full_units) ? IDESC_HALF : IDESC_FULL;
         const uint32_t as = it % ACC, aph = (it / ACC) & 1;
         if (PAIR)
           mbar_wait_cluster(&tempty[as], aph ^ 1);  // both CTAs' epilogues drained this buffer
@@ -556,10 +577,10 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     const bool side = f_aux_out || f_d2 || in_kind == 2 || c_side;
     const int main_bytes = (d_f32 || (in_kind == 1 && c_f32)) ? 4096 : 2048;
     const bool dual = main_bytes + (side ? 2048 : 0) <= 4096;
-    auto issue_in = [&](int tnb, int trow0, int tz1, int tz2, int c, uint32_t si) {  // lane 0 only
+    auto issue_in = [&](int tncol, int trow0, int tz1, int tz2, int c, uint32_t si) {  // lane 0 only
       uint8_t* base = stg_w + (dual ? si * 4096 : 0);
       uint64_t* bar = &inbar[e * 2 + si];
-      const int col0 = tnb * BN + c * 32;
+      const int col0 = tncol + c * 32;
       if (in_kind == 1 && c_f32) {
         mbar_arrive_expect_tx(bar, 4096);
         load_box(&tmC, base, bar, col0, trow0, tz2, tz1, p.c_b2_first);
@@ -573,8 +594,10 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     };
     bool pref_next = false;  // the next tile's first chunk input is in flight
     for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
-      int mb, nb, z1, z2;
-      decode_tile(p, t, mb, nb, z1, z2);
+      int mb, nb, z1, z2, half;
+      decode_unit(p, t, mb, nb, z1, z2, half);
+      const int ncol = half < 0 ? nb * BN : nb * BN + half * (BN / 2);  // first column of the unit
+      const int nch = half < 0 ? NCH : NCH / 2;                          // 32-column chunks of the unit
       const uint32_t as = it % ACC, aph = (it / ACC) & 1;
       const int row0 = mb * TM + (int)rank * kBM + q * 32;
       const int nrows = min(32, p.M - row0);
@@ -642,20 +665,20 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       // coalesced load, prefetched a chunk ahead), broadcast to the row threads via smem
       const float* vecp = f_bias ? p.bias : (f_ln ? p.ln_gamma : nullptr);
       auto load_bias = [&](int c) -> float {
-        const int col = nb * BN + c * 32 + lane;
-        return (vecp && c < NCH && col < p.N) ? __ldg(vecp + col) : 0.f;
+        const int col = ncol + c * 32 + lane;
+        return (vecp && c < nch && col < p.N) ? __ldg(vecp + col) : 0.f;
       };
       float bias_cur = load_bias(c_first), bias_nxt = 0.f;
 #pragma unroll 1
-      for (int c = c_first; c < NCH; c += CSTEP) {
-        const int col0 = nb * BN + c * 32;
+      for (int c = c_first; c < nch; c += CSTEP) {
+        const int col0 = ncol + c * 32;
         const bool active = col0 < p.N && nrows > 0;  // warp-uniform
         if (vecp) bias_nxt = load_bias(c + CSTEP);
         // accumulator chunk, thread = row
         uint32_t r[32];
         tmem_ld32(tacc + c * 32, r);
         tmem_wait_ld();
-        if (c + CSTEP >= NCH) {
+        if (c + CSTEP >= nch) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) release_acc(as);
@@ -668,19 +691,19 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
           if (lane == 0) {
             if (in_kind && !pref) {  // not prefetched (first chunk of the tile / one slot)
               bulk_wait_read<0>();
-              issue_in(nb, row0, z1, z2, c, si);
+              issue_in(ncol, row0, z1, z2, c, si);
             }
             const int cn = c + CSTEP;
-            if (in_kind && dual && cn < NCH && nb * BN + cn * 32 < p.N) {
+            if (in_kind && dual && cn < nch && ncol + cn * 32 < p.N) {
               bulk_wait_read<0>();  // the other slot's last store has read it
-              issue_in(nb, row0, z1, z2, cn, si ^ 1);
+              issue_in(ncol, row0, z1, z2, cn, si ^ 1);
             } else if (dual) {
               bulk_wait_read<1>();  // this slot's previous TMA stores have read it
             } else {
               bulk_wait_read<0>();
             }
           }
-          pref = in_kind && dual && c + CSTEP < NCH && nb * BN + (c + CSTEP) * 32 < p.N;
+          pref = in_kind && dual && c + CSTEP < nch && ncol + (c + CSTEP) * 32 < p.N;
           __syncwarp();
           if (in_kind) {
             mbar_wait(&inbar[e * 2 + si], (inph >> si) & 1);
@@ -815,13 +838,14 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         bias_cur = bias_nxt;
       }
       if (in_kind && dual && t + nunits < p.num_tiles) {
-        int mb2, nb2, y1, y2;
-        decode_tile(p, t + nunits, mb2, nb2, y1, y2);
+        int mb2, nb2, y1, y2, half2;
+        decode_unit(p, t + nunits, mb2, nb2, y1, y2, half2);
+        const int ncol2 = half2 < 0 ? nb2 * BN : nb2 * BN + half2 * (BN / 2);
         const int row0n = mb2 * TM + (int)rank * kBM + q * 32;
-        if (nb2 * BN + c_first * 32 < p.N && row0n < p.M) {
+        if (ncol2 + c_first * 32 < p.N && row0n < p.M) {
           if (lane == 0) {
             bulk_wait_read<0>();
-            issue_in(nb2, row0n, y1, y2, c_first, slot);
+            issue_in(ncol2, row0n, y1, y2, c_first, slot);
           }
           pref_next = true;
         }
@@ -1193,7 +1217,22 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   tiles *= p.k_splits;
   p.num_tiles = (int)tiles;
+  p.full_units = p.num_tiles;
   p.fd_tiles.set((uint32_t)(tiles / p.k_splits));
+  // last partial round as half-width units (pair tiles 256 x 256 only, no split-K):
+  // when at most half the pairs would work in it, twice as many 256 x 128 units finish
+  // it in about 0.7 of a tile time. SG_GEMM_HALF_TAIL=0 disables (experiments).
+  static const int env_half_tail = [] {
+    const char* e = getenv("SG_GEMM_HALF_TAIL");
+    return e ? atoi(e) : 1;
+  }();
+  if (env_half_tail && pair && bn == 256 && p.k_splits == 1) {
+    const long long tail = tiles % units;
+    if (tiles >= units && tail > 0 && 2 * tail <= units) {
+      p.full_units = (int)(tiles - tail);
+      p.num_tiles = (int)(tiles + tail);
+    }
+  }
   p.fd_per.set((uint32_t)(p.m_tiles * p.n_tiles));
   p.fd_span.set((uint32_t)(kGroupM * p.n_tiles));
   p.fd_nb2.set((uint32_t)p.nb2);
@@ -1264,7 +1303,7 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   if (!(a->C && !p.reduce_add)) m.c = m.d;
   if (!p.has_d2) m.d2 = m.d;
 
-  const int grid = (int)std::min<long long>(tiles, units) * (pair ? 2 : 1);
+  const int grid = (int)std::min<long long>(p.num_tiles, units) * (pair ? 2 : 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
   // 8 epilogue warps unless the epilogue needs whole rows (softmax modes)
