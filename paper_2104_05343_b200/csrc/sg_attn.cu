@@ -792,23 +792,46 @@ constexpr uint32_t kT64 = 128 * 64 * 2;  // one 128 x 64 bf16 tile (16 KB)
 constexpr int kMaxItems = 256;           // per-CTA work items of the persistent backward (item table in smem)
 
 // ----------------------------------------------------------------------------
-// Backward v2 (d = 64), persistent: CTA c walks work items t = c, c + grid, ...
-// with t = (key block, head, batch), key block fastest. Per query block:
-//   MMA   S_G+1, dP_G+1 are issued right after the softmax warps have read S_G / dP_G,
-//         ahead of dV_G, dK_G, dQ_G, so the next block's exponentials overlap this
-//         block's products — across item boundaries too (K double-buffered per
-//         item, V reloaded as soon as the item's last dP has read it); dV_G runs
-//         first and releases P at once, dS is double-buffered, so block G+1's P / dS
-//         stores wait only for dV_G (P) and for block G-1's dK / dQ (dS) instead of
-//         for all three products of block G; dQ alternates between two TMEM buffers
-//   warps 4-11 (lane quadrant x key half) compute P / dS for their 64 keys in
-//         registers; lse / D row statistics are prefetched a block ahead
-//   warps 12-15 (one per lane quadrant) drain dQ (TMEM -> smem -> TMA reduce-add)
-//         and at an item's end write its dK / dV (TMA stores, bias-gradient column
-//         sums) and release the TMEM accumulators
-//   setmaxnreg: producer / MMA warpgroup 56 registers, softmax 176, drain 96.
+// Backward (d = 64), persistent, transposed orientation: CTA c walks work items
+// t = c, c + grid, ... with t = (key block, head, batch), key block fastest. Per
+// query block G (128 queries) of an item (128 keys):
+//   S^T  = K Q^T,  dP^T = V dO^T                  (TMEM, M = keys, N = queries)
+//   P^T  = 2^(S^T scale log2e - lse log2e)        -> TMEM (packed bf16, own region)
+//   dS^T = P^T (dP^T - D) scale                   -> TMEM (packed, in place over dP^T)
+//                                                    and shared memory ([keys x queries])
+//   dV  += P^T dO,  dK += dS^T Q                   ("TS" MMAs: A read from TMEM)
+//   dQ   = dS K                                    (A = dS, MN-major from shared memory)
+// so per block the tensor core reads only Q, dO, K, V tiles and one copy of dS from
+// shared memory (the N = 64 products of the [queries x keys] orientation, with P / dS
+// from shared memory, are shared-memory bound: tools/micro/umma_rate.cu). Rows of the
+// softmax are keys, so the per-query statistics (lse; D = rowsum(dO * O) from
+// sg_attn_rowdot) are staged per warp in shared memory and read as broadcasts;
+// queries past s get lse = +inf (P = 0), keys past s are zeroed.
+//   warp 0      TMA producer: K per item (2 slots), V per item (1 slot), Q / dO per
+//               block (3 slots, the block after next prefetched into L2)
+//   warp 1      MMA issuer, per block G: S^T_G+1 as soon as the softmax warps have read
+//               S^T_G; dV_G as soon as P^T_G is in TMEM (before dS_G exists); dK_G,
+//               dP^T_G+1 and dQ_G once dS_G is stored. Four commits per block (each
+//               commit costs the tensor pipe ~70 clocks, tools/micro/bwd_seq.cu): the
+//               softmax warps reuse the Q / dO slot barrier (dK_G-1 done => dV_G-1 has
+//               read P^T) and the dQ barrier (dQ_G-1 has read the single dS buffer).
+//   warp 2      TMEM allocator: S^T | dP^T (dS^T) | P^T | dV | dK | dQ
+//   warps 4-11  softmax: warp e owns TMEM lane quadrant e % 4 (32 keys) and query
+//               half e / 4 (64 queries); NPOLY of every 16 exponent pairs run on the
+//               FMA pipe (ex2_poly2) instead of MUFU
+//   warps 12-15 drain: dQ_G (TMEM -> two 4 KB staging boxes -> TMA reduce-add into the
+//               fp32 accumulator) and, at an item's end, dK / dV (both read out of TMEM
+//               before the accumulators are released, then staged and TMA-stored)
+//   setmaxnreg: producer / MMA warpgroup 56 registers, softmax 160, drain 128.
 // G counts query blocks over all of the CTA's items (barrier phases).
 // ----------------------------------------------------------------------------
+constexpr int kQD = 3;  // Q / dO slots of the d = 64 backward
+#ifndef SG_BWD_POLY
+#define SG_BWD_POLY 0
+#endif
+constexpr int kBwdPoly = SG_BWD_POLY;  // exponent pairs of every 16 on the FMA pipe
+
+template <int NPOLY>
 __global__ void __launch_bounds__(512, 1)
     flash_bwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -819,29 +842,29 @@ __global__ void __launch_bounds__(512, 1)
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   uint8_t* sK = smem;                 // 2 slots (items)
   uint8_t* sV = sK + 2 * kT64;        // 1 slot
-  uint8_t* sQ = sV + kT64;            // 2 slots (query blocks)
-  uint8_t* sDO = sQ + 2 * kT64;       // 2 slots
-  uint8_t* sP = sDO + 2 * kT64;       // 32 KB (2 atoms of 64 keys)
-  uint8_t* sDS = sP + 2 * kT64;       // 2 buffers x 32 KB
-  uint8_t* sStg = sDS + 4 * kT64;     // 4 drain warps x 4 KB (dQ fp32 / dK, dV bf16 staging)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 4096);
+  uint8_t* sQ = sV + kT64;            // kQD slots (query blocks)
+  uint8_t* sDO = sQ + kQD * kT64;     // kQD slots
+  uint8_t* sDS = sDO + kQD * kT64;    // 32 KB: [keys x queries], 2 atoms of 64 queries
+  uint8_t* sStg = sDS + 2 * kT64;     // 4 drain warps x 2 x 4 KB (dQ fp32 boxes)
+  float* sStat = reinterpret_cast<float*>(sStg + 4 * 8192);  // 8 softmax warps x [64 -lse log2e | 64 -D scale]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 8 * 128);
   int* items_tab = reinterpret_cast<int*>(bars + 32);  // this CTA's items as packed (kb, h, b)
   uint64_t* k_full = bars;         // [2]
   uint64_t* k_empty = bars + 2;    // [2]
-  uint64_t* qd_full = bars + 4;    // [2]
-  uint64_t* qd_empty = bars + 6;   // [2]
-  uint64_t* s_full = bars + 8;
-  uint64_t* ds_full = bars + 9;
-  uint64_t* p_free = bars + 10;    // dV_G has read P_G
-  uint64_t* dq_full = bars + 11;   // [2]
-  uint64_t* dq_empty = bars + 13;  // [2]
-  uint64_t* acc_full = bars + 15;
-  uint64_t* acc_empty = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-  uint64_t* s_free = bars + 18;    // S_G / dP_G read out of TMEM (8 softmax warps)
-  uint64_t* v_full = bars + 19;
-  uint64_t* v_empty = bars + 20;   // the item's last dP has read V
-  uint64_t* ds_free = bars + 21;   // [2] dK_G / dQ_G have read dS buffer G & 1
+  uint64_t* v_full = bars + 4;
+  uint64_t* v_empty = bars + 5;
+  uint64_t* qd_full = bars + 6;    // [kQD]
+  uint64_t* qd_empty = bars + 9;   // [kQD] dK_G done (Q_G, dO_G free; P^T_G read by dV_G)
+  uint64_t* s_full = bars + 12;
+  uint64_t* s_free = bars + 13;    // S^T_G read out of TMEM (8 softmax warps)
+  uint64_t* p_full = bars + 14;    // P^T_G in TMEM (8 softmax warps)
+  uint64_t* dp_full = bars + 15;
+  uint64_t* ds_full = bars + 16;   // dS^T_G in TMEM and dS_G in smem (8 softmax warps)
+  uint64_t* dq_full = bars + 17;   // dQ_G done (the dS buffer is free)
+  uint64_t* dq_empty = bars + 18;  // 4 drain warps
+  uint64_t* acc_full = bars + 19;
+  uint64_t* acc_empty = bars + 20; // 4 drain warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (p.s + 127) / 128;
@@ -867,20 +890,22 @@ __global__ void __launch_bounds__(512, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < kQD; ++i) {
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
-      mbar_init(&dq_full[i], 1);
-      mbar_init(&dq_empty[i], 4);
-      mbar_init(&ds_free[i], 1);
     }
     mbar_init(v_full, 1);
     mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
+    mbar_init(s_free, 8);
+    mbar_init(p_full, 8);
+    mbar_init(dp_full, 1);
     mbar_init(ds_full, 8);
-    mbar_init(p_free, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4);
-    mbar_init(s_free, 8);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -895,9 +920,10 @@ __global__ void __launch_bounds__(512, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_begin();
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
-  // registers per warpgroup (set at the top of each role): producer / MMA / idle 56,
-  // softmax 176, drain 96
+  // TMEM columns: S^T 0..127 | dP^T (then dS^T packed in place) 128..255 | P^T packed
+  // 256..319 | dV 320..383 | dK 384..447 | dQ 448..511
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_p = tmem + 256, t_dv = tmem + 320, t_dk = tmem + 384,
+                 t_dq = tmem + 448;
   auto item = [&](int it, int& kb, int& h, int& b) {
     const int v = items_tab[it];
     kb = v & 1023;
@@ -920,11 +946,11 @@ __global__ void __launch_bounds__(512, 1)
         mbar_arrive_expect_tx(v_full, kT64);
         tma4(&tmV, sV, v_full, 0, kb * 128, h, b, p.v_b2_first);
         for (int i = 0; i < nqb; ++i, ++G) {
-          const int slot = G & 1;
+          const int slot = G % kQD, use = G / kQD;
           {
-            // Q / dO of block G + 2 into L2 now: with two smem slots its TMA load can only
-            // start when block G's products finish, shortly before it is needed
-            int i2 = i + 2, t2 = t, kb2 = kb, h2 = h, b2 = b;
+            // Q / dO of block G + kQD into L2 now (its smem slot frees only when block G's
+            // dK is done)
+            int i2 = i + kQD, t2 = t, kb2 = kb, h2 = h, b2 = b;
             while (i2 >= nqb) {
               i2 -= nqb;
               t2 += gridDim.x;
@@ -935,7 +961,7 @@ __global__ void __launch_bounds__(512, 1)
               tma4_l2(&tmDO, 0, i2 * 128, h2, b2, p.do_b2_first);
             }
           }
-          mbar_wait(&qd_empty[slot], ((G >> 1) & 1) ^ 1);
+          mbar_wait(&qd_empty[slot], (use & 1) ^ 1);
           mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
           tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
           tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
@@ -944,177 +970,301 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 1) {
     reg_dealloc<56>();
-    if (lane == 0) {
-      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: M = queries, N = keys
-      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, true, true);     // dV, dK: A = P^T / dS^T, B = dO / Q
-      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, false, true);    // dQ: A = dS, B = K
-      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
-      auto issue_sdp = [&](int G) {
-        const int it = G / nqb, slot = G & 1;
-        if (G % nqb == 0) {
-          mbar_wait(&k_full[it & 1], (it >> 1) & 1);
-          mbar_wait(v_full, it & 1);
-        }
-        mbar_wait(&qd_full[slot], (G >> 1) & 1);
+    // the whole warp walks the loop (warp-uniform operands live in uniform registers);
+    // one elected lane issues each MMA / commit
+    {
+      constexpr uint32_t ID_ST = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T: M = keys, N = queries
+      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 64, false, true);    // dV, dK: A = P^T / dS^T (TMEM), B = dO / Q
+      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 64, true, true);     // dQ: A = dS (MN-major), B = K
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t ts = tm, tdp = tm + 128, tp = tm + 256, tdv = tm + 320, tdk = tm + 384, tdq = tm + 448;
+      // descriptors: K-step advances add (bytes >> 4) to the start-address field
+      const uint64_t d_k0 = umma_desc_sw128(smem_u32(sK), 0, 1024), d_v0 = umma_desc_sw128(smem_u32(sV), 0, 1024);
+      const uint64_t d_q0 = umma_desc_sw128(smem_u32(sQ), 0, 1024), d_do0 = umma_desc_sw128(smem_u32(sDO), 0, 1024);
+      const uint64_t m_q0 = umma_desc_sw128(smem_u32(sQ), kT64, 1024), m_do0 = umma_desc_sw128(smem_u32(sDO), kT64, 1024);
+      const uint64_t m_k0 = umma_desc_sw128(smem_u32(sK), kT64, 1024), m_ds = umma_desc_sw128(smem_u32(sDS), kT64, 1024);
+      constexpr uint64_t kTile = kT64 >> 4;  // one 16 KB tile in descriptor units
+      const bool trm = blockIdx.x == 0 && lane == 0;
+      int tri = 0;
+      (void)trm; (void)tri;
+      auto issue_s = [&](int G) {  // S^T_G = K Q_G^T
+        const int it = G / nqb, slot = G % kQD;
+        if (G % nqb == 0) mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+        mbar_wait(&qd_full[slot], (G / kQD) & 1);
         tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64), v_base = smem_u32(sV);
-        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
+        SG_TR(trm, 0, tri, 8);
+        const uint64_t ak = d_k0 + (it & 1) * kTile, bq = d_q0 + slot * kTile;
+        if (elect_one()) {
+#ifndef SG_EXP_NOMMA
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // K-dim = d = 64: 4 x 16 inside one atom
-          umma_bf16(t_s, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
-                    ID_SQ, kk > 0 ? 1u : 0u);
-          umma_bf16(t_dp, umma_desc_sw128(do_base + kk * 32, 0, 1024), umma_desc_sw128(v_base + kk * 32, 0, 1024),
-                    ID_SQ, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)  // K-dim = d = 64: 4 x 16 inside one atom (32 B = 2 units)
+            umma_bf16(ts, ak + 2 * kk, bq + 2 * kk, ID_ST, kk > 0 ? 1u : 0u);
+#endif
+          umma_commit(s_full);
         }
-        umma_commit(s_full);
-        if (G % nqb == nqb - 1) umma_commit(v_empty);  // the item's last dP: V may be reloaded
+        __syncwarp();
       };
-      if (total > 0) issue_sdp(0);
+      auto issue_dp = [&](int G) {  // dP^T_G = V dO_G^T (Q_G / dO_G already waited for by issue_s(G))
+        const int it = G / nqb, slot = G % kQD;
+        if (G % nqb == 0) {
+          mbar_wait(v_full, it & 1);
+          tc_fence_after();
+        }
+        const uint64_t bdo = d_do0 + slot * kTile;
+        if (elect_one()) {
+#ifndef SG_EXP_NOMMA
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) umma_bf16(tdp, d_v0 + 2 * kk, bdo + 2 * kk, ID_ST, kk > 0 ? 1u : 0u);
+#endif
+          umma_commit(dp_full);
+          if (G % nqb == nqb - 1) umma_commit(v_empty);  // the item's last dP^T: V may be reloaded
+        }
+        __syncwarp();
+      };
+      if (total > 0) {
+        issue_s(0);
+        issue_dp(0);
+      }
       for (int G = 0; G < total; ++G) {
-        const int slot = G & 1, it = G / nqb, i = G % nqb;
-        // S_G+1 / dP_G+1 overwrite S_G / dP_G as soon as the softmax warps have read
-        // them, overlapping the second half of block G's exponentials
+        const int slot = G % kQD, it = G / nqb, i = G % nqb;
+        const uint64_t mk = m_k0 + (it & 1) * kTile, mq = m_q0 + slot * kTile, mdo = m_do0 + slot * kTile;
+        SG_TR(trm, 0, tri, 0);
+        // S^T_G+1 overwrites S^T_G as soon as the softmax warps have read it
         mbar_wait(s_free, G & 1);
         tc_fence_after();
-        if (G + 1 < total) issue_sdp(G + 1);
-        mbar_wait(ds_full, G & 1);  // P_G, dS_G in smem
+        SG_TR(trm, 0, tri, 1);
+        if (G + 1 < total) issue_s(G + 1);
+        SG_TR(trm, 0, tri, 2);
+        mbar_wait(p_full, G & 1);  // P^T_G in TMEM
         tc_fence_after();
         // the previous item's dK / dV have been read out before this item's first products
         if (i == 0 && it > 0) {
           mbar_wait(acc_empty, (it - 1) & 1);
           tc_fence_after();
         }
-        const uint32_t k_base = smem_u32(sK + (it & 1) * kT64);
-        const uint32_t q_base = smem_u32(sQ + slot * kT64), do_base = smem_u32(sDO + slot * kT64);
-        const uint32_t dsb = ds_base + slot * 2 * kT64;
+        SG_TR(trm, 0, tri, 3);
+#if !defined(SG_EXP_NOMMA) && !defined(SG_EXP_NOKV)
+        if (elect_one()) {
 #pragma unroll
-        for (int kq = 0; kq < 8; ++kq)  // dV += P^T dO, K-dim = 128 queries: 16 rows = 2048 B per step
-          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(do_base + kq * 2048, 8192 * 2, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
-        umma_commit(p_free);  // P_G read: block G+1 may store its P
-#pragma unroll
-        for (int kq = 0; kq < 8; ++kq)  // dK += dS^T Q
-          umma_bf16(t_dk, umma_desc_sw128(dsb + kq * 2048, 2 * 8192, 1024),
-                    umma_desc_sw128(q_base + kq * 2048, 8192 * 2, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
-        umma_commit(&qd_empty[slot]);
-        if (G >= 2) mbar_wait(&dq_empty[slot], ((G - 2) >> 1) & 1);  // dQ_G-2 drained from this buffer
+          for (int kq = 0; kq < 8; ++kq)  // dV += P^T dO, K-dim = 128 queries: 8 packed columns / 16 rows per step
+            umma_bf16_ts(tdv, tp + kq * 8, mdo + 128 * kq, ID_KV, (i | kq) != 0 ? 1u : 0u);
+        }
+        __syncwarp();
+#endif
+        SG_TR(trm, 0, tri, 9);
+        mbar_wait(ds_full, G & 1);  // dS^T_G in TMEM (over dP^T_G), dS_G in smem
         tc_fence_after();
+        SG_TR(trm, 0, tri, 4);
+        if (elect_one()) {
+#if !defined(SG_EXP_NOMMA) && !defined(SG_EXP_NOKV)
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
-          umma_bf16(t_dq + slot * 64, umma_desc_sw128(dsb + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
-                    umma_desc_sw128(k_base + kk * 2048, 8192 * 2, 1024), ID_DQ, kk > 0 ? 1u : 0u);
+          for (int kq = 0; kq < 8; ++kq)  // dK += dS^T Q: query half kq / 4 packed at column 64 (kq / 4)
+            umma_bf16_ts(tdk, tdp + (kq >> 2) * 64 + (kq & 3) * 8, mq + 128 * kq, ID_KV, (i | kq) != 0 ? 1u : 0u);
+#endif
+          umma_commit(&qd_empty[slot]);  // Q_G / dO_G free; P^T_G read (dV_G issued before dK_G)
         }
-        umma_commit(&dq_full[slot]);
-        umma_commit(&ds_free[slot]);  // dS buffer G & 1 no longer read
-        if (i == nqb - 1) {
-          umma_commit(acc_full);          // this item's dK / dV complete
-          umma_commit(&k_empty[it & 1]);  // and its K no longer needed
+        __syncwarp();
+        SG_TR(trm, 0, tri, 10);
+        // dP^T_G+1 overwrites dS^T_G once dK_G has read it (MMAs execute in issue order)
+        if (G + 1 < total) issue_dp(G + 1);
+        SG_TR(trm, 0, tri, 11);
+        if (G >= 1) mbar_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained
+        tc_fence_after();
+        SG_TR(trm, 0, tri, 5);
+        if (elect_one()) {
+#if !defined(SG_EXP_NOMMA) && !defined(SG_EXP_NODQ)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // dQ = dS K, K-dim = 128 keys: 16 key rows (2048 B) per step
+            umma_bf16(tdq, m_ds + 128 * kk, mk + 128 * kk, ID_DQ, kk > 0 ? 1u : 0u);
+#endif
+          SG_TR(trm, 0, tri, 12);
+          umma_commit(dq_full);  // dQ_G in TMEM; the dS buffer is free
+          if (i == nqb - 1) {
+            umma_commit(acc_full);          // this item's dK / dV complete
+            umma_commit(&k_empty[it & 1]);  // and its K no longer needed
+          }
         }
+        __syncwarp();
+        SG_TR(trm, 0, tri, 13);
       }
     }
   } else if (warp < 4) {
     reg_dealloc<56>();
+#ifdef SG_TRACE
+    // observer (instrumented build): completion times of the tensor-pipe commits
+    if (warp == 3 && lane == 0 && blockIdx.x == 0) {
+      int tri = 0;
+      for (int G = 0; G < total; ++G) {  // completion order: S^T_G+1, dK_G, dP^T_G+1, dQ_G
+        if (G + 1 < total) mbar_wait(s_full, (G + 1) & 1);
+        SG_TR(true, 3, tri, 0);
+        mbar_wait(&qd_empty[G % kQD], (G / kQD) & 1);
+        SG_TR(true, 3, tri, 1);
+        if (G + 1 < total) mbar_wait(dp_full, (G + 1) & 1);
+        SG_TR(true, 3, tri, 2);
+        mbar_wait(dq_full, G & 1);
+        SG_TR(true, 3, tri, 3);
+      }
+    }
+#endif
   } else if (warp < 12) {
-    reg_alloc<176>();
-    // 8 softmax warps: warp e owns TMEM lane quadrant e % 4 (32 query rows) and key half
-    // e / 4 (64 of the 128 key columns = one 64-key atom of P / dS)
+    reg_alloc<160>();
+    // 8 softmax warps: warp e owns TMEM lane quadrant e % 4 (32 keys) and query half e / 4
     const int e = warp - 4;
-    const int q = e & 3, half = e >> 2;
-    const int r = q * 32 + lane;
+    const int q = e & 3, hq = e >> 2;
+    const int r = q * 32 + lane;  // key row of the block
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    const float scale = p.scale, scale_log2 = p.scale_log2;
-    // raw loads only: converting here would make the prefetch wait for the load
-    auto row_stats = [&](int it, int i, float& lse, float& dd) {
-      lse = dd = 0.f;
+    float* st = sStat + e * 128;  // this warp's statistics: [0, 64) -lse log2e, [64, 128) -D scale
+    const float scale = p.scale;
+    // the warp's 64 queries' statistics of block (it, i): lane holds queries 64 hq + lane, + 32
+    auto load_stats = [&](int it, int i, float (&v)[4]) {
+      v[0] = v[1] = INFINITY;
+      v[2] = v[3] = 0.f;
       if (it >= my_items) return;
       int kb, h, b;
       item(it, kb, h, b);
-      const int qrow = i * 128 + r;
-      if (qrow >= p.s) return;
-      const size_t off = ((size_t)b * p.nh + h) * p.s + qrow;
-      lse = __ldg(p.lse + off);
-      dd = __ldg(p.drow + off);
+      const size_t off = ((size_t)b * p.nh + h) * p.s;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int qrow = i * 128 + hq * 64 + u * 32 + lane;
+        if (qrow < p.s) {
+          v[u] = __ldg(p.lse + off + qrow);
+          v[2 + u] = __ldg(p.drow + off + qrow);
+        }
+      }
     };
-    float lse_n, dd_n;
-    row_stats(0, 0, lse_n, dd_n);
-    int it = 0, i = 0;            // (item, query block) of G, advanced incrementally
+    const bool trs = blockIdx.x == 0 && lane == 0 && e == 0;
+    int tri = 0;
+    (void)trs; (void)tri;
+    float stn[4];
+    load_stats(0, 0, stn);
+    int it = 0, i = 0;  // (item, query block) of G, advanced incrementally
     int kb = 0, h = 0, b = 0;
     if (my_items > 0) item(0, kb, h, b);
+    const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2), sc2 = f2_pack(scale, scale);
     for (int G = 0; G < total; ++G) {
       const int kvalid = min(128, p.s - kb * 128);
-      const bool full_keys = kvalid == 128;
-      const float lse_c = lse_n, dd = dd_n;
+      __syncwarp();  // every lane has read block G-1's statistics
+      st[lane] = -stn[0] * 1.4426950408889634f;
+      st[32 + lane] = -stn[1] * 1.4426950408889634f;
+      st[64 + lane] = -stn[2] * scale;
+      st[96 + lane] = -stn[3] * scale;
+      __syncwarp();
       {
         const int ni = i + 1 == nqb ? 0 : i + 1, nit = i + 1 == nqb ? it + 1 : it;
-        row_stats(nit, ni, lse_n, dd_n);  // prefetch
+        load_stats(nit, ni, stn);  // prefetch
       }
-      const bool qok = i * 128 + r < p.s;
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 0);
       mbar_wait(s_full, G & 1);
       tc_fence_after();
-      const float lse2 = lse_c * 1.4426950408889634f;
-      uint32_t pk[2][16], dk[2][16];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;  // 32-key chunk
-        uint32_t sv[32], dv[32];
-        tmem_ld32(t_s + lane_base + c * 32, sv);
-        tmem_ld32(t_dp + lane_base + c * 32, dv);
-        tmem_wait_ld();
-        if (cc == 1) {  // both chunks of S / dP are in registers: the next block's products may start
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_free);
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 1);
+#ifdef SG_EXP_NOSM
+      {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+        if (G > 0) mbar_wait(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        mbar_wait(dp_full, G & 1);
+        if (G > 0) mbar_wait(dq_full, (G - 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+        if (i == nqb - 1) {
+          i = 0;
+          ++it;
+          if (it < my_items) item(it, kb, h, b);
+        } else {
+          ++i;
         }
-        // pairs of keys on the paired fp32 pipe: y = s * scale - lse, P = 2^y,
-        // dS = (P * scale) * (dP - D)
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nl2 = f2_pack(-lse2, -lse2);
-        const uint64_t nd2 = f2_pack(-dd, -dd), ss2 = f2_pack(scale, scale);
+        continue;
+      }
+#endif
+      uint32_t sv[64];
+      tmem_ld32(t_s + lane_base + hq * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+      tmem_ld32(t_s + lane_base + hq * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);  // the next block's S^T may overwrite these columns
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 2);
+      // P^T = 2^(s scale log2e - lse log2e), pairs of queries on the paired fp32 pipe;
+      // fp32 P kept (in sv) for dS, packed bf16 pairs for TMEM
+      uint32_t pk[32];
+      const bool key_ok = r < kvalid;
 #pragma unroll
-        for (int e2 = 0; e2 < 16; ++e2) {
-          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * e2]), __uint_as_float(sv[2 * e2 + 1])), sc2, nl2);
-          float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
-          float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
-          if (!full_keys || !qok) {
-            if (!qok || c * 32 + 2 * e2 >= kvalid) p0 = 0.f;
-            if (!qok || c * 32 + 2 * e2 + 1 >= kvalid) p1 = 0.f;
+      for (int j4 = 0; j4 < 16; ++j4) {
+        const float4 nl = *reinterpret_cast<const float4*>(st + 4 * j4);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = 2 * j4 + u;
+          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sl2,
+                                   u ? f2_pack(nl.z, nl.w) : f2_pack(nl.x, nl.y));
+          float p0, p1;
+          if ((j * NPOLY) % 16 < NPOLY) {  // NPOLY of 16 pairs, spread over the row
+            const uint64_t pp = ex2_poly2(y);
+            p0 = f2_lo(pp);
+            p1 = f2_hi(pp);
+          } else {
+            p0 = ex2f_fast(f2_lo(y));
+            p1 = ex2f_fast(f2_hi(y));
           }
-          const uint64_t pp = f2_pack(p0, p1);
-          const uint64_t dmd = fadd2(f2_pack(__uint_as_float(dv[2 * e2]), __uint_as_float(dv[2 * e2 + 1])), nd2);
-          const uint64_t ds = fmul2(fmul2(pp, ss2), dmd);
+          if (!key_ok) p0 = p1 = 0.f;
+          sv[2 * j] = __float_as_uint(p0);
+          sv[2 * j + 1] = __float_as_uint(p1);
           __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
-          __nv_bfloat162 hd = __floats2bfloat162_rn(__uint_as_float(static_cast<uint32_t>(ds)),
-                                                   __uint_as_float(static_cast<uint32_t>(ds >> 32)));
-          pk[cc][e2] = *reinterpret_cast<uint32_t*>(&hp);
-          dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
+          pk[j] = *reinterpret_cast<uint32_t*>(&hp);
         }
       }
-      // dS into buffer G & 1 once block G-2's dK / dQ have read it; P once dV_G-1 has
-      uint8_t* prow = sP + half * kT64 + r * 128;
-      uint8_t* drow_ = sDS + (G & 1) * 2 * kT64 + half * kT64 + r * 128;
-      if (G >= 2) mbar_wait(&ds_free[G & 1], ((G - 2) >> 1) & 1);
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 3);
+      if (G > 0) mbar_wait(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);  // dV_G-1 has read P^T_G-1
+      tc_fence_after();
+      tmem_st32(t_p + lane_base + hq * 32, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 4);
+      // dS^T = P^T (dP^T scale - D scale)
+      mbar_wait(dp_full, G & 1);
+      tc_fence_after();
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 5);
+      uint32_t dk[32];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld32(t_dp + lane_base + hq * 64 + c * 32, dv);
+        tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = (cc * 4 + k) ^ (r & 7);
-          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
-              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 nd = *reinterpret_cast<const float4*>(st + 64 + c * 32 + 4 * j4);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = 2 * j4 + u;
+            const uint64_t t = ffma2(f2_pack(__uint_as_float(dv[2 * j]), __uint_as_float(dv[2 * j + 1])), sc2,
+                                     u ? f2_pack(nd.z, nd.w) : f2_pack(nd.x, nd.y));
+            const uint64_t ds =
+                fmul2(f2_pack(__uint_as_float(sv[c * 32 + 2 * j]), __uint_as_float(sv[c * 32 + 2 * j + 1])), t);
+            __nv_bfloat162 hd = __floats2bfloat162_rn(f2_lo(ds), f2_hi(ds));
+            dk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&hd);
+          }
         }
       }
-      if (G > 0) mbar_wait(p_free, (G - 1) & 1);
+      // dS^T packed over this thread's own (already read) dP^T columns; dS into the smem
+      // buffer ([keys x queries] rows: the MN-major A operand of dQ) once dQ_G-1 has read it
+      tmem_st32(t_dp + lane_base + hq * 64, dk);
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 6);
+      if (G > 0) mbar_wait(dq_full, (G - 1) & 1);
+      uint8_t* drow_ = sDS + hq * kT64 + r * 128;
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = (cc * 4 + k) ^ (r & 7);
-          *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
-              make_uint4(pk[cc][4 * k], pk[cc][4 * k + 1], pk[cc][4 * k + 2], pk[cc][4 * k + 3]);
-        }
-      }
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<uint4*>(drow_ + ((k ^ (r & 7)) << 4)) =
+            make_uint4(dk[4 * k], dk[4 * k + 1], dk[4 * k + 2], dk[4 * k + 3]);
+      tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      SG_TR(trs, e == 0 ? 1 : 3, tri, 7);
       if (i == nqb - 1) {
         i = 0;
         ++it;
@@ -1124,76 +1274,124 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
   } else {
-    // 4 drain warps (lane quadrant q = warp % 4, 32 rows): dQ of every block (TMEM ->
-    // fp32 staging -> TMA reduce-add) and, at each item's end, its dK / dV (TMEM ->
-    // bf16 staging -> TMA stores, bias-gradient column sums), off the softmax warps'
-    // critical path
-    reg_dealloc<96>();
+    // 4 drain warps (lane quadrant q = warp % 4, 32 rows): dQ of every block and, at
+    // each item's end, its dK / dV, off the softmax warps' critical path
+    reg_alloc<128>();
     const int q = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sStg + (warp - 12) * 4096;
+    uint8_t* stg = sStg + (warp - 12) * 8192;
     int it = 0, i = 0, kb = 0, h = 0, b = 0;
     if (my_items > 0) item(0, kb, h, b);
+    const bool trd = blockIdx.x == 0 && lane == 0 && warp == 12;
+    int tri = 0;
+    (void)trd; (void)tri;
     for (int G = 0; G < total; ++G) {
-      const int slot = G & 1;
-      mbar_wait(&dq_full[slot], (G >> 1) & 1);
+      SG_TR(trd, 2, tri, 0);
+      mbar_wait(dq_full, G & 1);
       tc_fence_after();
-      uint32_t v[2][32];
-      tmem_ld32(t_dq + slot * 64 + lane_base, v[0]);
-      tmem_ld32(t_dq + slot * 64 + lane_base + 32, v[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_empty[slot]);
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        if (lane == 0) bulk_wait_read<0>();  // the previous TMA operation has read the staging box
+      SG_TR(trd, 2, tri, 1);
+#ifdef SG_EXP_NODRAIN
+      {
         __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(v[hf][4 * k]), __uint_as_float(v[hf][4 * k + 1]),
-                          __uint_as_float(v[hf][4 * k + 2]), __uint_as_float(v[hf][4 * k + 3]));
-        fence_proxy_async_smem();
+        if (lane == 0) mbar_arrive(dq_empty);
+        if (i == nqb - 1) {
+          mbar_wait(acc_full, it & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);
+          i = 0;
+          ++it;
+          if (it < my_items) item(it, kb, h, b);
+        } else {
+          ++i;
+        }
+        continue;
+      }
+#endif
+      {
+        uint32_t v[2][32];
+        tmem_ld32(t_dq + lane_base, v[0]);
+        tmem_ld32(t_dq + lane_base + 32, v[1]);
+        tmem_wait_ld();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (p.dq_b2_first)
-            tma_reduce_add_4d(&tmDQ, stg, hf * 32, h, i * 128 + q * 32, b);
-          else
-            tma_reduce_add_4d(&tmDQ, stg, hf * 32, i * 128 + q * 32, h, b);
-          bulk_commit();
+        if (lane == 0) mbar_arrive(dq_empty);
+        // two 32 x 32 fp32 boxes, each with its own staging slot: box hf of block G waits
+        // only for box hf of block G-1 to have been read by its reduce-add
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint8_t* box = stg + hf * 4096;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          SG_TR(trd, 2, tri, 2 + hf);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(v[hf][4 * k]), __uint_as_float(v[hf][4 * k + 1]),
+                            __uint_as_float(v[hf][4 * k + 2]), __uint_as_float(v[hf][4 * k + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.dq_b2_first)
+              tma_reduce_add_4d(&tmDQ, box, hf * 32, h, i * 128 + q * 32, b);
+            else
+              tma_reduce_add_4d(&tmDQ, box, hf * 32, i * 128 + q * 32, h, b);
+            bulk_commit();
+          }
         }
       }
+      SG_TR(trd, 2, tri, 4);
       if (i == nqb - 1) {
-        // this item's dK, then dV: bf16 rows -> two SW64 32 x 32 tiles (columns 0-31, 32-63)
-        // in the 4 KB staging box, TMA-stored, column sums read from the staged tiles
+        // this item's dK and dV: TMEM -> registers (both read before the accumulators are
+        // released), bf16 rows straight to global memory (thread = key row, 128 B each)
         mbar_wait(acc_full, it & 1);
         tc_fence_after();
+        SG_TR(trd, 2, tri, 5);
+        uint32_t kp[32];
+        {
+          uint32_t v2[2][32];
+          tmem_ld32(t_dk + lane_base, v2[0]);
+          tmem_ld32(t_dk + lane_base + 32, v2[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(v2[j >> 4][(2 * j) & 31]),
+                                                      __uint_as_float(v2[j >> 4][(2 * j + 1) & 31]));
+            kp[j] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+        }
+        uint32_t vp[32];
+        {
+          uint32_t v2[2][32];
+          tmem_ld32(t_dv + lane_base, v2[0]);
+          tmem_ld32(t_dv + lane_base + 32, v2[1]);
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(v2[j >> 4][(2 * j) & 31]),
+                                                      __uint_as_float(v2[j >> 4][(2 * j + 1) & 31]));
+            vp[j] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+        }
+        // staging: dK into box 0, dV into box 1 (each two SW64 32 x 32 bf16 tiles), each
+        // once the reduce-add before it has read the box; TMA stores; bias-gradient column
+        // sums read back from the staged tiles (rows past s hold zeros)
         const int key0 = kb * 128 + q * 32;
 #pragma unroll 1
         for (int which = 0; which < 2; ++which) {
-          uint32_t v2[2][32];
-          tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base, v2[0]);
-          tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + 32, v2[1]);
-          tmem_wait_ld();
-          if (which == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
-          }
-          if (lane == 0) bulk_wait_read<0>();  // earlier TMA operations have read the staging box
+          uint8_t* box = stg + which * 4096;
+          if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            uint8_t* row = stg + hf * 2048 + lane * 64;
+            uint8_t* row = box + hf * 2048 + lane * 64;
 #pragma unroll
             for (int k2 = 0; k2 < 4; ++k2) {
-              uint4 x;
-              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-              for (int e2 = 0; e2 < 4; ++e2)
-                hh[e2] = __floats2bfloat162_rn(__uint_as_float(v2[hf][8 * k2 + 2 * e2]),
-                                               __uint_as_float(v2[hf][8 * k2 + 2 * e2 + 1]));
+              const int j = hf * 16 + 4 * k2;
+              const uint4 x = which == 0 ? make_uint4(kp[j], kp[j + 1], kp[j + 2], kp[j + 3])
+                                         : make_uint4(vp[j], vp[j + 1], vp[j + 2], vp[j + 3]);
               *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
             }
           }
@@ -1204,18 +1402,16 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               if (p.dkv_b2_first)
-                tma_store_4d(tm, stg + hf * 2048, hf * 32, h, key0, b);
+                tma_store_4d(tm, box + hf * 2048, hf * 32, h, key0, b);
               else
-                tma_store_4d(tm, stg + hf * 2048, hf * 32, key0, h, b);
+                tma_store_4d(tm, box + hf * 2048, hf * 32, key0, h, b);
             }
             bulk_commit();
           }
           if (p.kv_colsum) {
-            // bias-gradient column sums of the staged bf16 tiles (rows past s hold zeros),
-            // lane = column within each 32-column tile, read while the TMA stores drain them
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
-              const uint8_t* tile = stg + hf * 2048;
+              const uint8_t* tile = box + hf * 2048;
               float acc2[2] = {0.f, 0.f};
 #pragma unroll
               for (int i2 = 0; i2 < 32; ++i2) {
@@ -1226,6 +1422,7 @@ __global__ void __launch_bounds__(512, 1)
             }
           }
         }
+        SG_TR(trd, 2, tri, 6);
         i = 0;
         ++it;
         if (it < my_items) item(it, kb, h, b);
@@ -1676,9 +1873,9 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (!rc) rc = tmap_bf16_tile_4d(&tdk, p.dK, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (!rc) rc = tmap_bf16_tile_4d(&tdv, p.dV, d, s, nh, b, ldg, d, s * ldg, &p.dkv_b2_first);
   if (rc) return rc;
-  // d = 64: 2 K, V, 2 Q, 2 dO, P, 2 dS (P / dS 2 atoms each), 4 x 4 KB staging;
+  // d = 64: 2 K, V, kQD Q, kQD dO, dS (2 atoms), 4 x 8 KB staging, 8 x 512 B statistics;
   // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
-  constexpr size_t SMEM64 = 13 * kT64 + 4 * 4096 + 256 + kMaxItems * 4;
+  constexpr size_t SMEM64 = (3 + 2 * kQD + 2) * kT64 + 4 * 8192 + 8 * 512 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
   const int nkb = (int)((s + 127) / 128);
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
@@ -1691,7 +1888,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   const int chunk = (int)std::max<long long>(1, std::min<long long>(2047, max_items / per_seq));
   if (per_seq > (long long)kMaxItems * sms) return set_error(SG_ERR_SHAPE, "flash bwd: one sequence exceeds the item table");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const void* kern = d == 64 ? reinterpret_cast<const void*>(flash_bwd2_kernel)
+  const void* kern = d == 64 ? reinterpret_cast<const void*>(flash_bwd2_kernel<kBwdPoly>)
                              : reinterpret_cast<const void*>(flash_bwd128_kernel);
   if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : SMEM128))) return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
   for (long long b0 = 0; b0 < b; b0 += chunk) {
@@ -1699,8 +1896,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
     const int items = (int)(per_seq * bc);
     p.b0 = (int)b0;
     if (d == 64)
-      launch_k(flash_bwd2_kernel, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq, tdk, tdv, p,
-               bc);
+      launch_k(flash_bwd2_kernel<kBwdPoly>, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq,
+               tdk, tdv, p, bc);
     else
       launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk,
                tdv, p, bc);

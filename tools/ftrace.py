@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import torch
 
-os.environ["SG_LIB_PATH"] = "paper_2104_05343_b200/libsg_trace.so"
+os.environ.setdefault("SG_LIB_PATH", "paper_2104_05343_b200/libsg_trace.so")
 sys.path.insert(0, ".")
 from paper_2104_05343_b200 import _lib, kernels as K  # noqa: E402
 
@@ -53,3 +53,20 @@ for w in range(4):
     for key in sorted(gaps):
         g = np.array(gaps[key])
         print(f"  {key[0]:2d} -> {key[1]:2d}: mean {g.mean():7.0f}  median {np.median(g):7.0f}  n={len(g)}")
+
+# absolute timeline (same SM clock for every buffer): events of blocks [G0, G0 + 3)
+if os.environ.get("SG_FTRACE_TIMELINE"):
+    G0 = int(os.environ["SG_FTRACE_TIMELINE"])
+    rows = []
+    for w in range(4):
+        n = int(np.count_nonzero(buf[w]))
+        ev = (buf[w][:n] >> np.uint64(56)).astype(int)
+        t = (buf[w][:n] & np.uint64(0xffffffffffffff)).astype(np.int64)
+        blk = np.cumsum(ev == 0) - 1  # event 0 opens a block
+        for k in range(n):
+            if G0 <= blk[k] < G0 + 3:
+                rows.append((int(t[k]), w, int(blk[k]), int(ev[k])))
+    rows.sort()
+    t0 = rows[0][0] if rows else 0
+    for t, w, g, e in rows:
+        print(f"{t - t0:7d}  buf{w} G{g} ev{e}")

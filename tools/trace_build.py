@@ -6,16 +6,17 @@ library is untouched.
 
     python tools/trace_build.py
 """
+import os
 import subprocess
 import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 CSRC = ROOT / "paper_2104_05343_b200" / "csrc"
-OUT = ROOT / "paper_2104_05343_b200" / "libsg_trace.so"
-TMP = Path("/tmp/sg_trace")
+OUT = ROOT / "paper_2104_05343_b200" / os.environ.get("SG_TRACE_OUT", "libsg_trace.so")
+TMP = Path("/tmp/sg_trace" + os.environ.get("SG_TRACE_OUT", ""))
 NVCC = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-        "-DSG_TRACE",
+        "-DSG_TRACE", *os.environ.get("SG_TRACE_DEFS", "").split(),
         "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 
 
