@@ -830,6 +830,14 @@ constexpr int kQD = 3;  // Q / dO slots of the d = 64 backward
 #define SG_BWD_POLY 0
 #endif
 constexpr int kBwdPoly = SG_BWD_POLY;  // exponent pairs of every 16 on the FMA pipe
+// the MMA warp of the d = 64 backward waits sleeping (SG_MMA_SPIN: spinning)
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SG_MMA_SPIN
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_sleep(bar, parity);
+#endif
+}
 
 template <int NPOLY>
 __global__ void __launch_bounds__(512, 1)
@@ -846,8 +854,8 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t* sDO = sQ + kQD * kT64;     // kQD slots
   uint8_t* sDS = sDO + kQD * kT64;    // 32 KB: [keys x queries], 2 atoms of 64 queries
   uint8_t* sStg = sDS + 2 * kT64;     // 4 drain warps x 2 x 4 KB (dQ fp32 boxes)
-  float* sStat = reinterpret_cast<float*>(sStg + 4 * 8192);  // 8 softmax warps x [64 -lse log2e | 64 -D scale]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 8 * 128);
+  float* sStat = reinterpret_cast<float*>(sStg + 4 * 8192);  // 2 slots x [128 -lse log2e | 128 -D scale]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 2 * 256);
   int* items_tab = reinterpret_cast<int*>(bars + 32);  // this CTA's items as packed (kb, h, b)
   uint64_t* k_full = bars;         // [2]
   uint64_t* k_empty = bars + 2;    // [2]
@@ -864,7 +872,9 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* dq_empty = bars + 18;  // 4 drain warps
   uint64_t* acc_full = bars + 19;
   uint64_t* acc_empty = bars + 20; // 4 drain warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* st_full = bars + 21;   // [2] statistics of block G in slot G & 1 (warp 3)
+  uint64_t* st_empty = bars + 23;  // [2] the 8 softmax warps have read them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (p.s + 127) / 128;
@@ -906,6 +916,10 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&st_full[i], 32);
+      mbar_init(&st_empty[i], 8);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -939,10 +953,10 @@ __global__ void __launch_bounds__(512, 1)
         int kb, h, b;
         decode(t, kb, h, b);
         const int ks = it & 1;
-        mbar_wait(&k_empty[ks], ((it >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&k_empty[ks], ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[ks], kT64);
         tma4(&tmK, sK + ks * kT64, &k_full[ks], 0, kb * 128, h, b, p.k_b2_first);
-        mbar_wait(v_empty, (it & 1) ^ 1);
+        mbar_wait_sleep(v_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(v_full, kT64);
         tma4(&tmV, sV, v_full, 0, kb * 128, h, b, p.v_b2_first);
         for (int i = 0; i < nqb; ++i, ++G) {
@@ -961,7 +975,7 @@ __global__ void __launch_bounds__(512, 1)
               tma4_l2(&tmDO, 0, i2 * 128, h2, b2, p.do_b2_first);
             }
           }
-          mbar_wait(&qd_empty[slot], (use & 1) ^ 1);
+          mbar_wait_sleep(&qd_empty[slot], (use & 1) ^ 1);
           mbar_arrive_expect_tx(&qd_full[slot], 2 * kT64);
           tma4(&tmQ, sQ + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.q_b2_first);
           tma4(&tmDO, sDO + slot * kT64, &qd_full[slot], 0, i * 128, h, b, p.do_b2_first);
@@ -989,8 +1003,8 @@ __global__ void __launch_bounds__(512, 1)
       (void)trm; (void)tri;
       auto issue_s = [&](int G) {  // S^T_G = K Q_G^T
         const int it = G / nqb, slot = G % kQD;
-        if (G % nqb == 0) mbar_wait(&k_full[it & 1], (it >> 1) & 1);
-        mbar_wait(&qd_full[slot], (G / kQD) & 1);
+        if (G % nqb == 0) mma_wait(&k_full[it & 1], (it >> 1) & 1);
+        mma_wait(&qd_full[slot], (G / kQD) & 1);
         tc_fence_after();
         SG_TR(trm, 0, tri, 8);
         const uint64_t ak = d_k0 + (it & 1) * kTile, bq = d_q0 + slot * kTile;
@@ -1007,7 +1021,7 @@ __global__ void __launch_bounds__(512, 1)
       auto issue_dp = [&](int G) {  // dP^T_G = V dO_G^T (Q_G / dO_G already waited for by issue_s(G))
         const int it = G / nqb, slot = G % kQD;
         if (G % nqb == 0) {
-          mbar_wait(v_full, it & 1);
+          mma_wait(v_full, it & 1);
           tc_fence_after();
         }
         const uint64_t bdo = d_do0 + slot * kTile;
@@ -1030,16 +1044,22 @@ __global__ void __launch_bounds__(512, 1)
         const uint64_t mk = m_k0 + (it & 1) * kTile, mq = m_q0 + slot * kTile, mdo = m_do0 + slot * kTile;
         SG_TR(trm, 0, tri, 0);
         // S^T_G+1 overwrites S^T_G as soon as the softmax warps have read it
-        mbar_wait(s_free, G & 1);
+        mma_wait(s_free, G & 1);
         tc_fence_after();
         SG_TR(trm, 0, tri, 1);
-        if (G + 1 < total) issue_s(G + 1);
+        // S^T_G+1 now if its Q tile (and, at an item start, K) has landed, else after dV_G
+        bool s_next = G + 1 >= total;
+        if (!s_next && mbar_test(&qd_full[(G + 1) % kQD], ((G + 1) / kQD) & 1) &&
+            ((G + 1) % nqb != 0 || mbar_test(&k_full[((G + 1) / nqb) & 1], (((G + 1) / nqb) >> 1) & 1))) {
+          issue_s(G + 1);
+          s_next = true;
+        }
         SG_TR(trm, 0, tri, 2);
-        mbar_wait(p_full, G & 1);  // P^T_G in TMEM
+        mma_wait(p_full, G & 1);  // P^T_G in TMEM
         tc_fence_after();
         // the previous item's dK / dV have been read out before this item's first products
         if (i == 0 && it > 0) {
-          mbar_wait(acc_empty, (it - 1) & 1);
+          mma_wait(acc_empty, (it - 1) & 1);
           tc_fence_after();
         }
         SG_TR(trm, 0, tri, 3);
@@ -1052,7 +1072,8 @@ __global__ void __launch_bounds__(512, 1)
         __syncwarp();
 #endif
         SG_TR(trm, 0, tri, 9);
-        mbar_wait(ds_full, G & 1);  // dS^T_G in TMEM (over dP^T_G), dS_G in smem
+        if (!s_next) issue_s(G + 1);
+        mma_wait(ds_full, G & 1);  // dS^T_G in TMEM (over dP^T_G), dS_G in smem
         tc_fence_after();
         SG_TR(trm, 0, tri, 4);
         if (elect_one()) {
@@ -1068,7 +1089,7 @@ __global__ void __launch_bounds__(512, 1)
         // dP^T_G+1 overwrites dS^T_G once dK_G has read it (MMAs execute in issue order)
         if (G + 1 < total) issue_dp(G + 1);
         SG_TR(trm, 0, tri, 11);
-        if (G >= 1) mbar_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained
+        if (G >= 1) mma_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained
         tc_fence_after();
         SG_TR(trm, 0, tri, 5);
         if (elect_one()) {
@@ -1088,20 +1109,56 @@ __global__ void __launch_bounds__(512, 1)
         SG_TR(trm, 0, tri, 13);
       }
     }
+  } else if (warp == 3) {
+    reg_dealloc<56>();
+    // statistics of every block into the shared table: -lse log2e and -D scale of its 128
+    // queries (queries past s: lse = +inf, so P = 0), prefetched a block ahead
+    float v[8];
+    auto load = [&](int G, float (&x)[8]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = INFINITY;
+        x[4 + u] = 0.f;
+      }
+      if (G >= total) return;
+      int kb, h, b;
+      item(G / nqb, kb, h, b);
+      const size_t off = ((size_t)b * p.nh + h) * p.s;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int qrow = (G % nqb) * 128 + u * 32 + lane;
+        if (qrow < p.s) {
+          x[u] = __ldg(p.lse + off + qrow);
+          x[4 + u] = __ldg(p.drow + off + qrow);
+        }
+      }
+    };
+    load(0, v);
+    for (int G = 0; G < total; ++G) {
+      float* t = sStat + (G & 1) * 256;
+      if (G >= 2) mbar_wait_sleep(&st_empty[G & 1], ((G - 2) >> 1) & 1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        t[u * 32 + lane] = -v[u] * 1.4426950408889634f;
+        t[128 + u * 32 + lane] = -v[4 + u] * p.scale;
+      }
+      mbar_arrive(&st_full[G & 1]);
+      load(G + 1, v);
+    }
   } else if (warp < 4) {
     reg_dealloc<56>();
 #ifdef SG_TRACE
     // observer (instrumented build): completion times of the tensor-pipe commits
-    if (warp == 3 && lane == 0 && blockIdx.x == 0) {
+    if (warp == 2 && lane == 0 && blockIdx.x == 0) {
       int tri = 0;
       for (int G = 0; G < total; ++G) {  // completion order: S^T_G+1, dK_G, dP^T_G+1, dQ_G
-        if (G + 1 < total) mbar_wait(s_full, (G + 1) & 1);
+        if (G + 1 < total) mbar_wait_sleep(s_full, (G + 1) & 1);
         SG_TR(true, 3, tri, 0);
-        mbar_wait(&qd_empty[G % kQD], (G / kQD) & 1);
+        mbar_wait_sleep(&qd_empty[G % kQD], (G / kQD) & 1);
         SG_TR(true, 3, tri, 1);
-        if (G + 1 < total) mbar_wait(dp_full, (G + 1) & 1);
+        if (G + 1 < total) mbar_wait_sleep(dp_full, (G + 1) & 1);
         SG_TR(true, 3, tri, 2);
-        mbar_wait(dq_full, G & 1);
+        mbar_wait_sleep(dq_full, G & 1);
         SG_TR(true, 3, tri, 3);
       }
     }
@@ -1113,60 +1170,34 @@ __global__ void __launch_bounds__(512, 1)
     const int q = e & 3, hq = e >> 2;
     const int r = q * 32 + lane;  // key row of the block
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    float* st = sStat + e * 128;  // this warp's statistics: [0, 64) -lse log2e, [64, 128) -D scale
     const float scale = p.scale;
-    // the warp's 64 queries' statistics of block (it, i): lane holds queries 64 hq + lane, + 32
-    auto load_stats = [&](int it, int i, float (&v)[4]) {
-      v[0] = v[1] = INFINITY;
-      v[2] = v[3] = 0.f;
-      if (it >= my_items) return;
-      int kb, h, b;
-      item(it, kb, h, b);
-      const size_t off = ((size_t)b * p.nh + h) * p.s;
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int qrow = i * 128 + hq * 64 + u * 32 + lane;
-        if (qrow < p.s) {
-          v[u] = __ldg(p.lse + off + qrow);
-          v[2 + u] = __ldg(p.drow + off + qrow);
-        }
-      }
-    };
     const bool trs = blockIdx.x == 0 && lane == 0 && e == 0;
     int tri = 0;
     (void)trs; (void)tri;
-    float stn[4];
-    load_stats(0, 0, stn);
     int it = 0, i = 0;  // (item, query block) of G, advanced incrementally
     int kb = 0, h = 0, b = 0;
     if (my_items > 0) item(0, kb, h, b);
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2), sc2 = f2_pack(scale, scale);
     for (int G = 0; G < total; ++G) {
       const int kvalid = min(128, p.s - kb * 128);
-      __syncwarp();  // every lane has read block G-1's statistics
-      st[lane] = -stn[0] * 1.4426950408889634f;
-      st[32 + lane] = -stn[1] * 1.4426950408889634f;
-      st[64 + lane] = -stn[2] * scale;
-      st[96 + lane] = -stn[3] * scale;
-      __syncwarp();
-      {
-        const int ni = i + 1 == nqb ? 0 : i + 1, nit = i + 1 == nqb ? it + 1 : it;
-        load_stats(nit, ni, stn);  // prefetch
-      }
+      const float* st = sStat + (G & 1) * 256 + hq * 64;  // this warp's 64 queries: [0, 64) lse, [128, 192) D
       SG_TR(trs, e == 0 ? 1 : 3, tri, 0);
-      mbar_wait(s_full, G & 1);
+      mbar_wait_sleep(s_full, G & 1);
+      mbar_wait_sleep(&st_full[G & 1], (G >> 1) & 1);
       tc_fence_after();
       SG_TR(trs, e == 0 ? 1 : 3, tri, 1);
 #ifdef SG_EXP_NOSM
       {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&st_empty[G & 1]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
-        if (G > 0) mbar_wait(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);
+        if (G > 0) mbar_wait_sleep(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
-        mbar_wait(dp_full, G & 1);
-        if (G > 0) mbar_wait(dq_full, (G - 1) & 1);
+        mbar_wait_sleep(dp_full, G & 1);
+        if (G > 0) mbar_wait_sleep(dq_full, (G - 1) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
         if (i == nqb - 1) {
@@ -1208,15 +1239,21 @@ __global__ void __launch_bounds__(512, 1)
             p0 = ex2f_fast(f2_lo(y));
             p1 = ex2f_fast(f2_hi(y));
           }
-          if (!key_ok) p0 = p1 = 0.f;
           sv[2 * j] = __float_as_uint(p0);
           sv[2 * j + 1] = __float_as_uint(p1);
           __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
           pk[j] = *reinterpret_cast<uint32_t*>(&hp);
         }
       }
+      if (kvalid < 128 && !key_ok) {  // keys past s (last key block only): P = 0
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sv[2 * j] = sv[2 * j + 1] = 0u;
+          pk[j] = 0u;
+        }
+      }
       SG_TR(trs, e == 0 ? 1 : 3, tri, 3);
-      if (G > 0) mbar_wait(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);  // dV_G-1 has read P^T_G-1
+      if (G > 0) mbar_wait_sleep(&qd_empty[(G - 1) % kQD], ((G - 1) / kQD) & 1);  // dV_G-1 has read P^T_G-1
       tc_fence_after();
       tmem_st32(t_p + lane_base + hq * 32, pk);
       tmem_wait_st();
@@ -1225,7 +1262,7 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0) mbar_arrive(p_full);
       SG_TR(trs, e == 0 ? 1 : 3, tri, 4);
       // dS^T = P^T (dP^T scale - D scale)
-      mbar_wait(dp_full, G & 1);
+      mbar_wait_sleep(dp_full, G & 1);
       tc_fence_after();
       SG_TR(trs, e == 0 ? 1 : 3, tri, 5);
       uint32_t dk[32];
@@ -1236,7 +1273,7 @@ __global__ void __launch_bounds__(512, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 nd = *reinterpret_cast<const float4*>(st + 64 + c * 32 + 4 * j4);
+          const float4 nd = *reinterpret_cast<const float4*>(st + 128 + c * 32 + 4 * j4);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int j = 2 * j4 + u;
@@ -1252,8 +1289,10 @@ __global__ void __launch_bounds__(512, 1)
       // dS^T packed over this thread's own (already read) dP^T columns; dS into the smem
       // buffer ([keys x queries] rows: the MN-major A operand of dQ) once dQ_G-1 has read it
       tmem_st32(t_dp + lane_base + hq * 64, dk);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[G & 1]);  // this warp has read block G's statistics
       SG_TR(trs, e == 0 ? 1 : 3, tri, 6);
-      if (G > 0) mbar_wait(dq_full, (G - 1) & 1);
+      if (G > 0) mbar_wait_sleep(dq_full, (G - 1) & 1);
       uint8_t* drow_ = sDS + hq * kT64 + r * 128;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -1287,7 +1326,7 @@ __global__ void __launch_bounds__(512, 1)
     (void)trd; (void)tri;
     for (int G = 0; G < total; ++G) {
       SG_TR(trd, 2, tri, 0);
-      mbar_wait(dq_full, G & 1);
+      mbar_wait_sleep(dq_full, G & 1);
       tc_fence_after();
       SG_TR(trd, 2, tri, 1);
 #ifdef SG_EXP_NODRAIN
@@ -1295,7 +1334,7 @@ __global__ void __launch_bounds__(512, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(dq_empty);
         if (i == nqb - 1) {
-          mbar_wait(acc_full, it & 1);
+          mbar_wait_sleep(acc_full, it & 1);
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty);
           i = 0;
@@ -1343,7 +1382,7 @@ __global__ void __launch_bounds__(512, 1)
       if (i == nqb - 1) {
         // this item's dK and dV: TMEM -> registers (both read before the accumulators are
         // released), bf16 rows straight to global memory (thread = key row, 128 B each)
-        mbar_wait(acc_full, it & 1);
+        mbar_wait_sleep(acc_full, it & 1);
         tc_fence_after();
         SG_TR(trd, 2, tri, 5);
         uint32_t kp[32];
@@ -1875,7 +1914,7 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (rc) return rc;
   // d = 64: 2 K, V, kQD Q, kQD dO, dS (2 atoms), 4 x 8 KB staging, 8 x 512 B statistics;
   // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
-  constexpr size_t SMEM64 = (3 + 2 * kQD + 2) * kT64 + 4 * 8192 + 8 * 512 + 256 + kMaxItems * 4;
+  constexpr size_t SMEM64 = (3 + 2 * kQD + 2) * kT64 + 4 * 8192 + 2 * 1024 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
   const int nkb = (int)((s + 127) / 128);
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;

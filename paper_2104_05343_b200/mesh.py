@@ -391,6 +391,18 @@ class Mesh:
             raise ConfigError(f"broadcast root row {root_row} out of range for r={self.r}")
         return self._bcast_async("col", root_row, src, recv, tag, views)
 
+    def step_boundary(self) -> None:
+        """End of a (graph-replayable) step on a peer-memory mesh: one whole-mesh barrier, so
+        every member's reads of this step's published slots are done, and the slot
+        parities restart. A CUDA graph of the step then replays with the slot order the
+        eager step used; without the barrier, a name published an odd number of times per
+        step would reuse its last slot for the next replay's first publish while a slower
+        member may still be pulling from it."""
+        if self.peer is None:
+            return
+        self.peer.barrier("all")
+        self.peer.transport.reset_slots()
+
     def publish(self, name: str, block) -> list | None:
         """Peer memory: make this position's ``block`` readable by the mesh (a copy into a
         symmetric slot unless it already is symmetric); returns the views by flat rank.

@@ -489,6 +489,7 @@ class MeshModel:
         grads = self.backward(saved, ws, eager_update=True, lr=lr, _fused_sgd_lr=None if checkpointing else lr)
         sgd_matrix(self.table, grads.table, lr)
         self._cls_sgd(grads, lr)
+        self.mesh.step_boundary()
         return loss
 
     def infer(self, tokens, labels, ws: Workspace) -> torch.Tensor:
@@ -505,6 +506,7 @@ class MeshModel:
         with K.tagged("logits"):
             logits = summa_abt(x, self.table, ws, tag="lmhead", out_dtype=self.logits_dtype)
         loss, _ = cross_entropy_forward(logits, labels, cfg, ws, return_tensor=True, label_ids=label_ids)
+        self.mesh.step_boundary()
         return loss
 
     # ------------------------------------------------------------------ checkpoint file

@@ -271,6 +271,10 @@ class Transport:
         self._parity: dict = {}
         self._ptrs: dict = {}
 
+    def reset_slots(self) -> None:
+        """Every name's next publish goes to slot 0 (after a whole-mesh barrier)."""
+        self._parity.clear()
+
     def _slot(self, name: str, shape, dtype):
         k = self._parity.get(name, 0)
         self._parity[name] = k ^ 1

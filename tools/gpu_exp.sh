@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-for v in x_a x_b x_c x_d; do
-  echo "== $v" >> gpurun_out/exp.txt
-  SG_LIB_PATH=paper_2104_05343_b200/libsg_$v.so timeout 120 python tools/flash_perf.py 32,512,16,64 >> gpurun_out/exp.txt 2>&1
-  SG_LIB_PATH=paper_2104_05343_b200/libsg_$v.so timeout 120 python tools/ftrace.py bwd 2>&1 | head -8 >> gpurun_out/exp.txt
-done
+for i in 1 2 3 4 5 6; do timeout 600 python -m pytest tests/test_dist.py -m gpu -q -p no:cacheprovider -k "graph and 2-4" 2>&1 | grep -E "^E  |passed|failed" | head -4 >> gpurun_out/dist_rep.log; done

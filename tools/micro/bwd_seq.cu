@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include "../../paper_2104_05343_b200/csrc/sg_ptx.cuh"
 using namespace sg;
 
@@ -14,7 +15,7 @@ constexpr uint32_t kT64 = 128 * 64 * 2;
 // MODE: 0 full sequence; 1 S/dP only; 2 dV/dK only (TS); 3 dQ only; 4 dV/dK as SS
 // (A MN-major from smem, the [queries x keys] orientation); 5 full, fixed K-step
 // addresses (no advance); 6 S/dP with the D target alternating but no dependency
-template <int MODE, int LDW = 0, int STW = 0, int TMAW = 0>
+template <int MODE, int LDW = 0, int STW = 0, int TMAW = 0, int MUW = 0>
 __global__ void __launch_bounds__(512, 1) k(unsigned long long* out, int iters, const uint8_t* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -177,6 +178,25 @@ __global__ void __launch_bounds__(512, 1) k(unsigned long long* out, int iters, 
       ++c;
     }
     if (acc == 1.2345f) out[2] = 1;
+  } else if (MUW > 0 && warp >= 4 && warp < 4 + MUW) {
+    // softmax-like math: independent ex2 + paired FMA streams, no waits
+    float a[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a[i] = -(threadIdx.x * 1e-3f + i * 0.01f);
+    uint32_t acc = 0;
+    while (!*reinterpret_cast<volatile int*>(&stop_flag)) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float p0, p1;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(a[i]));
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(a[i + 1]));
+        __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+        acc ^= *reinterpret_cast<uint32_t*>(&hv);
+        a[i] = fmaf(p0, 1e-9f, a[i]);
+        a[i + 1] = fmaf(p1, 1e-9f, a[i + 1]);
+      }
+    }
+    if (acc == 12345u) out[3] = acc;
   } else if (TMAW && warp == 3) {
     // bulk global -> smem copies (TMA engine), 16 KB at a time, back to back
     __shared__ uint64_t tb;
@@ -212,13 +232,13 @@ __global__ void __launch_bounds__(512, 1) k(unsigned long long* out, int iters, 
 }
 
 static uint8_t* g_src = nullptr;
-template <int MODE, int LDW = 0, int STW = 0, int TMAW = 0>
+template <int MODE, int LDW = 0, int STW = 0, int TMAW = 0, int MUW = 0>
 void run(unsigned long long* d, const char* name, int ideal) {
   const int iters = 2000;
   const int smem = 6 * kT64 + 4 * 4096 + 1024;
   if (!g_src) cudaMalloc(&g_src, 148 * 65536 + 65536);
-  cudaFuncSetAttribute(k<MODE, LDW, STW, TMAW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k<MODE, LDW, STW, TMAW><<<148, 512, smem>>>(d, iters, g_src);
+  cudaFuncSetAttribute(k<MODE, LDW, STW, TMAW, MUW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k<MODE, LDW, STW, TMAW, MUW><<<148, 512, smem>>>(d, iters, g_src);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
@@ -242,5 +262,8 @@ int main() {
   run<7, 0, 4>(d, "  + 4 warps STS", 1640);
   run<7, 8, 4>(d, "  + 8 ld warps + 4 STS warps", 1640);
   run<7, 0, 0, 1>(d, "  + TMA bulk loads (16 KB back to back)", 1640);
+  run<8, 0, 0, 0, 4>(d, "waits/fences + 4 MUFU/FMA warps", 1640);
+  run<8, 0, 0, 0, 8>(d, "waits/fences + 8 MUFU/FMA warps", 1640);
+  run<8, 0, 0, 0, 12>(d, "waits/fences + 12 MUFU/FMA warps", 1640);
   return 0;
 }
