@@ -472,11 +472,24 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
     }
   } else if (warp == 1) {
     if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       // ------------------------------------------------------------ MMA issuer
+      // The whole warp walks the loop with warp-uniform operands (descriptors in uniform
+      // registers, advanced by adding (bytes >> 4) to the start-address field); one
+      // elected lane issues. A single-lane issuer pays a per-MMA lane waterfall of ~12
+      // instructions, and the epilogue warps sharing its SMSP starve it of issue slots
+      // (the flash backward traces: tools/ftrace.py).
       constexpr uint32_t IDESC_FULL = umma_idesc_bf16(TM, Cfg::MMA_N, A_MN, B_MN);
       constexpr uint32_t IDESC_HALF = umma_idesc_bf16(TM, Cfg::MMA_N / 2, A_MN, B_MN);
-      constexpr uint32_t B_HALF = Cfg::MMA_N * kBK * 2;  // second MMA_N-wide half of B
+      // K-major SW128: K step of 16 bf16 = 32 B inside the 128 B swizzle row, SBO = 1024 B
+      //   between 8-row groups along M/N. MN-major SW128: K step of 16 rows = 2048 B,
+      //   LBO = 64-wide MN chunk stride (kBK rows x 128 B), SBO = 1024 B between 8-row K groups.
+      constexpr uint64_t A_KSTEP = A_MN ? (2048 >> 4) : (32 >> 4), B_KSTEP = B_MN ? (2048 >> 4) : (32 >> 4);
+      constexpr uint64_t A_STAGE = A_BYTES >> 4, B_STAGE = B_BYTES >> 4;
+      constexpr uint64_t B_HALF = (Cfg::MMA_N * kBK * 2) >> 4;  // second MMA_N-wide half of B
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), A_MN ? kBK * 128 : 0, 1024);
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), B_MN ? kBK * 128 : 0, 1024);
+      const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
       uint32_t stage = 0, phase = 0, it = 0;
       for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
         const uint32_t IDESC = (PAIR && t >= p.full_units) ? IDESC_HALF : IDESC_FULL;
@@ -486,46 +499,43 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         else
           mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + as * BN;
+        const uint32_t d_tmem = tbase + as * BN;
         int kb0, kb1;
         unit_k_range(p, t, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+          const uint64_t ad0 = a_desc0 + stage * A_STAGE, bd0 = b_desc0 + stage * B_STAGE;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // K-major SW128: K step of 16 bf16 = 32 B inside the 128 B swizzle row,
-            //   SBO = 1024 B between 8-row groups along M/N.
-            // MN-major SW128: K step of 16 rows = 2048 B, LBO = 64-wide MN chunk
-            //   stride (kBK rows x 128 B), SBO = 1024 B between 8-row K groups.
-            const uint64_t ad = A_MN ? umma_desc_sw128(a_base + k * 2048, kBK * 128, 1024)
-                                     : umma_desc_sw128(a_base + k * 32, 0, 1024);
+            for (int k = 0; k < kBK / 16; ++k) {
 #pragma unroll
-            for (int h = 0; h < Cfg::NSPLIT; ++h) {
-              const uint32_t bb = b_base + h * B_HALF;
-              const uint64_t bd = B_MN ? umma_desc_sw128(bb + k * 2048, kBK * 128, 1024)
-                                       : umma_desc_sw128(bb + k * 32, 0, 1024);
-              if (PAIR)
-                umma_bf16_pair(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
-              else
-                umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+              for (int h = 0; h < Cfg::NSPLIT; ++h) {
+                const uint64_t ad = ad0 + k * A_KSTEP, bd = bd0 + h * B_HALF + k * B_KSTEP;
+                if (PAIR)
+                  umma_bf16_pair(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+                else
+                  umma_bf16(d_tmem + h * Cfg::MMA_N, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+              }
             }
+            if (PAIR)
+              umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
+            else
+              umma_commit(&empty[stage]);
           }
-          if (PAIR)
-            umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
-          else
-            umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (PAIR)
-          umma_commit_pair(&tfull[as], 0x3);
-        else
-          umma_commit(&tfull[as]);
+        if (elect_one()) {
+          if (PAIR)
+            umma_commit_pair(&tfull[as], 0x3);
+          else
+            umma_commit(&tfull[as]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp < 4) {
