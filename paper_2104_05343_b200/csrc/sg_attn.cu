@@ -420,14 +420,14 @@ __global__ void __launch_bounds__(640, 1)
         int qb, h, b;
         decode(t, qb, h, b);
         const int qs = it & 1;
-        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&q_empty[qs], ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qs], kQT * T64);
 #pragma unroll
         for (int i = 0; i < kQT; ++i)
           tma4(&tmQ, sQ + (qs * kQT + i) * T64, &q_full[qs], 0, (qb * kQT + i) * kQB, h, b, p.q_b2_first);
         for (int j = 0; j < nkb; ++j, ++g) {
           const int slot = g % NS;
-          mbar_wait(&kv_empty[slot], ((g / NS) & 1) ^ 1);
+          mbar_wait_sleep(&kv_empty[slot], ((g / NS) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[slot], T64);
           tma4(&tmK, sK + slot * T64, &k_full[slot], 0, j * kKB, h, b, p.k_b2_first);
           mbar_arrive_expect_tx(&v_full[slot], T64);
@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(640, 1)
       }
     }
   } else if (warp == 1 || warp == 3) {
-    if (lane == 0) {
+    {
+      // whole warp walks the loop with warp-uniform operands; one elected lane issues
       // ------------------------------------------------------------ MMA issuer of tile i
       // one issuing thread per query tile, so neither tile's products wait for the
       // other tile's softmax progress (a shared issuer forces the tiles into lockstep
@@ -444,18 +445,23 @@ __global__ void __launch_bounds__(640, 1)
       const int i = warp >> 1;
       constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
       constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P (TMEM), V MN-major
-      const bool trm = blockIdx.x == 0 && i == 0;
+      const bool trm = blockIdx.x == 0 && i == 0 && lane == 0;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sQ), 0, 1024), k_desc0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
+      const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sV), kKB * 128, 1024);
+      constexpr uint64_t kTile = T64 >> 4;
       int tri = 0;
       (void)trm; (void)tri;
       // S_i for global block G (item G / nkb, key block G % nkb)
       auto issue_s = [&](int G) {
         const int it = G / nkb;
-        const uint32_t q_base = smem_u32(sQ + ((it & 1) * kQT + i) * T64), k_base = smem_u32(sK + (G % NS) * T64);
+        const uint64_t qd = q_desc0 + ((it & 1) * kQT + i) * kTile, kd = k_desc0 + (G % NS) * kTile;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tmem + i * 128, umma_desc_sw128(q_base + kk * 32, 0, 1024), umma_desc_sw128(k_base + kk * 32, 0, 1024),
-                    IDESC_S, kk > 0 ? 1u : 0u);
-        umma_commit(&s_full[i]);
+          for (int kk = 0; kk < 4; ++kk) umma_bf16(tm + i * 128, qd + 2 * kk, kd + 2 * kk, IDESC_S, kk > 0 ? 1u : 0u);
+          umma_commit(&s_full[i]);
+        }
+        __syncwarp();
       };
       auto ready_s = [&](int G) {  // Q of G's item (at its first block) and K_G landed
         if (G % nkb == 0) mbar_wait(&q_full[(G / nkb) & 1], ((G / nkb) >> 1) & 1);
@@ -477,21 +483,24 @@ __global__ void __launch_bounds__(640, 1)
           SG_TR(trm, 2, tri, 15);
           issue_s(G + 1);
         }
-        if (j == nkb - 1) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score product issued
+        if (j == nkb - 1 && elect_one()) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score product issued
+        __syncwarp();
         SG_TR(trm, 2, tri, 11);
         mbar_wait(&v_full[slot], (G / NS) & 1);
         mbar_wait(&p_full[i], G & 1);  // P_i,G in TMEM, O_i corrected (or read out, first block)
         tc_fence_after();
         SG_TR(trm, 2, tri, 12);
-        const uint32_t v_base = smem_u32(sV + slot * T64);
+        const uint64_t vd = v_desc0 + slot * kTile;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kKB / 16; ++kk)
-          umma_bf16_ts(tmem + 256 + i * 64, tmem + 384 + i * 64 + kk * 8,
-                       umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024), IDESC_PV, (j | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < kKB / 16; ++kk)
+            umma_bf16_ts(tm + 256 + i * 64, tm + 384 + i * 64 + kk * 8, vd + 128 * kk, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
+          umma_commit(&pv_done[i]);
+          if (j == nkb - 1) umma_commit(&o_full[i]);
+          umma_commit(&kv_empty[slot]);  // this tile is done with K_G, V_G
+        }
+        __syncwarp();
         SG_TR(trm, 2, tri, 13);
-        umma_commit(&pv_done[i]);
-        if (j == nkb - 1) umma_commit(&o_full[i]);
-        umma_commit(&kv_empty[slot]);  // this tile is done with K_G, V_G
       }
     }
   } else if (warp >= 4) {
@@ -525,7 +534,7 @@ __global__ void __launch_bounds__(640, 1)
       for (int j = 0; j < nkb; ++j, ++G) {
         const int kvalid = min(kKB, p.s - j * kKB) - kh * 64;  // valid keys of this half
         SG_TR(trs, i, tri, 0);
-        mbar_wait(&s_full[i], G & 1);
+        mbar_wait_sleep(&s_full[i], G & 1);
         tc_fence_after();
         SG_TR(trs, i, tri, 1);
         uint32_t sv[2][32];
@@ -555,10 +564,10 @@ __global__ void __launch_bounds__(640, 1)
         if (lane == 0) mbar_arrive(my_xbar);
         SG_TR(trs, i, tri, 2);
         // PV_i,G-1 has finished reading P_i (and writing O_i)
-        if (G > 0) mbar_wait(&pv_done[i], (G - 1) & 1);
+        if (G > 0) mbar_wait_sleep(&pv_done[i], (G - 1) & 1);
         // this tile's turn on MUFU
         if (i == 1 || G > 0) named_bar_sync(1 + (1 - i) * 4 + qd, 128);
-        mbar_wait(my_xbar, G & 1);
+        mbar_wait_sleep(my_xbar, G & 1);
         // (a volatile shared load after the barrier: no exponential is scheduled ahead of the turn)
         const float m_cand = fmax3f(m_use, m_loc, *static_cast<volatile float*>(&slot[(kh ^ 1) * 128 + r]));
         float alpha = 1.f;
@@ -619,9 +628,9 @@ __global__ void __launch_bounds__(640, 1)
       xl[kh * 128 + r] = l;
       __syncwarp();
       if (lane == 0) mbar_arrive(my_lbar);
-      mbar_wait(my_lbar, it & 1);
+      mbar_wait_sleep(my_lbar, it & 1);
       l += xl[(kh ^ 1) * 128 + r];
-      mbar_wait(&o_full[i], it & 1);
+      mbar_wait_sleep(&o_full[i], it & 1);
       tc_fence_after();
       const float inv = 1.f / l;
       // normalised bf16 rows -> this warp's 32 x 32 SW64 staging tile -> TMA store
