@@ -1625,62 +1625,76 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 1) {
     reg_dealloc<56>();
-    if (lane == 0) {
+    {
+      // whole warp walks the loop (warp-uniform operands); one elected lane issues
       constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: A, B K-major (over d)
       constexpr uint32_t ID_KV = umma_idesc_bf16(128, 128, true, true);    // dV, dK: A = P^T / dS^T, B = dO / Q
       constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 128, false, true);   // dQ: A = dS (K-major), B = K (MN-major)
-      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), q_base = smem_u32(sQ), do_base = smem_u32(sDO);
-      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t ts = tm, tdp = tm + 128, tdv = tm + 256, tdk = tm + 384, tdq = tm;
+      // K-major descriptors (K steps: 32 B = 2 units inside an atom, next atom kT64 >> 4),
+      // MN-major ones (K steps of 16 rows = 2048 B = 128 units, LBO = one atom)
+      const uint64_t k_k = umma_desc_sw128(smem_u32(sK), 0, 1024), v_k = umma_desc_sw128(smem_u32(sV), 0, 1024);
+      const uint64_t q_k = umma_desc_sw128(smem_u32(sQ), 0, 1024), do_k = umma_desc_sw128(smem_u32(sDO), 0, 1024);
+      const uint64_t ds_k = umma_desc_sw128(smem_u32(sDS), 0, 1024);
+      const uint64_t k_m = umma_desc_sw128(smem_u32(sK), kT64, 1024), p_m = umma_desc_sw128(smem_u32(sP), kT64, 1024);
+      const uint64_t do_m = umma_desc_sw128(smem_u32(sDO), kT64, 1024), ds_m = umma_desc_sw128(smem_u32(sDS), kT64, 1024);
+      const uint64_t q_m = umma_desc_sw128(smem_u32(sQ), kT64, 1024);
+      constexpr uint64_t kAtom = kT64 >> 4;
       for (int G = 0; G < total; ++G) {
         const int it = G / nqb, i = G % nqb;
         if (i == 0) mbar_wait(kv_full, it & 1);
         if (G > 0) mbar_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained from the S columns
         mbar_wait(do_full, G & 1);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K-dim = d = 128: two atoms of 4 x 16
-          const uint32_t off = (kk >> 2) * kT64 + (kk & 3) * 32;
-          umma_bf16(t_dp, umma_desc_sw128(do_base + off, 0, 1024), umma_desc_sw128(v_base + off, 0, 1024), ID_SQ,
-                    kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {  // K-dim = d = 128: two atoms of 4 x 16
+            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
+            umma_bf16(tdp, do_k + off, v_k + off, ID_SQ, kk > 0 ? 1u : 0u);
+          }
         }
+        __syncwarp();
         mbar_wait(q_full, G & 1);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * kT64 + (kk & 3) * 32;
-          umma_bf16(t_s, umma_desc_sw128(q_base + off, 0, 1024), umma_desc_sw128(k_base + off, 0, 1024), ID_SQ,
-                    kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
+            umma_bf16(ts, q_k + off, k_k + off, ID_SQ, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(s_full);
         }
-        umma_commit(s_full);
+        __syncwarp();
         mbar_wait(ds_full, G & 1);  // S / dP read, P / dS in smem
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
-          umma_bf16(t_dq, umma_desc_sw128(ds_base + (kk >> 2) * kT64 + (kk & 3) * 32, 0, 1024),
-                    umma_desc_sw128(k_base + kk * 2048, kT64, 1024), ID_DQ, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk)  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
+            umma_bf16(tdq, ds_k + (kk >> 2) * kAtom + (kk & 3) * 2, k_m + kk * 128, ID_DQ, kk > 0 ? 1u : 0u);
+          umma_commit(dq_full);
         }
-        umma_commit(dq_full);
+        __syncwarp();
         if (i == 0 && it > 0) {
           mbar_wait(acc_empty, (it - 1) & 1);  // the previous item's dK / dV were read out
           tc_fence_after();
         }
+        if (elect_one()) {
 #pragma unroll
-        for (int kq = 0; kq < 8; ++kq) {  // K-dim = 128 queries: 16 rows = 2048 B per step
-          umma_bf16(t_dv, umma_desc_sw128(p_base + kq * 2048, kT64, 1024),
-                    umma_desc_sw128(do_base + kq * 2048, kT64, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
-        }
-        umma_commit(do_empty);
+          for (int kq = 0; kq < 8; ++kq)  // K-dim = 128 queries: 16 rows = 2048 B per step
+            umma_bf16(tdv, p_m + kq * 128, do_m + kq * 128, ID_KV, (i | kq) != 0 ? 1u : 0u);
+          umma_commit(do_empty);
 #pragma unroll
-        for (int kq = 0; kq < 8; ++kq) {
-          umma_bf16(t_dk, umma_desc_sw128(ds_base + kq * 2048, kT64, 1024),
-                    umma_desc_sw128(q_base + kq * 2048, kT64, 1024), ID_KV, (i | kq) != 0 ? 1u : 0u);
+          for (int kq = 0; kq < 8; ++kq)
+            umma_bf16(tdk, ds_m + kq * 128, q_m + kq * 128, ID_KV, (i | kq) != 0 ? 1u : 0u);
+          umma_commit(q_empty);
+          umma_commit(bufs_free);
+          if (i == nqb - 1) {
+            umma_commit(acc_full);
+            umma_commit(kv_empty);
+          }
         }
-        umma_commit(q_empty);
-        umma_commit(bufs_free);
-        if (i == nqb - 1) {
-          umma_commit(acc_full);
-          umma_commit(kv_empty);
-        }
+        __syncwarp();
       }
     }
   } else if (warp < 4) {
