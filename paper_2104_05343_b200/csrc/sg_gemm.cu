@@ -409,8 +409,9 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
 
   if (warp == 0) {
     if constexpr (EpiCfg<EW>::kRealloc) reg_dealloc<40>();
-    if (lane == 0) {
+    {
       // ------------------------------------------------------------ producer
+      // whole warp walks the loop (warp-uniform coordinates); one elected lane issues
       uint32_t stage = 0, phase = 0;
       for (int t = unit0; t < p.num_tiles; t += nunits) {
         int mb, nb, z1, z2, half;
@@ -425,7 +426,8 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * A_BYTES;
           uint8_t* b_dst = sB + stage * B_BYTES;
-          if (PAIR) {
+          if (!elect_one()) {
+          } else if (PAIR) {
             // both CTAs' bytes complete on the leader's barrier
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
             const uint32_t fb = mapa_smem(&full[stage], 0);
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
                 load_box(&tmB, b_dst + i * 64 * kBK * 2, &full[stage], n0 + i * 64, kb * kBK, z2, z1, p.b_b2_first);
             }
           }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         ln_mu = p.ln_mean[row0 + lane];
         ln_rs = p.ln_rstd[row0 + lane];
       }
-      mbar_wait(&tfull[as], aph);
+      mbar_wait_sleep(&tfull[as], aph);  // sleeping: a spinning epilogue warp steals issue slots from the producer / MMA warps
       tc_fence_after();
       const uint32_t tacc = tmem_base + lane_base + as * BN;
 

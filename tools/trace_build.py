@@ -33,7 +33,7 @@ GEMM = [
      "constexpr int kBM = 128;\nconstexpr int kBK = 64;\n__device__ unsigned long long g_gtrace[4][4096];\n"
      "__device__ __forceinline__ void gtr(int which, int& i, int ev) {\n"
      "  if (i < 4096) g_gtrace[which][i++] = ((unsigned long long)ev << 56) | (clock64() & 0xffffffffffffffull);\n}"),
-    ("      mbar_wait(&tfull[as], aph);", "      if (trg) gtr(0, tri, 0);\n      mbar_wait(&tfull[as], aph);\n      if (trg) gtr(0, tri, 1);"),
+    ("      mbar_wait_sleep(&tfull[as], aph);", "      if (trg) gtr(0, tri, 0);\n      mbar_wait_sleep(&tfull[as], aph);\n      if (trg) gtr(0, tri, 1);"),
     ("        uint32_t r[32];\n        tmem_ld32(tacc + c * 32, r);\n        tmem_wait_ld();\n",
      "        uint32_t r[32];\n        if (trg) gtr(0, tri, 2);\n        tmem_ld32(tacc + c * 32, r);\n        tmem_wait_ld();\n"
      "        if (trg) gtr(0, tri, 3);\n"),
