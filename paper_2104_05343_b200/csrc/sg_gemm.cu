@@ -1225,7 +1225,11 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   const bool in_place = a->C == a->D && a->c_dtype == SG_DTYPE_F32 && a->ldc == a->ldd;
   const bool split_ok = !deterministic && a->mode == SG_EPI_NORMAL && a->d_dtype == SG_DTYPE_F32 && !a->bias &&
                         a->act == SG_ACT_NONE && !a->D2 && !a->colsum && batch == 1 && (a->C == nullptr || in_place);
-  p.k_splits = split_ok ? pick_splits(tiles, p.k_blocks, units) : 1;
+  static const int env_splits = [] {  // SG_GEMM_SPLITS=n forces n splits where allowed (experiments)
+    const char* e = getenv("SG_GEMM_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  p.k_splits = split_ok ? (env_splits > 0 ? env_splits : pick_splits(tiles, p.k_blocks, units)) : 1;
   p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   tiles *= p.k_splits;
