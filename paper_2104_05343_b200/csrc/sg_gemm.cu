@@ -67,6 +67,7 @@ struct GemmParams {
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int k_splits, kb_per_split;   // split-K: work unit = (split, tile), partial sums reduce-added into D
   int full_units;               // units >= full_units are half-width (BN / 2) tiles of the last round
+  int group_m, group_shift;     // rasterisation: groups of group_m (= 1 << group_shift) m-tiles
   int a_b2_first, b_b2_first, o_b2_first, x_b2_first, c_b2_first;
   int mode;
   int d_f32;
@@ -191,12 +192,12 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb,
   const int z = (int)p.fd_per.div((uint32_t)t);
   const int r = t - z * (int)p.fd_per.d;
   const int group = (int)p.fd_span.div((uint32_t)r);
-  const int first_m = group * kGroupM;
-  const int gm = min(kGroupM, p.m_tiles - first_m);
+  const int first_m = group * p.group_m;
+  const int gm = min(p.group_m, p.m_tiles - first_m);
   const int rr = r - group * (int)p.fd_span.d;
-  if (gm == kGroupM) {
-    mb = first_m + (rr & (kGroupM - 1));
-    nb = rr / kGroupM;
+  if (gm == p.group_m) {
+    mb = first_m + (rr & (p.group_m - 1));
+    nb = rr >> p.group_shift;
   } else {
     mb = first_m + rr % gm;
     nb = rr / gm;
@@ -1251,7 +1252,15 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     }
   }
   p.fd_per.set((uint32_t)(p.m_tiles * p.n_tiles));
-  p.fd_span.set((uint32_t)(kGroupM * p.n_tiles));
+  static const int env_group = [] {  // SG_GEMM_GROUP_M=g (power of two) overrides the group height (experiments)
+    const char* e = getenv("SG_GEMM_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  p.group_m = env_group > 0 ? env_group : kGroupM;
+  p.group_shift = 0;
+  while ((1 << p.group_shift) < p.group_m) ++p.group_shift;
+  p.group_m = 1 << p.group_shift;
+  p.fd_span.set((uint32_t)(p.group_m * p.n_tiles));
   p.fd_nb2.set((uint32_t)p.nb2);
   p.d_f32 = a->d_dtype == SG_DTYPE_F32;
   p.D = a->D; p.ldd = a->ldd; p.sd1 = a->sd1; p.sd2 = a->sd2;
