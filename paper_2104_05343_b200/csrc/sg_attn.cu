@@ -300,13 +300,20 @@ __global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
 // ============================================================================
 constexpr int kQT = 2;  // query tiles per CTA
 
+// d = 128 uses the same structure with P written over the consumed scores of S_i (TMEM:
+// S0 | S1 | O0 | O1, 4 x 128 columns), so S_i,G+1 is issued after PV_i,G has read P_i,G
+// (the other tile's softmax covers the gap); one Q slot, two K / V slots, O rows stored
+// straight from registers.
+template <int HD>
 struct Flash2Cfg {
-  static constexpr uint32_t T64 = 128 * 64 * 2;   // one 128 x 64 bf16 tile
-  static constexpr int KV_SLOTS = 3;
-  static constexpr int Q_SLOTS = 2;                // Q of the next item prefetched
-  static constexpr uint32_t O_STG = kQT * 8 * 2048;  // per softmax warp one 32 x 32 bf16 output tile
+  static constexpr uint32_t T64 = 128 * 64 * 2;    // one 128 x 64 bf16 atom tile
+  static constexpr uint32_t T = 128 * HD * 2;      // one 128-row tile (HD / 64 atoms)
+  static constexpr int KV_SLOTS = HD == 64 ? 3 : 2;
+  static constexpr int Q_SLOTS = HD == 64 ? 2 : 1; // d = 64: Q of the next item prefetched
+  static constexpr uint32_t O_STG = HD == 64 ? kQT * 8 * 2048 : 0;  // d = 64: per softmax warp one 32 x 32 bf16 output tile
   static constexpr uint32_t X_XCH = (kQT * 2 + kQT) * 256 * 4;  // row max (2 slots) / row sum exchange
-  static constexpr size_t SMEM = Q_SLOTS * kQT * T64 + KV_SLOTS * 2 * T64 + O_STG + X_XCH + 512;
+  static constexpr size_t SMEM = Q_SLOTS * kQT * T + KV_SLOTS * 2 * T + O_STG + X_XCH + 512;
+  static constexpr bool P_IN_S = HD == 128;
 };
 
 // 2^y for a pair of exponents on the FMA pipe (no MUFU): y = j + f with j = rint(y)
@@ -335,21 +342,23 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t y) {
 // next item's Q, first K / V block and first score products are in flight while
 // the current item finishes. NPOLY of every 16 exponent pairs go to the FMA-pipe
 // polynomial instead of MUFU.EX2 (the MUFU rate bounds the softmax warps).
-template <int NPOLY>
+template <int HD, int NPOLY>
 __global__ void __launch_bounds__(640, 1)
     flash_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                       const __grid_constant__ FlashFwdParams p, int bsz) {
-  using Cfg = Flash2Cfg;
-  constexpr uint32_t T64 = Cfg::T64;
-  constexpr int NS = Cfg::KV_SLOTS;
+  using Cfg = Flash2Cfg<HD>;
+  constexpr uint32_t T64 = Cfg::T64, T = Cfg::T;
+  constexpr int NS = Cfg::KV_SLOTS, QS = Cfg::Q_SLOTS;
+  constexpr bool P_IN_S = Cfg::P_IN_S;
+  constexpr int ATOMS = HD / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();
   uint8_t* sQ = smem;                             // [Q_SLOTS][kQT] tiles
-  uint8_t* sK = sQ + Cfg::Q_SLOTS * kQT * T64;    // [NS]
-  uint8_t* sV = sK + NS * T64;                    // [NS]
-  uint8_t* sO = sV + NS * T64;                    // [kQT][4 warps] x 4 KB output staging
+  uint8_t* sK = sQ + QS * kQT * T;                // [NS]
+  uint8_t* sV = sK + NS * T;                      // [NS]
+  uint8_t* sO = sV + NS * T;                      // d = 64: [kQT][4 warps] x 4 KB output staging
   float* sX = reinterpret_cast<float*>(sO + Cfg::O_STG);  // half-row exchange
   uint64_t* bars = reinterpret_cast<uint64_t*>(sO + Cfg::O_STG + Cfg::X_XCH);
   uint64_t* q_full = bars;                // [2]
@@ -384,7 +393,7 @@ __global__ void __launch_bounds__(640, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmO);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QS; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], kQT);
     }
@@ -412,26 +421,34 @@ __global__ void __launch_bounds__(640, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_begin();
-  // TMEM columns: S_i at 128 i, O_i at 256 + 64 i, P_i (packed bf16 pairs) at 384 + 64 i
+  // TMEM columns: S_i at 128 i, O_i at 256 + HD i, P_i (packed bf16 pairs) at 384 + 64 i
+  // (d = 64) or over the consumed scores of S_i (d = 128)
   if (warp == 0) {
     if (lane == 0) {
       int g = 0;
       for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
         int qb, h, b;
         decode(t, qb, h, b);
-        const int qs = it & 1;
-        mbar_wait_sleep(&q_empty[qs], ((it >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qs], kQT * T64);
+        const int qs = it % QS;
+        mbar_wait_sleep(&q_empty[qs], ((it / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], kQT * T);
 #pragma unroll
         for (int i = 0; i < kQT; ++i)
-          tma4(&tmQ, sQ + (qs * kQT + i) * T64, &q_full[qs], 0, (qb * kQT + i) * kQB, h, b, p.q_b2_first);
+#pragma unroll
+          for (int a = 0; a < ATOMS; ++a)
+            tma4(&tmQ, sQ + (qs * kQT + i) * T + a * T64, &q_full[qs], a * 64, (qb * kQT + i) * kQB, h, b,
+                 p.q_b2_first);
         for (int j = 0; j < nkb; ++j, ++g) {
           const int slot = g % NS;
           mbar_wait_sleep(&kv_empty[slot], ((g / NS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&k_full[slot], T64);
-          tma4(&tmK, sK + slot * T64, &k_full[slot], 0, j * kKB, h, b, p.k_b2_first);
-          mbar_arrive_expect_tx(&v_full[slot], T64);
-          tma4(&tmV, sV + slot * T64, &v_full[slot], 0, j * kKB, h, b, p.v_b2_first);
+          mbar_arrive_expect_tx(&k_full[slot], T);
+#pragma unroll
+          for (int a = 0; a < ATOMS; ++a)
+            tma4(&tmK, sK + slot * T + a * T64, &k_full[slot], a * 64, j * kKB, h, b, p.k_b2_first);
+          mbar_arrive_expect_tx(&v_full[slot], T);
+#pragma unroll
+          for (int a = 0; a < ATOMS; ++a)
+            tma4(&tmV, sV + slot * T + a * T64, &v_full[slot], a * 64, j * kKB, h, b, p.v_b2_first);
         }
       }
     }
@@ -444,27 +461,32 @@ __global__ void __launch_bounds__(640, 1)
       // and both softmax warpgroups then contend for MUFU at the same time)
       const int i = warp >> 1;
       constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
-      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, 64, false, true);   // P (TMEM), V MN-major
+      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, HD, false, true);   // P (TMEM), V MN-major
       const bool trm = blockIdx.x == 0 && i == 0 && lane == 0;
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       const uint64_t q_desc0 = umma_desc_sw128(smem_u32(sQ), 0, 1024), k_desc0 = umma_desc_sw128(smem_u32(sK), 0, 1024);
       const uint64_t v_desc0 = umma_desc_sw128(smem_u32(sV), kKB * 128, 1024);
-      constexpr uint64_t kTile = T64 >> 4;
+      constexpr uint64_t kTile = T >> 4, kAtom = T64 >> 4;
+      const uint32_t t_o = tm + 256 + i * HD;
       int tri = 0;
       (void)trm; (void)tri;
       // S_i for global block G (item G / nkb, key block G % nkb)
       auto issue_s = [&](int G) {
         const int it = G / nkb;
-        const uint64_t qd = q_desc0 + ((it & 1) * kQT + i) * kTile, kd = k_desc0 + (G % NS) * kTile;
+        const uint64_t qd = q_desc0 + ((it % QS) * kQT + i) * kTile, kd = k_desc0 + (G % NS) * kTile;
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) umma_bf16(tm + i * 128, qd + 2 * kk, kd + 2 * kk, IDESC_S, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {  // K-dim = d: 16-element steps, 64-wide atoms
+            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
+            umma_bf16(tm + i * 128, qd + off, kd + off, IDESC_S, kk > 0 ? 1u : 0u);
+          }
           umma_commit(&s_full[i]);
+          if (G % nkb == nkb - 1) umma_commit(&q_empty[(G / nkb) % QS]);  // the item's last score product
         }
         __syncwarp();
       };
       auto ready_s = [&](int G) {  // Q of G's item (at its first block) and K_G landed
-        if (G % nkb == 0) mbar_wait(&q_full[(G / nkb) & 1], ((G / nkb) >> 1) & 1);
+        if (G % nkb == 0) mbar_wait(&q_full[(G / nkb) % QS], ((G / nkb) / QS) & 1);
         mbar_wait(&k_full[G % NS], (G / NS) & 1);
         tc_fence_after();
       };
@@ -475,6 +497,28 @@ __global__ void __launch_bounds__(640, 1)
       for (int G = 0; G < total; ++G) {
         const int slot = G % NS, j = G % nkb;
         SG_TR(trm, 2, tri, 10);
+        if constexpr (P_IN_S) {
+          // PV_i,G reads P_i,G from S_i's columns, then S_i,G+1 overwrites them (in order)
+          mbar_wait(&v_full[slot], (G / NS) & 1);
+          mbar_wait(&p_full[i], G & 1);
+          tc_fence_after();
+          const uint64_t vd = v_desc0 + slot * kTile;
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < kKB / 16; ++kk)
+              umma_bf16_ts(t_o, tm + i * 128 + (kk >> 2) * 64 + (kk & 3) * 8, vd + 128 * kk, IDESC_PV,
+                           (j | kk) != 0 ? 1u : 0u);
+            umma_commit(&pv_done[i]);
+            if (j == nkb - 1) umma_commit(&o_full[i]);
+            umma_commit(&kv_empty[slot]);  // this tile is done with K_G, V_G
+          }
+          __syncwarp();
+          if (G + 1 < total) {
+            ready_s(G + 1);
+            issue_s(G + 1);
+          }
+          continue;
+        }
         if (G + 1 < total) {
           ready_s(G + 1);
           SG_TR(trm, 2, tri, 14);
@@ -483,8 +527,6 @@ __global__ void __launch_bounds__(640, 1)
           SG_TR(trm, 2, tri, 15);
           issue_s(G + 1);
         }
-        if (j == nkb - 1 && elect_one()) umma_commit(&q_empty[(G / nkb) & 1]);  // the item's last score product issued
-        __syncwarp();
         SG_TR(trm, 2, tri, 11);
         mbar_wait(&v_full[slot], (G / NS) & 1);
         mbar_wait(&p_full[i], G & 1);  // P_i,G in TMEM, O_i corrected (or read out, first block)
@@ -494,7 +536,7 @@ __global__ void __launch_bounds__(640, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kKB / 16; ++kk)
-            umma_bf16_ts(tm + 256 + i * 64, tm + 384 + i * 64 + kk * 8, vd + 128 * kk, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
+            umma_bf16_ts(t_o, tm + 384 + i * 64 + kk * 8, vd + 128 * kk, IDESC_PV, (j | kk) != 0 ? 1u : 0u);
           umma_commit(&pv_done[i]);
           if (j == nkb - 1) umma_commit(&o_full[i]);
           umma_commit(&kv_empty[slot]);  // this tile is done with K_G, V_G
@@ -516,8 +558,9 @@ __global__ void __launch_bounds__(640, 1)
     const int i = w >> 3, kh = (w >> 2) & 1, qd = warp & 3;
     const int r = qd * 32 + lane;                 // row inside the tile
     const uint32_t lane_base = static_cast<uint32_t>(qd * 32) << 16;
-    const uint32_t t_s = tmem + i * 128 + kh * 64 + lane_base, t_o = tmem + 256 + i * 64 + kh * 32 + lane_base,
-                   t_p = tmem + 384 + i * 64 + kh * 32 + lane_base;
+    // this warp's S_i columns (its 64 keys), O_i columns (its HD / 2) and packed P_i columns
+    const uint32_t t_s = tmem + i * 128 + kh * 64 + lane_base, t_o = tmem + 256 + i * HD + kh * (HD / 2) + lane_base,
+                   t_p = P_IN_S ? t_s : tmem + 384 + i * 64 + kh * 32 + lane_base;
     uint64_t* my_xbar = &xbar[i * 4 + qd];
     uint64_t* my_lbar = &lbar[i * 4 + qd];
     float* xm = sX + (i * 2) * 2 * 128;           // [2 slots][2 halves][128] row maxima
@@ -609,12 +652,15 @@ __global__ void __launch_bounds__(640, 1)
         l = l * alpha + (f2_lo(ps2) + f2_hi(ps2));
         if (correct) {
           // this half's O_i columns *= 2^(m_old - m_new) before PV_i,G accumulates into them
-          uint32_t ov[32];
-          tmem_ld32(t_o, ov);
-          tmem_wait_ld();
+#pragma unroll 1
+          for (int oc = 0; oc < HD / 64; ++oc) {
+            uint32_t ov[32];
+            tmem_ld32(t_o + oc * 32, ov);
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-          tmem_st32(t_o, ov);
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st32(t_o + oc * 32, ov);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
@@ -633,6 +679,34 @@ __global__ void __launch_bounds__(640, 1)
       mbar_wait_sleep(&o_full[i], it & 1);
       tc_fence_after();
       const float inv = 1.f / l;
+      if constexpr (HD == 128) {
+        // normalised bf16 rows straight to the context block: 64 columns = 128 B per row
+        // (the TMEM loads are warp-collective: every lane loads, rows past s do not store)
+        uint4* dst = reinterpret_cast<uint4*>(p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * HD + kh * 64);
+#pragma unroll
+        for (int oc = 0; oc < 2; ++oc) {
+          uint32_t ov[32];
+          tmem_ld32(t_o + oc * 32, ov);
+          tmem_wait_ld();
+          if (qrow < p.s) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint4 x;
+              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                hh[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * k + 2 * e]) * inv,
+                                              __uint_as_float(ov[8 * k + 2 * e + 1]) * inv);
+              dst[oc * 4 + k] = x;
+            }
+          }
+        }
+        __syncwarp();
+        tc_fence_before();
+        if (kh == 0 && qrow < p.s && p.lse)
+          p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m_use + __log2f(l)) * 0.6931471805599453f;
+        continue;
+      }
       // normalised bf16 rows -> this warp's 32 x 32 SW64 staging tile -> TMA store
       // into the context block (rows past s clipped)
       uint8_t* ostg = sO + w * 2048;
@@ -676,37 +750,32 @@ __global__ void __launch_bounds__(640, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-template <int NPOLY>
+template <int HD, int NPOLY>
 static void launch_fwd2_k(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                           const FlashFwdParams& p, int b, int grid, cudaStream_t stream) {
-  launch_k(flash_fwd2_kernel<NPOLY>, dim3(grid), dim3(640), Flash2Cfg::SMEM, stream, q, k, v, o, p, b);
+  launch_k(flash_fwd2_kernel<HD, NPOLY>, dim3(grid), dim3(640), Flash2Cfg<HD>::SMEM, stream, q, k, v, o, p, b);
 }
 
+template <int HD>
 static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& o,
                        const FlashFwdParams& p, int b, cudaStream_t stream) {
   // SG_FLASH_POLY = pairs of 16 on the FMA-pipe exp2 (experiments; default below)
-  static const int npoly = [] {  // measured at b=32 s=512 / b=4 s=2048: 0 -> 63.6 / 115.9 us, 2 -> 62.7 / 113.0,
+  static const int npoly = [] {  // measured (d = 64) at b=32 s=512 / b=4 s=2048: 0 -> 63.6 / 115.9 us, 2 -> 62.7 / 113.0,
     const char* e = getenv("SG_FLASH_POLY");  // 4 -> 63.7 / 115.1, 6 -> 67.2 / 123.2
     return e ? atoi(e) : 2;
   }();
-  const void* kern = npoly >= 8 ? (const void*)flash_fwd2_kernel<8>
-                     : npoly >= 6 ? (const void*)flash_fwd2_kernel<6>
-                     : npoly >= 4 ? (const void*)flash_fwd2_kernel<4>
-                     : npoly >= 2 ? (const void*)flash_fwd2_kernel<2> : (const void*)flash_fwd2_kernel<0>;
-  if (!ensure_smem(kern, (int)Flash2Cfg::SMEM)) return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
+  const void* kern = npoly >= 4 ? (const void*)flash_fwd2_kernel<HD, 4>
+                     : npoly >= 2 ? (const void*)flash_fwd2_kernel<HD, 2> : (const void*)flash_fwd2_kernel<HD, 0>;
+  if (!ensure_smem(kern, (int)Flash2Cfg<HD>::SMEM)) return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
   const int items = (p.s + kQT * kQB - 1) / (kQT * kQB) * p.nh * b;
   const int sms = sg_device_sm_count();
   const int grid = std::min(items, sms > 0 ? sms : 148);
-  if (npoly >= 8)
-    launch_fwd2_k<8>(q, k, v, o, p, b, grid, stream);
-  else if (npoly >= 6)
-    launch_fwd2_k<6>(q, k, v, o, p, b, grid, stream);
-  else if (npoly >= 4)
-    launch_fwd2_k<4>(q, k, v, o, p, b, grid, stream);
+  if (npoly >= 4)
+    launch_fwd2_k<HD, 4>(q, k, v, o, p, b, grid, stream);
   else if (npoly >= 2)
-    launch_fwd2_k<2>(q, k, v, o, p, b, grid, stream);
+    launch_fwd2_k<HD, 2>(q, k, v, o, p, b, grid, stream);
   else
-    launch_fwd2_k<0>(q, k, v, o, p, b, grid, stream);
+    launch_fwd2_k<HD, 0>(q, k, v, o, p, b, grid, stream);
   count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
@@ -761,13 +830,12 @@ extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_
   if (!rc) rc = tmap_bf16_4d(&tv, base + 2 * hb, d, s, nh, b, ldq, d, s * ldq, 64, kKB, &p.v_b2_first);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (d == 64) {
-    CUtensorMap to;
-    rc = tmap_bf16_tile_4d(&to, out, d, s, nh, b, ldo, d, s * ldo, &p.o_b2_first);
-    if (rc) return rc;
-    return launch_fwd2(tq, tk, tv, to, p, (int)b, st);
-  }
-  return launch_fwd<128>(tq, tk, tv, p, (int)b, st);
+  CUtensorMap to;
+  rc = tmap_bf16_tile_4d(&to, out, d, s, nh, b, ldo, d, s * ldo, &p.o_b2_first);
+  if (rc) return rc;
+  if (d == 64) return launch_fwd2<64>(tq, tk, tv, to, p, (int)b, st);
+  if (getenv("SG_FLASH_FWD128_V1")) return launch_fwd<128>(tq, tk, tv, p, (int)b, st);  // A/B experiments
+  return launch_fwd2<128>(tq, tk, tv, to, p, (int)b, st);
 }
 
 // ============================================================================
