@@ -1,18 +1,13 @@
-// Flash-style multi-head attention forward on the 5th-gen tensor cores
-// (layers.py:404-416 of the reference: softmax(Q K^T / sqrt(d)) V per head, no
-// mask), without materialising the [b, n, s, s] probability matrix.
+// Flash-style multi-head attention on the 5th-gen tensor cores (layers.py:404-459 of
+// the reference: softmax(Q K^T / sqrt(d)) V per head and its backward, no mask),
+// without materialising the [b, n, s, s] probability matrix.
 //
-// One CTA = (128 query rows, head, batch); 256 threads:
-//   warp 0   TMA producer: Q once, then K_j / V_j key blocks (double-buffered)
-//   warp 1   MMA issuer: S_j = Q K_j^T (128 x 128 x d) into TMEM, then
-//            PV_j = P_j V_j (128 x d x 128) with P_j from shared memory
-//   warp 2   TMEM allocator (256 columns: S | PV)
-//   warps 4-7 softmax, thread = query row: online max / sum in the log2
-//            domain, P_j -> swizzled smem (the UMMA A operand), O kept in
-//            registers and rescaled per block (O = O * alpha + PV_j)
-// Outputs: O (bf16) straight into the interleaved context block and the row
-// log-sum-exp (fp32) for the backward. Q/K/V are read in place from the QKV
-// block through 4-D TMA maps (no head split copies).
+// Forward (flash_fwd2_kernel, head_dim 64 and 128): persistent, two 128-row query
+// tiles per CTA ping-ponging on the tensor core, P in TMEM as the A operand of PV,
+// O accumulated in TMEM; outputs O (bf16) into the interleaved context block and the
+// row log-sum-exp (fp32) for the backward. Backward: flash_bwd2_kernel (d = 64,
+// transposed orientation) and flash_bwd128_kernel (d = 128). Q/K/V are read in place
+// from the QKV block through 4-D TMA maps (no head split copies).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -43,18 +38,6 @@ struct FlashFwdParams {
 constexpr int kQB = 128;   // query rows per CTA
 constexpr int kKB = 128;   // keys per block
 
-template <int HD>
-struct FlashCfg {
-  static constexpr int ATOMS = HD / 64;                    // 64-wide swizzle atoms along d
-  static constexpr uint32_t Q_BYTES = kQB * HD * 2;
-  static constexpr uint32_t KV_BYTES = kKB * HD * 2;
-  static constexpr uint32_t P_BYTES = kQB * kKB * 2;       // 2 atoms of 64 keys
-  // no alignment slack: the dynamic window starts 1024-aligned (no static smem), which
-  // keeps d = 64 at 112 KB + barriers -> two CTAs per SM
-  static constexpr size_t SMEM = Q_BYTES + 4 * KV_BYTES + P_BYTES + 128;
-  static constexpr uint32_t TMEM_COLS = 128 + (HD < 128 ? 128 : HD);  // S | PV (power of two)
-};
-
 __device__ __forceinline__ void tma4(const CUtensorMap* tm, void* dst, uint64_t* bar, int inner, int outer, int z2,
                                      int z1, int b2f) {
   if (b2f)
@@ -76,206 +59,8 @@ __device__ __forceinline__ float ex2f_fast(float x) {
   return y;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(256, HD == 64 ? 2 : 1)
-    flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ FlashFwdParams p) {
-  using Cfg = FlashCfg<HD>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Cfg::Q_BYTES;            // 2 slots
-  uint8_t* sV = sK + 2 * Cfg::KV_BYTES;       // 2 slots
-  uint8_t* sP = sV + 2 * Cfg::KV_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
-  uint64_t* s_full = bars + 7;
-  uint64_t* p_full = bars + 8;
-  uint64_t* pv_full = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int nkb = (p.s + kKB - 1) / kKB;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(pv_full, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_begin();
-  const uint32_t t_s = tmem, t_pv = tmem + 128;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ producer
-      mbar_arrive_expect_tx(q_full, Cfg::Q_BYTES);
-#pragma unroll
-      for (int a = 0; a < Cfg::ATOMS; ++a)
-        tma4(&tmQ, sQ + a * kQB * 128, q_full, a * 64, qb * kQB, h, b, p.q_b2_first);
-      for (int j = 0; j < nkb; ++j) {
-        const int slot = j & 1;
-        mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[slot], Cfg::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < Cfg::ATOMS; ++a)
-          tma4(&tmK, sK + slot * Cfg::KV_BYTES + a * kKB * 128, &k_full[slot], a * 64, j * kKB, h, b, p.k_b2_first);
-        mbar_arrive_expect_tx(&v_full[slot], Cfg::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < Cfg::ATOMS; ++a)
-          tma4(&tmV, sV + slot * Cfg::KV_BYTES + a * kKB * 128, &v_full[slot], a * 64, j * kKB, h, b, p.v_b2_first);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t IDESC_S = umma_idesc_bf16(kQB, kKB, false, false);  // Q, K both K-major
-      constexpr uint32_t IDESC_PV = umma_idesc_bf16(kQB, HD, false, true);   // P K-major, V MN-major
-      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int slot = j & 1;
-        mbar_wait(&k_full[slot], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + slot * Cfg::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (kQB * 128) + (kk & 3) * 32;  // atom, 16-element step inside it
-          umma_bf16(t_s, umma_desc_sw128(q_base + off, 0, 1024), umma_desc_sw128(k_base + off, 0, 1024), IDESC_S,
-                    kk > 0 ? 1u : 0u);
-        }
-        umma_commit(s_full);
-      };
-      issue_s(0);
-      for (int j = 0; j < nkb; ++j) {
-        const int slot = j & 1;
-        mbar_wait(p_full, j & 1);  // P_j in smem (and S_j fully read)
-        mbar_wait(&v_full[slot], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + slot * Cfg::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < kKB / 16; ++kk) {
-          // A = P [128 q x 128 keys] K-major: atom kk/4, 32 B per 16 keys inside it.
-          // B = V [128 keys x HD] MN-major: 16 key rows = 2048 B, 64-wide d chunks kKB*128 B apart.
-          const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * (kQB * 128) + (kk & 3) * 32, 0, 1024);
-          const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, kKB * 128, 1024);
-          umma_bf16(t_pv, ad, bd, IDESC_PV, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(pv_full);
-        umma_commit(&kv_empty[slot]);
-        if (j + 1 < nkb) issue_s(j + 1);
-      }
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax / output
-    const int q = warp & 3;
-    const int r = q * 32 + lane;               // row inside the 128-row tile
-    const int qrow = qb * kQB + r;             // query position
-    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    float o[HD];
-#pragma unroll
-    for (int i = 0; i < HD; ++i) o[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkb; ++j) {
-      const int kvalid = min(kKB, p.s - j * kKB);
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      float bm = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < kKB / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_s + lane_base + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kvalid) bm = fmaxf(bm, __uint_as_float(v[i]));
-      }
-      const float m_new = fmaxf(m, bm * p.scale_log2);
-      const float alpha = ex2f_fast(m - m_new);  // 0 on the first block (m = -inf)
-      float psum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < kKB / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_s + lane_base + c * 32, v);
-        tmem_wait_ld();
-        float pv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          pv[i] = (c * 32 + i < kvalid) ? ex2f_fast(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
-          psum += pv[i];
-        }
-        // P row r, keys [32c, 32c+32): atom c/2, 16-byte chunks ((c%2)*4 .. +3) swizzled by r % 8
-        uint8_t* prow = sP + (c >> 1) * (kQB * 128) + r * 128;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 x;
-          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) hh[e] = __floats2bfloat162_rn(pv[8 * k + 2 * e], pv[8 * k + 2 * e + 1]);
-          const int chunk = (c & 1) * 4 + k;
-          *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = x;
-        }
-      }
-      l = l * alpha + psum;
-      m = m_new;
-      // P visible to the tensor core (async proxy); S slot fully read
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-      // O = O * alpha + P_j V_j
-      mbar_wait(pv_full, j & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_pv + lane_base + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[c * 32 + i] = fmaf(o[c * 32 + i], alpha, __uint_as_float(v[i]));
-      }
-      tc_fence_before();
-    }
-    if (qrow < p.s) {
-      const float inv = 1.f / l;
-      __nv_bfloat16* dst = p.O + ((size_t)b * p.s + qrow) * p.ldo + (size_t)h * HD;
-#pragma unroll
-      for (int k = 0; k < HD / 8; ++k) {
-        uint4 x;
-        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) hh[e] = __floats2bfloat162_rn(o[8 * k + 2 * e] * inv, o[8 * k + 2 * e + 1] * inv);
-        *reinterpret_cast<uint4*>(dst + 8 * k) = x;
-      }
-      if (p.lse) p.lse[((size_t)b * p.nh + h) * p.s + qrow] = (m + __log2f(l)) * 0.6931471805599453f;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<Cfg::TMEM_COLS>(tmem);
-}
-
 // ============================================================================
-// Forward, d = 64, two query tiles per CTA ("ping-pong"): 640 threads
+// Forward, two query tiles per CTA ("ping-pong"): 640 threads (d = 64; d = 128 below)
 //   warp 0      TMA: Q0, Q1 once per item; K_j / V_j blocks (three slots)
 //   warps 1, 3  MMA issuers of tile 0 / tile 1: S_i,G+1 = Q_i K_G+1^T as soon as the
 //               softmax warps hold S_i,G in registers, PV_i,G = P_i,G V_G once P_i,G
@@ -781,19 +566,6 @@ static int launch_fwd2(const CUtensorMap& q, const CUtensorMap& k, const CUtenso
   return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
 }
 
-template <int HD>
-static int launch_fwd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const FlashFwdParams& p,
-                      int b, cudaStream_t stream) {
-  using Cfg = FlashCfg<HD>;
-  if (!ensure_smem(reinterpret_cast<const void*>(flash_fwd_kernel<HD>), (int)Cfg::SMEM))
-    return set_error(SG_ERR_CUDA, "flash fwd: smem attribute");
-  dim3 grid((p.s + kQB - 1) / kQB, p.nh, b);
-  launch_k(flash_fwd_kernel<HD>, grid, dim3(256), Cfg::SMEM, stream, q, k, v, p);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? SG_OK : set_error(SG_ERR_CUDA, cudaGetErrorString(e));
-}
-
 }  // namespace sg
 
 using namespace sg;
@@ -834,7 +606,6 @@ extern "C" int sg_flash_attn_fwd(const void* qkv, int64_t ldq, int64_t b, int64_
   rc = tmap_bf16_tile_4d(&to, out, d, s, nh, b, ldo, d, s * ldo, &p.o_b2_first);
   if (rc) return rc;
   if (d == 64) return launch_fwd2<64>(tq, tk, tv, to, p, (int)b, st);
-  if (getenv("SG_FLASH_FWD128_V1")) return launch_fwd<128>(tq, tk, tv, p, (int)b, st);  // A/B experiments
   return launch_fwd2<128>(tq, tk, tv, to, p, (int)b, st);
 }
 

@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-for i in 1 2 3 4 5 6; do timeout 600 python -m pytest tests/test_dist.py -m gpu -q -p no:cacheprovider -k "graph and 2-4" 2>&1 | grep -E "^E  |passed|failed" | head -4 >> gpurun_out/dist_rep.log; done
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "pytest rc $?" >> gpurun_out/gputest.log
+timeout 900 python bench.py --workload gpt --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/gpt_train.json 2> gpurun_out/gpt_train.err
+timeout 900 python bench.py --workload gpt --mode infer --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/gpt_infer.json 2> gpurun_out/gpt_infer.err
