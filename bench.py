@@ -295,7 +295,7 @@ def main():
         # NCCL's panel broadcasts run beside the persistent GEMMs, which leave SG_SM_RESERVE
         # SMs free (mesh.py); cap NCCL's channels (one CTA each) to that budget
         os.environ.setdefault("NCCL_MAX_NCHANNELS", os.environ.get("SG_SM_RESERVE", "8"))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        sg.init_dist("nccl", device_id=torch.device("cuda", local))  # async NCCL errors + collective timeout
     w = workload(args)
     mc = sg.mesh_for_world(world)
     mc = sg.MeshConfig(rows=mc.rows, cols=mc.cols, node_size=args.node_size or world,

@@ -708,6 +708,25 @@ def check_same_mesh(*objs) -> Mesh:
     return mesh
 
 
+def init_dist(backend: str = "nccl", timeout_s: float | None = None, **kwargs) -> None:
+    """torch.distributed set-up for a dist mesh with failure detection: NCCL errors are
+    raised asynchronously on the host (TORCH_NCCL_ASYNC_ERROR_HANDLING=1) and every
+    collective carries a timeout (SG_DIST_TIMEOUT_S, default 600 s), so a dead or hung
+    peer surfaces as an exception instead of a hang. The peer-memory step has its own
+    device-side barrier timeout (PeerNet.check, ~10 s of spinning per barrier)."""
+    import datetime
+    import os
+
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        return
+    if backend == "nccl":
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    t = timeout_s if timeout_s is not None else float(os.environ.get("SG_DIST_TIMEOUT_S", "600"))
+    dist.init_process_group(backend, timeout=datetime.timedelta(seconds=t), **kwargs)
+
+
 def mesh_for_world(world: int) -> MeshConfig:
     """The north-star grid for a GPU count: 1 -> 1x1, 2 -> 1x2, 4 -> 2x2, 8 -> 2x4."""
     table = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}

@@ -28,10 +28,42 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _init(rank, world, port):
+def _init(rank, world, port, timeout_s=None):
+    import paper_2104_05343_b200 as sg
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sg.init_dist("gloo", timeout_s=timeout_s, rank=rank, world_size=world)
+
+
+def _timeout_worker(rank, world, port, out_dir):
+    import time
+
+    import torch
+
+    _init(rank, world, port, timeout_s=3.0)
+    try:
+        if rank == 0:  # the peer never joins this collective: it must fail, not hang
+            t0 = time.time()
+            try:
+                dist.all_reduce(torch.ones(4))
+                res = "no error"
+            except RuntimeError as e:
+                res = f"raised after {time.time() - t0:.1f} s: {str(e)[:60]}"
+            (out_dir / "r0.txt").write_text(res)
+        else:
+            time.sleep(8.0)
+    finally:
+        if rank != 0:
+            dist.destroy_process_group()
+
+
+def test_collective_timeout_raises(tmp_path):
+    """Failure detection: a collective whose peer never arrives raises after the
+    init_dist timeout instead of hanging the process."""
+    mp.spawn(_timeout_worker, args=(2, _free_port(), tmp_path), nprocs=2, join=True)
+    res = (tmp_path / "r0.txt").read_text()
+    assert res.startswith("raised after"), res
 
 
 def _collectives_worker(rank, world, port, rows, cols, out_dir):
