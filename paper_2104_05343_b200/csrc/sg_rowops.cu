@@ -778,6 +778,58 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ ids, long long n, l
   }
 }
 
+// Deterministic variant (SG_DETERMINISTIC=1): one warp per table row scans the ids in
+// order, collects the matching token positions into a shared-memory list (ballot order =
+// token order) and folds their rows into the gradient row in that order, flushing every
+// kDetList tokens; a single writer per row, so the sums are bit-reproducible (the
+// atomic scatter-add above adds in arrival order).
+constexpr int kDetList = 128;
+template <typename TD>
+__global__ void __launch_bounds__(256) embed_bwd_det_kernel(const int64_t* __restrict__ ids, long long n, long long lo,
+                                                            long long vb, const TD* __restrict__ dout, long long ldd,
+                                                            int hc, float* __restrict__ grad, long long ldg) {
+  pdl_begin();
+  __shared__ int list[8][kDetList];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  int* lst = list[wl];
+  for (long long row = wid; row < vb; row += nw) {
+    const long long id = row + lo;
+    int cnt = 0;
+    auto flush = [&]() {
+      __syncwarp();
+      for (int c = lane * 8; c < hc; c += 256) {
+        const int k = min(8, hc - c);
+        float acc[8];
+        ld8(grad + row * ldg + c, k, acc);
+        for (int m = 0; m < cnt; ++m) {
+          float v[8];
+          ld8(dout + (long long)lst[m] * ldd + c, k, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] += v[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < k) grad[row * ldg + c + i] = acc[i];
+      }
+      __syncwarp();
+      cnt = 0;
+    };
+    for (long long t0 = 0; t0 < n; t0 += 32) {
+      const long long t = t0 + lane;
+      const bool hit = t < n && ids[t] == id;
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (m == 0) continue;
+      const int nm = __popc(m);
+      if (cnt + nm > kDetList) flush();
+      if (hit) lst[cnt + __popc(m & ((1u << lane) - 1))] = (int)t;
+      cnt += nm;
+    }
+    if (cnt > 0) flush();
+  }
+}
+
 // ============================================================ element-wise
 template <typename TS, typename TD>
 __global__ void cast_kernel(const TS* __restrict__ s, TD* __restrict__ d, long long n) {
@@ -1383,7 +1435,17 @@ extern "C" int sg_embed_bwd(const int64_t* ids, int64_t n, int64_t lo, int64_t v
   if (n < 0 || hc < 1 || vb < 0) return set_error(SG_ERR_SHAPE, "embed_bwd: bad extents");
   if (!aligned16(dout, ldd, ddt == SG_DTYPE_F32 ? 4 : 2)) return set_error(SG_ERR_SHAPE, "embed_bwd: unaligned");
   if (n == 0) return SG_OK;
-  SG_DISPATCH_T(ddt, TD, (launch_k(embed_bwd_kernel<TD>, dim3(grid_for(n, 8)), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
+  static const bool deterministic = [] {
+    const char* e = getenv("SG_DETERMINISTIC");
+    return e && atoi(e) != 0;
+  }();
+  if (deterministic) {
+    if (n > INT32_MAX) return set_error(SG_ERR_SHAPE, "embed_bwd: too many tokens for the deterministic path");
+    const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((vb + 7) / 8, 148LL * 16));
+    SG_DISPATCH_T(ddt, TD, (launch_k(embed_bwd_det_kernel<TD>, dim3(blocks), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
+  } else {
+    SG_DISPATCH_T(ddt, TD, (launch_k(embed_bwd_kernel<TD>, dim3(grid_for(n, 8)), dim3(256), 0, S(stream), ids, n, lo, vb, static_cast<const TD*>(dout), ldd, (int)hc, grad, ldg)));
+  }
   return launch_check();
 }
 

@@ -264,3 +264,41 @@ def test_golden_operator_fixtures_q2():
         assert rel(got, g[f"ops.v{v}.ce_dlogits"]) < TOL_BF16
         eg = layers.embedding_backward(sg.scatter(g["ops.dy"], m), g[f"ops.v{v}.tokens"], mv.table, cfgv, ws)
         assert rel(sg.gather(eg), g[f"ops.v{v}.emb_grad"]) < 1e-5
+
+
+_DET_EMBED = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2104_05343_b200 import kernels as K
+torch.manual_seed(5)
+n, v, hc = 3000, 97, 320
+ids = torch.randint(0, v, (n,), device="cuda")
+ids[:400] = 7  # a hot row: more matches than one flush list
+dout = torch.randn(n, hc, device="cuda")
+ref = torch.zeros(v, hc, dtype=torch.float64, device="cuda").index_add_(0, ids, dout.double())
+outs = []
+for _ in range(2):
+    g = torch.zeros(v, hc, device="cuda")
+    K.embed_bwd(ids, 0, v, dout, g)
+    outs.append(g)
+torch.cuda.synchronize()
+err = ((outs[0].double() - ref).abs().max() / ref.abs().max()).item()
+same = bool(torch.equal(outs[0], outs[1]))
+print(f"{err:.3e} {same}")
+'''
+
+
+@pytest.mark.gpu
+def test_embedding_backward_deterministic():
+    """SG_DETERMINISTIC=1: the embedding backward sums each row in token order (bit-identical
+    across calls) and matches the float64 index-add."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SG_DETERMINISTIC="1")
+    out = subprocess.run([sys.executable, "-c", _DET_EMBED], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    err, same = out.stdout.split()
+    assert float(err) < 1e-5 and same == "True", out.stdout
