@@ -1341,6 +1341,526 @@ __global__ void __launch_bounds__(512, 1)
 // ----------------------------------------------------------------------------
 constexpr uint32_t kT128 = 128 * 128 * 2;  // one 128 x 128 bf16 tile (2 atoms, 32 KB)
 
+// ----------------------------------------------------------------------------
+// Backward (d = 128), transposed orientation (round 2): the d = 64 design with the
+// shared-memory and TMEM budgets of 128-wide tiles. Per query block G of an item:
+//   S^T = K Q^T, dP^T = V dO^T (M = keys); P^T packed over the consumed scores of S^T,
+//   dS^T packed over dP^T (TS A operands of dV += P^T dO, dK += dS^T Q); dS once into
+//   shared memory as the MN-major A operand of dQ = dS K, whose accumulator reuses the
+//   dP^T columns after dK has read dS^T.
+// TMEM: S^T 0..127 | dP^T (dS^T, then dQ) 128..255 | dV 256..383 | dK 384..511.
+// Per block the MMA warp issues dV_G (as soon as P^T_G is in TMEM), S^T_G+1 (it
+// overwrites P^T_G after dV_G, in issue order), dK_G and dQ_G (once dS_G exists) and
+// dP^T_G+1 (once the drain warps have read dQ_G), so the exponentials of block G+1 run
+// while dK_G / dQ_G / dP^T_G+1 execute. Shared memory (226.75 KB): K 2 x 32 KB
+// (items), V 32 KB, Q 2 x 32 KB, dO 32 KB, dS 32 KB — the drain warps stage dQ and,
+// at an item's end, dK / dV through the dS buffer once dQ_G has read it (the softmax
+// warps write dS_G+1 after the drain released it).
+// ----------------------------------------------------------------------------
+constexpr int kMaxItems128 = 128;
+
+__global__ void __launch_bounds__(512, 1)
+    flash_bwd3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                      const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
+                      const __grid_constant__ CUtensorMap tmDV, const __grid_constant__ FlashBwdParams p, int bsz) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+  uint8_t* sK = smem;                   // 2 slots (items) x 2 atoms
+  uint8_t* sV = sK + 2 * kT128;         // 1 slot
+  uint8_t* sQ = sV + kT128;             // 2 slots (query blocks)
+  uint8_t* sDO = sQ + 2 * kT128;        // 1 slot
+  uint8_t* sDS = sDO + kT128;           // [keys x queries] 2 atoms; drain staging between uses
+  float* sStat = reinterpret_cast<float*>(sDS + kT128);  // 2 slots x [128 -lse log2e | 128 -D scale]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStat + 2 * 256);
+  int* items_tab = reinterpret_cast<int*>(bars + 32);
+  uint64_t* k_full = bars;          // [2]
+  uint64_t* k_empty = bars + 2;     // [2]
+  uint64_t* v_full = bars + 4;
+  uint64_t* v_empty = bars + 5;
+  uint64_t* q_full = bars + 6;      // [2]
+  uint64_t* q_empty = bars + 8;     // [2] dK_G done
+  uint64_t* do_full = bars + 10;
+  uint64_t* do_empty = bars + 11;   // dV_G done (dO free, P^T read)
+  uint64_t* s_full = bars + 12;
+  uint64_t* p_full = bars + 13;     // P^T_G in TMEM (8 softmax warps)
+  uint64_t* dp_full = bars + 14;
+  uint64_t* ds_full = bars + 15;    // dS^T_G in TMEM, dS_G in smem (8 softmax warps)
+  uint64_t* dq_full = bars + 16;    // dQ_G done (dS buffer no longer read by the MMA)
+  uint64_t* dq_empty = bars + 17;   // 4 drain warps: dQ_G read out of TMEM
+  uint64_t* stg_free = bars + 18;   // 4 drain warps: staging in the dS buffer read by the TMA
+  uint64_t* acc_full = bars + 19;
+  uint64_t* acc_empty = bars + 20;  // 4 drain warps
+  uint64_t* st_full = bars + 21;    // [2] statistics of block G in slot G & 1 (warp 3)
+  uint64_t* st_empty = bars + 23;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (p.s + 127) / 128;
+  const int nkb = nqb;
+  const int n_items = nkb * p.nh * bsz;
+  auto decode = [&](int t, int& kb, int& h, int& b) {
+    kb = t % nkb;
+    const int r = t / nkb;
+    h = r % p.nh;
+    b = r / p.nh + p.b0;
+  };
+  const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_items * nqb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmDQ);
+    tma_prefetch_desc(&tmDK);
+    tma_prefetch_desc(&tmDV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&st_full[i], 32);
+      mbar_init(&st_empty[i], 8);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(stg_free, 4);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  for (int it = threadIdx.x; it < my_items && it < kMaxItems128; it += blockDim.x) {
+    int kb, h, b;
+    decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
+    items_tab[it] = kb | (h << 10) | ((b - p.b0) << 20);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_begin();
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384, t_dq = tmem + 128;
+  auto item = [&](int it, int& kb, int& h, int& b) {
+    const int v = items_tab[it];
+    kb = v & 1023;
+    h = (v >> 10) & 1023;
+    b = (v >> 20) + p.b0;
+  };
+
+  if (warp == 0) {
+    reg_dealloc<56>();
+    if (lane == 0) {
+      int G = 0;
+      for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
+        int kb, h, b;
+        decode(t, kb, h, b);
+        const int ks = it & 1;
+        mbar_wait_sleep(&k_empty[ks], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[ks], kT128);
+#pragma unroll
+        for (int a = 0; a < 2; ++a) tma4(&tmK, sK + ks * kT128 + a * kT64, &k_full[ks], a * 64, kb * 128, h, b, p.k_b2_first);
+        for (int i = 0; i < nqb; ++i, ++G) {
+          {
+            // Q / dO of block G + 2 into L2 now
+            int i2 = i + 2, t2 = t, kb2 = kb, h2 = h, b2 = b;
+            while (i2 >= nqb) {
+              i2 -= nqb;
+              t2 += gridDim.x;
+            }
+            if (t2 != t && t2 < n_items) decode(t2, kb2, h2, b2);
+            if (t2 < n_items) {
+#pragma unroll
+              for (int a = 0; a < 2; ++a) {
+                tma4_l2(&tmQ, a * 64, i2 * 128, h2, b2, p.q_b2_first);
+                tma4_l2(&tmDO, a * 64, i2 * 128, h2, b2, p.do_b2_first);
+              }
+            }
+          }
+          const int qs = G & 1;
+          mbar_wait_sleep(&q_empty[qs], ((G >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], kT128);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tma4(&tmQ, sQ + qs * kT128 + a * kT64, &q_full[qs], a * 64, i * 128, h, b, p.q_b2_first);
+          if (i == 0) {
+            // this item's V once the previous item's last dP^T has read the slot
+            mbar_wait_sleep(v_empty, (it & 1) ^ 1);
+            mbar_arrive_expect_tx(v_full, kT128);
+#pragma unroll
+            for (int a = 0; a < 2; ++a) tma4(&tmV, sV + a * kT64, v_full, a * 64, kb * 128, h, b, p.v_b2_first);
+          }
+          mbar_wait_sleep(do_empty, (G & 1) ^ 1);
+          mbar_arrive_expect_tx(do_full, kT128);
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tma4(&tmDO, sDO + a * kT64, do_full, a * 64, i * 128, h, b, p.do_b2_first);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    reg_dealloc<56>();
+    {
+      // whole warp walks the loop (warp-uniform operands); one elected lane issues
+      constexpr uint32_t ID_ST = umma_idesc_bf16(128, 128, false, false);  // S^T, dP^T: K-major over d
+      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 128, false, true);   // dV, dK: A TMEM, B = dO / Q MN-major
+      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 128, true, true);    // dQ: A = dS MN-major, B = K MN-major
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t ts = tm, tdp = tm + 128, tdv = tm + 256, tdk = tm + 384;
+      constexpr uint64_t kAtom = kT64 >> 4, kTile = kT128 >> 4;
+      const uint64_t k_k = umma_desc_sw128(smem_u32(sK), 0, 1024), v_k = umma_desc_sw128(smem_u32(sV), 0, 1024);
+      const uint64_t q_k = umma_desc_sw128(smem_u32(sQ), 0, 1024), do_k = umma_desc_sw128(smem_u32(sDO), 0, 1024);
+      const uint64_t q_m = umma_desc_sw128(smem_u32(sQ), kT64, 1024), do_m = umma_desc_sw128(smem_u32(sDO), kT64, 1024);
+      const uint64_t k_m = umma_desc_sw128(smem_u32(sK), kT64, 1024), ds_m = umma_desc_sw128(smem_u32(sDS), kT64, 1024);
+      auto issue_s = [&](int G) {  // S^T_G = K Q_G^T
+        const int it = G / nqb;
+        if (G % nqb == 0) mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+        mbar_wait(&q_full[G & 1], (G >> 1) & 1);
+        tc_fence_after();
+        const uint64_t kd = k_k + (it & 1) * kTile, qd = q_k + (G & 1) * kTile;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {  // K-dim = d = 128: two atoms of 4 x 16
+            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
+            umma_bf16(ts, kd + off, qd + off, ID_ST, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(s_full);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int G) {  // dP^T_G = V dO_G^T
+        const int it = G / nqb;
+        if (G % nqb == 0) mbar_wait(v_full, it & 1);
+        mbar_wait(do_full, G & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
+            umma_bf16(tdp, v_k + off, do_k + off, ID_ST, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(dp_full);
+          if (G % nqb == nqb - 1) umma_commit(v_empty);  // the item's last dP^T: V may be reloaded
+        }
+        __syncwarp();
+      };
+      if (total > 0) {
+        issue_s(0);
+        issue_dp(0);
+      }
+      for (int G = 0; G < total; ++G) {
+        const int it = G / nqb, i = G % nqb;
+        mbar_wait(p_full, G & 1);  // P^T_G in TMEM (S^T_G read)
+        tc_fence_after();
+        if (i == 0 && it > 0) {  // the previous item's dK / dV read out
+          mbar_wait(acc_empty, (it - 1) & 1);
+          tc_fence_after();
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq)  // dV += P^T dO: 16 queries = 8 packed columns / 16 rows per step
+            umma_bf16_ts(tdv, ts + (kq >> 2) * 64 + (kq & 3) * 8, do_m + 128 * kq, ID_KV, (i | kq) != 0 ? 1u : 0u);
+          umma_commit(do_empty);  // dO_G free, P^T_G read
+        }
+        __syncwarp();
+        if (G + 1 < total) issue_s(G + 1);  // overwrites P^T_G after dV_G (issue order)
+        mbar_wait(ds_full, G & 1);  // dS^T_G in TMEM, dS_G in smem
+        tc_fence_after();
+        const uint64_t qm = q_m + (G & 1) * kTile, km = k_m + (it & 1) * kTile;
+        if (elect_one()) {
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq)  // dK += dS^T Q
+            umma_bf16_ts(tdk, tdp + (kq >> 2) * 64 + (kq & 3) * 8, qm + 128 * kq, ID_KV, (i | kq) != 0 ? 1u : 0u);
+          umma_commit(&q_empty[G & 1]);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // dQ = dS K into the dP^T columns (after dK read dS^T)
+            umma_bf16(tdp, ds_m + 128 * kk, km + 128 * kk, ID_DQ, kk > 0 ? 1u : 0u);
+          umma_commit(dq_full);
+          if (i == nqb - 1) {
+            umma_commit(acc_full);
+            umma_commit(&k_empty[it & 1]);
+          }
+        }
+        __syncwarp();
+        if (G + 1 < total) {
+          mbar_wait(dq_empty, G & 1);  // dQ_G read out of the dP^T columns
+          tc_fence_after();
+          issue_dp(G + 1);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    reg_dealloc<56>();
+    float v[8];
+    auto load = [&](int G, float (&x)[8]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = INFINITY;
+        x[4 + u] = 0.f;
+      }
+      if (G >= total) return;
+      int kb, h, b;
+      item(G / nqb, kb, h, b);
+      const size_t off = ((size_t)b * p.nh + h) * p.s;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int qrow = (G % nqb) * 128 + u * 32 + lane;
+        if (qrow < p.s) {
+          x[u] = __ldg(p.lse + off + qrow);
+          x[4 + u] = __ldg(p.drow + off + qrow);
+        }
+      }
+    };
+    load(0, v);
+    for (int G = 0; G < total; ++G) {
+      float* t = sStat + (G & 1) * 256;
+      if (G >= 2) mbar_wait_sleep(&st_empty[G & 1], ((G - 2) >> 1) & 1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        t[u * 32 + lane] = -v[u] * 1.4426950408889634f;
+        t[128 + u * 32 + lane] = -v[4 + u] * p.scale;
+      }
+      mbar_arrive(&st_full[G & 1]);
+      load(G + 1, v);
+    }
+  } else if (warp < 4) {
+    reg_dealloc<56>();
+  } else if (warp < 12) {
+    reg_alloc<160>();
+    const int e = warp - 4;
+    const int q = e & 3, hq = e >> 2;
+    const int r = q * 32 + lane;  // key row of the block
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const float scale = p.scale;
+    int it = 0, i = 0;
+    int kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
+    const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2), sc2 = f2_pack(scale, scale);
+    for (int G = 0; G < total; ++G) {
+      const int kvalid = min(128, p.s - kb * 128);
+      const float* st = sStat + (G & 1) * 256 + hq * 64;
+      mbar_wait_sleep(s_full, G & 1);
+      mbar_wait_sleep(&st_full[G & 1], (G >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[64];
+      tmem_ld32(t_s + lane_base + hq * 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+      tmem_ld32(t_s + lane_base + hq * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+      tmem_wait_ld();
+      uint32_t pk[32];
+      const bool key_ok = r < kvalid;
+#pragma unroll
+      for (int j4 = 0; j4 < 16; ++j4) {
+        const float4 nl = *reinterpret_cast<const float4*>(st + 4 * j4);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = 2 * j4 + u;
+          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sl2,
+                                   u ? f2_pack(nl.z, nl.w) : f2_pack(nl.x, nl.y));
+          const float p0 = ex2f_fast(f2_lo(y)), p1 = ex2f_fast(f2_hi(y));
+          sv[2 * j] = __float_as_uint(p0);
+          sv[2 * j + 1] = __float_as_uint(p1);
+          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
+          pk[j] = *reinterpret_cast<uint32_t*>(&hp);
+        }
+      }
+      if (kvalid < 128 && !key_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sv[2 * j] = sv[2 * j + 1] = 0u;
+          pk[j] = 0u;
+        }
+      }
+      // P^T packed over this thread's own (already read) score columns
+      tmem_st32(t_s + lane_base + hq * 64, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      mbar_wait_sleep(dp_full, G & 1);
+      tc_fence_after();
+      uint32_t dk[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld32(t_dp + lane_base + hq * 64 + c * 32, dv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 nd = *reinterpret_cast<const float4*>(st + 128 + c * 32 + 4 * j4);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = 2 * j4 + u;
+            const uint64_t t = ffma2(f2_pack(__uint_as_float(dv[2 * j]), __uint_as_float(dv[2 * j + 1])), sc2,
+                                     u ? f2_pack(nd.z, nd.w) : f2_pack(nd.x, nd.y));
+            const uint64_t ds =
+                fmul2(f2_pack(__uint_as_float(sv[c * 32 + 2 * j]), __uint_as_float(sv[c * 32 + 2 * j + 1])), t);
+            __nv_bfloat162 hd = __floats2bfloat162_rn(f2_lo(ds), f2_hi(ds));
+            dk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&hd);
+          }
+        }
+      }
+      tmem_st32(t_dp + lane_base + hq * 64, dk);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[G & 1]);
+      if (G > 0) mbar_wait_sleep(stg_free, (G - 1) & 1);  // the drain warps released the dS buffer
+      uint8_t* drow_ = sDS + hq * kT64 + r * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<uint4*>(drow_ + ((k ^ (r & 7)) << 4)) =
+            make_uint4(dk[4 * k], dk[4 * k + 1], dk[4 * k + 2], dk[4 * k + 3]);
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (i == nqb - 1) {
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
+      }
+    }
+  } else {
+    // 4 drain warps (lane quadrant q): dQ_G (TMEM dP^T columns -> fp32 boxes in this warp's
+    // 8 KB of the dS buffer -> TMA reduce-add), at an item's end dK / dV (bf16 boxes ->
+    // TMA stores, bias-gradient column sums); then the dS buffer is released
+    reg_alloc<128>();
+    const int q = warp & 3;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sDS + (warp - 12) * 8192;
+    int it = 0, i = 0, kb = 0, h = 0, b = 0;
+    if (my_items > 0) item(0, kb, h, b);
+    for (int G = 0; G < total; ++G) {
+      mbar_wait_sleep(dq_full, G & 1);  // dQ_G done: the MMA no longer reads dS_G
+      tc_fence_after();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        uint32_t v[2][32];
+        tmem_ld32(t_dq + lane_base + half * 64, v[0]);
+        tmem_ld32(t_dq + lane_base + half * 64 + 32, v[1]);
+        tmem_wait_ld();
+        if (half == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);  // dP^T_G+1 may overwrite the columns
+        }
+        if (lane == 0) bulk_wait_read<0>();  // the boxes' previous reduce-adds have read them
+        __syncwarp();
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          uint8_t* box = stg + hf * 4096;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(v[hf][4 * k]), __uint_as_float(v[hf][4 * k + 1]),
+                            __uint_as_float(v[hf][4 * k + 2]), __uint_as_float(v[hf][4 * k + 3]));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int col = half * 64 + hf * 32;
+            if (p.dq_b2_first)
+              tma_reduce_add_4d(&tmDQ, stg + hf * 4096, col, h, i * 128 + q * 32, b);
+            else
+              tma_reduce_add_4d(&tmDQ, stg + hf * 4096, col, i * 128 + q * 32, h, b);
+          }
+          bulk_commit();
+        }
+      }
+      if (i == nqb - 1) {
+        mbar_wait_sleep(acc_full, it & 1);
+        tc_fence_after();
+        const int key0 = kb * 128 + q * 32;
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {
+          // 128 columns as four SW64 32 x 32 bf16 tiles (2 KB each) in this warp's 8 KB
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            uint32_t v2[2][32];
+            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + half * 64, v2[0]);
+            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + half * 64 + 32, v2[1]);
+            tmem_wait_ld();
+            if (which == 1 && half == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
+            }
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              uint8_t* row = stg + (half * 2 + hf) * 2048 + lane * 64;
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) {
+                uint4 x;
+                __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2)
+                  hh[e2] = __floats2bfloat162_rn(__uint_as_float(v2[hf][8 * k2 + 2 * e2]),
+                                                 __uint_as_float(v2[hf][8 * k2 + 2 * e2 + 1]));
+                *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const CUtensorMap* tmap = which == 0 ? &tmDK : &tmDV;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (p.dkv_b2_first)
+                tma_store_4d(tmap, stg + c * 2048, c * 32, h, key0, b);
+              else
+                tma_store_4d(tmap, stg + c * 2048, c * 32, key0, h, b);
+            }
+            bulk_commit();
+          }
+          if (p.kv_colsum) {
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              const uint8_t* tile = stg + c * 2048;
+              float acc2[2] = {0.f, 0.f};
+#pragma unroll
+              for (int i2 = 0; i2 < 32; ++i2) {
+                const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
+                acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
+              }
+              atomicAdd(p.kv_colsum + which * p.nh * 128 + h * 128 + c * 32 + lane, acc2[0] + acc2[1]);
+            }
+          }
+        }
+      }
+      // release the dS buffer once every staged box has been read by its TMA operation
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(stg_free);
+      if (i == nqb - 1) {
+        i = 0;
+        ++it;
+        if (it < my_items) item(it, kb, h, b);
+      } else {
+        ++i;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 __global__ void __launch_bounds__(512, 1)
     flash_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
@@ -1778,20 +2298,26 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
   constexpr size_t SMEM64 = (3 + 2 * kQD + 2) * kT64 + 4 * 8192 + 2 * 1024 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
+  constexpr size_t SMEM128T = 7 * kT128 + 2 * 1024 + 256 + kMaxItems128 * 4;
+  static const bool v1_128 = getenv("SG_FLASH_BWD128_V1") != nullptr;  // A/B experiments
+  const bool t128 = d == 128 && !v1_128;
   const int nkb = (int)((s + 127) / 128);
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
   if (nkb > 1024 || nh > 1024) return set_error(SG_ERR_SHAPE, "flash bwd: more than 1024 key blocks / heads");
   // sequences per launch: every CTA's items must fit its item table (large batches run
   // as several back-to-back launches over batch chunks)
   const long long per_seq = (long long)nkb * nh;
-  long long max_items = (long long)kMaxItems * sms;
+  const long long table = t128 ? kMaxItems128 : kMaxItems;  // per-CTA item table entries
+  long long max_items = table * sms;
   if (const char* e = getenv("SG_FLASH_ITEMS_MAX")) max_items = std::max(1LL, std::min(max_items, atoll(e)));  // tests
   const int chunk = (int)std::max<long long>(1, std::min<long long>(2047, max_items / per_seq));
-  if (per_seq > (long long)kMaxItems * sms) return set_error(SG_ERR_SHAPE, "flash bwd: one sequence exceeds the item table");
+  if (per_seq > table * sms) return set_error(SG_ERR_SHAPE, "flash bwd: one sequence exceeds the item table");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const void* kern = d == 64 ? reinterpret_cast<const void*>(flash_bwd2_kernel<kBwdPoly>)
+                     : t128  ? reinterpret_cast<const void*>(flash_bwd3_kernel)
                              : reinterpret_cast<const void*>(flash_bwd128_kernel);
-  if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : SMEM128))) return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
+  if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : t128 ? SMEM128T : SMEM128)))
+    return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
   for (long long b0 = 0; b0 < b; b0 += chunk) {
     const int bc = (int)std::min<long long>(chunk, b - b0);
     const int items = (int)(per_seq * bc);
@@ -1799,6 +2325,9 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
     if (d == 64)
       launch_k(flash_bwd2_kernel<kBwdPoly>, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq,
                tdk, tdv, p, bc);
+    else if (t128)
+      launch_k(flash_bwd3_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128T, st, tq, tk, tv, tdo, tdq, tdk,
+               tdv, p, bc);
     else
       launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk,
                tdv, p, bc);
