@@ -6,7 +6,7 @@
 // tiles per CTA ping-ponging on the tensor core, P in TMEM as the A operand of PV,
 // O accumulated in TMEM; outputs O (bf16) into the interleaved context block and the
 // row log-sum-exp (fp32) for the backward. Backward: flash_bwd2_kernel (d = 64,
-// transposed orientation) and flash_bwd128_kernel (d = 128). Q/K/V are read in place
+// transposed orientation) and flash_bwd3_kernel (d = 128, transposed). Q/K/V are read in place
 // from the QKV block through 4-D TMA maps (no head split copies).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -1325,20 +1325,6 @@ __global__ void __launch_bounds__(512, 1)
 }
 
 
-// ----------------------------------------------------------------------------
-// Backward, d = 128 (the GPT configs), persistent over work items t = (key block,
-// head, batch) like bwd2. TMEM holds S | dP | dV | dK (4 x 128 columns), so the
-// 128-column dQ product of a query block is written into the S columns once the
-// softmax warps have read S (ds_full), drained by the drain warps while dV / dK
-// run, and the next block's S waits for that drain. Shared memory (224 KB): K, V,
-// Q, dO, P, dS as 128 x 128 bf16 tiles (two SWIZZLE_128B atoms along the 128-wide
-// dimension) and 4 x 8 KB drain staging; Q / dO are single-buffered, with the next
-// block's tiles prefetched into L2 a block ahead. Per query block:
-//   MMA    dP_G = dO_G V^T, S_G = Q_G K^T                 (M = queries, N = keys)
-//   warps 4-11 (lane quadrant x key half): P, dS -> smem    (as bwd2)
-//   MMA    dQ_G = dS K -> S columns; dV += P^T dO; dK += dS^T Q
-//   warps 12-15 dQ_G: TMEM -> fp32 staging -> TMA reduce-add; dK / dV at item end
-// ----------------------------------------------------------------------------
 constexpr uint32_t kT128 = 128 * 128 * 2;  // one 128 x 128 bf16 tile (2 atoms, 32 KB)
 
 // ----------------------------------------------------------------------------
@@ -1861,405 +1847,6 @@ __global__ void __launch_bounds__(512, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-__global__ void __launch_bounds__(512, 1)
-    flash_bwd128_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-                        const __grid_constant__ CUtensorMap tmDQ, const __grid_constant__ CUtensorMap tmDK,
-                        const __grid_constant__ CUtensorMap tmDV, const __grid_constant__ FlashBwdParams p, int bsz) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  if ((smem_u32(smem_raw) & 1023) != 0) __trap();
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + kT128;
-  uint8_t* sQ = sV + kT128;
-  uint8_t* sDO = sQ + kT128;
-  uint8_t* sP = sDO + kT128;
-  uint8_t* sDS = sP + kT128;
-  uint8_t* sStg = sDS + kT128;  // 4 drain warps x 8 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 4 * 8192);
-  int* items_tab = reinterpret_cast<int*>(bars + 32);
-  uint64_t* kv_full = bars;
-  uint64_t* kv_empty = bars + 1;
-  uint64_t* q_full = bars + 2;
-  uint64_t* q_empty = bars + 3;
-  uint64_t* do_full = bars + 4;
-  uint64_t* do_empty = bars + 5;
-  uint64_t* s_full = bars + 6;
-  uint64_t* ds_full = bars + 7;
-  uint64_t* bufs_free = bars + 8;
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_empty = bars + 10;
-  uint64_t* acc_full = bars + 11;
-  uint64_t* acc_empty = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (p.s + 127) / 128;
-  const int nkb = nqb;
-  const int n_items = nkb * p.nh * bsz;
-  auto decode = [&](int t, int& kb, int& h, int& b) {
-    kb = t % nkb;
-    const int r = t / nkb;
-    h = r % p.nh;
-    b = r / p.nh + p.b0;
-  };
-  const int my_items = n_items > (int)blockIdx.x ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int total = my_items * nqb;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    tma_prefetch_desc(&tmDO);
-    tma_prefetch_desc(&tmDQ);
-    tma_prefetch_desc(&tmDK);
-    tma_prefetch_desc(&tmDV);
-    for (uint64_t* bar : {kv_full, kv_empty, q_full, q_empty, do_full, do_empty, s_full, bufs_free, dq_full, acc_full})
-      mbar_init(bar, 1);
-    mbar_init(ds_full, 8);
-    mbar_init(dq_empty, 4);
-    mbar_init(acc_empty, 4);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  for (int it = threadIdx.x; it < my_items && it < kMaxItems; it += blockDim.x) {
-    int kb, h, b;
-    decode((int)blockIdx.x + it * (int)gridDim.x, kb, h, b);
-    items_tab[it] = kb | (h << 10) | ((b - p.b0) << 20);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_begin();
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384, t_dq = t_s;
-  auto item = [&](int it, int& kb, int& h, int& b) {
-    const int v = items_tab[it];
-    kb = v & 1023;
-    h = (v >> 10) & 1023;
-    b = (v >> 20) + p.b0;
-  };
-
-  if (warp == 0) {
-    reg_dealloc<56>();
-    if (lane == 0) {
-      int G = 0;
-      for (int t = blockIdx.x, it = 0; t < n_items; t += gridDim.x, ++it) {
-        int kb, h, b;
-        decode(t, kb, h, b);
-        mbar_wait(kv_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(kv_full, 2 * kT128);
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          tma4(&tmK, sK + a * kT64, kv_full, a * 64, kb * 128, h, b, p.k_b2_first);
-          tma4(&tmV, sV + a * kT64, kv_full, a * 64, kb * 128, h, b, p.v_b2_first);
-        }
-        for (int i = 0; i < nqb; ++i, ++G) {
-          {
-            // the next block's Q / dO into L2 while this block's products run
-            int i2 = i + 1, t2 = t, kb2 = kb, h2 = h, b2 = b;
-            if (i2 >= nqb) {
-              i2 = 0;
-              t2 += gridDim.x;
-            }
-            if (t2 != t && t2 < n_items) decode(t2, kb2, h2, b2);
-            if (t2 < n_items) {
-#pragma unroll
-              for (int a = 0; a < 2; ++a) {
-                tma4_l2(&tmQ, a * 64, i2 * 128, h2, b2, p.q_b2_first);
-                tma4_l2(&tmDO, a * 64, i2 * 128, h2, b2, p.do_b2_first);
-              }
-            }
-          }
-          mbar_wait(do_empty, (G & 1) ^ 1);
-          mbar_arrive_expect_tx(do_full, kT128);
-#pragma unroll
-          for (int a = 0; a < 2; ++a) tma4(&tmDO, sDO + a * kT64, do_full, a * 64, i * 128, h, b, p.do_b2_first);
-          mbar_wait(q_empty, (G & 1) ^ 1);
-          mbar_arrive_expect_tx(q_full, kT128);
-#pragma unroll
-          for (int a = 0; a < 2; ++a) tma4(&tmQ, sQ + a * kT64, q_full, a * 64, i * 128, h, b, p.q_b2_first);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    reg_dealloc<56>();
-    {
-      // whole warp walks the loop (warp-uniform operands); one elected lane issues
-      constexpr uint32_t ID_SQ = umma_idesc_bf16(128, 128, false, false);  // S, dP: A, B K-major (over d)
-      constexpr uint32_t ID_KV = umma_idesc_bf16(128, 128, true, true);    // dV, dK: A = P^T / dS^T, B = dO / Q
-      constexpr uint32_t ID_DQ = umma_idesc_bf16(128, 128, false, true);   // dQ: A = dS (K-major), B = K (MN-major)
-      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      const uint32_t ts = tm, tdp = tm + 128, tdv = tm + 256, tdk = tm + 384, tdq = tm;
-      // K-major descriptors (K steps: 32 B = 2 units inside an atom, next atom kT64 >> 4),
-      // MN-major ones (K steps of 16 rows = 2048 B = 128 units, LBO = one atom)
-      const uint64_t k_k = umma_desc_sw128(smem_u32(sK), 0, 1024), v_k = umma_desc_sw128(smem_u32(sV), 0, 1024);
-      const uint64_t q_k = umma_desc_sw128(smem_u32(sQ), 0, 1024), do_k = umma_desc_sw128(smem_u32(sDO), 0, 1024);
-      const uint64_t ds_k = umma_desc_sw128(smem_u32(sDS), 0, 1024);
-      const uint64_t k_m = umma_desc_sw128(smem_u32(sK), kT64, 1024), p_m = umma_desc_sw128(smem_u32(sP), kT64, 1024);
-      const uint64_t do_m = umma_desc_sw128(smem_u32(sDO), kT64, 1024), ds_m = umma_desc_sw128(smem_u32(sDS), kT64, 1024);
-      const uint64_t q_m = umma_desc_sw128(smem_u32(sQ), kT64, 1024);
-      constexpr uint64_t kAtom = kT64 >> 4;
-      for (int G = 0; G < total; ++G) {
-        const int it = G / nqb, i = G % nqb;
-        if (i == 0) mbar_wait(kv_full, it & 1);
-        if (G > 0) mbar_wait(dq_empty, (G - 1) & 1);  // dQ_G-1 drained from the S columns
-        mbar_wait(do_full, G & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {  // K-dim = d = 128: two atoms of 4 x 16
-            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
-            umma_bf16(tdp, do_k + off, v_k + off, ID_SQ, kk > 0 ? 1u : 0u);
-          }
-        }
-        __syncwarp();
-        mbar_wait(q_full, G & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t off = (kk >> 2) * kAtom + (kk & 3) * 2;
-            umma_bf16(ts, q_k + off, k_k + off, ID_SQ, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(s_full);
-        }
-        __syncwarp();
-        mbar_wait(ds_full, G & 1);  // S / dP read, P / dS in smem
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)  // K-dim = 128 keys: dS K-major (2 atoms), K tile MN-major
-            umma_bf16(tdq, ds_k + (kk >> 2) * kAtom + (kk & 3) * 2, k_m + kk * 128, ID_DQ, kk > 0 ? 1u : 0u);
-          umma_commit(dq_full);
-        }
-        __syncwarp();
-        if (i == 0 && it > 0) {
-          mbar_wait(acc_empty, (it - 1) & 1);  // the previous item's dK / dV were read out
-          tc_fence_after();
-        }
-        if (elect_one()) {
-#pragma unroll
-          for (int kq = 0; kq < 8; ++kq)  // K-dim = 128 queries: 16 rows = 2048 B per step
-            umma_bf16(tdv, p_m + kq * 128, do_m + kq * 128, ID_KV, (i | kq) != 0 ? 1u : 0u);
-          umma_commit(do_empty);
-#pragma unroll
-          for (int kq = 0; kq < 8; ++kq)
-            umma_bf16(tdk, ds_m + kq * 128, q_m + kq * 128, ID_KV, (i | kq) != 0 ? 1u : 0u);
-          umma_commit(q_empty);
-          umma_commit(bufs_free);
-          if (i == nqb - 1) {
-            umma_commit(acc_full);
-            umma_commit(kv_empty);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp < 4) {
-    reg_dealloc<56>();
-  } else if (warp < 12) {
-    reg_alloc<176>();
-    const int e = warp - 4;
-    const int q = e & 3, half = e >> 2;
-    const int r = q * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    const float scale = p.scale, scale_log2 = p.scale_log2;
-    auto row_stats = [&](int it, int i, float& lse, float& dd) {
-      lse = dd = 0.f;
-      if (it >= my_items) return;
-      int kb, h, b;
-      item(it, kb, h, b);
-      const int qrow = i * 128 + r;
-      if (qrow >= p.s) return;
-      const size_t off = ((size_t)b * p.nh + h) * p.s + qrow;
-      lse = __ldg(p.lse + off);
-      dd = __ldg(p.drow + off);
-    };
-    float lse_n, dd_n;
-    row_stats(0, 0, lse_n, dd_n);
-    int it = 0, i = 0;
-    int kb = 0, h = 0, b = 0;
-    if (my_items > 0) item(0, kb, h, b);
-    for (int G = 0; G < total; ++G) {
-      const int kvalid = min(128, p.s - kb * 128);
-      const bool full_keys = kvalid == 128;
-      const float lse_c = lse_n, dd = dd_n;
-      {
-        const int ni = i + 1 == nqb ? 0 : i + 1, nit = i + 1 == nqb ? it + 1 : it;
-        row_stats(nit, ni, lse_n, dd_n);
-      }
-      const bool qok = i * 128 + r < p.s;
-      mbar_wait(s_full, G & 1);
-      tc_fence_after();
-      const float lse2 = lse_c * 1.4426950408889634f;
-      uint32_t pk[2][16], dk[2][16];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
-        uint32_t sv[32], dv[32];
-        tmem_ld32(t_s + lane_base + c * 32, sv);
-        tmem_ld32(t_dp + lane_base + c * 32, dv);
-        tmem_wait_ld();
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nl2 = f2_pack(-lse2, -lse2);
-        const uint64_t nd2 = f2_pack(-dd, -dd), ss2 = f2_pack(scale, scale);
-#pragma unroll
-        for (int e2 = 0; e2 < 16; ++e2) {
-          const uint64_t y = ffma2(f2_pack(__uint_as_float(sv[2 * e2]), __uint_as_float(sv[2 * e2 + 1])), sc2, nl2);
-          float p0 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y)));
-          float p1 = ex2f_fast(__uint_as_float(static_cast<uint32_t>(y >> 32)));
-          if (!full_keys || !qok) {
-            if (!qok || c * 32 + 2 * e2 >= kvalid) p0 = 0.f;
-            if (!qok || c * 32 + 2 * e2 + 1 >= kvalid) p1 = 0.f;
-          }
-          const uint64_t pp = f2_pack(p0, p1);
-          const uint64_t dmd = fadd2(f2_pack(__uint_as_float(dv[2 * e2]), __uint_as_float(dv[2 * e2 + 1])), nd2);
-          const uint64_t ds = fmul2(fmul2(pp, ss2), dmd);
-          __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1);
-          __nv_bfloat162 hd = __floats2bfloat162_rn(__uint_as_float(static_cast<uint32_t>(ds)),
-                                                   __uint_as_float(static_cast<uint32_t>(ds >> 32)));
-          pk[cc][e2] = *reinterpret_cast<uint32_t*>(&hp);
-          dk[cc][e2] = *reinterpret_cast<uint32_t*>(&hd);
-        }
-      }
-      if (G > 0) mbar_wait(bufs_free, (G - 1) & 1);  // block G-1's products have read P / dS
-      uint8_t* prow = sP + half * kT64 + r * 128;
-      uint8_t* drow_ = sDS + half * kT64 + r * 128;
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = (cc * 4 + k) ^ (r & 7);
-          *reinterpret_cast<uint4*>(prow + (chunk << 4)) =
-              make_uint4(pk[cc][4 * k], pk[cc][4 * k + 1], pk[cc][4 * k + 2], pk[cc][4 * k + 3]);
-          *reinterpret_cast<uint4*>(drow_ + (chunk << 4)) =
-              make_uint4(dk[cc][4 * k], dk[cc][4 * k + 1], dk[cc][4 * k + 2], dk[cc][4 * k + 3]);
-        }
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
-      if (i == nqb - 1) {
-        i = 0;
-        ++it;
-        if (it < my_items) item(it, kb, h, b);
-      } else {
-        ++i;
-      }
-    }
-  } else {
-    // 4 drain warps (lane quadrant q, 32 rows): dQ of every block in four 32-column
-    // fp32 chunks through two 4 KB staging buffers; dK / dV at each item's end as
-    // 32 x 32 bf16 tiles (4 per tensor)
-    reg_dealloc<96>();
-    const int q = warp & 3;
-    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sStg + (warp - 12) * 8192;
-    int it = 0, i = 0, kb = 0, h = 0, b = 0;
-    if (my_items > 0) item(0, kb, h, b);
-    for (int G = 0; G < total; ++G) {
-      mbar_wait(dq_full, G & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_dq + lane_base + c * 32, v);
-        tmem_wait_ld();
-        if (c == 3) {  // all of dQ_G in registers / staging: the S columns may take the next scores
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dq_empty);
-        }
-        if (lane == 0) bulk_wait_read<1>();  // the reduce-add two chunks back has read this buffer
-        __syncwarp();
-        uint8_t* box = stg + (c & 1) * 4096;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          *reinterpret_cast<float4*>(box + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
-                          __uint_as_float(v[4 * k + 3]));
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (p.dq_b2_first)
-            tma_reduce_add_4d(&tmDQ, box, c * 32, h, i * 128 + q * 32, b);
-          else
-            tma_reduce_add_4d(&tmDQ, box, c * 32, i * 128 + q * 32, h, b);
-          bulk_commit();
-        }
-      }
-      if (i == nqb - 1) {
-        mbar_wait(acc_full, it & 1);
-        tc_fence_after();
-        const int key0 = kb * 128 + q * 32;
-#pragma unroll 1
-        for (int which = 0; which < 2; ++which) {
-          if (lane == 0) bulk_wait_read<0>();  // earlier TMA operations have read the staging
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t w[32];
-            tmem_ld32((which == 0 ? t_dk : t_dv) + lane_base + c * 32, w);
-            tmem_wait_ld();
-            if (which == 1 && c == 3) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(acc_empty);  // the next item's dK / dV may overwrite TMEM
-            }
-            uint8_t* row = stg + c * 2048 + lane * 64;
-#pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2) {
-              uint4 x;
-              __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&x);
-#pragma unroll
-              for (int e2 = 0; e2 < 4; ++e2)
-                hh[e2] = __floats2bfloat162_rn(__uint_as_float(w[8 * k2 + 2 * e2]),
-                                               __uint_as_float(w[8 * k2 + 2 * e2 + 1]));
-              *reinterpret_cast<uint4*>(row + ((k2 ^ ((lane >> 1) & 3)) << 4)) = x;
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            const CUtensorMap* tm = which == 0 ? &tmDK : &tmDV;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              if (p.dkv_b2_first)
-                tma_store_4d(tm, stg + c * 2048, c * 32, h, key0, b);
-              else
-                tma_store_4d(tm, stg + c * 2048, c * 32, key0, h, b);
-            }
-            bulk_commit();
-          }
-          if (p.kv_colsum) {
-            // bias-gradient column sums from the staged bf16 tiles (rows past s are zero)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint8_t* tile = stg + c * 2048;
-              float acc2[2] = {0.f, 0.f};
-#pragma unroll
-              for (int i2 = 0; i2 < 32; ++i2) {
-                const int off = i2 * 64 + ((((lane >> 3) ^ ((i2 >> 1) & 3))) << 4) + (lane & 7) * 2;
-                acc2[i2 & 1] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
-              }
-              atomicAdd(p.kv_colsum + which * p.nh * 128 + h * 128 + c * 32 + lane, acc2[0] + acc2[1]);
-            }
-          }
-        }
-        i = 0;
-        ++it;
-        if (it < my_items) item(it, kb, h, b);
-      } else {
-        ++i;
-      }
-    }
-    if (lane == 0) bulk_wait_all();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc<512>(tmem);
-}
 
 }  // namespace sg
 
@@ -2297,10 +1884,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   // d = 64: 2 K, V, kQD Q, kQD dO, dS (2 atoms), 4 x 8 KB staging, 8 x 512 B statistics;
   // d = 128: K, V, Q, dO, P, dS as 32 KB tiles, 4 x 8 KB staging
   constexpr size_t SMEM64 = (3 + 2 * kQD + 2) * kT64 + 4 * 8192 + 2 * 1024 + 256 + kMaxItems * 4;
-  constexpr size_t SMEM128 = 6 * kT128 + 4 * 8192 + 256 + kMaxItems * 4;
   constexpr size_t SMEM128T = 7 * kT128 + 2 * 1024 + 256 + kMaxItems128 * 4;
-  static const bool v1_128 = getenv("SG_FLASH_BWD128_V1") != nullptr;  // A/B experiments
-  const bool t128 = d == 128 && !v1_128;
+  const bool t128 = d == 128;
   const int nkb = (int)((s + 127) / 128);
   const int sms = sg_device_sm_count() > 0 ? sg_device_sm_count() : 148;
   if (nkb > 1024 || nh > 1024) return set_error(SG_ERR_SHAPE, "flash bwd: more than 1024 key blocks / heads");
@@ -2314,9 +1899,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
   if (per_seq > table * sms) return set_error(SG_ERR_SHAPE, "flash bwd: one sequence exceeds the item table");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const void* kern = d == 64 ? reinterpret_cast<const void*>(flash_bwd2_kernel<kBwdPoly>)
-                     : t128  ? reinterpret_cast<const void*>(flash_bwd3_kernel)
-                             : reinterpret_cast<const void*>(flash_bwd128_kernel);
-  if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : t128 ? SMEM128T : SMEM128)))
+                             : reinterpret_cast<const void*>(flash_bwd3_kernel);
+  if (!ensure_smem(kern, (int)(d == 64 ? SMEM64 : SMEM128T)))
     return set_error(SG_ERR_CUDA, "flash bwd: smem attribute");
   for (long long b0 = 0; b0 < b; b0 += chunk) {
     const int bc = (int)std::min<long long>(chunk, b - b0);
@@ -2325,11 +1909,8 @@ extern "C" int sg_flash_attn_bwd(const void* qkv, int64_t ldq, const void* dout,
     if (d == 64)
       launch_k(flash_bwd2_kernel<kBwdPoly>, dim3(std::min(items, sms)), dim3(512), SMEM64, st, tq, tk, tv, tdo, tdq,
                tdk, tdv, p, bc);
-    else if (t128)
-      launch_k(flash_bwd3_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128T, st, tq, tk, tv, tdo, tdq, tdk,
-               tdv, p, bc);
     else
-      launch_k(flash_bwd128_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128, st, tq, tk, tv, tdo, tdq, tdk,
+      launch_k(flash_bwd3_kernel, dim3(std::min(items, sms)), dim3(512), SMEM128T, st, tq, tk, tv, tdo, tdq, tdk,
                tdv, p, bc);
     count_launch();
   }
