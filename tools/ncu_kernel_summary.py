@@ -28,7 +28,7 @@ def summarize(rep):
         try:
             x = float(v.replace(",", ""))
             if k == "gpu__time_duration.sum":
-                x = x / 1000.0 if u.get(k) in ("nsecond", "ns") else (x * 1000.0 if u.get(k) == "msecond" else x)
+                x = x / 1000.0 if u.get(k) in ("nsecond", "ns") else (x * 1000.0 if u.get(k) in ("msecond", "ms") else x)
             res[name] = f"{x:.2f}"
         except ValueError:
             res[name] = "n/a"
