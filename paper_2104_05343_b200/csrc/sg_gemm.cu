@@ -981,8 +981,15 @@ static int make_map(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, i
     strides[0] = ld * esz; strides[1] = s2 * esz; strides[2] = s1 * esz;
     box[1] = box_outer; box[2] = 1; box[3] = 1;
   }
+  static const CUtensorMapL2promotion promo = [] {  // SG_TMA_L2_PROMOTION=0/64/128/256 (experiments)
+    const char* e = getenv("SG_TMA_L2_PROMOTION");
+    const int v = e ? atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+           : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   CUresult r = enc(map, dt, 4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char msg[256];
     snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (%d): dims %lld,%lld,%lld,%lld ld=%lld s2=%lld s1=%lld",
