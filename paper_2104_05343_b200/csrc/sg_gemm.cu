@@ -68,6 +68,12 @@ struct GemmParams {
   int k_splits, kb_per_split;   // split-K: work unit = (split, tile), partial sums reduce-added into D
   int full_units;               // units >= full_units are half-width (BN / 2) tiles of the last round
   int group_m, group_shift;     // rasterisation: groups of group_m (= 1 << group_shift) m-tiles
+  // die-local tile streams (large pair-tile products): the CTA pairs of each of the two
+  // dies take alternate 8-m-tile halves of every 16-m-tile group, so A rows are shared
+  // by pairs of one die (whose L2 then fetches them once); pair c works on die die_of[c]
+  // as its slot_of[c]-th pair (a bijection measured once per device, sg_gemm_die_table)
+  int die_mode, die_pairs;
+  uint8_t die_of[128], slot_of[128];
   int a_b2_first, b_b2_first, o_b2_first, x_b2_first, c_b2_first;
   int mode;
   int d_f32;
@@ -360,6 +366,18 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  // this pair's unit stream: units u0, u0 + ustep, ... < ucount, tile tile_of(u)
+  const bool dm = PAIR && p.die_mode;
+  const int udie = dm ? p.die_of[unit0] : 0;
+  const int u0 = dm ? p.slot_of[unit0] : unit0, ustep = dm ? p.die_pairs : nunits;
+  const int ucount = dm ? (p.num_tiles >> 1) : p.num_tiles;
+  auto tile_of = [&](int u) -> int {
+    if (!dm) return u;
+    const int hs = p.group_shift - 1, hg = 1 << hs;  // this die's half of a group: hg m-tiles
+    const int per_g = hg * p.n_tiles;
+    const int g = u / per_g, r = u - g * per_g;
+    return (g * p.n_tiles + (r >> hs)) * p.group_m + udie * hg + (r & (hg - 1));  // the standard grouped order's index
+  };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -414,7 +432,8 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       // ------------------------------------------------------------ producer
       // whole warp walks the loop (warp-uniform coordinates); one elected lane issues
       uint32_t stage = 0, phase = 0;
-      for (int t = unit0; t < p.num_tiles; t += nunits) {
+      for (int u = u0; u < ucount; u += ustep) {
+        const int t = tile_of(u);
         int mb, nb, z1, z2, half;
         decode_unit(p, t, mb, nb, z1, z2, half);
         int kb0, kb1;
@@ -495,7 +514,8 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), B_MN ? kBK * 128 : 0, 1024);
       const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
       uint32_t stage = 0, phase = 0, it = 0;
-      for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
+      for (int u = u0; u < ucount; u += ustep, ++it) {
+        const int t = tile_of(u);
         const uint32_t IDESC = (PAIR && t >= p.full_units) ? IDESC_HALF : IDESC_FULL;
         const uint32_t as = it % ACC, aph = (it / ACC) & 1;
         if (PAIR)
@@ -607,7 +627,8 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
       }
     };
     bool pref_next = false;  // the next tile's first chunk input is in flight
-    for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {
+    for (int u = u0; u < ucount; u += ustep, ++it) {
+      const int t = tile_of(u);
       int mb, nb, z1, z2, half;
       decode_unit(p, t, mb, nb, z1, z2, half);
       const int ncol = half < 0 ? nb * BN : nb * BN + half * (BN / 2);  // first column of the unit
@@ -851,9 +872,9 @@ __global__ void __launch_bounds__(EpiCfg<EW>::kThreads, 1)
         }
         bias_cur = bias_nxt;
       }
-      if (in_kind && dual && t + nunits < p.num_tiles) {
+      if (in_kind && dual && u + ustep < ucount) {
         int mb2, nb2, y1, y2, half2;
-        decode_unit(p, t + nunits, mb2, nb2, y1, y2, half2);
+        decode_unit(p, tile_of(u + ustep), mb2, nb2, y1, y2, half2);
         const int ncol2 = half2 < 0 ? nb2 * BN : nb2 * BN + half2 * (BN / 2);
         const int row0n = mb2 * TM + (int)rank * kBM + q * 32;
         if (ncol2 + c_first * 32 < p.N && row0n < p.M) {
@@ -1151,6 +1172,69 @@ static int pick_splits(long long tiles, int k_blocks, int sms) {
   return best;
 }
 
+// ------------------------------------------------------------------ die table
+// Which die each CTA pair of a full-grid pair launch lands on: the pairs are placed
+// deterministically on an idle GPU (cluster c on SMs 2c + const, one CTA per SM); the
+// probe (same one-CTA-per-SM footprint) records the SM of every cluster once per
+// device, die = SM id >= SMs / 2. The table only has to be a bijection onto the two
+// dies' pair slots for correctness (each die-local unit then has exactly one owner);
+// when the hardware places a launch differently only the L2 locality is lost.
+__global__ void __cluster_dims__(2, 1, 1) die_probe_kernel(int* out) {
+  extern __shared__ uint8_t probe_smem[];
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x == 0) out[blockIdx.x] = (int)smid;
+  if (threadIdx.x == 1) probe_smem[0] = 0;
+}
+
+struct DieTable {
+  bool ok = false;
+  int pairs = 0;
+  uint8_t die_of[128], slot_of[128];
+};
+
+static const DieTable* die_table(int sms, cudaStream_t stream) {
+  static std::mutex mu;
+  static DieTable tabs[64];
+  static bool done[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return &tabs[dev];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  DieTable& t = tabs[dev];
+  done[dev] = true;
+  const int pairs = sms / 2;
+  if (sms % 4 != 0 || pairs > 128) return &t;
+  int* d = nullptr;
+  if (cudaMalloc(&d, sms * sizeof(int)) != cudaSuccess) return &t;
+  const int smem = 200 * 1024;  // one CTA per SM, as the pair GEMMs
+  int host[256];
+  bool ran = cudaFuncSetAttribute(die_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  if (ran) {
+    die_probe_kernel<<<sms, 32, smem, stream>>>(d);
+    ran = cudaStreamSynchronize(stream) == cudaSuccess &&
+          cudaMemcpy(host, d, sms * sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  cudaFree(d);
+  if (!ran) {
+    cudaGetLastError();
+    return &t;
+  }
+  int count[2] = {0, 0};
+  for (int c = 0; c < pairs; ++c) {
+    const int die = host[2 * c] >= sms / 2 ? 1 : 0;
+    if (host[2 * c + 1] / (sms / 2) != die) return &t;  // a pair across the die boundary: no table
+    t.die_of[c] = (uint8_t)die;
+    t.slot_of[c] = (uint8_t)count[die]++;
+  }
+  if (count[0] != pairs / 2 || count[1] != pairs / 2) return &t;
+  t.pairs = pairs;
+  t.ok = true;
+  return &t;
+}
+
 static int launch_simt(const sg_gemm_args* a, int sms, void* stream) {
   if (a->mode != SG_EPI_NORMAL) return set_error(SG_ERR_SHAPE, "gemm: softmax epilogues need TMA-aligned operands");
   const long long total = a->nb1 * a->nb2 * a->M * a->N;
@@ -1251,14 +1335,6 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
     const char* e = getenv("SG_GEMM_HALF_TAIL");
     return e ? atoi(e) : 1;
   }();
-  if (env_half_tail && pair && bn == 256 && p.k_splits == 1) {
-    const long long tail = tiles % units;
-    if (tiles >= units && tail > 0 && 2 * tail <= units) {
-      p.full_units = (int)(tiles - tail);
-      p.num_tiles = (int)(tiles + tail);
-    }
-  }
-  p.fd_per.set((uint32_t)(p.m_tiles * p.n_tiles));
   static const int env_group = [] {  // SG_GEMM_GROUP_M=g (power of two) overrides the group height (experiments)
     const char* e = getenv("SG_GEMM_GROUP_M");
     return e ? atoi(e) : 0;
@@ -1267,6 +1343,32 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   p.group_shift = 0;
   while ((1 << p.group_shift) < p.group_m) ++p.group_shift;
   p.group_m = 1 << p.group_shift;
+  // die-local tile streams for large, full-grid pair products (SG_GEMM_DIE=0 disables):
+  // on two-die parts the A rows a group shares are then read by one die's pairs (the
+  // die-local streams replace the half-width last round)
+  p.die_mode = 0;
+  static const int env_die = [] {
+    const char* e = getenv("SG_GEMM_DIE");
+    return e ? atoi(e) : 1;
+  }();
+  if (env_die && pair && bn == 256 && batch == 1 && p.k_splits == 1 && units * 2 == sms && p.group_m >= 2 &&
+      p.m_tiles % p.group_m == 0 && tiles >= 4 * units && (double)a->M * (double)a->N * (double)a->K >= 4.0e11) {
+    const DieTable* dt = die_table(sms, static_cast<cudaStream_t>(stream));
+    if (dt && dt->ok && dt->pairs == units) {
+      p.die_mode = 1;
+      p.die_pairs = units / 2;
+      memcpy(p.die_of, dt->die_of, sizeof p.die_of);
+      memcpy(p.slot_of, dt->slot_of, sizeof p.slot_of);
+    }
+  }
+  if (env_half_tail && pair && bn == 256 && p.k_splits == 1 && !p.die_mode) {
+    const long long tail = tiles % units;
+    if (tiles >= units && tail > 0 && 2 * tail <= units) {
+      p.full_units = (int)(tiles - tail);
+      p.num_tiles = (int)(tiles + tail);
+    }
+  }
+  p.fd_per.set((uint32_t)(p.m_tiles * p.n_tiles));
   p.fd_span.set((uint32_t)(p.group_m * p.n_tiles));
   p.fd_nb2.set((uint32_t)p.nb2);
   p.d_f32 = a->d_dtype == SG_DTYPE_F32;
@@ -1338,6 +1440,9 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
 
   const int grid = (int)std::min<long long>(p.num_tiles, units) * (pair ? 2 : 1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // die-local tile streams for large, full-grid pair products (SG_GEMM_DIE=0 disables):
+  // on two-die parts the A rows a 16-m-tile group shares are then read by one die's pairs
+  (void)grid;
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
   // 8 epilogue warps unless the epilogue needs whole rows (softmax modes)
   static const int force_ew = [] {

@@ -229,3 +229,40 @@ def test_gemm_in_place_update_with_alpha(M, N, K):
     want = w + (-0.125) * (a.float().t() @ b.float())
     k.gemm(a.t(), b, w, c=w, alpha=-0.125)
     assert _rel(w, want) < 5e-5  # fp32 accumulation order over K = 16384
+
+
+_DIE_CASE = r'''
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2104_05343_b200 import kernels as K
+torch.manual_seed(2)
+M, N, Kd = 16384, 8192, 4096  # 2048 pair tiles: 27.7 waves (a partial last round)
+a = torch.randn(M, Kd, device="cuda").bfloat16()
+b = torch.randn(Kd, N, device="cuda").bfloat16()
+o = torch.empty(M, N, device="cuda", dtype=torch.float32)
+K.gemm(a, b, o)
+ref = a.float() @ b.float()
+err = ((o - ref).abs().max() / ref.abs().max()).item()
+torch.cuda.synchronize()
+torch.save((o.cpu(), err), sys.argv[1])
+'''
+
+
+@pytest.mark.gpu
+def test_gemm_die_local_tile_order(tmp_path):
+    """Large pair-tile products run their tiles in die-local streams (SG_GEMM_DIE): the same
+    tiles with the same K order, so the result equals the standard order bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for die in ("1", "0"):
+        f = tmp_path / f"o{die}.pt"
+        r = subprocess.run([sys.executable, "-c", _DIE_CASE, str(f)], env=dict(os.environ, SG_GEMM_DIE=die),
+                           capture_output=True, text=True, timeout=300, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(torch.load(f))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert outs[0][1] < 1e-3, outs[0][1]
