@@ -328,7 +328,9 @@ def test_dist_backend_on_one_gpu(tmp_path, rows, cols, peer):
         err = json.loads((tmp_path / f"r{rank}.json").read_text())
         assert err["ab"] < 1e-4 and err["abt"] < 1e-4 and err["atb"] < 1e-4, err
         assert err["loss"] < 1e-3 and err["grads"] < 2e-2, err
-        assert err["train_step"] < 1e-5 and err["train_step_vs_1x1"] < 2e-2, err
+        # train_step's SGD lands in the masters by remote reduce-adds in arrival order: a
+        # last-bit difference can flip a bf16 twin, so not bit-exact on 2x4
+        assert err["train_step"] < 5e-3 and err["train_step_vs_1x1"] < 2e-2, err
         calls = err["summa_calls"]
         if peer:
             assert calls.get("reduce", 0) == 0 and calls.get("allreduce", 0) == 0, calls
