@@ -51,12 +51,12 @@ GEMM = [
      'extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {'),
     ("        if (PAIR)\n          mbar_wait_cluster(&tempty[as], aph ^ 1);  // both CTAs' epilogues drained this buffer\n"
      "        else\n          mbar_wait(&tempty[as], aph ^ 1);",
-     "        if (blockIdx.x == 0) gtr(1, trm, 10);\n        if (PAIR)\n"
+     "        if (blockIdx.x == 0 && lane == 0) gtr(1, trm, 10);\n        if (PAIR)\n"
      "          mbar_wait_cluster(&tempty[as], aph ^ 1);  // both CTAs' epilogues drained this buffer\n"
-     "        else\n          mbar_wait(&tempty[as], aph ^ 1);\n        if (blockIdx.x == 0) gtr(1, trm, 11);"),
-    ("      uint32_t stage = 0, phase = 0, it = 0;\n      for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {",
+     "        else\n          mbar_wait(&tempty[as], aph ^ 1);\n        if (blockIdx.x == 0 && lane == 0) gtr(1, trm, 11);"),
+    ("      uint32_t stage = 0, phase = 0, it = 0;\n      for (int u = u0; u < ucount; u += ustep, ++it) {",
      "      uint32_t stage = 0, phase = 0, it = 0;\n      int trm = 0;\n"
-     "      for (int t = unit0; t < p.num_tiles; t += nunits, ++it) {"),
+     "      for (int u = u0; u < ucount; u += ustep, ++it) {"),
 ]
 
 
