@@ -1442,7 +1442,6 @@ extern "C" int sg_gemm(const sg_gemm_args* a, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // die-local tile streams for large, full-grid pair products (SG_GEMM_DIE=0 disables):
   // on two-die parts the A rows a 16-m-tile group shares are then read by one die's pairs
-  (void)grid;
   const bool amn = a->a_mn_major != 0, bmn = a->b_mn_major != 0;
   // 8 epilogue warps unless the epilogue needs whole rows (softmax modes)
   static const int force_ew = [] {
